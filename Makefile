@@ -1,0 +1,35 @@
+# Builds the product library paper_2407_12820_b200/lib/libpqkv.so for sm_100a
+# (and the test-only oracle via oracle/Makefile).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC,-fvisibility=hidden -Iinclude \
+           -Ipaper_2407_12820_b200/csrc --expt-relaxed-constexpr -diag-suppress 128
+CSRC := paper_2407_12820_b200/csrc
+OBJDIR := build/obj
+LIB := paper_2407_12820_b200/lib/libpqkv.so
+CU := ctx capi kmeans select attend
+OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(OBJDIR)/api.o
+HDRS := include/pqkv_c.h $(CSRC)/common.cuh $(CSRC)/internal.cuh
+
+.PHONY: all lib oracle clean
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJDIR)/api.o: $(CSRC)/api.cpp include/pqkv/pqkv.hpp include/pqkv_c.h
+	@mkdir -p $(OBJDIR)
+	g++ -std=c++20 -O2 -fPIC -fvisibility=hidden -Iinclude -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -Xlinker --exclude-libs,ALL
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)

@@ -1,0 +1,214 @@
+/*
+ * pqkv_c.h -- C ABI of the B200-native PQCache hot paths (libpqkv.so).
+ *
+ * This is the drop-in boundary for the two data-parallel hot paths of the
+ * reference `pqkv` library (/root/reference/proj):
+ *
+ *   (A) prefill PQ codebook build   pq_construct -> kmeans_fit   (pq.cpp:42-72,
+ *                                                                kmeans.cpp:159-190)
+ *   (B) decode retrieval             pq_score_gqa -> approx_topk -> fetch_topk /
+ *                                    selective_attention          (pq.cpp:152-177,
+ *                                    topk.cpp:8-25, kv_store.cpp:115-153,
+ *                                    attention.cpp:35-104)
+ *
+ * Every entry point is `extern "C"`, takes plain pointers and sizes (no torch
+ * or C++ types), returns a pqkv_status and records a thread-local message for
+ * pqkv_last_error().  Pointers named d_* are device (HBM) pointers, h_* are
+ * host pointers.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream).  Calls are asynchronous on `stream` unless documented.
+ *
+ * Status mapping back to the reference's exception types (the C++ layer in
+ * include/pqkv/pqkv.hpp re-throws them):
+ *   PQKV_EINVAL  -> std::invalid_argument   PQKV_ERANGE -> std::out_of_range
+ *   PQKV_ESTATE  -> std::logic_error        PQKV_ERUNTIME / PQKV_ECUDA -> std::runtime_error
+ *
+ * Exactness contract (checked by tests/ against oracle/):
+ *   codes, k-means assignments, ADC scores and top-k index sets are
+ *   bit-identical to the reference; centroids are the reference's fp64 means
+ *   rounded once to f32 (bit-identical); attention outputs are within 1e-3
+ *   relative on the fp32 fast path (PQKV_PREC_F32) and follow the reference's
+ *   fp64 arithmetic order on PQKV_PREC_F64.
+ *
+ * Threading: one pqkv_ctx owns a scratch arena and must not be used by two
+ * host threads at once; create one context per host thread / stream.
+ */
+#ifndef PQKV_C_H
+#define PQKV_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQKV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PQKV_API __attribute__((visibility("default")))
+#else
+#define PQKV_API
+#endif
+
+typedef enum {
+    PQKV_OK = 0,
+    PQKV_EINVAL = 1,   /* std::invalid_argument */
+    PQKV_ERANGE = 2,   /* std::out_of_range */
+    PQKV_ESTATE = 3,   /* std::logic_error */
+    PQKV_ERUNTIME = 4, /* std::runtime_error */
+    PQKV_ECUDA = 5     /* CUDA error (runtime_error) */
+} pqkv_status;
+
+typedef enum { PQKV_PREC_F32 = 0, PQKV_PREC_F64 = 1 } pqkv_precision;
+
+/* k-means assign-step arithmetic.  Both produce bit-identical assignments:
+ * EXACT evaluates every distance in the reference's fp64 order;
+ * FILTERED evaluates fp32 distances with a rigorous error bound and
+ * re-evaluates only the points whose nearest centroid is not certified. */
+typedef enum { PQKV_ASSIGN_FILTERED = 0, PQKV_ASSIGN_EXACT = 1 } pqkv_assign_mode;
+
+typedef struct pqkv_ctx pqkv_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+PQKV_API int pqkv_abi_version(void);
+PQKV_API const char* pqkv_last_error(void);
+/* Binds `device` and allocates the scratch arena lazily. */
+PQKV_API int pqkv_ctx_create(int device, pqkv_ctx** out);
+PQKV_API int pqkv_ctx_destroy(pqkv_ctx* ctx);
+/* Assign-step mode for subsequent builds on this context (default FILTERED). */
+PQKV_API int pqkv_ctx_set_assign_mode(pqkv_ctx* ctx, int mode);
+/* Counters of the last build on this context: fp64 re-checked points. */
+PQKV_API int pqkv_ctx_last_build_stats(pqkv_ctx* ctx, uint64_t* rechecked_points, uint64_t* total_points);
+
+/* ---- device memory helpers (for FFI hosts without a CUDA runtime) ----- */
+PQKV_API int pqkv_device_alloc(pqkv_ctx* ctx, size_t bytes, void** out);
+PQKV_API int pqkv_device_free(pqkv_ctx* ctx, void* ptr);
+/* kind: 0 host->device, 1 device->host, 2 device->device; synchronous. */
+PQKV_API int pqkv_copy(pqkv_ctx* ctx, void* dst, const void* src, size_t bytes, int kind);
+PQKV_API int pqkv_stream_sync(pqkv_ctx* ctx, void* stream);
+
+/* ---- geometry: PqConfig::create (pq.cpp:13-25) ------------------------- */
+PQKV_API int pqkv_pq_config(size_t m, size_t b, size_t d_h, size_t* d_m, size_t* n_clusters);
+/* codes_memory_ratio (pq.cpp:179-182) */
+PQKV_API int pqkv_codes_memory_ratio(size_t m, size_t b, size_t d_h, double* ratio);
+
+/* ---- (A) build --------------------------------------------------------- */
+
+/* kmeans_fit (kmeans.cpp:159-190) for n_problems independent problems.
+ * Problem q's point i is the `dim` contiguous floats at
+ *   d_points + q*problem_stride + i*row_stride.
+ * h_seeds[q] is the kmeans_fit seed.  Outputs: d_centroids [q][k][dim] f32,
+ * d_assign [q][n] u32, d_iterations [q] u32 (nullable), d_inertia
+ * [q][max_iter] f64 (nullable; computed only when non-NULL). */
+PQKV_API int pqkv_kmeans_fit(pqkv_ctx* ctx, const float* d_points, size_t n_problems,
+                    size_t problem_stride, size_t row_stride, size_t n, size_t dim, size_t k,
+                    size_t max_iter, const uint64_t* h_seeds, float* d_centroids,
+                    uint32_t* d_assign, uint32_t* d_iterations, double* d_inertia,
+                    void* stream);
+
+/* pq_construct (pq.cpp:42-72) for n_heads heads at once: the m subspace
+ * problems of every head run concurrently.  d_keys: head p's token i at
+ * d_keys + p*key_head_stride + i*d_h.  h_seeds[p] is head p's pq_construct
+ * seed (subspace j uses seed + 0x9e3779b97f4a7c15*(j+1)).  Outputs:
+ * d_centroids [p][m][2^b][d_m] f32; d_codes: head p's token i row of m u16 at
+ * d_codes + p*codes_head_stride + i*m. */
+PQKV_API int pqkv_pq_build(pqkv_ctx* ctx, const float* d_keys, size_t n_heads, size_t key_head_stride,
+                  size_t s, size_t d_h, size_t m, size_t b, size_t max_iter,
+                  const uint64_t* h_seeds, float* d_centroids, uint16_t* d_codes,
+                  size_t codes_head_stride, void* stream);
+
+/* pq_encode_one (pq.cpp:74-99) + append_code (pq.cpp:101-108) for n_heads
+ * heads: key p (d_keys + p*key_stride) is encoded against head p's f32
+ * centroids and its m-entry code row is written to
+ * d_codes + p*codes_head_stride + row*m. */
+PQKV_API int pqkv_pq_encode(pqkv_ctx* ctx, const float* d_keys, size_t n_heads, size_t key_stride,
+                   size_t d_h, size_t m, size_t b, const float* d_centroids,
+                   uint16_t* d_codes, size_t codes_head_stride, size_t row, void* stream);
+
+/* assign_nearest (kmeans.cpp:192-220). */
+PQKV_API int pqkv_assign_nearest(pqkv_ctx* ctx, const float* d_points, size_t n, size_t dim,
+                        const float* d_centroids, size_t k, uint32_t* d_assign, void* stream);
+
+/* ---- (B) decode retrieval ---------------------------------------------- */
+
+/* pq_score_gqa (pq.cpp:113-161) for n_heads heads: d_queries [p][g][d_h],
+ * codes as in pqkv_pq_build, d_scores + p*scores_head_stride + i. */
+PQKV_API int pqkv_pq_score(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
+                  size_t m, size_t b, const float* d_centroids, const uint16_t* d_codes,
+                  size_t codes_head_stride, size_t s, float* d_scores,
+                  size_t scores_head_stride, void* stream);
+
+/* top_k_desc / approx_topk (topk.cpp:8-25, pq.cpp:174-177) for n_rows rows:
+ * the k largest of d_scores + r*scores_stride [0..n) that are not excluded
+ * (d_excluded + r*n, u8, nullable), written to d_ids + r*k in (score desc,
+ * id asc) order.  EINVAL when k exceeds the candidate count (checked on
+ * device; the call synchronizes `stream` to report it). */
+PQKV_API int pqkv_topk(pqkv_ctx* ctx, const float* d_scores, size_t n_rows, size_t n,
+              size_t scores_stride, size_t k, const uint8_t* d_excluded, int64_t* d_ids,
+              void* stream);
+
+/* Fused pq_score_gqa + approx_topk without materialising scores: builds the
+ * fp64 ADC table in shared memory, scans the codes and radix-selects the k
+ * best middle rows of each head with the reference's tie rule.  Writes the
+ * selection bitmap d_bitmap [p][ceil(s/32)] u32 (bit r of the middle row r;
+ * nullable) and/or the ordered ids d_ids [p][k] (nullable). */
+PQKV_API int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
+                   size_t m, size_t b, const float* d_centroids, const uint16_t* d_codes,
+                   size_t codes_head_stride, size_t s, size_t k, uint32_t* d_bitmap,
+                   int64_t* d_ids, void* stream);
+
+/* Softmax attention over explicit row lists (softmax_attention,
+ * gqa_group_attention, selective_attention: attention.cpp:35-104).  For head
+ * p, query row r: softmax over d_rows[p][0..t) of K/V rows
+ * (d_keys + p*kv_head_stride + row*d_h) -> d_out [p][g][d_h]. */
+PQKV_API int pqkv_attend_rows(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g,
+                     size_t d_h, const float* d_keys, const float* d_values,
+                     size_t kv_head_stride, const int64_t* d_rows, size_t t, int precision,
+                     float* d_out, void* stream);
+
+/* exact_scores (attention.cpp:11-26): f32(fp64 dot * 1/sqrt(d_h)) for every
+ * head p, query row r and list row i -> d_scores [p][g][t].  Bit-identical. */
+PQKV_API int pqkv_exact_scores(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g,
+                               size_t d_h, const float* d_keys, size_t kv_head_stride,
+                               const int64_t* d_rows, size_t t, float* d_scores, void* stream);
+
+/* One decode layer's KV cache + PQ index, device resident.  Token ids of a
+ * head are its row indices: init [0,n_init), middle [n_init, total-n_local)
+ * (middle row r = token n_init+r = code row r), local [total-n_local, total),
+ * i.e. the reference's three segments (kv_store.hpp:61-79) collapsed into one
+ * HBM buffer per head. */
+typedef struct {
+    const float* keys;        /* [n_heads][kv_head_stride] f32, row = token id */
+    const float* values;      /* same layout as keys */
+    size_t kv_head_stride;    /* floats between heads (>= total*d_h) */
+    size_t n_heads;           /* (request, layer, kv_head) units */
+    size_t total;             /* tokens per head */
+    size_t n_init, n_local;   /* SegmentConfig (model.hpp:30-36) */
+    size_t d_h, m, b;         /* PqConfig */
+    const float* centroids;   /* [n_heads][m][2^b][d_m] f32 */
+    const uint16_t* codes;    /* head p, middle row r at codes + p*codes_head_stride + r*m */
+    size_t codes_head_stride;
+} pqkv_layer;
+
+/* Fused decode retrieval + sparse attention for one layer (the hot path):
+ * ADC table -> code scan -> top-k select (bitmap) -> K/V gather of
+ * init + selected + local rows -> split-K fp32 online softmax -> combine.
+ * d_queries/d_out [n_heads][g][d_h].  d_ids (nullable) additionally receives
+ * the selected middle rows in (score desc, id asc) order. */
+PQKV_API int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* layer, const float* d_queries, size_t g,
+                size_t k, float* d_out, int64_t* d_ids, void* stream);
+
+/* pqkv_decode with HOST query/output buffers: copies h_queries in, runs the
+ * fused layer, copies d_out back and synchronizes `stream`. */
+PQKV_API int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* layer, const float* h_queries,
+                     size_t g, size_t k, float* h_out, void* stream);
+
+/* Number of kernels pqkv_decode launches for this geometry (for the bench's
+ * gpu_launches accounting). */
+PQKV_API int pqkv_decode_launches(const pqkv_layer* layer, size_t g, int with_ids);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PQKV_C_H */

@@ -1,0 +1,306 @@
+"""B200-native PQCache hot paths (arxiv 2407.12820): Python host binding.
+
+Thin ctypes layer over the C ABI in ``include/pqkv_c.h`` (the product is the
+CUDA library ``lib/libpqkv.so``; PyTorch is only used here for device memory
+and streams).  Every function takes CUDA tensors, launches on the current
+torch stream and raises the reference's exception type on error
+(``ValueError`` for std::invalid_argument, ``IndexError`` for
+std::out_of_range, ``RuntimeError`` otherwise).
+
+There is no CPU fallback: importing works without a GPU, but every compute
+call needs the CUDA library and a device and fails loudly otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libpqkv.so")
+
+PQKV_OK, PQKV_EINVAL, PQKV_ERANGE, PQKV_ESTATE, PQKV_ERUNTIME, PQKV_ECUDA = range(6)
+PREC_F32, PREC_F64 = 0, 1
+ASSIGN_FILTERED, ASSIGN_EXACT = 0, 1
+
+_sz, _vp, _i, _u64 = C.c_size_t, C.c_void_p, C.c_int, C.c_uint64
+
+
+class pqkv_layer(C.Structure):
+    """Mirror of the C struct pqkv_layer (pqkv_c.h)."""
+
+    _fields_ = [
+        ("keys", _vp), ("values", _vp), ("kv_head_stride", _sz), ("n_heads", _sz),
+        ("total", _sz), ("n_init", _sz), ("n_local", _sz), ("d_h", _sz), ("m", _sz),
+        ("b", _sz), ("centroids", _vp), ("codes", _vp), ("codes_head_stride", _sz),
+    ]
+
+
+_SIGS = {
+    "pqkv_abi_version": (_i, []),
+    "pqkv_last_error": (C.c_char_p, []),
+    "pqkv_ctx_create": (_i, [_i, C.POINTER(_vp)]),
+    "pqkv_ctx_destroy": (_i, [_vp]),
+    "pqkv_ctx_set_assign_mode": (_i, [_vp, _i]),
+    "pqkv_ctx_last_build_stats": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
+    "pqkv_device_alloc": (_i, [_vp, _sz, C.POINTER(_vp)]),
+    "pqkv_device_free": (_i, [_vp, _vp]),
+    "pqkv_copy": (_i, [_vp, _vp, _vp, _sz, _i]),
+    "pqkv_stream_sync": (_i, [_vp, _vp]),
+    "pqkv_pq_config": (_i, [_sz, _sz, _sz, C.POINTER(_sz), C.POINTER(_sz)]),
+    "pqkv_codes_memory_ratio": (_i, [_sz, _sz, _sz, C.POINTER(C.c_double)]),
+    "pqkv_kmeans_fit": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pqkv_pq_build": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _sz, _vp]),
+    "pqkv_pq_encode": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _vp]),
+    "pqkv_assign_nearest": (_i, [_vp, _vp, _sz, _sz, _vp, _sz, _vp, _vp]),
+    "pqkv_pq_score": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
+    "pqkv_topk": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _vp, _vp]),
+    "pqkv_pq_search": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _vp, _vp]),
+    "pqkv_exact_scores": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp, _sz, _vp, _vp]),
+    "pqkv_attend_rows": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp, _sz, _i, _vp, _vp]),
+    "pqkv_decode": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp, _vp]),
+    "pqkv_decode_host": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp]),
+    "pqkv_decode_launches": (_i, [C.POINTER(pqkv_layer), _sz, _i]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """The loaded product library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"pqkv CUDA library missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class PqkvError(RuntimeError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == PQKV_OK:
+        return
+    msg = lib().pqkv_last_error().decode()
+    if rc == PQKV_EINVAL:
+        raise ValueError(msg)
+    if rc == PQKV_ERANGE:
+        raise IndexError(msg)
+    raise PqkvError(f"pqkv status {rc}: {msg}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("pqkv: expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("pqkv: expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Context:
+    """Owns a pqkv_ctx (scratch arena) bound to one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = _vp()
+        _check(lib().pqkv_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().pqkv_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_assign_mode(self, mode: int) -> None:
+        _check(lib().pqkv_ctx_set_assign_mode(self.h, mode))
+
+    def last_build_stats(self):
+        a, b = _u64(0), _u64(0)
+        _check(lib().pqkv_ctx_last_build_stats(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    # ---- (A) build ---------------------------------------------------------
+    def kmeans_fit(self, points, k: int, max_iter: int, seeds, inertia: bool = False):
+        """points [Q][n][dim] f32 -> (centroids [Q][k][dim], assign [Q][n] i32,
+        iterations [Q] i32, inertia [Q][max_iter] f64 | None)."""
+        import torch
+
+        Q, n, dim = points.shape
+        cen = torch.empty((Q, k, dim), dtype=torch.float32, device=points.device)
+        asg = torch.empty((Q, n), dtype=torch.int32, device=points.device)
+        its = torch.empty((Q,), dtype=torch.int32, device=points.device)
+        inr = torch.zeros((Q, max_iter), dtype=torch.float64, device=points.device) if inertia else None
+        sd = (C.c_uint64 * Q)(*[int(s) & (2**64 - 1) for s in seeds])
+        _check(lib().pqkv_kmeans_fit(self.h, _ptr(points), Q, n * dim, dim, n, dim, k, max_iter, sd,
+                                     _ptr(cen), _ptr(asg), _ptr(its), _ptr(inr), _stream()))
+        return cen, asg, its, inr
+
+    def pq_build(self, keys, m: int, b: int, max_iter: int, seeds):
+        """keys [P][s][d_h] f32 -> (centroids [P][m][2^b][d_m] f32, codes [P][s][m] i16 (u16 bits))."""
+        import torch
+
+        P, s, d_h = keys.shape
+        cen = torch.empty((P, m, 1 << b, d_h // m), dtype=torch.float32, device=keys.device)
+        codes = torch.empty((P, s, m), dtype=torch.int16, device=keys.device)
+        sd = (C.c_uint64 * P)(*[int(x) & (2**64 - 1) for x in seeds])
+        _check(lib().pqkv_pq_build(self.h, _ptr(keys), P, s * d_h, s, d_h, m, b, max_iter, sd, _ptr(cen),
+                                   _ptr(codes), s * m, _stream()))
+        return cen, codes
+
+    def pq_encode(self, keys, centroids, b: int, codes, row: int):
+        """Encode keys [P][d_h] and write code row `row` of codes [P][cap][m]."""
+        P, d_h = keys.shape
+        m = centroids.shape[1]
+        _check(lib().pqkv_pq_encode(self.h, _ptr(keys), P, d_h, d_h, m, b, _ptr(centroids), _ptr(codes),
+                                    codes.shape[1] * m, row, _stream()))
+
+    def assign_nearest(self, points, centroids):
+        import torch
+
+        n, dim = points.shape
+        out = torch.empty((n,), dtype=torch.int32, device=points.device)
+        _check(lib().pqkv_assign_nearest(self.h, _ptr(points), n, dim, _ptr(centroids), centroids.shape[0],
+                                         _ptr(out), _stream()))
+        return out
+
+    # ---- (B) decode retrieval ------------------------------------------------
+    def pq_score(self, queries, centroids, codes, b: int):
+        """queries [P][g][d_h], codes [P][s][m] -> scores [P][s] f32 (pq_score_gqa)."""
+        import torch
+
+        P, g, d_h = queries.shape
+        m = centroids.shape[1]
+        s = codes.shape[1]
+        out = torch.empty((P, s), dtype=torch.float32, device=queries.device)
+        _check(lib().pqkv_pq_score(self.h, _ptr(queries), P, g, d_h, m, b, _ptr(centroids), _ptr(codes),
+                                   s * m, s, _ptr(out), s, _stream()))
+        return out
+
+    def topk(self, scores, k: int, excluded=None):
+        """scores [R][n] -> ids [R][k] int64 in (score desc, id asc) order."""
+        import torch
+
+        R, n = scores.shape
+        ids = torch.empty((R, max(k, 1)), dtype=torch.int64, device=scores.device)
+        _check(lib().pqkv_topk(self.h, _ptr(scores), R, n, n, k, _ptr(excluded), _ptr(ids), _stream()))
+        return ids[:, :k]
+
+    def pq_search(self, queries, centroids, codes, b: int, k: int, s: int | None = None,
+                  bitmap: bool = True, ordered: bool = True):
+        """Fused ADC + select -> (bitmap [P][ceil(s/32)] i32 | None, ids [P][k] | None)."""
+        import torch
+
+        P, g, d_h = queries.shape
+        m = centroids.shape[1]
+        cap = codes.shape[1]
+        s = cap if s is None else s
+        words = (s + 31) // 32
+        bm = torch.empty((P, max(words, 1)), dtype=torch.int32, device=queries.device) if bitmap else None
+        ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device) if ordered else None
+        _check(lib().pqkv_pq_search(self.h, _ptr(queries), P, g, d_h, m, b, _ptr(centroids), _ptr(codes),
+                                    cap * m, s, k, _ptr(bm), _ptr(ids), _stream()))
+        return bm, (ids[:, :k] if ids is not None else None)
+
+    def exact_scores(self, queries, keys, rows):
+        import torch
+
+        P, g, d_h = queries.shape
+        t = rows.shape[1]
+        out = torch.empty((P, g, t), dtype=torch.float32, device=queries.device)
+        _check(lib().pqkv_exact_scores(self.h, _ptr(queries), P, g, d_h, _ptr(keys), keys[0].numel(),
+                                       _ptr(rows), t, _ptr(out), _stream()))
+        return out
+
+    def attend_rows(self, queries, keys, values, rows, precision: int = PREC_F32):
+        """Softmax attention of queries [P][g][d_h] over rows [P][t] of keys/values [P][S][d_h]."""
+        import torch
+
+        P, g, d_h = queries.shape
+        t = rows.shape[1]
+        out = torch.empty((P, g, d_h), dtype=torch.float32, device=queries.device)
+        _check(lib().pqkv_attend_rows(self.h, _ptr(queries), P, g, d_h, _ptr(keys), _ptr(values),
+                                      keys[0].numel(), _ptr(rows), t, precision, _ptr(out), _stream()))
+        return out
+
+    def decode(self, layer: "DecodeLayer", queries, k: int, want_ids: bool = False):
+        import torch
+
+        P, g, d_h = queries.shape
+        out = torch.empty((P, g, d_h), dtype=torch.float32, device=queries.device)
+        ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device) if want_ids else None
+        L = layer.struct()
+        _check(lib().pqkv_decode(self.h, C.byref(L), _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
+        return (out, ids[:, :k]) if want_ids else out
+
+    def decode_host(self, layer: "DecodeLayer", h_queries, h_out, k: int):
+        """h_queries / h_out: pinned CPU tensors [P][g][d_h]; synchronous."""
+        P, g, d_h = h_queries.shape
+        L = layer.struct()
+        _check(lib().pqkv_decode_host(self.h, C.byref(L), C.c_void_p(h_queries.data_ptr()), g, k,
+                                      C.c_void_p(h_out.data_ptr()), _stream()))
+
+
+@dataclass
+class DecodeLayer:
+    """Device-resident KV cache + PQ index of one layer (pqkv_layer).
+
+    keys/values [P][S][d_h] f32 (row = token id, S >= total), centroids
+    [P][m][2^b][d_m] f32, codes [P][cap][m] int16 (middle row r = token n_init+r).
+    """
+
+    keys: object
+    values: object
+    centroids: object
+    codes: object
+    total: int
+    n_init: int
+    n_local: int
+    b: int
+
+    def struct(self) -> pqkv_layer:
+        P, S, d_h = self.keys.shape
+        m = self.centroids.shape[1]
+        return pqkv_layer(
+            keys=self.keys.data_ptr(), values=self.values.data_ptr(), kv_head_stride=S * d_h,
+            n_heads=P, total=self.total, n_init=self.n_init, n_local=self.n_local, d_h=d_h, m=m,
+            b=self.b, centroids=self.centroids.data_ptr(), codes=self.codes.data_ptr(),
+            codes_head_stride=self.codes.shape[1] * m,
+        )
+
+    def launches(self, g: int, with_ids: bool = False) -> int:
+        L = self.struct()
+        return lib().pqkv_decode_launches(C.byref(L), g, int(with_ids))
+
+
+def pq_config(m: int, b: int, d_h: int):
+    """PqConfig::create -> (d_m, n_clusters); ValueError on the reference's rejections."""
+    d_m, c = _sz(0), _sz(0)
+    _check(lib().pqkv_pq_config(m, b, d_h, C.byref(d_m), C.byref(c)))
+    return d_m.value, c.value
+
+
+def codes_memory_ratio(m: int, b: int, d_h: int) -> float:
+    r = C.c_double(0)
+    _check(lib().pqkv_codes_memory_ratio(m, b, d_h, C.byref(r)))
+    return r.value

@@ -1,0 +1,284 @@
+// capi.cu -- C-ABI entry points (include/pqkv_c.h): argument validation with
+// the reference's rejection rules, then the launchers in kmeans.cu,
+// select.cu and attend.cu.  Nothing here computes on the host.
+#include <cmath>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace pqkv_dev;
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void need_ctx(pqkv_ctx* ctx) {
+    if (!ctx) fail(PQKV_EINVAL, "pqkv: context is NULL");
+    bind_device(ctx);
+}
+
+// PqConfig::create / validate (pq.cpp:13-31)
+void check_pq(size_t m, size_t b, size_t d_h) {
+    if (m < 1) fail(PQKV_EINVAL, "pq: m must be >= 1");
+    if (b < 1 || b > 16) fail(PQKV_EINVAL, "pq: b must be in [1, 16]");
+    if (d_h < 1 || d_h % m != 0) fail(PQKV_EINVAL, "pq: head_dim must be a positive multiple of m");
+}
+
+}  // namespace
+
+extern "C" {
+
+int pqkv_kmeans_fit(pqkv_ctx* ctx, const float* d_points, size_t n_problems, size_t problem_stride,
+                    size_t row_stride, size_t n, size_t dim, size_t k, size_t max_iter,
+                    const uint64_t* h_seeds, float* d_centroids, uint32_t* d_assign,
+                    uint32_t* d_iterations, double* d_inertia, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        // kmeans_fit argument checks (kmeans.cpp:160-164)
+        if (n < 1 || dim < 1) fail(PQKV_EINVAL, "kmeans: points must be a non-empty 2-d grid");
+        if (k < 1) fail(PQKV_EINVAL, "kmeans: n_clusters must be >= 1");
+        if (max_iter < 1) fail(PQKV_EINVAL, "kmeans: max_iter must be >= 1");
+        if (!d_points || !d_centroids || (!d_assign) || (!h_seeds && n > k))
+            fail(PQKV_EINVAL, "kmeans: NULL buffer");
+        std::vector<uint64_t> seeds(n_problems, 0);
+        if (h_seeds) seeds.assign(h_seeds, h_seeds + n_problems);
+        KmeansBatch b{};
+        b.points = d_points;
+        b.n_problems = n_problems;
+        b.problem_stride = problem_stride;
+        b.row_stride = row_stride;
+        b.n = n;
+        b.dim = dim;
+        b.k = k;
+        b.max_iter = max_iter;
+        b.m_sub = 1;
+        b.seeds = seeds.data();
+        b.centroids = d_centroids;
+        b.assign = d_assign;
+        b.iterations = d_iterations;
+        b.inertia = d_inertia;
+        launch_kmeans(ctx, b, as_stream(stream));
+    });
+}
+
+int pqkv_pq_build(pqkv_ctx* ctx, const float* d_keys, size_t n_heads, size_t key_head_stride,
+                  size_t s, size_t d_h, size_t m, size_t b, size_t max_iter,
+                  const uint64_t* h_seeds, float* d_centroids, uint16_t* d_codes,
+                  size_t codes_head_stride, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_pq(m, b, d_h);
+        if (s < 1) fail(PQKV_EINVAL, "pq: need at least one key");
+        if (max_iter < 1) fail(PQKV_EINVAL, "kmeans: max_iter must be >= 1");
+        if (!d_keys || !d_centroids || !d_codes || !h_seeds) fail(PQKV_EINVAL, "pq: NULL buffer");
+        // subspace j of head p uses seed_p + 0x9e3779b97f4a7c15 * (j + 1)  (pq.cpp:64-65)
+        std::vector<uint64_t> seeds(n_heads * m);
+        for (size_t p = 0; p < n_heads; ++p)
+            for (size_t j = 0; j < m; ++j)
+                seeds[p * m + j] = h_seeds[p] + 0x9e3779b97f4a7c15ull * (uint64_t)(j + 1);
+        KmeansBatch kb{};
+        kb.points = d_keys;
+        kb.n_problems = n_heads * m;
+        kb.problem_stride = key_head_stride;
+        kb.row_stride = d_h;
+        kb.n = s;
+        kb.dim = d_h / m;
+        kb.k = size_t{1} << b;
+        kb.max_iter = max_iter;
+        kb.m_sub = m;
+        kb.seeds = seeds.data();
+        kb.centroids = d_centroids;
+        kb.codes = d_codes;
+        kb.codes_head_stride = codes_head_stride;
+        launch_kmeans(ctx, kb, as_stream(stream));
+    });
+}
+
+int pqkv_pq_encode(pqkv_ctx* ctx, const float* d_keys, size_t n_heads, size_t key_stride,
+                   size_t d_h, size_t m, size_t b, const float* d_centroids, uint16_t* d_codes,
+                   size_t codes_head_stride, size_t row, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_pq(m, b, d_h);
+        if (n_heads == 0) return;
+        launch_encode(ctx, d_keys, n_heads, key_stride, d_h, m, size_t{1} << b, d_centroids, d_codes,
+                      codes_head_stride, row, as_stream(stream));
+    });
+}
+
+int pqkv_assign_nearest(pqkv_ctx* ctx, const float* d_points, size_t n, size_t dim,
+                        const float* d_centroids, size_t k, uint32_t* d_assign, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (dim < 1) fail(PQKV_EINVAL, "assign_nearest: dimension mismatch");
+        if (k < 1) fail(PQKV_EINVAL, "assign_nearest: need at least one centroid");
+        launch_assign_nearest(ctx, d_points, n, dim, d_centroids, k, d_assign, as_stream(stream));
+    });
+}
+
+int pqkv_pq_score(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
+                  size_t m, size_t b, const float* d_centroids, const uint16_t* d_codes,
+                  size_t codes_head_stride, size_t s, float* d_scores, size_t scores_head_stride,
+                  void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_pq(m, b, d_h);
+        if (g < 1) fail(PQKV_EINVAL, "pq: queries must be a non-empty 2-d grid");
+        if (n_heads == 0) return;
+        launch_score(ctx, d_queries, n_heads, g, d_h, m, size_t{1} << b, d_centroids, d_codes,
+                     codes_head_stride, s, d_scores, scores_head_stride, as_stream(stream));
+    });
+}
+
+int pqkv_topk(pqkv_ctx* ctx, const float* d_scores, size_t n_rows, size_t n, size_t scores_stride,
+              size_t k, const uint8_t* d_excluded, int64_t* d_ids, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (k > n) fail(PQKV_EINVAL, "top_k: k too large for the candidate set");
+        if (k == 0 || n_rows == 0) return;
+        if (!d_ids) fail(PQKV_EINVAL, "top_k: NULL output");
+        SelectSource src;
+        src.scores = d_scores;
+        src.scores_stride = scores_stride;
+        src.excluded = d_excluded;
+        if (!launch_select(ctx, src, n_rows, n, k, nullptr, d_ids, as_stream(stream), nullptr))
+            fail(PQKV_EINVAL, "top_k: k too large for the candidate set");
+    });
+}
+
+int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
+                   size_t m, size_t b, const float* d_centroids, const uint16_t* d_codes,
+                   size_t codes_head_stride, size_t s, size_t k, uint32_t* d_bitmap,
+                   int64_t* d_ids, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_pq(m, b, d_h);
+        if (g < 1) fail(PQKV_EINVAL, "pq: queries must be a non-empty 2-d grid");
+        if (k > s) fail(PQKV_EINVAL, "top_k: k too large for the candidate set");
+        SelectSource src;
+        src.queries = d_queries;
+        src.g = g;
+        src.d_h = d_h;
+        src.m = m;
+        src.C = size_t{1} << b;
+        src.centroids = d_centroids;
+        src.codes = d_codes;
+        src.codes_head_stride = codes_head_stride;
+        launch_select(ctx, src, n_heads, s, k, d_bitmap, k ? d_ids : nullptr, as_stream(stream), nullptr);
+    });
+}
+
+int pqkv_attend_rows(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
+                     const float* d_keys, const float* d_values, size_t kv_head_stride,
+                     const int64_t* d_rows, size_t t, int precision, float* d_out, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (d_h < 1) fail(PQKV_EINVAL, "attention: query dim must match key dim");
+        if (g < 1) fail(PQKV_EINVAL, "attention: queries must be a non-empty 2-d grid");
+        if (precision != PQKV_PREC_F32 && precision != PQKV_PREC_F64)
+            fail(PQKV_EINVAL, "attention: unknown precision");
+        launch_attend_rows(ctx, d_queries, n_heads, g, d_h, d_keys, d_values, kv_head_stride, d_rows,
+                           t, precision, d_out, as_stream(stream));
+    });
+}
+
+int pqkv_exact_scores(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
+                      const float* d_keys, size_t kv_head_stride, const int64_t* d_rows, size_t t,
+                      float* d_scores, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (d_h < 1) fail(PQKV_EINVAL, "attention: query dim must match key dim");
+        launch_exact_scores(ctx, d_queries, n_heads, g, d_h, d_keys, kv_head_stride, d_rows, t, d_scores,
+                            as_stream(stream));
+    });
+}
+
+static void check_layer(const pqkv_layer* L, size_t g, size_t k) {
+    if (!L) fail(PQKV_EINVAL, "decode: layer is NULL");
+    check_pq(L->m, L->b, L->d_h);
+    if (g < 1) fail(PQKV_EINVAL, "decode: g must be >= 1");
+    if (L->n_local < 1) fail(PQKV_EINVAL, "segments: n_local must be >= 1");
+    if (L->n_init + L->n_local > L->total)
+        fail(PQKV_EINVAL, "segments: n_init + n_local must be <= sequence length");
+    size_t s_mid = L->total - L->n_init - L->n_local;
+    if (s_mid < 1) fail(PQKV_EINVAL, "e2e: middle segment must be non-empty");
+    if (k > s_mid) fail(PQKV_EINVAL, "e2e: k exceeds the middle segment");
+    if (L->kv_head_stride < L->total * L->d_h) fail(PQKV_EINVAL, "decode: kv_head_stride too small");
+    if (L->total > 0x7fffffff) fail(PQKV_EINVAL, "decode: context too long");
+}
+
+int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size_t g, size_t k,
+                float* d_out, int64_t* d_ids, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_layer(L, g, k);
+        if (L->n_heads == 0) return;
+        cudaStream_t st = as_stream(stream);
+        const size_t s_mid = L->total - L->n_init - L->n_local;
+        const size_t words = ceil_div(s_mid, 32);
+        // the bitmap lives in the arena after the kernels' own scratch; keep a
+        // dedicated allocation so later Scratch plans cannot alias it
+        static thread_local uint32_t* bm = nullptr;
+        static thread_local size_t bm_words = 0;
+        static thread_local int bm_dev = -1;
+        if (L->n_heads * words > bm_words || bm_dev != ctx->device) {
+            if (bm) { cudaStreamSynchronize(st); cudaFree(bm); }
+            bm_words = L->n_heads * words;
+            PQKV_CUDA(cudaMalloc(&bm, bm_words * 4));
+            bm_dev = ctx->device;
+        }
+        SelectSource src;
+        src.queries = d_queries;
+        src.g = g;
+        src.d_h = L->d_h;
+        src.m = L->m;
+        src.C = size_t{1} << L->b;
+        src.centroids = L->centroids;
+        src.codes = L->codes;
+        src.codes_head_stride = L->codes_head_stride;
+        launch_select(ctx, src, L->n_heads, s_mid, k, bm, d_ids, st, nullptr);
+        if (launch_decode_attend(ctx, *L, d_queries, g, bm, d_out, st, nullptr)) return;
+        // generic geometry: ascending row lists, then the fp64 kernels
+        const size_t T = L->n_init + k + L->n_local;
+        int64_t* rows = nullptr;
+        PQKV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), L->n_heads * T * 8, st));
+        launch_bitmap_rows(ctx, bm, L->n_heads, words, L->n_init, L->n_local, L->total, T, rows, st);
+        launch_exact(ctx, d_queries, L->n_heads, g, L->d_h, L->keys, L->values, L->kv_head_stride, rows,
+                     T, d_out, st);
+        PQKV_CUDA(cudaFreeAsync(rows, st));
+    });
+}
+
+int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries, size_t g, size_t k,
+                     float* h_out, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_layer(L, g, k);
+        cudaStream_t st = as_stream(stream);
+        const size_t qbytes = L->n_heads * g * L->d_h * sizeof(float);
+        static thread_local float* dq = nullptr;
+        static thread_local size_t dq_bytes = 0;
+        if (2 * qbytes > dq_bytes) {
+            if (dq) { cudaStreamSynchronize(st); cudaFree(dq); }
+            dq_bytes = 2 * qbytes;
+            PQKV_CUDA(cudaMalloc(&dq, dq_bytes));
+        }
+        float* d_q = dq;
+        float* d_o = dq + L->n_heads * g * L->d_h;
+        PQKV_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, st));
+        int rc = pqkv_decode(ctx, L, d_q, g, k, d_o, nullptr, stream);
+        if (rc != PQKV_OK) fail(rc, pqkv_last_error());
+        PQKV_CUDA(cudaMemcpyAsync(h_out, d_o, qbytes, cudaMemcpyDeviceToHost, st));
+        PQKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int pqkv_decode_launches(const pqkv_layer* L, size_t g, int with_ids) {
+    if (!L) return 0;
+    bool fast = L->d_h == 128 && (g == 1 || g == 2 || g == 4) && L->kv_head_stride % 4 == 0;
+    int n = 1 /*select*/ + (with_ids ? 1 : 0) /*sort*/;
+    n += fast ? 2 /*attend + combine*/ : 3 /*rows + scores + softmax*/;
+    return n;
+}
+
+}  // extern "C"

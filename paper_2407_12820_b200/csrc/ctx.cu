@@ -1,0 +1,162 @@
+// ctx.cu -- context, scratch arena, status plumbing and the geometry entry
+// points of the C ABI (include/pqkv_c.h).
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.cuh"
+
+namespace {
+thread_local std::string g_last_error;
+}  // namespace
+
+namespace pqkv_dev {
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+void bind_device(pqkv_ctx* ctx) {
+    int cur = -1;
+    PQKV_CUDA(cudaGetDevice(&cur));
+    if (cur != ctx->device) PQKV_CUDA(cudaSetDevice(ctx->device));
+}
+
+void Scratch::commit() {
+    if (total_ > ctx_->arena_bytes) {
+        size_t want = round_up(total_ + total_ / 4, size_t(1) << 20);
+        if (ctx_->arena) {
+            PQKV_CUDA(cudaDeviceSynchronize());
+            PQKV_CUDA(cudaFree(ctx_->arena));
+            ctx_->arena = nullptr;
+            ctx_->arena_bytes = 0;
+        }
+        PQKV_CUDA(cudaMalloc(&ctx_->arena, want));
+        ctx_->arena_bytes = want;
+    }
+}
+
+void* pinned_staging(pqkv_ctx* ctx, size_t bytes) {
+    if (bytes > ctx->pinned_bytes) {
+        if (ctx->pinned) {
+            PQKV_CUDA(cudaDeviceSynchronize());
+            PQKV_CUDA(cudaFreeHost(ctx->pinned));
+        }
+        ctx->pinned = nullptr;
+        PQKV_CUDA(cudaMallocHost(&ctx->pinned, bytes));
+        ctx->pinned_bytes = bytes;
+    }
+    return ctx->pinned;
+}
+
+}  // namespace pqkv_dev
+
+using namespace pqkv_dev;
+
+extern "C" {
+
+int pqkv_abi_version(void) { return PQKV_ABI_VERSION; }
+
+const char* pqkv_last_error(void) { return g_last_error.c_str(); }
+
+int pqkv_ctx_create(int device, pqkv_ctx** out) {
+    return guard([&] {
+        if (!out) fail(PQKV_EINVAL, "pqkv_ctx_create: out is NULL");
+        int n = 0;
+        PQKV_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) fail(PQKV_EINVAL, "pqkv_ctx_create: bad device");
+        auto* c = new pqkv_ctx();
+        c->device = device;
+        bind_device(c);
+        PQKV_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+        PQKV_CUDA(cudaMalloc(&c->d_stats, 4 * sizeof(unsigned long long)));
+        *out = c;
+    });
+}
+
+int pqkv_ctx_destroy(pqkv_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        bind_device(ctx);
+        cudaDeviceSynchronize();
+        if (ctx->arena) cudaFree(ctx->arena);
+        if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        if (ctx->d_stats) cudaFree(ctx->d_stats);
+        delete ctx;
+    });
+}
+
+int pqkv_ctx_set_assign_mode(pqkv_ctx* ctx, int mode) {
+    return guard([&] {
+        if (!ctx) fail(PQKV_EINVAL, "ctx is NULL");
+        if (mode != PQKV_ASSIGN_FILTERED && mode != PQKV_ASSIGN_EXACT)
+            fail(PQKV_EINVAL, "unknown assign mode");
+        ctx->assign_mode = mode;
+    });
+}
+
+int pqkv_ctx_last_build_stats(pqkv_ctx* ctx, uint64_t* rechecked, uint64_t* total) {
+    return guard([&] {
+        if (!ctx) fail(PQKV_EINVAL, "ctx is NULL");
+        if (rechecked) *rechecked = ctx->last_rechecked;
+        if (total) *total = ctx->last_total;
+    });
+}
+
+int pqkv_device_alloc(pqkv_ctx* ctx, size_t bytes, void** out) {
+    return guard([&] {
+        if (!ctx || !out) fail(PQKV_EINVAL, "pqkv_device_alloc: NULL argument");
+        bind_device(ctx);
+        *out = nullptr;
+        if (bytes) PQKV_CUDA(cudaMalloc(out, bytes));
+    });
+}
+
+int pqkv_device_free(pqkv_ctx* ctx, void* ptr) {
+    return guard([&] {
+        if (!ctx) fail(PQKV_EINVAL, "pqkv_device_free: NULL context");
+        bind_device(ctx);
+        if (ptr) PQKV_CUDA(cudaFree(ptr));
+    });
+}
+
+int pqkv_copy(pqkv_ctx* ctx, void* dst, const void* src, size_t bytes, int kind) {
+    return guard([&] {
+        if (!ctx) fail(PQKV_EINVAL, "pqkv_copy: NULL context");
+        bind_device(ctx);
+        if (!bytes) return;
+        cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                           : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        PQKV_CUDA(cudaMemcpy(dst, src, bytes, k));
+    });
+}
+
+int pqkv_stream_sync(pqkv_ctx* ctx, void* stream) {
+    return guard([&] {
+        if (!ctx) fail(PQKV_EINVAL, "pqkv_stream_sync: NULL context");
+        bind_device(ctx);
+        PQKV_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+    });
+}
+
+// PqConfig::create (pq.cpp:13-25): same rejection rules and messages.
+int pqkv_pq_config(size_t m, size_t b, size_t d_h, size_t* d_m, size_t* n_clusters) {
+    return guard([&] {
+        if (m < 1) fail(PQKV_EINVAL, "pq: m must be >= 1");
+        if (b < 1 || b > 16) fail(PQKV_EINVAL, "pq: b must be in [1, 16]");
+        if (d_h < 1 || d_h % m != 0)
+            fail(PQKV_EINVAL, "pq: head_dim must be a positive multiple of m");
+        if (d_m) *d_m = d_h / m;
+        if (n_clusters) *n_clusters = size_t{1} << b;
+    });
+}
+
+// codes_memory_ratio (pq.cpp:179-182): bytes of codes per token over an fp16 key.
+int pqkv_codes_memory_ratio(size_t m, size_t b, size_t d_h, double* ratio) {
+    return guard([&] {
+        if (d_h < 1) fail(PQKV_EINVAL, "pq: head_dim must be >= 1");
+        if (!ratio) fail(PQKV_EINVAL, "ratio is NULL");
+        *ratio = static_cast<double>(m * b) / (16.0 * static_cast<double>(d_h));
+    });
+}
+
+}  // extern "C"

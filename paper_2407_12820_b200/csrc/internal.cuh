@@ -1,0 +1,142 @@
+// internal.cuh -- context object and the host-side launch API shared by the
+// C-ABI translation units.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct pqkv_ctx {
+    int device = 0;
+    int sm_count = 148;
+    int assign_mode = PQKV_ASSIGN_FILTERED;
+    // Scratch arena: one device allocation grown on demand; carved per call.
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    // Pinned + device staging for the host-buffer entry points.
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    // Device counters written by the build kernels (rechecked, total).
+    unsigned long long* d_stats = nullptr;
+    uint64_t last_rechecked = 0, last_total = 0;
+};
+
+namespace pqkv_dev {
+
+// Bump allocator over the context arena.  reserve() grows the arena (after a
+// device synchronize) when a call needs more than is currently allocated, so
+// one call's scratch never aliases another live buffer of the same call.
+class Scratch {
+public:
+    Scratch(pqkv_ctx* ctx) : ctx_(ctx) {}
+    // Two-phase use: plan() sizes, then commit() returns pointers in order.
+    template <typename T>
+    size_t plan(size_t count) {
+        size_t off = round_up(total_, 256);
+        total_ = off + count * sizeof(T);
+        offsets_.push_back(off);
+        return offsets_.size() - 1;
+    }
+    void commit();
+    template <typename T>
+    T* get(size_t handle) const {
+        return reinterpret_cast<T*>(static_cast<char*>(ctx_->arena) + offsets_[handle]);
+    }
+
+private:
+    pqkv_ctx* ctx_;
+    size_t total_ = 0;
+    std::vector<size_t> offsets_;
+};
+
+void bind_device(pqkv_ctx* ctx);
+void set_last_error(const std::string& msg);
+
+// Runs `f`, converting exceptions into a pqkv_status + pqkv_last_error().
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        set_last_error(std::string());
+        return PQKV_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return PQKV_ERUNTIME;
+    }
+}
+void* pinned_staging(pqkv_ctx* ctx, size_t bytes);
+
+// ---- launchers implemented in the kernel translation units -----------------
+
+struct KmeansBatch {
+    const float* points;
+    size_t n_problems, problem_stride, row_stride, n, dim, k, max_iter;
+    // problem q = (head q / m_sub, subspace q % m_sub): element (q, i) lives at
+    // points + (q / m_sub) * problem_stride + (q % m_sub) * dim + i*row_stride
+    size_t m_sub;
+    const uint64_t* seeds;  // host, one per problem (final kmeans_fit seed)
+    float* centroids;       // [q][k][dim]
+    uint32_t* assign;       // [q][n] (nullable when codes given)
+    uint16_t* codes;        // pq_build output: head h row i entry j (nullable)
+    size_t codes_head_stride;
+    uint32_t* iterations;   // nullable
+    double* inertia;        // nullable
+};
+void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t stream);
+
+void launch_encode(pqkv_ctx* ctx, const float* keys, size_t n_heads, size_t key_stride,
+                   size_t d_h, size_t m, size_t C, const float* centroids, uint16_t* codes,
+                   size_t codes_head_stride, size_t row, cudaStream_t stream);
+void launch_assign_nearest(pqkv_ctx* ctx, const float* points, size_t n, size_t dim,
+                           const float* centroids, size_t k, uint32_t* assign,
+                           cudaStream_t stream);
+
+void launch_score(pqkv_ctx* ctx, const float* queries, size_t n_heads, size_t g, size_t d_h,
+                  size_t m, size_t C, const float* centroids, const uint16_t* codes,
+                  size_t codes_head_stride, size_t s, float* scores, size_t scores_stride,
+                  cudaStream_t stream);
+
+// Selection source: either ADC (queries + index) or explicit scores.
+struct SelectSource {
+    // ADC mode
+    const float* queries = nullptr;
+    size_t g = 0, d_h = 0, m = 0, C = 0;
+    const float* centroids = nullptr;
+    const uint16_t* codes = nullptr;
+    size_t codes_head_stride = 0;
+    // score mode
+    const float* scores = nullptr;
+    size_t scores_stride = 0;
+    const uint8_t* excluded = nullptr;
+};
+// Returns false (after synchronizing) when k exceeds some row's candidates
+// (only possible with an exclusion mask).
+bool launch_select(pqkv_ctx* ctx, const SelectSource& src, size_t n_rows, size_t n, size_t k,
+                   uint32_t* bitmap, int64_t* ids, cudaStream_t stream, int* launches);
+
+void launch_attend_rows(pqkv_ctx* ctx, const float* queries, size_t n_heads, size_t g,
+                        size_t d_h, const float* keys, const float* values,
+                        size_t kv_head_stride, const int64_t* rows, size_t t, int precision,
+                        float* out, cudaStream_t stream);
+
+// Fused fast path (d_h == 128, g in {1,2,4}); returns false for other shapes.
+bool launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t g,
+                          const uint32_t* bitmap, float* out, cudaStream_t stream,
+                          int* launches);
+void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_t d_h,
+                  const float* keys, const float* values, size_t kv_head_stride,
+                  const int64_t* rows, size_t t, float* out, cudaStream_t st);
+void launch_exact_scores(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_t d_h,
+                         const float* keys, size_t kv_head_stride, const int64_t* rows, size_t t,
+                         float* scores, cudaStream_t st);
+void launch_bitmap_rows(pqkv_ctx* ctx, const uint32_t* bitmap, size_t P, size_t words,
+                        size_t n_init, size_t n_local, size_t total, size_t T, int64_t* rows,
+                        cudaStream_t st);
+
+}  // namespace pqkv_dev

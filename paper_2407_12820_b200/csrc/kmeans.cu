@@ -1,0 +1,787 @@
+// kmeans.cu -- prefill PQ codebook build on sm_100a (hot path A).
+//
+// Re-implements kmeans_fit (kmeans.cpp:159-190) and pq_construct
+// (pq.cpp:42-72) with bit-identical results: every quantity the reference
+// computes in fp64 is computed here in fp64 in the same order, with the
+// same tie rules.  One CTA owns one (head, subspace) k-means problem for its
+// whole life (seed -> assign -> [update -> assign]* -> emit), so a batch of
+// P heads x m subspaces is one launch with P*m independent CTAs and no host
+// round trips between iterations.
+//
+// Assign step (kmeans.cpp:86-130).  Two interchangeable evaluators:
+//  * EXACT: dist2 (kmeans.cpp:14-21) in fp64 with separate DSUB/DMUL/DADD
+//    (no contraction) for every (point, centroid).
+//  * FILTERED (default): fp32 distances from the f32-rounded centroids plus a
+//    rigorous bound E on |fp32 - fp64| (see certify()).  A point whose
+//    best fp32 candidate beats the runner-up by more than both bounds has the
+//    same fp64 argmin; every other point is queued and re-evaluated with the
+//    exact fp64 scan.  Assignments are therefore identical to EXACT.
+// The k-means++ seed (kmeans.cpp:59-84) keeps its two serial fp64 running
+// sums (a warp-wide serial scan, prefix stored for the binary search) and
+// uses the same filter to skip fp64 distance work that cannot lower min_d2.
+// update_means (kmeans.cpp:133-147) accumulates in ascending point order per
+// (cluster, dim): warp w owns clusters c = w (mod W) and walks the assignment
+// array in order.
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace pqkv_dev {
+namespace {
+
+constexpr int KM_THREADS = 256;
+constexpr int KM_WARPS = KM_THREADS / 32;
+
+struct KmArgs {
+    const float* points;
+    long long problem_stride, row_stride;
+    int m_sub, n, dim, K, T;
+    const unsigned long long* draws;  // [q][K]
+    float* centroids_out;             // [q][K][dim]
+    uint32_t* assign_out;             // [q][n] or null
+    uint16_t* codes;                  // head row-major codes or null
+    long long codes_head_stride;
+    uint32_t* iterations;
+    double* inertia;
+    // scratch, per-problem strides in elements
+    uint32_t* asg0;
+    uint32_t* asg1;
+    double* aux0;
+    double* aux1;
+    double* cen64;   // [q][K*dim]
+    double* gsums;   // [q][K*dim] when sums not in smem
+    uint32_t* gcounts;
+    uint32_t* queue;  // [q][n]
+    unsigned long long* stats;
+    int counts_smem, sums_smem, cen64_smem, cenf_smem;
+};
+
+struct Smem {
+    uint32_t* counts;
+    double* sums;
+    double* cen64;   // authoritative fp64 centroids (smem copy or global)
+    float* cenf;     // f32-rounded centroids (filter)
+    float* cnorm;    // ||cenf_c|| * (1 + 2^-20)
+    int* iscratch;   // small block-reduction scratch (64 ints)
+    double* dscratch;  // 64 doubles
+};
+
+__device__ __forceinline__ const float* point_ptr(const KmArgs& a, int q, int i) {
+    return a.points + (long long)(q / a.m_sub) * a.problem_stride +
+           (long long)(q % a.m_sub) * a.dim + (long long)i * a.row_stride;
+}
+
+// dist2 (kmeans.cpp:14-21) with x read from global, fp64, no contraction.
+__device__ __forceinline__ double dist2_g(const float* x, const double* c, int dim) {
+    double acc = 0.0;
+    for (int t = 0; t < dim; ++t) {
+        double diff = __dsub_rn((double)__ldg(x + t), c[t]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    return acc;
+}
+
+template <int D>
+__device__ __forceinline__ double dist2_r(const double (&x)[D], const double* c) {
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        double diff = __dsub_rn(x[t], c[t]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    return acc;
+}
+
+// Exact nearest (kmeans.cpp:86-97): strict <, lowest index on ties.
+__device__ uint32_t nearest_g(const float* x, const double* cen, int K, int dim) {
+    uint32_t best = 0;
+    double best_d = dist2_g(x, cen, dim);
+    for (int c = 1; c < K; ++c) {
+        double d = dist2_g(x, cen + (long long)c * dim, dim);
+        if (d < best_d) {
+            best_d = d;
+            best = c;
+        }
+    }
+    return best;
+}
+
+template <int D>
+__device__ uint32_t nearest_r(const double (&x)[D], const double* __restrict__ cen, int K) {
+    uint32_t best = 0;
+    double best_d = dist2_r<D>(x, cen);
+    int c = 1;
+    for (; c + 4 <= K; c += 4) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const double* c0 = cen + c * D;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            double d0 = __dsub_rn(x[t], c0[t]);
+            double d1 = __dsub_rn(x[t], c0[D + t]);
+            double d2 = __dsub_rn(x[t], c0[2 * D + t]);
+            double d3 = __dsub_rn(x[t], c0[3 * D + t]);
+            a0 = __dadd_rn(a0, __dmul_rn(d0, d0));
+            a1 = __dadd_rn(a1, __dmul_rn(d1, d1));
+            a2 = __dadd_rn(a2, __dmul_rn(d2, d2));
+            a3 = __dadd_rn(a3, __dmul_rn(d3, d3));
+        }
+        if (a0 < best_d) { best_d = a0; best = c; }
+        if (a1 < best_d) { best_d = a1; best = c + 1; }
+        if (a2 < best_d) { best_d = a2; best = c + 2; }
+        if (a3 < best_d) { best_d = a3; best = c + 3; }
+    }
+    for (; c < K; ++c) {
+        double d = dist2_r<D>(x, cen + c * D);
+        if (d < best_d) { best_d = d; best = c; }
+    }
+    return best;
+}
+
+// ---- fp32 filter ----------------------------------------------------------
+//
+// For one (point, centroid): S_f = fl32 sum_t fma(d_t, d_t, .) with
+// d_t = fl32(x_t - cf_t), cf = f32(c).  With u = 2^-24, S = exact real
+// sum (x - c)^2 and S64 the reference's fp64 value:
+//   |S_f - S64| <= (D+2)u(1+o(u)) sum(x-cf)^2 + 2u sqrt(S)||c|| + u^2||c||^2
+//                  + (D+2) 2^-53 S + subnormal slack,
+// and sum(x-cf)^2 <= S + 2u sqrt(S)||c|| + u^2||c||^2.  E() below doubles a
+// looser closed form of this (so the rounding of E itself and of the final
+// comparison are covered) and adds D*2^-140 for fp32 subnormal underflow.
+__device__ __forceinline__ float err_bound(float s, float cnorm, int D) {
+    const float u = 5.9604645e-8f;  // 2^-24
+    float su = sqrtf(fmaxf(s, 0.0f));
+    return 2.0f * ((D + 6) * u * s + 2.0f * u * su * cnorm + (D + 3) * u * u * cnorm * cnorm) +
+           D * 7.2e-43f;
+}
+
+template <int D>
+__device__ __forceinline__ float dist_f(const float (&x)[D], const float* c) {
+    float acc = 0.0f;
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        float d = x[t] - c[t];
+        acc = fmaf(d, d, acc);
+    }
+    return acc;
+}
+
+// Filtered nearest: returns the certified index or -1 (needs fp64 re-check).
+template <int D>
+__device__ int nearest_filtered(const float (&x)[D], const float* __restrict__ cenf,
+                                const float* __restrict__ cnorm, float cnorm_max, int K) {
+    float b1 = FLT_MAX, b2 = FLT_MAX;
+    int i1 = 0;
+    int c = 0;
+    for (; c + 4 <= K; c += 4) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        const float* c0 = cenf + c * D;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            float d0 = x[t] - c0[t];
+            float d1 = x[t] - c0[D + t];
+            float d2 = x[t] - c0[2 * D + t];
+            float d3 = x[t] - c0[3 * D + t];
+            a0 = fmaf(d0, d0, a0);
+            a1 = fmaf(d1, d1, a1);
+            a2 = fmaf(d2, d2, a2);
+            a3 = fmaf(d3, d3, a3);
+        }
+        float av[4] = {a0, a1, a2, a3};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float v = av[e];
+            if (v < b1) { b2 = b1; b1 = v; i1 = c + e; }
+            else if (v < b2) { b2 = v; }
+        }
+    }
+    for (; c < K; ++c) {
+        float v = dist_f<D>(x, cenf + c * D);
+        if (v < b1) { b2 = b1; b1 = v; i1 = c; }
+        else if (v < b2) { b2 = v; }
+    }
+    if (K == 1) return 0;
+    if (!(b1 < 1e37f) || !(b2 < 1e37f)) return -1;
+    // b2 must lie where v - E(v) is increasing (v > ~u^2 ||c||max^2) so that
+    // the runner-up bound also covers every farther centroid.
+    const float u = 5.9604645e-8f;
+    if (!(b2 > 8.0f * u * u * cnorm_max * cnorm_max)) return -1;
+    float e1 = err_bound(b1, cnorm[i1], D);
+    float e2 = err_bound(b2, cnorm_max, D);
+    return (b2 - e2 > b1 + e1) ? i1 : -1;
+}
+
+// ---- block helpers --------------------------------------------------------
+
+__device__ __forceinline__ void block_sync() { __syncthreads(); }
+
+// Serial fp64 running sum over v[0..n) in index order (kmeans.cpp:64-65,
+// 149-154), run by one warp; every lane carries the identical sum.  If
+// `prefix` is non-null the running value after element i is stored there.
+__device__ double warp_serial_sum(const double* v, int n, double* prefix) {
+    int lane = threadIdx.x & 31;
+    double total = 0.0;
+    double cur = (lane < n) ? v[lane] : 0.0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        int nxt = i0 + 32 + lane;
+        double pre = (nxt < n) ? v[nxt] : 0.0;  // prefetch next tile
+        double mine = 0.0;
+        int cnt = min(32, n - i0);
+        if (cnt == 32) {
+#pragma unroll
+            for (int l = 0; l < 32; ++l) {
+                double e = __shfl_sync(FULL, cur, l);
+                total = __dadd_rn(total, e);
+                if (lane == l) mine = total;
+            }
+        } else {
+            for (int l = 0; l < cnt; ++l) {
+                double e = __shfl_sync(FULL, cur, l);
+                total = __dadd_rn(total, e);
+                if (lane == l) mine = total;
+            }
+        }
+        if (prefix && lane < cnt) prefix[i0 + lane] = mine;
+        cur = pre;
+    }
+    return total;
+}
+
+// ---- the per-problem kernel -------------------------------------------------
+
+// D > 0: compile-time subspace dim, point held in registers (fp32 for the
+// filter, fp64 for EXACT).  D == 0: runtime dim, exact, global centroids.
+template <int D, bool FILTER>
+__global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int q = blockIdx.x;
+    const int n = a.n, K = a.K, dim = (D > 0 ? D : a.dim), T = a.T;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long KD = (long long)K * dim;
+
+    // ---- carve shared memory (layout planned on the host, same order) ----
+    Smem s;
+    {
+        unsigned char* p = smem_raw;
+        s.iscratch = reinterpret_cast<int*>(p);
+        p += 64 * sizeof(int);
+        s.dscratch = reinterpret_cast<double*>(p);
+        p += 64 * sizeof(double);
+        if (a.counts_smem) { s.counts = reinterpret_cast<uint32_t*>(p); p += ((K * 4 + 15) / 16) * 16; }
+        else s.counts = a.gcounts + (long long)q * K;
+        if (a.sums_smem) { s.sums = reinterpret_cast<double*>(p); p += KD * 8; }
+        else s.sums = a.gsums + q * KD;
+        if (a.cen64_smem) { s.cen64 = reinterpret_cast<double*>(p); p += KD * 8; }
+        else s.cen64 = a.cen64 + q * KD;
+        if (a.cenf_smem) {
+            s.cenf = reinterpret_cast<float*>(p); p += ((KD * 4 + 15) / 16) * 16;
+            s.cnorm = reinterpret_cast<float*>(p); p += ((K * 4 + 15) / 16) * 16;
+        } else { s.cenf = nullptr; s.cnorm = nullptr; }
+    }
+    uint32_t* asg = a.asg0 + (long long)q * n;
+    uint32_t* nxt = a.asg1 + (long long)q * n;
+    double* aux0 = a.aux0 + (long long)q * n;
+    double* aux1 = a.aux1 + (long long)q * n;
+    uint32_t* queue = a.queue + (long long)q * n;
+    __shared__ int sh_int[4];
+    __shared__ float sh_cmax;
+
+    // refresh the f32 copy + norms after the fp64 centroids change
+    auto refresh_f32 = [&]() {
+        if (!FILTER) return;
+        for (long long e = tid; e < KD; e += KM_THREADS) s.cenf[e] = (float)s.cen64[e];
+        block_sync();
+        if (tid == 0) sh_cmax = 0.f;
+        block_sync();
+        for (int c = tid; c < K; c += KM_THREADS) {
+            float acc = 0.f;
+            for (int t = 0; t < dim; ++t) acc = fmaf(s.cenf[c * dim + t], s.cenf[c * dim + t], acc);
+            float nrm = sqrtf(acc) * (1.0f + 9.6e-7f) + 1e-30f;
+            s.cnorm[c] = nrm;
+            atomicMax(reinterpret_cast<int*>(&sh_cmax), __float_as_int(nrm));  // nrm >= 0
+        }
+        block_sync();
+    };
+    auto set_centroid_from_point = [&](int c, int i) {
+        const float* x = point_ptr(a, q, i);
+        for (int t = tid; t < dim; t += KM_THREADS) s.cen64[(long long)c * dim + t] = (double)x[t];
+    };
+
+    // exact nearest for one point, x from global
+    auto exact_nearest_g = [&](int i) -> uint32_t {
+        return nearest_g(point_ptr(a, q, i), s.cen64, K, dim);
+    };
+
+    // ---- one assignment pass with repair (kmeans.cpp:103-130) ----
+    // writes out[], s.counts; returns after the block has synchronised.
+    auto assign_with_repair = [&](uint32_t* out) {
+        for (int c = tid; c < K; c += KM_THREADS) s.counts[c] = 0;
+        if (tid == 0) sh_int[0] = 0;  // queue length
+        block_sync();
+        if constexpr (FILTER) {
+            float cmax = sh_cmax;
+            for (int i = tid; i < n; i += KM_THREADS) {
+                float x[D > 0 ? D : 1];
+                const float* xp = point_ptr(a, q, i);
+#pragma unroll
+                for (int t = 0; t < (D > 0 ? D : 1); ++t) x[t] = __ldg(xp + t);
+                int c = nearest_filtered<(D > 0 ? D : 1)>(x, s.cenf, s.cnorm, cmax, K);
+                if (c >= 0) {
+                    out[i] = (uint32_t)c;
+                    atomicAdd(&s.counts[c], 1u);
+                } else {
+                    int slot = atomicAdd(&sh_int[0], 1);
+                    queue[slot] = (uint32_t)i;
+                }
+            }
+            block_sync();
+            int qn = sh_int[0];
+            for (int e = tid; e < qn; e += KM_THREADS) {
+                int i = (int)queue[e];
+                uint32_t c = exact_nearest_g(i);
+                out[i] = c;
+                atomicAdd(&s.counts[c], 1u);
+            }
+            if (tid == 0 && a.stats) {
+                atomicAdd(&a.stats[0], (unsigned long long)qn);
+                atomicAdd(&a.stats[1], (unsigned long long)n);
+            }
+        } else {
+            for (int i = tid; i < n; i += KM_THREADS) {
+                uint32_t c;
+                if constexpr (D > 0) {
+                    double x[D];
+                    const float* xp = point_ptr(a, q, i);
+#pragma unroll
+                    for (int t = 0; t < D; ++t) x[t] = (double)__ldg(xp + t);
+                    c = nearest_r<D>(x, s.cen64, K);
+                } else {
+                    c = exact_nearest_g(i);
+                }
+                out[i] = c;
+                atomicAdd(&s.counts[c], 1u);
+            }
+        }
+        block_sync();
+        if (n < K) return;
+        // any empty cluster?
+        int empty = 0;
+        for (int c = tid; c < K; c += KM_THREADS) empty |= (s.counts[c] == 0);
+        if (!__syncthreads_or(empty)) return;
+        // Rare path: donor repair.  d_i = dist2(p_i, mu_assign[i]) is fixed for
+        // every point that stays put; a moved donor becomes ineligible.
+        for (int i = tid; i < n; i += KM_THREADS)
+            aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64 + (long long)out[i] * dim, dim);
+        block_sync();
+        for (int c = 0; c < K; ++c) {
+            if (s.counts[c] != 0) continue;  // uniform: counts read after a sync
+            double best = -1.0;
+            int bi = n;
+            for (int i = tid; i < n; i += KM_THREADS) {
+                if (s.counts[out[i]] < 2) continue;
+                double d = aux0[i];
+                if (d > best) { best = d; bi = i; }  // ascending i per thread: first max kept
+            }
+            // block arg-max: larger d wins, then lower index
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                double ob = __shfl_xor_sync(FULL, best, o);
+                int oi = __shfl_xor_sync(FULL, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (lane == 0) { s.dscratch[warp] = best; s.iscratch[warp] = bi; }
+            block_sync();
+            if (tid == 0) {
+                double b = s.dscratch[0];
+                int ii = s.iscratch[0];
+                for (int w = 1; w < KM_WARPS; ++w) {
+                    double ob = s.dscratch[w];
+                    int oi = s.iscratch[w];
+                    if (ob > b || (ob == b && oi < ii)) { b = ob; ii = oi; }
+                }
+                sh_int[1] = ii;
+            }
+            block_sync();
+            int donor = sh_int[1];
+            if (donor >= n) break;  // fewer distinct points than clusters
+            if (tid == 0) {
+                s.counts[out[donor]] -= 1;
+                out[donor] = (uint32_t)c;
+                s.counts[c] += 1;
+            }
+            block_sync();
+        }
+        block_sync();
+    };
+
+    // ---- update_means (kmeans.cpp:133-147), ordered per (cluster, dim) ----
+    auto update_means = [&](const uint32_t* as) {
+        for (long long e = tid; e < KD; e += KM_THREADS) s.sums[e] = 0.0;
+        block_sync();
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            int i = i0 + lane;
+            uint32_t c = (i < n) ? as[i] : 0xffffffffu;
+            unsigned mine = __ballot_sync(FULL, i < n && (int)(c % KM_WARPS) == warp);
+            while (mine) {
+                int l = __ffs(mine) - 1;
+                mine &= mine - 1;
+                uint32_t cc = __shfl_sync(FULL, c, l);
+                const float* xp = point_ptr(a, q, i0 + l);
+                double* srow = s.sums + (long long)cc * dim;
+                for (int t = lane; t < dim; t += 32) srow[t] = __dadd_rn(srow[t], (double)__ldg(xp + t));
+            }
+        }
+        block_sync();
+        for (long long e = tid; e < KD; e += KM_THREADS) {
+            uint32_t cnt = s.counts[e / dim];
+            if (cnt != 0) s.cen64[e] = __ddiv_rn(s.sums[e], (double)cnt);
+        }
+        block_sync();
+    };
+
+    // =====================================================================
+    // 1. seeding
+    // =====================================================================
+    const unsigned long long* draws = a.draws + (long long)q * K;
+    if (n <= K) {
+        // seed_from_distinct (kmeans.cpp:44-57): first appearance, memcmp
+        for (int i = tid; i < n; i += KM_THREADS) {
+            const uint32_t* xi = reinterpret_cast<const uint32_t*>(point_ptr(a, q, i));
+            int seen = 0;
+            for (int j = 0; j < i && !seen; ++j) {
+                const uint32_t* xj = reinterpret_cast<const uint32_t*>(point_ptr(a, q, j));
+                int eq = 1;
+                for (int t = 0; t < dim && eq; ++t) eq = (xi[t] == xj[t]);
+                seen = eq;
+            }
+            asg[i] = seen ? 0u : 1u;  // distinct flag (asg reused as scratch)
+        }
+        block_sync();
+        if (tid == 0) {  // n <= K is small; ordered compaction by one thread
+            int nd = 0;
+            for (int i = 0; i < n; ++i)
+                if (asg[i]) nxt[nd++] = (uint32_t)i;
+            sh_int[2] = nd;
+        }
+        block_sync();
+        int nd = sh_int[2];
+        for (long long e = tid; e < KD; e += KM_THREADS) {
+            int c = (int)(e / dim), t = (int)(e % dim);
+            int src = (int)nxt[c < nd - 1 ? c : nd - 1];
+            s.cen64[e] = (double)point_ptr(a, q, src)[t];
+        }
+        block_sync();
+    } else {
+        // seed_plus_plus (kmeans.cpp:59-84) with the pre-drawn mt19937_64 stream
+        int c0 = (int)(draws[0] % (unsigned long long)n);
+        set_centroid_from_point(0, c0);
+        block_sync();
+        for (int i = tid; i < n; i += KM_THREADS)
+            aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64, dim);
+        for (int c = 1; c < K; ++c) {
+            block_sync();
+            if (warp == 0) {
+                double total = warp_serial_sum(aux0, n, aux1);
+                __syncwarp();
+                if (lane == 0) {
+                    int chosen;
+                    if (total > 0.0) {
+                        double u = (double)(draws[c] >> 11) * 0x1.0p-53;
+                        double target = __dmul_rn(u, total);
+                        // first i with prefix[i] >= target (prefix is non-decreasing)
+                        int lo = 0, hi = n - 1;
+                        while (lo < hi) {
+                            int mid = (lo + hi) >> 1;
+                            if (aux1[mid] >= target) hi = mid; else lo = mid + 1;
+                        }
+                        chosen = (aux1[lo] >= target) ? lo : n - 1;
+                    } else {
+                        chosen = (int)(draws[c] % (unsigned long long)n);
+                    }
+                    sh_int[3] = chosen;
+                }
+            }
+            block_sync();
+            set_centroid_from_point(c, sh_int[3]);
+            block_sync();
+            const double* cc = s.cen64 + (long long)c * dim;
+            if constexpr (FILTER) {
+                // fp32 screen: skip the fp64 distance when it cannot be < min_d2
+                float cf[D > 0 ? D : 1];
+                float cn = 0.f;
+#pragma unroll
+                for (int t = 0; t < (D > 0 ? D : 1); ++t) { cf[t] = (float)cc[t]; cn = fmaf(cf[t], cf[t], cn); }
+                cn = sqrtf(cn) * (1.0f + 9.6e-7f) + 1e-30f;
+                for (int i = tid; i < n; i += KM_THREADS) {
+                    const float* xp = point_ptr(a, q, i);
+                    float acc = 0.f;
+#pragma unroll
+                    for (int t = 0; t < (D > 0 ? D : 1); ++t) {
+                        float d = __ldg(xp + t) - cf[t];
+                        acc = fmaf(d, d, acc);
+                    }
+                    double old = aux0[i];
+                    if (acc < 1e37f && (double)(acc - err_bound(acc, cn, D)) > old) continue;
+                    double d = dist2_g(xp, cc, dim);
+                    if (d < old) aux0[i] = d;
+                }
+            } else {
+                for (int i = tid; i < n; i += KM_THREADS) {
+                    double d = dist2_g(point_ptr(a, q, i), cc, dim);
+                    if (d < aux0[i]) aux0[i] = d;
+                }
+            }
+        }
+        block_sync();
+    }
+    refresh_f32();
+
+    // =====================================================================
+    // 2. Lloyd iterations (kmeans.cpp:174-183)
+    // =====================================================================
+    assign_with_repair(asg);
+    int iters = 0;
+    for (int iter = 1; iter <= T; ++iter) {
+        update_means(asg);
+        if (a.inertia) {
+            for (int i = tid; i < n; i += KM_THREADS)
+                aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64 + (long long)asg[i] * dim, dim);
+            block_sync();
+            if (warp == 0) {
+                double tot = warp_serial_sum(aux0, n, nullptr);
+                if (lane == 0) a.inertia[(long long)q * T + iter - 1] = tot;
+            }
+            block_sync();
+        }
+        iters = iter;
+        refresh_f32();
+        assign_with_repair(nxt);
+        int changed = 0;
+        for (int i = tid; i < n; i += KM_THREADS) changed |= (nxt[i] != asg[i]);
+        if (!__syncthreads_or(changed)) break;
+        uint32_t* t = asg;
+        asg = nxt;
+        nxt = t;
+    }
+
+    // =====================================================================
+    // 3. emit: f32 centroids (kmeans.cpp:186-188), codes (pq.cpp:68-69)
+    // =====================================================================
+    for (long long e = tid; e < KD; e += KM_THREADS) a.centroids_out[q * KD + e] = (float)s.cen64[e];
+    if (a.assign_out)
+        for (int i = tid; i < n; i += KM_THREADS) a.assign_out[(long long)q * n + i] = asg[i];
+    if (a.codes) {
+        int head = q / a.m_sub, j = q % a.m_sub;
+        uint16_t* cd = a.codes + (long long)head * a.codes_head_stride + j;
+        for (int i = tid; i < n; i += KM_THREADS) cd[(long long)i * a.m_sub] = (uint16_t)asg[i];
+    }
+    if (a.iterations && tid == 0) a.iterations[q] = (uint32_t)iters;
+}
+
+// ---- pq_encode_one (pq.cpp:74-99): one CTA per head, one warp per subspace
+__global__ void encode_kernel(const float* keys, long long key_stride, int d_h, int m, int C,
+                              const float* centroids, uint16_t* codes,
+                              long long codes_head_stride, long long row) {
+    int p = blockIdx.x;
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int d_m = d_h / m;
+    const float* key = keys + p * key_stride;
+    const float* cen = centroids + (long long)p * m * C * d_m;
+    for (int j = warp; j < m; j += nw) {
+        double best = INFINITY;
+        int bi = 0x7fffffff;
+        for (int c = lane; c < C; c += 32) {
+            const float* cc = cen + ((long long)j * C + c) * d_m;
+            double acc = 0.0;
+            for (int t = 0; t < d_m; ++t) {
+                double diff = __dsub_rn((double)key[j * d_m + t], (double)cc[t]);
+                acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+            }
+            if (acc < best) { best = acc; bi = c; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            double ob = __shfl_xor_sync(FULL, best, o);
+            int oi = __shfl_xor_sync(FULL, bi, o);
+            if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) codes[p * codes_head_stride + row * m + j] = (uint16_t)(bi == 0x7fffffff ? 0 : bi);
+    }
+}
+
+// ---- assign_nearest (kmeans.cpp:192-220): thread per point ----------------
+__global__ void assign_nearest_kernel(const float* points, int n, int dim, const float* cen,
+                                      int K, uint32_t* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* x = points + (long long)i * dim;
+    uint32_t best = 0;
+    double best_d = INFINITY;
+    for (int c = 0; c < K; ++c) {
+        const float* cc = cen + (long long)c * dim;
+        double acc = 0.0;
+        for (int t = 0; t < dim; ++t) {
+            double diff = __dsub_rn((double)x[t], (double)cc[t]);
+            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+        }
+        if (acc < best_d) { best_d = acc; best = c; }
+    }
+    out[i] = best;
+}
+
+template <int D, bool F>
+void launch_problem(const KmArgs& a, int problems, size_t smem, cudaStream_t st) {
+    auto kern = kmeans_problem_kernel<D, F>;
+    PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<problems, KM_THREADS, smem, st>>>(a);
+    PQKV_LAUNCHED("kmeans_problem_kernel");
+}
+
+}  // namespace
+
+void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
+    const size_t Q = b.n_problems, n = b.n, dim = b.dim, K = b.k;
+    if (Q == 0) return;
+    if (n > 0x7fffffff || K > 0x7fffffff) fail(PQKV_EINVAL, "kmeans: problem too large");
+    const bool exact = ctx->assign_mode == PQKV_ASSIGN_EXACT;
+    // pick the compile-time dimension
+    int D = 0;
+    for (int d : {2, 4, 8, 16, 32, 64, 128})
+        if ((size_t)d == dim) D = d;
+    bool filter = !exact && D > 0;
+    if (!filter && D > 64) D = 0;  // fp64 point registers would spill
+
+    // shared-memory plan (same carve order as the kernel)
+    const size_t KD = K * dim;
+    const size_t budget = 200 * 1024;
+    size_t smem = 64 * 4 + 64 * 8;
+    int counts_smem = 0, sums_smem = 0, cen64_smem = 0, cenf_smem = 0;
+    auto take = [&](size_t bytes, int& flag) {
+        bytes = round_up(bytes, 16);
+        if (smem + bytes <= budget) { smem += bytes; flag = 1; }
+    };
+    take(K * 4, counts_smem);
+    if (filter) {
+        // the filter needs the f32 table in smem; fp64 centroids may stay global
+        size_t need = round_up(KD * 4, 16) + round_up(K * 4, 16);
+        if (smem + need > budget) { filter = false; if (D > 64) D = 0; }
+    }
+    if (filter) {
+        take(KD * 8, sums_smem);
+        size_t need = round_up(KD * 4, 16) + round_up(K * 4, 16);
+        smem += need;
+        cenf_smem = 1;
+        take(KD * 8, cen64_smem);
+    } else {
+        take(KD * 8, cen64_smem);
+        take(KD * 8, sums_smem);
+        if (D > 0 && !cen64_smem) D = 0;  // register path reads smem centroids
+    }
+
+    Scratch sc(ctx);
+    size_t h_draws = sc.plan<unsigned long long>(Q * K);
+    size_t h_a0 = sc.plan<uint32_t>(Q * n), h_a1 = sc.plan<uint32_t>(Q * n);
+    size_t h_x0 = sc.plan<double>(Q * n), h_x1 = sc.plan<double>(Q * n);
+    size_t h_cen = sc.plan<double>(Q * KD);
+    size_t h_sums = sc.plan<double>(sums_smem ? 1 : Q * KD);
+    size_t h_cnt = sc.plan<uint32_t>(counts_smem ? 1 : Q * K);
+    size_t h_q = sc.plan<uint32_t>(Q * n);
+    sc.commit();
+
+    // mt19937_64 draws (rng.hpp:13-33): k-means++ consumes exactly K raw
+    // draws per problem regardless of the data (kmeans.cpp:60, 68, 78).
+    std::vector<unsigned long long> draws(Q * K, 0ull);
+    for (size_t q = 0; q < Q; ++q) {
+        if (n <= K) continue;
+        std::mt19937_64 eng(b.seeds[q]);
+        for (size_t c = 0; c < K; ++c) draws[q * K + c] = eng();
+    }
+    PQKV_CUDA(cudaMemcpyAsync(sc.get<unsigned long long>(h_draws), draws.data(),
+                              draws.size() * 8, cudaMemcpyHostToDevice, st));
+    PQKV_CUDA(cudaMemsetAsync(ctx->d_stats, 0, 2 * sizeof(unsigned long long), st));
+
+    KmArgs a{};
+    a.points = b.points;
+    a.problem_stride = (long long)b.problem_stride;
+    a.row_stride = (long long)b.row_stride;
+    a.m_sub = (int)b.m_sub;
+    a.n = (int)n;
+    a.dim = (int)dim;
+    a.K = (int)K;
+    a.T = (int)b.max_iter;
+    a.draws = sc.get<unsigned long long>(h_draws);
+    a.centroids_out = b.centroids;
+    a.assign_out = b.assign;
+    a.codes = b.codes;
+    a.codes_head_stride = (long long)b.codes_head_stride;
+    a.iterations = b.iterations;
+    a.inertia = b.inertia;
+    a.asg0 = sc.get<uint32_t>(h_a0);
+    a.asg1 = sc.get<uint32_t>(h_a1);
+    a.aux0 = sc.get<double>(h_x0);
+    a.aux1 = sc.get<double>(h_x1);
+    a.cen64 = sc.get<double>(h_cen);
+    a.gsums = sc.get<double>(h_sums);
+    a.gcounts = sc.get<uint32_t>(h_cnt);
+    a.queue = sc.get<uint32_t>(h_q);
+    a.stats = ctx->d_stats;
+    a.counts_smem = counts_smem;
+    a.sums_smem = sums_smem;
+    a.cen64_smem = cen64_smem;
+    a.cenf_smem = cenf_smem;
+
+    bind_device(ctx);
+    int P = (int)Q;
+    if (filter) {
+        switch (D) {
+            case 2: launch_problem<2, true>(a, P, smem, st); break;
+            case 4: launch_problem<4, true>(a, P, smem, st); break;
+            case 8: launch_problem<8, true>(a, P, smem, st); break;
+            case 16: launch_problem<16, true>(a, P, smem, st); break;
+            case 32: launch_problem<32, true>(a, P, smem, st); break;
+            case 64: launch_problem<64, true>(a, P, smem, st); break;
+            case 128: launch_problem<128, true>(a, P, smem, st); break;
+            default: fail(PQKV_ERUNTIME, "kmeans: bad filter dim");
+        }
+    } else {
+        switch (D) {
+            case 2: launch_problem<2, false>(a, P, smem, st); break;
+            case 4: launch_problem<4, false>(a, P, smem, st); break;
+            case 8: launch_problem<8, false>(a, P, smem, st); break;
+            case 16: launch_problem<16, false>(a, P, smem, st); break;
+            case 32: launch_problem<32, false>(a, P, smem, st); break;
+            case 64: launch_problem<64, false>(a, P, smem, st); break;
+            default: launch_problem<0, false>(a, P, smem, st); break;
+        }
+    }
+    unsigned long long stats[2] = {0, 0};
+    PQKV_CUDA(cudaMemcpyAsync(stats, ctx->d_stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
+    PQKV_CUDA(cudaStreamSynchronize(st));
+    ctx->last_rechecked = stats[0];
+    ctx->last_total = stats[1];
+}
+
+void launch_encode(pqkv_ctx* ctx, const float* keys, size_t n_heads, size_t key_stride,
+                   size_t d_h, size_t m, size_t C, const float* centroids, uint16_t* codes,
+                   size_t codes_head_stride, size_t row, cudaStream_t st) {
+    bind_device(ctx);
+    int threads = (int)std::min<size_t>(32 * m, 256);
+    encode_kernel<<<(unsigned)n_heads, threads, 0, st>>>(keys, (long long)key_stride, (int)d_h,
+                                                         (int)m, (int)C, centroids, codes,
+                                                         (long long)codes_head_stride, (long long)row);
+    PQKV_LAUNCHED("encode_kernel");
+}
+
+void launch_assign_nearest(pqkv_ctx* ctx, const float* points, size_t n, size_t dim,
+                           const float* centroids, size_t k, uint32_t* assign, cudaStream_t st) {
+    bind_device(ctx);
+    if (n == 0) return;
+    assign_nearest_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(points, (int)n, (int)dim,
+                                                                     centroids, (int)k, assign);
+    PQKV_LAUNCHED("assign_nearest_kernel");
+}
+
+}  // namespace pqkv_dev

@@ -1,0 +1,550 @@
+// select.cu -- ADC scoring and exact top-k selection on sm_100a (hot path B).
+//
+// pq_score_gqa (pq.cpp:113-161) + approx_topk/top_k_desc (pq.cpp:174-177,
+// topk.cpp:8-25) as one fused kernel per head, run by a thread-block CLUSTER
+// of SEL_CL CTAs that split the head's middle tokens:
+//
+//  1. every CTA builds the fp64 ADC table T[j][c] in shared memory
+//     (sequential-t dot per (j,c), query rows summed in order -- the
+//     products are exact in fp64 so FMA is harmless, pq.cpp:118-124);
+//  2. scans its slice of codes, score_i = f32(((0.0 + T[0][c_i0]) + ...)),
+//     bit-identical to gather_scores (pq.cpp:128-140), and keeps the
+//     order-preserving 32-bit keys in shared memory;
+//  3. radix-selects the k-th largest key in three digit passes
+//     (11/11/10 bits); per-CTA histograms are merged through distributed
+//     shared memory (DSMEM), so no global atomics and no extra launches;
+//  4. resolves the tie at the threshold exactly like partial_sort with the
+//     (score desc, id asc) comparator: all keys above the threshold are
+//     selected, plus the lowest-id keys equal to it -- a cluster-wide
+//     exclusive prefix of per-CTA equal counts tells each CTA how many of
+//     its own equal keys it takes;
+//  5. writes the selection bitmap (one ballot per 32 tokens) and optionally
+//     the selected (key, id) pairs compacted in id order, which the
+//     stable radix sort kernel below orders into approx_topk's output.
+//
+// The same kernel serves top_k_desc over explicit scores (with the
+// reference's optional exclusion set, topk.cpp:10-15).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pqkv_dev {
+namespace {
+
+constexpr int SEL_CL = 8;         // CTAs per head (portable cluster size)
+constexpr int SEL_THREADS = 512;  // 16 warps
+constexpr int SEL_WARPS = SEL_THREADS / 32;
+constexpr int NB = 2048;          // bins of the two 11-bit digit passes
+
+struct SelArgs {
+    // ADC source
+    const float* queries;
+    int g, d_h, m, C;
+    const float* centroids;
+    const uint16_t* codes;
+    long long codes_head_stride;
+    // score source
+    const float* scores;
+    long long scores_stride;
+    const uint8_t* excluded;
+    // geometry
+    int n, k, slice, keys_smem;
+    uint32_t* gkeys;  // [rows][n] when !keys_smem
+    // outputs
+    uint32_t* bitmap;  // [rows][words] or null
+    int words;
+    uint32_t* sel_key;  // [rows][k] compacted in id order, or null
+    uint32_t* sel_id;
+    int* status;  // [rows]
+};
+
+// Builds T[j][c] (pq.cpp:113-126, rows accumulated as in pq.cpp:157-159).
+__device__ void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
+                          int C) {
+    const int d_m = d_h / m;
+    for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
+        const int j = e / C;
+        const float* cc = cen + (long long)e * d_m;
+        double acc[8];
+        double t = 0.0;
+        for (int r0 = 0; r0 < g; r0 += 8) {
+            const int rn = min(8, g - r0);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+            for (int tt = 0; tt < d_m; ++tt) {
+                double cv = (double)__ldg(cc + tt);
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (r < rn)
+                        acc[r] = __fma_rn((double)__ldg(q + (long long)(r0 + r) * d_h + j * d_m + tt), cv, acc[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < rn) t = __dadd_rn(t, acc[r]);
+        }
+        lut[e] = t;
+    }
+}
+
+__device__ __forceinline__ uint32_t adc_key(const double* lut, const uint16_t* code, int m, int C) {
+    double acc = 0.0;
+    for (int j = 0; j < m; ++j) acc = __dadd_rn(acc, lut[j * C + code[j]]);
+    return score_key((float)acc);
+}
+
+// Warp-aggregated shared-memory histogram increment; bin == ~0u is a no-op.
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin) {
+    unsigned peers = __match_any_sync(FULL, bin);
+    int leader = __ffs(peers) - 1;
+    if ((threadIdx.x & 31) == leader && bin != 0xffffffffu) atomicAdd(&hist[bin], __popc(peers));
+}
+
+// Block-wide exclusive scan (SEL_THREADS) of one u32 per thread.
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* wsum, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < SEL_WARPS ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(FULL, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < SEL_WARPS) wsum[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    uint32_t before = (warp ? wsum[warp - 1] : 0) + x - v;
+    if (total) *total = wsum[SEL_WARPS - 1];
+    __syncthreads();
+    return before;
+}
+
+// Finds the digit holding the k_rem-th largest element of hist[0..nb).
+// Returns (digit, count strictly above it) via out[0], out[1].
+__device__ void find_digit(const uint32_t* hist, int nb, uint32_t k_rem, uint32_t* wsum,
+                           uint32_t* out) {
+    const int per = nb / SEL_THREADS;  // 4 or 2
+    const int hi = nb - per * (int)threadIdx.x;  // this thread owns [hi-per, hi), from the top
+    uint32_t local = 0;
+    for (int b = hi - 1; b >= hi - per; --b) local += hist[b];
+    uint32_t above = block_excl_scan(local, wsum, nullptr);
+    if (above < k_rem && k_rem <= above + local) {
+        uint32_t acc = above;
+        for (int b = hi - 1; b >= hi - per; --b) {
+            if (k_rem <= acc + hist[b]) {
+                out[0] = (uint32_t)b;
+                out[1] = acc;
+                break;
+            }
+            acc += hist[b];
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelArgs a) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int row = blockIdx.x / SEL_CL;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lo = rank * a.slice;
+    const int hi = min(a.n, lo + a.slice);
+    const int cnt = max(0, hi - lo);
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* hist0 = reinterpret_cast<uint32_t*>(smem);  // 3 digit passes
+    uint32_t* hist1 = hist0 + NB;
+    uint32_t* hist2 = hist1 + NB;
+    uint32_t* tot = hist2 + NB;             // merged histogram [NB]
+    uint32_t* pub = tot + NB;               // published per-CTA counts [8]
+    uint32_t* wsum = pub + 8;               // [32]
+    uint32_t* sh = wsum + 32;               // misc [8]
+    double* lut = reinterpret_cast<double*>(sh + 8);
+    const int lut_elems = a.codes ? a.m * a.C : 0;
+    uint32_t* skeys = reinterpret_cast<uint32_t*>(lut + lut_elems);
+    uint32_t* keys = a.keys_smem ? skeys : a.gkeys + (long long)row * a.n + lo;
+
+    for (int b = tid; b < 4 * NB; b += SEL_THREADS) hist0[b] = 0;
+    if (a.codes) {
+        build_lut(lut, a.queries + (long long)row * a.g * a.d_h,
+                  a.centroids + (long long)row * a.m * a.C * (a.d_h / a.m), a.g, a.d_h, a.m, a.C);
+    }
+    __syncthreads();
+
+    // ---- keys + first digit histogram ----
+    for (int i0 = 0; i0 < cnt + SEL_THREADS - 1; i0 += SEL_THREADS) {
+        int li = i0 + tid;
+        uint32_t bin = 0xffffffffu;
+        if (li < cnt) {
+            int i = lo + li;
+            uint32_t key;
+            if (a.codes) {
+                key = adc_key(lut, a.codes + (long long)row * a.codes_head_stride + (long long)i * a.m, a.m, a.C);
+            } else {
+                bool ex = a.excluded && a.excluded[(long long)row * a.n + i];
+                key = ex ? 0u : score_key(a.scores[(long long)row * a.scores_stride + i]);
+            }
+            keys[li] = key;
+            if (key) bin = key >> 21;
+        }
+        hist_add(hist0, bin);
+    }
+    cluster.sync();
+
+    // ---- three digit passes ----
+    uint32_t k_rem = (uint32_t)a.k, prefix = 0;
+    const int shifts[3] = {21, 10, 0};
+    const int nbins[3] = {2048, 2048, 1024};
+    uint32_t* hists[3] = {hist0, hist1, hist2};
+    for (int p = 0; p < 3; ++p) {
+        if (p > 0) {
+            // local histogram of the next digit among keys matching the prefix
+            const int sh_hi = shifts[p - 1];
+            const uint32_t mask = (uint32_t)(nbins[p] - 1);
+            for (int i0 = 0; i0 < cnt + SEL_THREADS - 1; i0 += SEL_THREADS) {
+                int li = i0 + tid;
+                uint32_t bin = 0xffffffffu;
+                if (li < cnt) {
+                    uint32_t key = keys[li];
+                    if (key && (key >> sh_hi) == prefix) bin = (key >> shifts[p]) & mask;
+                }
+                hist_add(hists[p], bin);
+            }
+            cluster.sync();
+        }
+        // merge through DSMEM
+        for (int b = tid; b < nbins[p]; b += SEL_THREADS) {
+            uint32_t s = 0;
+#pragma unroll
+            for (int r = 0; r < SEL_CL; ++r) s += cluster.map_shared_rank(hists[p], r)[b];
+            tot[b] = s;
+        }
+        __syncthreads();
+        if (p == 0) {
+            // candidate count check (exclusions can leave fewer than k)
+            uint32_t local = 0;
+            for (int b = tid; b < NB; b += SEL_THREADS) local += tot[b];
+            uint32_t total;
+            block_excl_scan(local, wsum, &total);
+            if (total < k_rem) {
+                if (tid == 0 && rank == 0) a.status[row] = 1;
+                cluster.sync();
+                return;  // uniform across the cluster
+            }
+        }
+        find_digit(tot, nbins[p], k_rem, wsum, sh);
+        uint32_t digit = sh[0];
+        k_rem -= sh[1];
+        prefix = (prefix << (p == 0 ? 11 : (p == 1 ? 11 : 10))) | digit;
+        __syncthreads();
+    }
+    const uint32_t kstar = prefix;  // the k-th largest key; take k_rem of the ties
+
+    // ---- per-CTA counts of keys above / equal to the threshold ----
+    uint32_t ngt = 0, neq = 0;
+    for (int li = tid; li < cnt; li += SEL_THREADS) {
+        uint32_t key = keys[li];
+        ngt += key > kstar;
+        neq += key == kstar;
+    }
+    uint32_t cta_gt, cta_eq;
+    block_excl_scan(ngt, wsum, &cta_gt);
+    block_excl_scan(neq, wsum, &cta_eq);
+    if (tid == 0) { pub[0] = cta_gt; pub[1] = cta_eq; }
+    cluster.sync();
+    // how many equal keys this CTA takes, and where its selections start
+    uint32_t eq_before = 0, sel_before = 0;
+    for (int r = 0; r < rank; ++r) {
+        const uint32_t* rp = cluster.map_shared_rank(pub, r);
+        uint32_t rgt = rp[0], req = rp[1];
+        uint32_t take_r = k_rem > eq_before ? min(req, k_rem - eq_before) : 0;
+        sel_before += rgt + take_r;
+        eq_before += req;
+    }
+    const uint32_t take = k_rem > eq_before ? min(cta_eq, k_rem - eq_before) : 0;
+
+    // ---- ordered pass: bitmap words + compacted (key, id) ----
+    uint32_t eq_run = 0, sel_run = 0;
+    uint32_t* bm = a.bitmap ? a.bitmap + (long long)row * a.words : nullptr;
+    for (int i0 = 0; i0 < cnt; i0 += SEL_THREADS) {
+        int li = i0 + tid;
+        uint32_t key = li < cnt ? keys[li] : 0u;
+        bool gt = li < cnt && key > kstar;
+        bool eq = li < cnt && key == kstar;
+        unsigned eqm = __ballot_sync(FULL, eq);
+        // eq rank within the CTA's slice, in id order
+        if (lane == 0) wsum[warp] = __popc(eqm);
+        __syncthreads();
+        uint32_t wbefore = 0, tile_eq = 0;
+        for (int w = 0; w < SEL_WARPS; ++w) {
+            uint32_t c = wsum[w];
+            if (w < warp) wbefore += c;
+            tile_eq += c;
+        }
+        __syncthreads();
+        uint32_t my_eq_rank = eq_run + wbefore + __popc(eqm & lanemask_lt());
+        bool sel = gt || (eq && my_eq_rank < take);
+        unsigned selm = __ballot_sync(FULL, sel);
+        if (bm && lane == 0) {
+            int word = (lo + i0) / 32 + warp;
+            if ((lo + i0 + warp * 32) < hi) bm[word] = selm;
+        }
+        if (a.sel_key) {
+            if (lane == 0) wsum[warp] = __popc(selm);
+            __syncthreads();
+            uint32_t sbefore = 0, tile_sel = 0;
+            for (int w = 0; w < SEL_WARPS; ++w) {
+                uint32_t c = wsum[w];
+                if (w < warp) sbefore += c;
+                tile_sel += c;
+            }
+            __syncthreads();
+            if (sel) {
+                uint32_t pos = sel_before + sel_run + sbefore + __popc(selm & lanemask_lt());
+                a.sel_key[(long long)row * a.k + pos] = key;
+                a.sel_id[(long long)row * a.k + pos] = (uint32_t)(lo + li);
+            }
+            sel_run += tile_sel;
+        }
+        eq_run += tile_eq;
+    }
+    cluster.sync();  // keep this CTA's smem alive for remote readers
+}
+
+// ---- stable LSD radix sort of k (key, id) pairs by key, descending --------
+// One CTA per row; ids arrive in ascending order so stability yields the
+// reference's (score desc, id asc) order (topk.cpp:17-22).
+constexpr int SORT_THREADS = 1024;
+constexpr int SORT_WARPS = SORT_THREADS / 32;
+
+__global__ void __launch_bounds__(SORT_THREADS, 1)
+    sort_desc_kernel(const uint32_t* key_in, const uint32_t* id_in, uint32_t* key_tmp,
+                     uint32_t* id_tmp, int k, int64_t* ids_out) {
+    __shared__ uint32_t base[256];
+    __shared__ uint32_t cnt[SORT_WARPS][256];
+    __shared__ uint32_t tile_tot[256];
+    const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t* kin = key_in + (long long)row * k;
+    const uint32_t* iin = id_in + (long long)row * k;
+    uint32_t* kout = key_tmp + (long long)row * k;
+    uint32_t* iout = id_tmp + (long long)row * k;
+    // Ping-pong: pass 0 in->tmp, 1 tmp->in(copy area), ... we use the input
+    // buffers as the second half (they are scratch owned by the launcher).
+    uint32_t* ka = const_cast<uint32_t*>(kin);
+    uint32_t* ia = const_cast<uint32_t*>(iin);
+    uint32_t* kb = kout;
+    uint32_t* ib = iout;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 8 * pass;
+        for (int d = tid; d < 256; d += SORT_THREADS) base[d] = 0;
+        __syncthreads();
+        for (int i = tid; i < k; i += SORT_THREADS) atomicAdd(&base[255 - ((ka[i] >> shift) & 255)], 1u);
+        __syncthreads();
+        if (tid < 32) {  // exclusive scan of 256 counters by one warp
+            uint32_t v[8], s = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { v[e] = base[lane * 8 + e]; s += v[e]; }
+            uint32_t x = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            uint32_t run = x - s;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { base[lane * 8 + e] = run; run += v[e]; }
+        }
+        __syncthreads();
+        for (int t0 = 0; t0 < k; t0 += SORT_THREADS) {
+            for (int e = tid; e < SORT_WARPS * 256; e += SORT_THREADS) (&cnt[0][0])[e] = 0;
+            __syncthreads();
+            int i = t0 + tid;
+            uint32_t d = 0xffffffffu, key = 0, id = 0;
+            if (i < k) { key = ka[i]; id = ia[i]; d = 255 - ((key >> shift) & 255); }
+            unsigned peers = __match_any_sync(FULL, d);
+            uint32_t rank = __popc(peers & lanemask_lt());
+            if (d != 0xffffffffu && rank == 0) cnt[warp][d] = __popc(peers);
+            __syncthreads();
+            if (tid < 256) {
+                uint32_t run = 0;
+                for (int w = 0; w < SORT_WARPS; ++w) {
+                    uint32_t c = cnt[w][tid];
+                    cnt[w][tid] = run;
+                    run += c;
+                }
+                tile_tot[tid] = run;
+            }
+            __syncthreads();
+            if (d != 0xffffffffu) {
+                uint32_t pos = base[d] + cnt[warp][d] + rank;
+                kb[pos] = key;
+                ib[pos] = id;
+            }
+            __syncthreads();
+            if (tid < 256) base[tid] += tile_tot[tid];
+            __syncthreads();
+        }
+        uint32_t* t;
+        t = ka; ka = kb; kb = t;
+        t = ia; ia = ib; ib = t;
+    }
+    // after 4 passes the sorted data is back in the input buffers
+    for (int i = tid; i < k; i += SORT_THREADS) ids_out[(long long)row * k + i] = (int64_t)ia[i];
+}
+
+// ---- pq_score (materialised scores): LUT kernel + gather kernel ----------
+__global__ void lut_kernel(const float* queries, int g, int d_h, int m, int C,
+                           const float* centroids, double* lut_out) {
+    int p = blockIdx.x;
+    build_lut(lut_out + (long long)p * m * C, queries + (long long)p * g * d_h,
+              centroids + (long long)p * m * C * (d_h / m), g, d_h, m, C);
+}
+
+__global__ void gather_scores_kernel(const double* lut_g, int m, int C, const uint16_t* codes,
+                                     long long codes_head_stride, int s, float* scores,
+                                     long long scores_stride, int lut_smem) {
+    extern __shared__ double lut_s[];
+    int p = blockIdx.y;
+    const double* lut = lut_g + (long long)p * m * C;
+    if (lut_smem) {
+        for (int e = threadIdx.x; e < m * C; e += blockDim.x) lut_s[e] = lut[e];
+        __syncthreads();
+        lut = lut_s;
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s; i += gridDim.x * blockDim.x) {
+        const uint16_t* code = codes + p * codes_head_stride + (long long)i * m;
+        double acc = 0.0;
+        for (int j = 0; j < m; ++j) acc = __dadd_rn(acc, lut[j * C + code[j]]);
+        scores[p * scores_stride + i] = (float)acc;
+    }
+}
+
+}  // namespace
+
+void launch_score(pqkv_ctx* ctx, const float* queries, size_t n_heads, size_t g, size_t d_h,
+                  size_t m, size_t C, const float* centroids, const uint16_t* codes,
+                  size_t codes_head_stride, size_t s, float* scores, size_t scores_stride,
+                  cudaStream_t st) {
+    bind_device(ctx);
+    Scratch sc(ctx);
+    size_t h_lut = sc.plan<double>(n_heads * m * C);
+    sc.commit();
+    double* lut = sc.get<double>(h_lut);
+    lut_kernel<<<(unsigned)n_heads, 256, 0, st>>>(queries, (int)g, (int)d_h, (int)m, (int)C,
+                                                  centroids, lut);
+    PQKV_LAUNCHED("lut_kernel");
+    if (s == 0) return;
+    size_t lut_bytes = m * C * sizeof(double);
+    int lut_smem = lut_bytes <= 96 * 1024;
+    if (lut_smem)
+        PQKV_CUDA(cudaFuncSetAttribute(gather_scores_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lut_bytes));
+    unsigned bx = (unsigned)std::min<size_t>(ceil_div(s, 256), std::max(1, 2 * ctx->sm_count / (int)std::max<size_t>(1, n_heads)) + 1);
+    dim3 grid(bx, (unsigned)n_heads);
+    gather_scores_kernel<<<grid, 256, lut_smem ? lut_bytes : 0, st>>>(
+        lut, (int)m, (int)C, codes, (long long)codes_head_stride, (int)s, scores,
+        (long long)scores_stride, lut_smem);
+    PQKV_LAUNCHED("gather_scores_kernel");
+}
+
+bool launch_select(pqkv_ctx* ctx, const SelectSource& src, size_t rows, size_t n, size_t k,
+                   uint32_t* bitmap, int64_t* ids, cudaStream_t st, int* launches) {
+    bind_device(ctx);
+    int nl = 0;
+    const size_t words = ceil_div(n, 32);
+    if (rows == 0) return true;
+    if (k == 0 || n == 0) {
+        if (bitmap) PQKV_CUDA(cudaMemsetAsync(bitmap, 0, rows * words * 4, st)), ++nl;
+        if (launches) *launches = nl;
+        return true;
+    }
+    if (n > 0x7fffffff) fail(PQKV_EINVAL, "select: too many tokens");
+    const bool adc = src.codes != nullptr;
+    if (adc && src.m * src.C * 8 > 64 * 1024)
+        fail(PQKV_EINVAL, "select: fused ADC search needs m * 2^b <= 8192 (use pqkv_pq_score + pqkv_topk)");
+    const size_t slice = round_up(ceil_div(n, SEL_CL), 32);
+    const size_t fixed = (4 * NB + 8 + 32 + 8) * 4 + (adc ? src.m * src.C * 8 : 0);
+    int keys_smem = fixed + slice * 4 <= 200 * 1024;
+    size_t smem = fixed + (keys_smem ? slice * 4 : 0);
+
+    Scratch sc(ctx);
+    size_t h_keys = sc.plan<uint32_t>(keys_smem ? 1 : rows * n);
+    size_t h_sk = sc.plan<uint32_t>(ids ? rows * k : 1), h_si = sc.plan<uint32_t>(ids ? rows * k : 1);
+    size_t h_tk = sc.plan<uint32_t>(ids ? rows * k : 1), h_ti = sc.plan<uint32_t>(ids ? rows * k : 1);
+    size_t h_status = sc.plan<int>(rows);
+    sc.commit();
+
+    SelArgs a{};
+    a.queries = src.queries;
+    a.g = (int)src.g;
+    a.d_h = (int)src.d_h;
+    a.m = (int)src.m;
+    a.C = (int)src.C;
+    a.centroids = src.centroids;
+    a.codes = src.codes;
+    a.codes_head_stride = (long long)src.codes_head_stride;
+    a.scores = src.scores;
+    a.scores_stride = (long long)src.scores_stride;
+    a.excluded = src.excluded;
+    a.n = (int)n;
+    a.k = (int)k;
+    a.slice = (int)slice;
+    a.keys_smem = keys_smem;
+    a.gkeys = sc.get<uint32_t>(h_keys);
+    a.bitmap = bitmap;
+    a.words = (int)words;
+    a.sel_key = ids ? sc.get<uint32_t>(h_sk) : nullptr;
+    a.sel_id = ids ? sc.get<uint32_t>(h_si) : nullptr;
+    a.status = sc.get<int>(h_status);
+    if (src.excluded) PQKV_CUDA(cudaMemsetAsync(a.status, 0, rows * sizeof(int), st)), ++nl;
+
+    PQKV_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(rows * SEL_CL));
+    cfg.blockDim = dim3(SEL_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = SEL_CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PQKV_CUDA(cudaLaunchKernelEx(&cfg, select_kernel, a));
+    ++nl;
+    bool ok = true;
+    if (src.excluded) {
+        std::vector<int> status(rows);
+        PQKV_CUDA(cudaMemcpyAsync(status.data(), a.status, rows * sizeof(int), cudaMemcpyDeviceToHost, st));
+        PQKV_CUDA(cudaStreamSynchronize(st));
+        for (int s : status) ok = ok && s == 0;
+        if (!ok) {
+            if (launches) *launches = nl;
+            return false;
+        }
+    }
+    if (ids) {
+        sort_desc_kernel<<<(unsigned)rows, SORT_THREADS, 0, st>>>(a.sel_key, a.sel_id,
+                                                                 sc.get<uint32_t>(h_tk),
+                                                                 sc.get<uint32_t>(h_ti), (int)k, ids);
+        PQKV_LAUNCHED("sort_desc_kernel");
+        ++nl;
+    }
+    if (launches) *launches = nl;
+    return ok;
+}
+
+}  // namespace pqkv_dev
