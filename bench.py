@@ -1,0 +1,390 @@
+#!/usr/bin/env python3
+"""Benchmark: decode PQ-retrieve+attend us/layer @128K ctx (+ PQ build tokens/s, HBM GB/s).
+
+Workload (BASELINE.json north_star, N=1): one decoder layer with 32 heads x 128
+dim (MHA, g=1), 131072-token context, PQ m=2 b=6 (64 centroids), top-k =
+round(s/5) = 26214 middle tokens + 4 initial + 64 local, decode batch 1.  A
+"step" is one fused decode of that layer (ADC table -> code scan -> radix
+select -> K/V gather -> split-K softmax -> combine) for all 32 heads.
+Four independent layers (4 x 4.3 GB of fp32 K/V, each with its own GPU-built
+PQ index) rotate across steps, so the 0.86 GB of selected rows per step never
+fits the 126 MB L2; queries drift per step as in run_e2e
+(experiments.cpp:212-216).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 runs under torchrun, one rank per GPU; every rank decodes its own
+layers (weak scaling, no collective on the data path); the timed region is
+bracketed by barrier + synchronize and the max over ranks is reported.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+S, H, DH, G = 131072, 32, 128, 1
+M, B, T_ITERS = 2, 6, 10
+N_INIT, N_LOCAL = 4, 64
+K_SEL = round(S / 5)  # 26214 (k = round(s * ratio))
+S_MID = S - N_INIT - N_LOCAL
+N_LAYERS = 4
+METRIC = "decode PQ-retrieve+attend us/layer @128K ctx"
+WORKLOAD = "northstar-1layer-32h-128d-128Kctx-m2b6-top1/5+4init+64local-bs1"
+
+
+def algorithmic_bytes_per_layer():
+    """B = h_kv [s_mid m b/8 + C d_h 4 + T_att d_h 4 2 + 2 g d_h 4]."""
+    t_att = N_INIT + K_SEL + N_LOCAL
+    return H * (S_MID * M * B / 8 + (1 << B) * DH * 4 + t_att * DH * 4 * 2 + 2 * G * DH * 4)
+
+
+def attend_bytes_per_launch():
+    """Bytes the attention kernel pair must move: K+V of the T_att selected rows,
+    the selection bitmap, queries in, outputs out."""
+    t_att = N_INIT + K_SEL + N_LOCAL
+    words = (S_MID + 31) // 32
+    return H * (t_att * DH * 4 * 2 + words * 4 + 2 * G * DH * 4)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_layer_inputs(torch, seed, device):
+    """Gaussian-mixture keys (workload.cpp:39-51 distribution: 8 shared means,
+    spread 0.5), N(0,1) values and base queries, generated on the GPU."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    keys = torch.empty((H, S, DH), dtype=torch.float32, device=device)
+    vals = torch.empty((H, S, DH), dtype=torch.float32, device=device)
+    for h in range(H):
+        means = torch.randn((8, DH), generator=g, device=device)
+        comp = torch.randint(0, 8, (S,), generator=g, device=device)
+        keys[h] = means[comp] + 0.5 * torch.randn((S, DH), generator=g, device=device)
+        vals[h] = torch.randn((S, DH), generator=g, device=device)
+    base_q = torch.randn((H, G, DH), generator=g, device=device)
+    return keys, vals, base_q
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU decode (oracle/_ref) on all host
+    cores, bounded sample of the same workload, extrapolated to us/layer."""
+    import numpy as np
+
+    import oracle
+
+    if rank != 0:
+        return
+    line = {"impl": "reference", "metric": METRIC, "unit": "us/layer", "higher_is_better": False,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "scaling": "weak",
+            "dtype": "f32 storage, f64 arithmetic", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "global_batch": 1, "seq_len": S}}
+    if not oracle.has_ref():
+        line["unavailable"] = "oracle/_ref/libpqkv_ref.so was not built (needs /root/reference at build time)"
+        print(json.dumps(line), flush=True)
+        return
+    ref = oracle.ref()
+    cores = os.cpu_count() or 1
+    P = min(H, max(1, cores))  # one head per host thread
+    rng = np.random.default_rng(17)
+    keys = np.empty((P, S, DH), np.float32)
+    vals = rng.standard_normal((P, S, DH), dtype=np.float32)
+    for p in range(P):
+        means = rng.standard_normal((8, DH)).astype(np.float32)
+        keys[p] = means[rng.integers(0, 8, S)] + 0.5 * rng.standard_normal((S, DH), dtype=np.float32)
+    queries = rng.standard_normal((P, G, DH)).astype(np.float32)
+    # the reference builds its own index (pq_construct, untimed setup)
+    mids = np.ascontiguousarray(keys[:, N_INIT:N_INIT + S_MID])
+    _, cen, codes = ref.bench_build(mids, M, B, T_ITERS, np.arange(P, dtype=np.uint64) + 11, 0)
+    times = []
+    for it in range(args.warmup + args.steps):
+        secs, _ = ref.bench_decode(keys, vals, queries, cen, codes, N_INIT, N_LOCAL, K_SEL, 0)
+        if it >= args.warmup:
+            times.append(secs)
+    per_layer_us = float(np.median(times)) * 1e6 * (H / P)
+    line.update({"value": per_layer_us, "ms_per_step": per_layer_us / 1e3,
+                 "cpu_baseline": {"value": per_layer_us, "unit": "us/layer", "cores": min(cores, P),
+                                  "kind": "reference",
+                                  "sample": f"{P} of {H} heads per step (x{H / P:g} to a layer), "
+                                            "pq_score_gqa+approx_topk+selective_attention"},
+                 "e2e": {"value": per_layer_us, "unit": "us/layer", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(layer0, cen, codes, torch):
+    """The reference (oracle/_ref) on this box's host cores for a bounded sample
+    (8 heads of layer 0, same GPU-built index -- bit-identical to the
+    reference's), extrapolated x4 to the 32-head layer; plus a 1-head 32K-token
+    pq_construct sample for the build."""
+    import numpy as np
+
+    import oracle
+
+    if not oracle.has_ref():
+        return None, None
+    ref = oracle.ref()
+    P = 8
+    keys, vals, base_q = layer0
+    k = keys[:P].cpu().numpy()
+    v = vals[:P].cpu().numpy()
+    q = base_q[:P].cpu().numpy()
+    c = cen[:P].cpu().numpy()
+    cd = codes[:P].cpu().numpy().view(np.uint16)
+    cores = min(os.cpu_count() or 1, P)
+    ts = [ref.bench_decode(k, v, q, c, cd, N_INIT, N_LOCAL, K_SEL, cores)[0] for _ in range(3)]
+    dec = {"value": float(np.median(ts)) * 1e6 * (H / P), "unit": "us/layer", "cores": cores,
+           "kind": "reference", "sample": f"{P} of {H} heads of one 128K layer, x{H // P} to a layer, median of 3"}
+    sb = 32768
+    secs, _, _ = ref.bench_build(np.ascontiguousarray(k[:1, N_INIT:N_INIT + sb]), M, B, T_ITERS,
+                                 np.array([5], np.uint64), 1)
+    bld = {"value": sb / secs, "unit": "key vectors/s", "cores": 1, "kind": "reference",
+           "sample": f"pq_construct m2b6 T={T_ITERS} on 1 head x {sb} tokens"}
+    return dec, bld
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+
+    import paper_2407_12820_b200 as pq
+
+    assert args.warmup >= 3, "timing rules: >= 3 warm-up steps"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = pq.Context(local)
+
+    # ---- per-rank layers: inputs + GPU PQ build (timed separately) ----
+    layers, build_s = [], []
+    keep0 = None
+    for li in range(N_LAYERS):
+        keys, vals, base_q = make_layer_inputs(torch, 1000 * rank + li, dev)
+        mids = keys[:, N_INIT:N_INIT + S_MID]  # middle rows, strided view of the cache
+        mids = mids.contiguous()
+        seeds = [7 + 100 * rank + 10 * li + h for h in range(H)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cen, codes = ctx.pq_build(mids, M, B, T_ITERS, seeds)
+        torch.cuda.synchronize()
+        build_s.append(time.perf_counter() - t0)
+        rech, tot = ctx.last_build_stats()
+        del mids
+        layer = pq.DecodeLayer(keys=keys, values=vals, centroids=cen, codes=codes, total=S,
+                               n_init=N_INIT, n_local=N_LOCAL, b=B)
+        layers.append((layer, base_q))
+        if li == 0:
+            keep0 = ((keys, vals, base_q), cen, codes)
+    # per-step query drift (experiments.cpp:212-216)
+    gq = torch.Generator(device=dev)
+    gq.manual_seed(99 + rank)
+    n_total = args.warmup + args.steps
+    sigma = 0.25 / math.sqrt(DH)
+    queries = [layers[i % N_LAYERS][1] + sigma * torch.randn((H, G, DH), generator=gq, device=dev)
+               for i in range(n_total)]
+    out = torch.empty((H, G, DH), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        layer = layers[i % N_LAYERS][0]
+        return ctx.decode(layer, queries[i], K_SEL)
+
+    # ---- device-resident timing ----
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.warmup, n_total):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    layers_done = args.steps * world
+    us_per_layer = ms * 1e3 / layers_done
+
+    # ---- dominant kernel (attention gather + combine) timed alone ----
+    bms = []
+    for i in range(N_LAYERS):
+        bm, _ = ctx.pq_search(queries[i], layers[i][0].centroids, layers[i][0].codes, B, K_SEL, s=S_MID,
+                              bitmap=True, ordered=False)
+        bms.append(bm)
+    sel_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
+    reps = max(args.steps, 8)
+    for i in range(3):
+        ctx.decode_attend(layers[i % N_LAYERS][0], queries[i], bms[i % N_LAYERS], out)
+    torch.cuda.synchronize()
+    sel_ev[0][0].record(stream)
+    for i in range(reps):
+        ctx.decode_attend(layers[i % N_LAYERS][0], queries[i % N_LAYERS], bms[i % N_LAYERS], out)
+    sel_ev[0][1].record(stream)
+    sel_ev[1][0].record(stream)
+    for i in range(reps):
+        ctx.pq_search(queries[i % N_LAYERS], layers[i % N_LAYERS][0].centroids, layers[i % N_LAYERS][0].codes,
+                      B, K_SEL, s=S_MID, bitmap=True, ordered=False)
+    sel_ev[1][1].record(stream)
+    torch.cuda.synchronize()
+    attend_ms = sel_ev[0][0].elapsed_time(sel_ev[0][1]) / reps
+    select_ms = sel_ev[1][0].elapsed_time(sel_ev[1][1]) / reps
+
+    # ---- end to end through the C ABI with HOST buffers ----
+    hq = [q.cpu().pin_memory() for q in queries[:N_LAYERS]]
+    ho = torch.empty((H, G, DH), dtype=torch.float32).pin_memory()
+    for i in range(3):
+        ctx.decode_host(layers[i % N_LAYERS][0], hq[i % N_LAYERS], ho, K_SEL)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        ctx.decode_host(layers[i % N_LAYERS][0], hq[i % N_LAYERS], ho, K_SEL)
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_us = e2e_s * 1e6 / (args.steps * world)
+
+    # ---- numbers ----
+    peak, peak_kind = peaks()
+    attend_bytes = attend_bytes_per_launch()
+    achieved = attend_bytes / (attend_ms * 1e-3) / 1e9
+    layer_gbs = algorithmic_bytes_per_layer() / (ms_per_step * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("attend_kernel")
+        except Exception:
+            traffic = None
+    build_layer_s = float(np.median(build_s))
+    launches_per_step = layers[0][0].launches(G)
+    line = {
+        "metric": METRIC, "value": us_per_layer, "unit": "us/layer", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (K/V, attention), f64 (ADC table), u16 codes", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": 1, "seq_len": S, "heads": H, "head_dim": DH,
+                   "m": M, "b": B, "k": K_SEL, "n_init": N_INIT, "n_local": N_LOCAL,
+                   "layers_rotated": N_LAYERS, "parallelism": f"dp{world} (independent layers per GPU)",
+                   "l2": "inputs larger than L2: 4 rotating layers x 4.3 GB K/V, 0.86 GB gathered per step"},
+        "hbm_gbs_layer": layer_gbs,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "attend_kernel+combine_kernel", "kernel_ms": attend_ms,
+                     "algorithmic_bytes": attend_bytes, "select_kernel_ms": select_ms},
+        "layer_roofline_frac": layer_gbs / peak,
+        "e2e": {"value": e2e_us, "unit": "us/layer", "h2d_bytes_per_step": H * G * DH * 4,
+                "d2h_bytes_per_step": H * G * DH * 4},
+        "gpu_launches": launches_per_step * args.steps,
+        "build": {"layer_s": build_layer_s, "key_vectors_per_s": H * S_MID / build_layer_s,
+                  "context_tokens_per_s": S_MID / build_layer_s, "layers": N_LAYERS,
+                  "fp64_rechecked_points": rech, "points": tot},
+    }
+    with_clk = clk.summary()
+    line["clocks"] = with_clk
+    if rank == 0 and not args.no_cpu_baseline:
+        dec, bld = cpu_baseline_leg(keep0[0], keep0[1], keep0[2], torch)
+        line["cpu_baseline"] = dec
+        line["cpu_baseline_build"] = bld
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

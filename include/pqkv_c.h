@@ -198,6 +198,13 @@ typedef struct {
 PQKV_API int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* layer, const float* d_queries, size_t g,
                 size_t k, float* d_out, int64_t* d_ids, void* stream);
 
+/* The attention half of pqkv_decode for a given selection bitmap
+ * d_bitmap [n_heads][ceil(s_mid/32)] (bit r = middle row r, as written by
+ * pqkv_pq_search): gather of init + selected + local rows, split-K fp32
+ * online softmax and the partial combine. */
+PQKV_API int pqkv_decode_attend(pqkv_ctx* ctx, const pqkv_layer* layer, const float* d_queries,
+                                size_t g, const uint32_t* d_bitmap, float* d_out, void* stream);
+
 /* pqkv_decode with HOST query/output buffers: copies h_queries in, runs the
  * fused layer, copies d_out back and synchronizes `stream`. */
 PQKV_API int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* layer, const float* h_queries,

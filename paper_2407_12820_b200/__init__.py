@@ -59,6 +59,7 @@ _SIGS = {
     "pqkv_exact_scores": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp, _sz, _vp, _vp]),
     "pqkv_attend_rows": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp, _sz, _i, _vp, _vp]),
     "pqkv_decode": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp, _vp]),
+    "pqkv_decode_attend": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _vp, _vp, _vp]),
     "pqkv_decode_host": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp]),
     "pqkv_decode_launches": (_i, [C.POINTER(pqkv_layer), _sz, _i]),
 }
@@ -252,6 +253,18 @@ class Context:
         L = layer.struct()
         _check(lib().pqkv_decode(self.h, C.byref(L), _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
         return (out, ids[:, :k]) if want_ids else out
+
+    def decode_attend(self, layer: "DecodeLayer", queries, bitmap, out=None):
+        """Attention half of decode for a selection bitmap from pq_search."""
+        import torch
+
+        P, g, d_h = queries.shape
+        if out is None:
+            out = torch.empty((P, g, d_h), dtype=torch.float32, device=queries.device)
+        L = layer.struct()
+        _check(lib().pqkv_decode_attend(self.h, C.byref(L), _ptr(queries), g, _ptr(bitmap), _ptr(out),
+                                        _stream()))
+        return out
 
     def decode_host(self, layer: "DecodeLayer", h_queries, h_out, k: int):
         """h_queries / h_out: pinned CPU tensors [P][g][d_h]; synchronous."""

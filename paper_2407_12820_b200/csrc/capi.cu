@@ -249,6 +249,17 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
     });
 }
 
+int pqkv_decode_attend(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size_t g,
+                       const uint32_t* d_bitmap, float* d_out, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_layer(L, g, 0);
+        if (L->n_heads == 0) return;
+        if (!launch_decode_attend(ctx, *L, d_queries, g, d_bitmap, d_out, as_stream(stream), nullptr))
+            fail(PQKV_EINVAL, "decode_attend: needs d_h == 128 and g in {1, 2, 4}");
+    });
+}
+
 int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries, size_t g, size_t k,
                      float* h_out, void* stream) {
     return guard([&] {
