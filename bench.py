@@ -21,7 +21,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -64,52 +63,57 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled through NVML every 100 ms while the
+    timed region runs (the recipe's nvidia-smi clocks line, without pipes)."""
 
     def __init__(self, device):
         self.device = device
         self.rows = []
-        self.proc = None
+        self.stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: report unsampled
+            self.nv = None
+            self.err = str(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                try:
+                    reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.rows.append((mhz, reasons))
+            except Exception:
+                pass
+            self.stop.wait(0.1)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.nv:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
+        if not self.nv or not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        bits = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({name for _, rs in self.rows for bit, name in bits.items() if rs & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows)}
 
 
 def make_layer_inputs(torch, seed, device):
@@ -246,12 +250,13 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         cen, codes = ctx.pq_build(mids, M, B, T_ITERS, seeds)
+        tables = ctx.tuple_tables(codes, B)  # code-pair histograms (part of the build)
         torch.cuda.synchronize()
         build_s.append(time.perf_counter() - t0)
         rech, tot = ctx.last_build_stats()
         del mids
         layer = pq.DecodeLayer(keys=keys, values=vals, centroids=cen, codes=codes, total=S,
-                               n_init=N_INIT, n_local=N_LOCAL, b=B)
+                               n_init=N_INIT, n_local=N_LOCAL, b=B, tables=tables)
         layers.append((layer, base_q))
         if li == 0:
             keep0 = ((keys, vals, base_q), cen, codes)
@@ -299,7 +304,7 @@ def main():
     bms = []
     for i in range(N_LAYERS):
         bm, _ = ctx.pq_search(queries[i], layers[i][0].centroids, layers[i][0].codes, B, K_SEL, s=S_MID,
-                              bitmap=True, ordered=False)
+                              bitmap=True, ordered=False, tables=layers[i][0].tables)
         bms.append(bm)
     sel_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
     reps = max(args.steps, 8)
@@ -313,7 +318,7 @@ def main():
     sel_ev[1][0].record(stream)
     for i in range(reps):
         ctx.pq_search(queries[i % N_LAYERS], layers[i % N_LAYERS][0].centroids, layers[i % N_LAYERS][0].codes,
-                      B, K_SEL, s=S_MID, bitmap=True, ordered=False)
+                      B, K_SEL, s=S_MID, bitmap=True, ordered=False, tables=layers[i % N_LAYERS][0].tables)
     sel_ev[1][1].record(stream)
     torch.cuda.synchronize()
     attend_ms = sel_ev[0][0].elapsed_time(sel_ev[0][1]) / reps
@@ -363,8 +368,8 @@ def main():
         "hbm_gbs_layer": layer_gbs,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "attend_kernel+combine_kernel", "kernel_ms": attend_ms,
-                     "algorithmic_bytes": attend_bytes, "select_kernel_ms": select_ms},
+                     "kernel": "attend_kernel (gather + split-K softmax + fused combine)", "kernel_ms": attend_ms,
+                     "algorithmic_bytes": attend_bytes, "select_ms": select_ms},
         "layer_roofline_frac": layer_gbs / peak,
         "e2e": {"value": e2e_us, "unit": "us/layer", "h2d_bytes_per_step": H * G * DH * 4,
                 "d2h_bytes_per_step": H * G * DH * 4},

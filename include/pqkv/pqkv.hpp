@@ -54,7 +54,7 @@ struct PQKV_CXX_API TensorF32 {
 };
 
 /// mt19937_64 with explicit draw math (bit-identical streams to the reference).
-class Rng {
+class PQKV_CXX_API Rng {
 public:
     explicit Rng(std::uint64_t seed) : engine_(seed) {}
     std::uint64_t next_u64() { return engine_(); }

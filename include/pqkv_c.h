@@ -61,6 +61,10 @@ typedef enum {
 
 typedef enum { PQKV_PREC_F32 = 0, PQKV_PREC_F64 = 1 } pqkv_precision;
 
+/* Middle rows per chunk of the code-pair chunk histogram (see
+ * pqkv_pq_tuple_tables). */
+#define PQKV_TUPLE_CHUNK 4096
+
 /* k-means assign-step arithmetic.  Both produce bit-identical assignments:
  * EXACT evaluates every distance in the reference's fp64 order;
  * FILTERED evaluates fp32 distances with a rigorous error bound and
@@ -131,6 +135,18 @@ PQKV_API int pqkv_assign_nearest(pqkv_ctx* ctx, const float* d_points, size_t n,
 
 /* ---- (B) decode retrieval ---------------------------------------------- */
 
+/* Code-pair tables for the m == 2 fast selection path (b <= 7): for every
+ * head, d_tuple_hist [p][C*C] u32 counts middle rows per code pair
+ * (c0*C + c1) and d_tuple_chunk_hist [p][ceil(cap/PQKV_TUPLE_CHUNK)][C*C] u16
+ * counts them per PQKV_TUPLE_CHUNK-row chunk.  ADDS the rows
+ * [row_begin, row_end) of every head (zero the tables before the first call;
+ * after an append call it again with the appended rows).  n_chunks is the
+ * chunk dimension of d_tuple_chunk_hist. */
+PQKV_API int pqkv_pq_tuple_tables(pqkv_ctx* ctx, size_t n_heads, size_t b, const uint16_t* d_codes,
+                                  size_t codes_head_stride, size_t row_begin, size_t row_end,
+                                  uint32_t* d_tuple_hist, uint16_t* d_tuple_chunk_hist,
+                                  size_t n_chunks, void* stream);
+
 /* pq_score_gqa (pq.cpp:113-161) for n_heads heads: d_queries [p][g][d_h],
  * codes as in pqkv_pq_build, d_scores + p*scores_head_stride + i. */
 PQKV_API int pqkv_pq_score(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
@@ -151,11 +167,14 @@ PQKV_API int pqkv_topk(pqkv_ctx* ctx, const float* d_scores, size_t n_rows, size
  * fp64 ADC table in shared memory, scans the codes and radix-selects the k
  * best middle rows of each head with the reference's tie rule.  Writes the
  * selection bitmap d_bitmap [p][ceil(s/32)] u32 (bit r of the middle row r;
- * nullable) and/or the ordered ids d_ids [p][k] (nullable). */
+ * nullable) and/or the ordered ids d_ids [p][k] (nullable).  With m == 2,
+ * b <= 7 and the code-pair tables of pqkv_pq_tuple_tables (nullable) the
+ * selection runs over code pairs instead of tokens. */
 PQKV_API int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
                    size_t m, size_t b, const float* d_centroids, const uint16_t* d_codes,
                    size_t codes_head_stride, size_t s, size_t k, uint32_t* d_bitmap,
-                   int64_t* d_ids, void* stream);
+                   int64_t* d_ids, const uint32_t* d_tuple_hist,
+                   const uint16_t* d_tuple_chunk_hist, void* stream);
 
 /* Softmax attention over explicit row lists (softmax_attention,
  * gqa_group_attention, selective_attention: attention.cpp:35-104).  For head
@@ -188,6 +207,9 @@ typedef struct {
     const float* centroids;   /* [n_heads][m][2^b][d_m] f32 */
     const uint16_t* codes;    /* head p, middle row r at codes + p*codes_head_stride + r*m */
     size_t codes_head_stride;
+    /* optional code-pair tables (pqkv_pq_tuple_tables) for m == 2, b <= 7 */
+    const uint32_t* tuple_hist;
+    const uint16_t* tuple_chunk_hist;
 } pqkv_layer;
 
 /* Fused decode retrieval + sparse attention for one layer (the hot path):

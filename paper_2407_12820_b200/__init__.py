@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libpqkv.so")
 PQKV_OK, PQKV_EINVAL, PQKV_ERANGE, PQKV_ESTATE, PQKV_ERUNTIME, PQKV_ECUDA = range(6)
 PREC_F32, PREC_F64 = 0, 1
 ASSIGN_FILTERED, ASSIGN_EXACT = 0, 1
+TUPLE_CHUNK = 4096  # PQKV_TUPLE_CHUNK
 
 _sz, _vp, _i, _u64 = C.c_size_t, C.c_void_p, C.c_int, C.c_uint64
 
@@ -33,6 +34,7 @@ class pqkv_layer(C.Structure):
         ("keys", _vp), ("values", _vp), ("kv_head_stride", _sz), ("n_heads", _sz),
         ("total", _sz), ("n_init", _sz), ("n_local", _sz), ("d_h", _sz), ("m", _sz),
         ("b", _sz), ("centroids", _vp), ("codes", _vp), ("codes_head_stride", _sz),
+        ("tuple_hist", _vp), ("tuple_chunk_hist", _vp),
     ]
 
 
@@ -55,7 +57,8 @@ _SIGS = {
     "pqkv_assign_nearest": (_i, [_vp, _vp, _sz, _sz, _vp, _sz, _vp, _vp]),
     "pqkv_pq_score": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
     "pqkv_topk": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _vp, _vp]),
-    "pqkv_pq_search": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _vp, _vp]),
+    "pqkv_pq_tuple_tables": (_i, [_vp, _sz, _sz, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp]),
+    "pqkv_pq_search": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
     "pqkv_exact_scores": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp, _sz, _vp, _vp]),
     "pqkv_attend_rows": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp, _sz, _i, _vp, _vp]),
     "pqkv_decode": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp, _vp]),
@@ -207,8 +210,25 @@ class Context:
         _check(lib().pqkv_topk(self.h, _ptr(scores), R, n, n, k, _ptr(excluded), _ptr(ids), _stream()))
         return ids[:, :k]
 
+    def tuple_tables(self, codes, b: int, s: int | None = None, tables=None, row_begin: int = 0):
+        """Code-pair tables for the m == 2 selection path: (thist [P][C*C] i32,
+        chist [P][chunks][C*C] i16).  Adds rows [row_begin, s) to `tables`."""
+        import torch
+
+        P, cap, m = codes.shape
+        s = cap if s is None else s
+        C2 = (1 << b) ** 2
+        chunks = max(1, (cap + TUPLE_CHUNK - 1) // TUPLE_CHUNK)
+        if tables is None:
+            tables = (torch.zeros((P, C2), dtype=torch.int32, device=codes.device),
+                      torch.zeros((P, chunks, C2), dtype=torch.int16, device=codes.device))
+        th, ch = tables
+        _check(lib().pqkv_pq_tuple_tables(self.h, P, b, _ptr(codes), cap * m, row_begin, s, _ptr(th), _ptr(ch),
+                                          ch.shape[1], _stream()))
+        return tables
+
     def pq_search(self, queries, centroids, codes, b: int, k: int, s: int | None = None,
-                  bitmap: bool = True, ordered: bool = True):
+                  bitmap: bool = True, ordered: bool = True, tables=None):
         """Fused ADC + select -> (bitmap [P][ceil(s/32)] i32 | None, ids [P][k] | None)."""
         import torch
 
@@ -219,8 +239,9 @@ class Context:
         words = (s + 31) // 32
         bm = torch.empty((P, max(words, 1)), dtype=torch.int32, device=queries.device) if bitmap else None
         ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device) if ordered else None
+        th, ch = tables if tables is not None else (None, None)
         _check(lib().pqkv_pq_search(self.h, _ptr(queries), P, g, d_h, m, b, _ptr(centroids), _ptr(codes),
-                                    cap * m, s, k, _ptr(bm), _ptr(ids), _stream()))
+                                    cap * m, s, k, _ptr(bm), _ptr(ids), _ptr(th), _ptr(ch), _stream()))
         return bm, (ids[:, :k] if ids is not None else None)
 
     def exact_scores(self, queries, keys, rows):
@@ -290,6 +311,7 @@ class DecodeLayer:
     n_init: int
     n_local: int
     b: int
+    tables: tuple | None = None  # (thist, chist) from Context.tuple_tables
 
     def struct(self) -> pqkv_layer:
         P, S, d_h = self.keys.shape
@@ -299,6 +321,8 @@ class DecodeLayer:
             n_heads=P, total=self.total, n_init=self.n_init, n_local=self.n_local, d_h=d_h, m=m,
             b=self.b, centroids=self.centroids.data_ptr(), codes=self.codes.data_ptr(),
             codes_head_stride=self.codes.shape[1] * m,
+            tuple_hist=self.tables[0].data_ptr() if self.tables is not None else None,
+            tuple_chunk_hist=self.tables[1].data_ptr() if self.tables is not None else None,
         )
 
     def launches(self, g: int, with_ids: bool = False) -> int:

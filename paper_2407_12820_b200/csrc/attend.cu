@@ -31,7 +31,6 @@ constexpr int AT_THREADS = 256;
 constexpr int AT_WARPS = AT_THREADS / 32;
 constexpr int CHUNK = 4096;  // middle rows per CTA (bitmap mode) / list positions (rows mode)
 constexpr int DH = 128;
-constexpr float LOG2E = 1.4426950408889634f;
 
 struct AtArgs {
     const float* queries;  // [P][G][128]
@@ -47,6 +46,8 @@ struct AtArgs {
     int n_chunks;          // chunks per head including the init/local chunk (bitmap mode)
     float scale_log2;      // log2(e) / sqrt(d_h)
     float* part;           // [P][n_chunks][G][DH + 2]
+    unsigned* arrivals;    // [P] zero on entry; reset by the combining CTA
+    float* out;            // [P][G][DH]
 };
 
 __device__ __forceinline__ float safe_scale(float m_old, float m_new) {
@@ -250,22 +251,42 @@ __global__ void __launch_bounds__(AT_THREADS) attend_kernel(AtArgs a) {
         out[2 + d] = O;
         if (d == 0) { out[0] = M; out[1] = L; }
     }
-}
 
-__global__ void combine_kernel(const float* part, int n_chunks, int G, float* out) {
-    const int pr = blockIdx.x;  // p*G + r
-    const int p = pr / G, r = pr % G;
-    const int d = threadIdx.x;
-    float M = -INFINITY;
-    for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, part[(((long long)p * n_chunks + c) * G + r) * (DH + 2)]);
-    float L = 0.f, O = 0.f;
-    for (int c = 0; c < n_chunks; ++c) {
-        const float* pc = part + (((long long)p * n_chunks + c) * G + r) * (DH + 2);
-        float sc = safe_scale(pc[0], M);
-        L += pc[1] * sc;
-        O += pc[2 + d] * sc;
+    // ---- 6. the last CTA of this head merges all partials (no extra launch) ----
+    __shared__ unsigned ticket;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) ticket = atomicAdd(&a.arrivals[p], 1u);
+    __syncthreads();
+    if (ticket != (unsigned)a.n_chunks - 1) return;
+    __threadfence();
+    float* sc = reinterpret_cast<float*>(rows_s);  // [G][n_chunks] scale, then [G] sums
+    const int nc = a.n_chunks;
+    const float* pb = a.part + (long long)p * nc * G * (DH + 2);
+    for (int r = warp; r < G; r += AT_WARPS) {
+        float M = -INFINITY;
+        for (int cc = lane; cc < nc; cc += 32) M = fmaxf(M, __ldcg(pb + ((long long)cc * G + r) * (DH + 2)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(FULL, M, o));
+        float L = 0.f;
+        for (int cc = lane; cc < nc; cc += 32) {
+            const float* pc = pb + ((long long)cc * G + r) * (DH + 2);
+            float f = safe_scale(__ldcg(pc), M);
+            sc[r * nc + cc] = f;
+            L += __ldcg(pc + 1) * f;
+        }
+        L = warp_sum(L);
+        if (lane == 0) sc[G * nc + r] = L;
     }
-    out[(long long)pr * DH + d] = O / L;
+    __syncthreads();
+    for (int e = tid; e < G * DH; e += AT_THREADS) {
+        const int r = e / DH, d = e % DH;
+        float O = 0.f;
+#pragma unroll 4
+        for (int cc = 0; cc < nc; ++cc) O = fmaf(__ldcg(pb + ((long long)cc * G + r) * (DH + 2) + 2 + d), sc[r * nc + cc], O);
+        a.out[((long long)p * G + r) * DH + d] = O / sc[G * nc + r];
+    }
+    if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
 }
 
 // ---- exact (fp64) path ------------------------------------------------------
@@ -434,9 +455,9 @@ void launch_attend_rows(pqkv_ctx* ctx, const float* queries, size_t P, size_t G,
     a.n_chunks = chunks;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d_h));
     a.part = sc.get<float>(h_part);
+    a.arrivals = arrival_counters(ctx, P, st);
+    a.out = out;
     launch_fast_any((int)G, a, dim3((unsigned)chunks, (unsigned)P), st);
-    combine_kernel<<<(unsigned)(P * G), DH, 0, st>>>(a.part, chunks, (int)G, out);
-    PQKV_LAUNCHED("combine_kernel");
 }
 
 bool launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
@@ -465,10 +486,10 @@ bool launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
         a.n_chunks = chunks;
         a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
         a.part = sc.get<float>(h_part);
+        a.arrivals = arrival_counters(ctx, L.n_heads, st);
+        a.out = out;
         launch_fast_any((int)G, a, dim3((unsigned)chunks, (unsigned)L.n_heads), st);
-        combine_kernel<<<(unsigned)(L.n_heads * G), DH, 0, st>>>(a.part, chunks, (int)G, out);
-        PQKV_LAUNCHED("combine_kernel");
-        if (launches) *launches = 2;
+        if (launches) *launches = 1;
         return true;
     }
     return false;  // caller materialises row lists and runs the exact kernels

@@ -146,10 +146,27 @@ int pqkv_topk(pqkv_ctx* ctx, const float* d_scores, size_t n_rows, size_t n, siz
     });
 }
 
+static bool tuple_ok(size_t m, size_t b, const void* th, const void* ch) {
+    return m == 2 && b <= 7 && th && ch;
+}
+
+int pqkv_pq_tuple_tables(pqkv_ctx* ctx, size_t n_heads, size_t b, const uint16_t* d_codes,
+                         size_t codes_head_stride, size_t row_begin, size_t row_end, uint32_t* d_tuple_hist,
+                         uint16_t* d_tuple_chunk_hist, size_t n_chunks, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (b < 1 || b > 7) fail(PQKV_EINVAL, "tuple tables: need b in [1, 7] (m == 2)");
+        if (!d_codes || !d_tuple_hist || !d_tuple_chunk_hist) fail(PQKV_EINVAL, "tuple tables: NULL buffer");
+        launch_tuple_tables(ctx, d_codes, n_heads, codes_head_stride, size_t{1} << b, row_begin, row_end,
+                            d_tuple_hist, d_tuple_chunk_hist, n_chunks, as_stream(stream));
+    });
+}
+
 int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
                    size_t m, size_t b, const float* d_centroids, const uint16_t* d_codes,
                    size_t codes_head_stride, size_t s, size_t k, uint32_t* d_bitmap,
-                   int64_t* d_ids, void* stream) {
+                   int64_t* d_ids, const uint32_t* d_tuple_hist, const uint16_t* d_tuple_chunk_hist,
+                   void* stream) {
     return guard([&] {
         need_ctx(ctx);
         check_pq(m, b, d_h);
@@ -164,7 +181,11 @@ int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t
         src.centroids = d_centroids;
         src.codes = d_codes;
         src.codes_head_stride = codes_head_stride;
-        launch_select(ctx, src, n_heads, s, k, d_bitmap, k ? d_ids : nullptr, as_stream(stream), nullptr);
+        if (tuple_ok(m, b, d_tuple_hist, d_tuple_chunk_hist))
+            launch_select_tuple(ctx, src, d_tuple_hist, d_tuple_chunk_hist, n_heads, s, k, d_bitmap,
+                                k ? d_ids : nullptr, as_stream(stream), nullptr);
+        else
+            launch_select(ctx, src, n_heads, s, k, d_bitmap, k ? d_ids : nullptr, as_stream(stream), nullptr);
     });
 }
 
@@ -236,7 +257,11 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         src.centroids = L->centroids;
         src.codes = L->codes;
         src.codes_head_stride = L->codes_head_stride;
-        launch_select(ctx, src, L->n_heads, s_mid, k, bm, d_ids, st, nullptr);
+        if (tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist))
+            launch_select_tuple(ctx, src, L->tuple_hist, L->tuple_chunk_hist, L->n_heads, s_mid, k, bm, d_ids, st,
+                                nullptr);
+        else
+            launch_select(ctx, src, L->n_heads, s_mid, k, bm, d_ids, st, nullptr);
         if (launch_decode_attend(ctx, *L, d_queries, g, bm, d_out, st, nullptr)) return;
         // generic geometry: ascending row lists, then the fp64 kernels
         const size_t T = L->n_init + k + L->n_local;
@@ -287,8 +312,10 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
 int pqkv_decode_launches(const pqkv_layer* L, size_t g, int with_ids) {
     if (!L) return 0;
     bool fast = L->d_h == 128 && (g == 1 || g == 2 || g == 4) && L->kv_head_stride % 4 == 0;
-    int n = 1 /*select*/ + (with_ids ? 1 : 0) /*sort*/;
-    n += fast ? 2 /*attend + combine*/ : 3 /*rows + scores + softmax*/;
+    int n = (L->m == 2 && L->b <= 7 && L->tuple_hist && L->tuple_chunk_hist) ? 2 /*pair select+bitmap*/
+                                                                             : 1 /*cluster select*/;
+    n += with_ids ? 1 : 0 /*sort*/;
+    n += fast ? 1 /*attend with fused combine*/ : 3 /*rows + scores + softmax*/;
     return n;
 }
 

@@ -1,5 +1,6 @@
 // ctx.cu -- context, scratch arena, status plumbing and the geometry entry
 // points of the C ABI (include/pqkv_c.h).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -48,6 +49,20 @@ void* pinned_staging(pqkv_ctx* ctx, size_t bytes) {
     return ctx->pinned;
 }
 
+unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st) {
+    if (n > ctx->n_arrivals) {
+        if (ctx->d_arrivals) {
+            PQKV_CUDA(cudaDeviceSynchronize());
+            PQKV_CUDA(cudaFree(ctx->d_arrivals));
+        }
+        size_t want = std::max<size_t>(n, 1024);
+        PQKV_CUDA(cudaMalloc(&ctx->d_arrivals, want * sizeof(unsigned)));
+        PQKV_CUDA(cudaMemsetAsync(ctx->d_arrivals, 0, want * sizeof(unsigned), st));
+        ctx->n_arrivals = want;
+    }
+    return ctx->d_arrivals;
+}
+
 }  // namespace pqkv_dev
 
 using namespace pqkv_dev;
@@ -81,6 +96,7 @@ int pqkv_ctx_destroy(pqkv_ctx* ctx) {
         if (ctx->arena) cudaFree(ctx->arena);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
         if (ctx->d_stats) cudaFree(ctx->d_stats);
+        if (ctx->d_arrivals) cudaFree(ctx->d_arrivals);
         delete ctx;
     });
 }

@@ -19,6 +19,10 @@ struct pqkv_ctx {
     // Pinned + device staging for the host-buffer entry points.
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
+    // Per-head arrival counters of the fused attention combine (kept zero
+    // between launches by the kernel itself).
+    unsigned* d_arrivals = nullptr;
+    size_t n_arrivals = 0;
     // Device counters written by the build kernels (rechecked, total).
     unsigned long long* d_stats = nullptr;
     uint64_t last_rechecked = 0, last_total = 0;
@@ -71,6 +75,7 @@ int guard(F&& f) {
     }
 }
 void* pinned_staging(pqkv_ctx* ctx, size_t bytes);
+unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st);
 
 // ---- launchers implemented in the kernel translation units -----------------
 
@@ -119,6 +124,14 @@ struct SelectSource {
 // (only possible with an exclusion mask).
 bool launch_select(pqkv_ctx* ctx, const SelectSource& src, size_t n_rows, size_t n, size_t k,
                    uint32_t* bitmap, int64_t* ids, cudaStream_t stream, int* launches);
+
+// Tuple path (m == 2): per-head pair histograms + pair-level radix select.
+void launch_tuple_tables(pqkv_ctx* ctx, const uint16_t* codes, size_t P, size_t codes_head_stride,
+                         size_t C, size_t row_begin, size_t row_end, uint32_t* thist, uint16_t* chist,
+                         size_t n_chunks, cudaStream_t st);
+void launch_select_tuple(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
+                         const uint16_t* chist, size_t rows, size_t n, size_t k, uint32_t* bitmap,
+                         int64_t* ids, cudaStream_t st, int* launches);
 
 void launch_attend_rows(pqkv_ctx* ctx, const float* queries, size_t n_heads, size_t g,
                         size_t d_h, const float* keys, const float* values,

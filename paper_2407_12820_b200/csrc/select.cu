@@ -104,8 +104,10 @@ __device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin) {
     if ((threadIdx.x & 31) == leader && bin != 0xffffffffu) atomicAdd(&hist[bin], __popc(peers));
 }
 
-// Block-wide exclusive scan (SEL_THREADS) of one u32 per thread.
+// Block-wide exclusive scan (NT threads) of one u32 per thread.
+template <int NT = SEL_THREADS>
 __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* wsum, uint32_t* total) {
+    constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -116,30 +118,31 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* wsum, uint32_t* total)
     if (lane == 31) wsum[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = lane < SEL_WARPS ? wsum[lane] : 0;
+        uint32_t w = lane < NW ? wsum[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t y = __shfl_up_sync(FULL, w, o);
             if (lane >= o) w += y;
         }
-        if (lane < SEL_WARPS) wsum[lane] = w;  // inclusive
+        if (lane < NW) wsum[lane] = w;  // inclusive
     }
     __syncthreads();
     uint32_t before = (warp ? wsum[warp - 1] : 0) + x - v;
-    if (total) *total = wsum[SEL_WARPS - 1];
+    if (total) *total = wsum[NW - 1];
     __syncthreads();
     return before;
 }
 
 // Finds the digit holding the k_rem-th largest element of hist[0..nb).
 // Returns (digit, count strictly above it) via out[0], out[1].
+template <int NT = SEL_THREADS>
 __device__ void find_digit(const uint32_t* hist, int nb, uint32_t k_rem, uint32_t* wsum,
                            uint32_t* out) {
-    const int per = nb / SEL_THREADS;  // 4 or 2
+    const int per = nb / NT;  // bins per thread (>= 1)
     const int hi = nb - per * (int)threadIdx.x;  // this thread owns [hi-per, hi), from the top
     uint32_t local = 0;
     for (int b = hi - 1; b >= hi - per; --b) local += hist[b];
-    uint32_t above = block_excl_scan(local, wsum, nullptr);
+    uint32_t above = block_excl_scan<NT>(local, wsum, nullptr);
     if (above < k_rem && k_rem <= above + local) {
         uint32_t acc = above;
         for (int b = hi - 1; b >= hi - per; --b) {
@@ -431,6 +434,236 @@ __global__ void gather_scores_kernel(const double* lut_g, int m, int C, const ui
     }
 }
 
+
+// ===========================================================================
+// Tuple path (m == 2, C^2 <= 16384): the ADC score of a token is a function
+// of its code pair only, f32((0.0 + T[0][c0]) + T[1][c1]) (pq.cpp:128-140),
+// so the radix select runs over the C^2 pair keys weighted by how many middle
+// tokens carry each pair.  Per head the index keeps
+//   thist[p][t]        tokens with pair t                (u32)
+//   chist[p][c][t]     same, per TCHUNK-row chunk c      (u16)
+// maintained by tuple_tables_kernel at build and on append.  tuple_select
+// (one CTA per head) finds the threshold key K*, classifies every pair
+// (above / equal / below) and -- from chist -- the chunk c* that holds the
+// lowest-id boundary of the equal keys and how many of c*'s equal tokens are
+// taken.  tuple_bitmap then streams the codes once per chunk.
+// ===========================================================================
+constexpr int TUP_THREADS = 1024;
+
+__global__ void tuple_tables_kernel(const uint16_t* codes, long long codes_head_stride, int C,
+                                    int row_begin, int row_end, uint32_t* thist, uint16_t* chist,
+                                    int n_chunks) {
+    extern __shared__ uint32_t cnt[];  // [C*C]
+    const int p = blockIdx.y, c = blockIdx.x, C2 = C * C;
+    const int r0 = max(row_begin, c * PQKV_TUPLE_CHUNK), r1 = min(row_end, (c + 1) * PQKV_TUPLE_CHUNK);
+    if (r0 >= r1) return;
+    for (int t = threadIdx.x; t < C2; t += blockDim.x) cnt[t] = 0;
+    __syncthreads();
+    const uint16_t* cd = codes + p * codes_head_stride;
+    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        uint32_t t = (uint32_t)cd[2LL * i] * C + cd[2LL * i + 1];
+        atomicAdd(&cnt[t], 1u);
+    }
+    __syncthreads();
+    uint16_t* ch = chist + ((long long)p * n_chunks + c) * C2;
+    uint32_t* th = thist + (long long)p * C2;
+    for (int t = threadIdx.x; t < C2; t += blockDim.x) {
+        uint32_t v = cnt[t];
+        if (v) {
+            ch[t] = (uint16_t)(ch[t] + v);
+            atomicAdd(&th[t], v);
+        }
+    }
+}
+
+struct TupArgs {
+    const float* queries;
+    int g, d_h, C;
+    const float* centroids;
+    const uint32_t* thist;
+    const uint16_t* chist;
+    int n, k, n_chunks;
+    uint8_t* cls;           // [P][C2]: 0 below, 1 above, 2 equal
+    uint32_t* tkey;         // [P][C2] pair keys (ids mode) or null
+    int* cut;               // [P][2]: c*, take
+    uint32_t* sel_before;   // [P][n_chunks] exclusive prefix of selected rows (ids mode) or null
+};
+
+__global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int p = blockIdx.x, tid = threadIdx.x, C = a.C, C2 = C * C;
+    double* lut = reinterpret_cast<double*>(smem);                 // [2C]
+    uint32_t* key = reinterpret_cast<uint32_t*>(lut + 2 * C);      // [C2]
+    uint32_t* w = key + C2;                                        // [C2]
+    uint32_t* hist = w + C2;                                       // [2048]
+    uint32_t* ceq = hist + NB;                                     // [n_chunks]
+    uint32_t* eql = ceq + a.n_chunks;                              // [C2] equal pairs
+    uint32_t* wsum = eql + C2;                                     // [32]
+    uint32_t* sh = wsum + 32;                                      // [8]
+
+    build_lut(lut, a.queries + (long long)p * a.g * a.d_h,
+              a.centroids + (long long)p * 2 * C * (a.d_h / 2), a.g, a.d_h, 2, C);
+    for (int c = tid; c < a.n_chunks; c += TUP_THREADS) ceq[c] = 0;
+    if (tid == 0) sh[2] = 0;
+    __syncthreads();
+    const uint32_t* th = a.thist + (long long)p * C2;
+    for (int t = tid; t < C2; t += TUP_THREADS) {
+        double acc = __dadd_rn(0.0, lut[t / C]);
+        acc = __dadd_rn(acc, lut[C + t % C]);
+        key[t] = score_key((float)acc);
+        w[t] = th[t];
+    }
+    uint32_t k_rem = (uint32_t)a.k, prefix = 0;
+    const int shifts[3] = {21, 10, 0};
+    const int nbins[3] = {2048, 2048, 1024};
+    for (int pass = 0; pass < 3; ++pass) {
+        for (int b = tid; b < NB; b += TUP_THREADS) hist[b] = 0;
+        __syncthreads();
+        const uint32_t mask = (uint32_t)(nbins[pass] - 1);
+        for (int t = tid; t < C2; t += TUP_THREADS) {
+            uint32_t kk = key[t], ww = w[t];
+            if (!ww) continue;
+            if (pass > 0 && (kk >> shifts[pass - 1]) != prefix) continue;
+            atomicAdd(&hist[(kk >> shifts[pass]) & mask], ww);
+        }
+        __syncthreads();
+        find_digit<TUP_THREADS>(hist, nbins[pass], k_rem, wsum, sh);
+        k_rem -= sh[1];
+        prefix = (prefix << (pass == 2 ? 10 : 11)) | sh[0];
+        __syncthreads();
+    }
+    const uint32_t kstar = prefix;
+    // classify pairs, collect the equal ones
+    uint8_t* cls = a.cls + (long long)p * C2;
+    for (int t = tid; t < C2; t += TUP_THREADS) {
+        uint32_t kk = key[t];
+        uint8_t c = kk > kstar ? 1 : (kk == kstar ? 2 : 0);
+        cls[t] = c;
+        if (c == 2 && w[t]) eql[atomicAdd(&sh[2], 1u)] = (uint32_t)t;
+        if (a.tkey) a.tkey[(long long)p * C2 + t] = kk;
+    }
+    __syncthreads();
+    const int neq = (int)sh[2];
+    const uint16_t* ch = a.chist + (long long)p * a.n_chunks * C2;
+    for (int e = tid; e < neq * a.n_chunks; e += TUP_THREADS) {
+        int c = e / neq, t = (int)eql[e % neq];
+        uint32_t v = ch[(long long)c * C2 + t];
+        if (v) atomicAdd(&ceq[c], v);
+    }
+    __syncthreads();
+    if (tid == 0) {  // chunk holding the k_rem-th equal token in id order
+        uint32_t run = 0;
+        int cstar = a.n_chunks - 1;
+        uint32_t take = 0;
+        for (int c = 0; c < a.n_chunks; ++c) {
+            if (run + ceq[c] >= k_rem) { cstar = c; take = k_rem - run; break; }
+            run += ceq[c];
+        }
+        a.cut[2 * p] = cstar;
+        a.cut[2 * p + 1] = (int)take;
+        sh[3] = (uint32_t)cstar;
+        sh[4] = take;
+    }
+    __syncthreads();
+    if (a.sel_before) {  // selected rows per chunk -> exclusive prefix (ordered ids)
+        const int cstar = (int)sh[3];
+        const uint32_t take = sh[4];
+        for (int c = tid >> 5; c < a.n_chunks; c += TUP_THREADS / 32) {
+            uint32_t gt = 0;
+            for (int t = tid & 31; t < C2; t += 32)
+                if (cls[t] == 1) gt += ch[(long long)c * C2 + t];
+            gt = warp_sum(gt);
+            if ((tid & 31) == 0) {
+                uint32_t eqc = c < cstar ? ceq[c] : (c == cstar ? take : 0);
+                hist[c] = gt + eqc;  // hist reused as per-chunk counts
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t run = 0;
+            for (int c = 0; c < a.n_chunks; ++c) {
+                a.sel_before[(long long)p * a.n_chunks + c] = run;
+                run += hist[c];
+            }
+        }
+    }
+}
+
+constexpr int TB_THREADS = 256;
+constexpr int TB_WARPS = TB_THREADS / 32;
+
+__global__ void __launch_bounds__(TB_THREADS) tuple_bitmap_kernel(
+    const uint16_t* codes, long long codes_head_stride, int n, int C, const uint8_t* cls_g,
+    const int* cut, uint32_t* bitmap, int words, const uint32_t* tkey_g,
+    const uint32_t* sel_before, uint32_t* sel_key, uint32_t* sel_id, int k, int n_chunks) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int c = blockIdx.x, p = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C2 = C * C;
+    uint8_t* cls = smem;
+    uint32_t* tkey = reinterpret_cast<uint32_t*>(smem + ((C2 + 15) / 16) * 16);
+    __shared__ uint32_t wc[TB_WARPS], ws[TB_WARPS];
+    const bool ids = sel_key != nullptr;
+    for (int t = tid; t < C2; t += TB_THREADS) {
+        cls[t] = cls_g[(long long)p * C2 + t];
+        if (ids) tkey[t] = tkey_g[(long long)p * C2 + t];
+    }
+    __syncthreads();
+    const int cstar = cut[2 * p];
+    const uint32_t take = (uint32_t)cut[2 * p + 1];
+    const int r0 = c * PQKV_TUPLE_CHUNK, r1 = min(n, r0 + PQKV_TUPLE_CHUNK);
+    const uint32_t* cd = reinterpret_cast<const uint32_t*>(codes + p * codes_head_stride);
+    uint32_t eq_run = 0, sel_run = ids ? sel_before[(long long)p * n_chunks + c] : 0;
+    for (int base = r0; base < r1; base += TB_THREADS) {
+        const int i = base + tid;
+        uint32_t t = 0;
+        uint8_t cl = 0;
+        if (i < r1) {
+            uint32_t pr = cd[i];  // (c0, c1) little-endian u16 pair
+            t = (pr & 0xffffu) * (uint32_t)C + (pr >> 16);
+            cl = cls[t];
+        }
+        bool gt = cl == 1, eq = cl == 2;
+        bool sel;
+        if (c < cstar) sel = gt || eq;
+        else if (c > cstar) sel = gt;
+        else {  // the boundary chunk: equal pairs in id order, first `take`
+            unsigned em = __ballot_sync(FULL, eq);
+            if (lane == 0) wc[warp] = __popc(em);
+            __syncthreads();
+            uint32_t before = 0, tile = 0;
+#pragma unroll
+            for (int w = 0; w < TB_WARPS; ++w) {
+                uint32_t v = wc[w];
+                before += w < warp ? v : 0;
+                tile += v;
+            }
+            __syncthreads();
+            sel = gt || (eq && eq_run + before + __popc(em & lanemask_lt()) < take);
+            eq_run += tile;
+        }
+        unsigned sm = __ballot_sync(FULL, sel);
+        if (lane == 0 && base + warp * 32 < r1) bitmap[(long long)p * words + (base >> 5) + warp] = sm;
+        if (ids) {
+            if (lane == 0) ws[warp] = __popc(sm);
+            __syncthreads();
+            uint32_t before = 0, tile = 0;
+#pragma unroll
+            for (int w = 0; w < TB_WARPS; ++w) {
+                uint32_t v = ws[w];
+                before += w < warp ? v : 0;
+                tile += v;
+            }
+            __syncthreads();
+            if (sel) {
+                uint32_t pos = sel_run + before + __popc(sm & lanemask_lt());
+                sel_key[(long long)p * k + pos] = tkey[t];
+                sel_id[(long long)p * k + pos] = (uint32_t)i;
+            }
+            sel_run += tile;
+        }
+    }
+}
+
 }  // namespace
 
 void launch_score(pqkv_ctx* ctx, const float* queries, size_t n_heads, size_t g, size_t d_h,
@@ -545,6 +778,82 @@ bool launch_select(pqkv_ctx* ctx, const SelectSource& src, size_t rows, size_t n
     }
     if (launches) *launches = nl;
     return ok;
+}
+
+
+void launch_tuple_tables(pqkv_ctx* ctx, const uint16_t* codes, size_t P, size_t codes_head_stride,
+                         size_t C, size_t row_begin, size_t row_end, uint32_t* thist, uint16_t* chist,
+                         size_t n_chunks, cudaStream_t st) {
+    bind_device(ctx);
+    if (row_end <= row_begin || P == 0) return;
+    const size_t c1 = ceil_div(row_end, PQKV_TUPLE_CHUNK);
+    if (c1 > n_chunks) fail(PQKV_EINVAL, "tuple tables: row range exceeds the chunk table");
+    size_t smem = C * C * 4;
+    PQKV_CUDA(cudaFuncSetAttribute(tuple_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // blockIdx.x indexes absolute chunks; chunks before c0 exit at once
+    tuple_tables_kernel<<<dim3((unsigned)c1, (unsigned)P), 512, smem, st>>>(
+        codes, (long long)codes_head_stride, (int)C, (int)row_begin, (int)row_end, thist, chist, (int)n_chunks);
+    PQKV_LAUNCHED("tuple_tables_kernel");
+}
+
+void launch_select_tuple(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
+                         const uint16_t* chist, size_t rows, size_t n, size_t k, uint32_t* bitmap,
+                         int64_t* ids, cudaStream_t st, int* launches) {
+    bind_device(ctx);
+    const size_t words = ceil_div(n, 32), C = src.C, C2 = C * C;
+    const size_t n_chunks = ceil_div(n, PQKV_TUPLE_CHUNK);
+    int nl = 0;
+    if (rows == 0) return;
+    if (k == 0) {
+        if (bitmap) PQKV_CUDA(cudaMemsetAsync(bitmap, 0, rows * words * 4, st)), ++nl;
+        if (launches) *launches = nl;
+        return;
+    }
+    Scratch sc(ctx);
+    size_t h_cls = sc.plan<uint8_t>(rows * C2), h_cut = sc.plan<int>(rows * 2);
+    size_t h_tk = sc.plan<uint32_t>(ids ? rows * C2 : 1), h_sb = sc.plan<uint32_t>(ids ? rows * n_chunks : 1);
+    size_t h_bm = sc.plan<uint32_t>(bitmap ? 1 : rows * words);
+    size_t h_sk = sc.plan<uint32_t>(ids ? rows * k : 1), h_si = sc.plan<uint32_t>(ids ? rows * k : 1);
+    size_t h_xk = sc.plan<uint32_t>(ids ? rows * k : 1), h_xi = sc.plan<uint32_t>(ids ? rows * k : 1);
+    sc.commit();
+    TupArgs a{};
+    a.queries = src.queries;
+    a.g = (int)src.g;
+    a.d_h = (int)src.d_h;
+    a.C = (int)C;
+    a.centroids = src.centroids;
+    a.thist = thist;
+    a.chist = chist;
+    a.n = (int)n;
+    a.k = (int)k;
+    a.n_chunks = (int)n_chunks;
+    a.cls = sc.get<uint8_t>(h_cls);
+    a.tkey = ids ? sc.get<uint32_t>(h_tk) : nullptr;
+    a.cut = sc.get<int>(h_cut);
+    a.sel_before = ids ? sc.get<uint32_t>(h_sb) : nullptr;
+    size_t smem = 2 * C * 8 + (3 * C2 + NB + n_chunks + 40) * 4;
+    if (smem > 220 * 1024) fail(PQKV_EINVAL, "tuple select: table too large");
+    PQKV_CUDA(cudaFuncSetAttribute(tuple_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    tuple_select_kernel<<<(unsigned)rows, TUP_THREADS, smem, st>>>(a);
+    PQKV_LAUNCHED("tuple_select_kernel");
+    ++nl;
+    uint32_t* bm = bitmap ? bitmap : sc.get<uint32_t>(h_bm);
+    size_t smem2 = round_up(C2, 16) + (ids ? C2 * 4 : 0);
+    PQKV_CUDA(cudaFuncSetAttribute(tuple_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    tuple_bitmap_kernel<<<dim3((unsigned)n_chunks, (unsigned)rows), TB_THREADS, smem2, st>>>(
+        src.codes, (long long)src.codes_head_stride, (int)n, (int)C, a.cls, a.cut, bm, (int)words, a.tkey,
+        a.sel_before, ids ? sc.get<uint32_t>(h_sk) : nullptr, ids ? sc.get<uint32_t>(h_si) : nullptr, (int)k,
+        (int)n_chunks);
+    PQKV_LAUNCHED("tuple_bitmap_kernel");
+    ++nl;
+    if (ids) {
+        sort_desc_kernel<<<(unsigned)rows, SORT_THREADS, 0, st>>>(sc.get<uint32_t>(h_sk), sc.get<uint32_t>(h_si),
+                                                                 sc.get<uint32_t>(h_xk), sc.get<uint32_t>(h_xi),
+                                                                 (int)k, ids);
+        PQKV_LAUNCHED("sort_desc_kernel");
+        ++nl;
+    }
+    if (launches) *launches = nl;
 }
 
 }  // namespace pqkv_dev

@@ -118,6 +118,42 @@ def test_fused_search_matches_score_then_topk(ctx, orc, index4k, k):
         assert np.array_equal(np.flatnonzero(bits), np.sort(want).astype(np.int64))
 
 
+@pytest.mark.parametrize("k", [1, 205, 819, 4096])
+def test_tuple_search_matches_score_then_topk(ctx, orc, index4k, k):
+    """m == 2 code-pair path: weighted pair radix select + chunked bitmap."""
+    k_, v, q, cen, codes = index4k
+    dc = _t(_u16_as_i16(codes))
+    tables = ctx.tuple_tables(dc, 6)
+    bm, ids = ctx.pq_search(_t(q), _t(cen), dc, 6, k, tables=tables)
+    ids = ids.cpu().numpy()
+    bm = bm.cpu().numpy().view(np.uint32)
+    for h in range(3):
+        want = orc.top_k_desc(orc.pq_score_gqa(q[h], cen[h], codes[h]), k)
+        assert np.array_equal(ids[h].astype(np.uint64), want)
+        bits = np.unpackbits(bm[h].view(np.uint8), bitorder="little")[:4096]
+        assert np.array_equal(np.flatnonzero(bits), np.sort(want).astype(np.int64))
+
+
+@pytest.mark.parametrize("s,k,b,C_used", [(37, 10, 6, 64), (20000, 4000, 6, 3), (9000, 8999, 4, 16),
+                                          (32700, 6554, 6, 64), (12345, 100, 7, 128), (5000, 2500, 1, 2)])
+def test_tuple_search_ties_and_chunks(ctx, orc, s, k, b, C_used):
+    """Heavy ties (few distinct pairs), boundaries spanning chunks, incremental tables."""
+    rng = np.random.default_rng(s + k)
+    C = 1 << b
+    cen = rng.standard_normal((2, 2, C, 64)).astype(np.float32)
+    codes = rng.integers(0, C_used, size=(2, s, 2)).astype(np.uint16)
+    q = rng.standard_normal((2, 2, 128)).astype(np.float32)
+    dc = _t(_u16_as_i16(codes))
+    half = s // 2
+    tables = ctx.tuple_tables(dc, b, s=half)
+    tables = ctx.tuple_tables(dc, b, s=s, tables=tables, row_begin=half)  # append path
+    bm, ids = ctx.pq_search(_t(q), _t(cen), dc, b, k, tables=tables)
+    ids = ids.cpu().numpy()
+    for h in range(2):
+        want = orc.top_k_desc(orc.pq_score_gqa(q[h], cen[h], codes[h]), k)
+        assert np.array_equal(ids[h].astype(np.uint64), want)
+
+
 def test_fused_search_ragged_and_large(ctx, orc):
     """s not a multiple of 32 or of the cluster slice; 32K tokens, tie-heavy m2b6."""
     rng = np.random.default_rng(5)
@@ -169,7 +205,7 @@ def test_attend_rows_f32_fast_path(ctx, orc, t, g):
             assert _rel(got[p, r], want) < 1e-3
 
 
-def _decode_case(orc, s, h, g, n_init, n_local, k, m=2, b=6, seed=3, T=6):
+def _decode_case(orc, s, h, g, n_init, n_local, k, m=2, b=6, seed=3, T=6, tuple_tables=False, ctx=None):
     import paper_2407_12820_b200 as pq
 
     kk, vv, qq = orc.gen_workload(s, 128, h, g, oracle.POWERLAW, seed=seed)
@@ -179,15 +215,18 @@ def _decode_case(orc, s, h, g, n_init, n_local, k, m=2, b=6, seed=3, T=6):
     for p in range(h):
         c, cd = orc.pq_construct(kk[p, n_init:n_init + s_mid], m, b, T, 11 + p)
         cen[p], codes[p] = c, cd
-    layer = pq.DecodeLayer(keys=_t(kk), values=_t(vv), centroids=_t(cen), codes=_t(_u16_as_i16(codes)),
-                           total=s, n_init=n_init, n_local=n_local, b=b)
+    dc = _t(_u16_as_i16(codes))
+    tables = ctx.tuple_tables(dc, b) if tuple_tables else None
+    layer = pq.DecodeLayer(keys=_t(kk), values=_t(vv), centroids=_t(cen), codes=dc,
+                           total=s, n_init=n_init, n_local=n_local, b=b, tables=tables)
     return kk, vv, qq, cen, codes, layer
 
 
+@pytest.mark.parametrize("tup", [False, True])
 @pytest.mark.parametrize("s,h,g,n_init,n_local,k", [(4096, 3, 1, 4, 64, 819), (2000, 2, 4, 16, 64, 300),
-                                                    (700, 2, 2, 0, 1, 50)])
-def test_fused_decode_matches_reference_pipeline(ctx, orc, s, h, g, n_init, n_local, k):
-    kk, vv, qq, cen, codes, layer = _decode_case(orc, s, h, g, n_init, n_local, k)
+                                                    (700, 2, 2, 0, 1, 50), (9000, 2, 1, 4, 64, 1800)])
+def test_fused_decode_matches_reference_pipeline(ctx, orc, s, h, g, n_init, n_local, k, tup):
+    kk, vv, qq, cen, codes, layer = _decode_case(orc, s, h, g, n_init, n_local, k, tuple_tables=tup, ctx=ctx)
     out, ids = ctx.decode(layer, _t(qq), k, want_ids=True)
     out, ids = out.cpu().numpy(), ids.cpu().numpy()
     for p in range(h):
@@ -202,7 +241,7 @@ def test_fused_decode_matches_reference_pipeline(ctx, orc, s, h, g, n_init, n_lo
 def test_decode_host_buffers(ctx, orc):
     import torch
 
-    kk, vv, qq, cen, codes, layer = _decode_case(orc, 3000, 2, 1, 4, 64, 500)
+    kk, vv, qq, cen, codes, layer = _decode_case(orc, 3000, 2, 1, 4, 64, 500, tuple_tables=True, ctx=ctx)
     hq = torch.from_numpy(qq).pin_memory()
     ho = torch.zeros_like(hq).pin_memory()
     ctx.decode_host(layer, hq, ho, 500)
