@@ -4,21 +4,26 @@
 // the selected middle tokens in ascending id ++ the local window: on the flat
 // per-head layout that is simply the selected token ids in ascending order.
 //
-// Fast path (d_h = 128, fp32, PQKV_PREC_F32) -- the decode hot loop:
-//   grid = (chunks + 1) x heads.  CTA c of a head owns middle rows
-//   [c*CHUNK, (c+1)*CHUNK); it expands that slice of the selection bitmap
-//   into row ids in shared memory, then every 8-lane group of a warp gathers
-//   one 512 B K row and one V row per step with coalesced 128-bit loads
-//   (16 floats per lane) and folds it into a warp-level online softmax
-//   (log2 domain, exp2f).  The last CTA of a head takes the init + local
-//   rows.  Groups, then warps, then CTAs are merged with the usual
-//   (max, sum, acc) rescaling; combine_kernel merges the per-CTA partials.
+// Fast path (d_h = 128, g in {1,2,4}, fp32, PQKV_PREC_F32) -- the decode hot loop:
+//   grid = chunks x heads, sized so every CTA is resident in one wave.  A CTA
+//   owns a PQKV_TUPLE_CHUNK-multiple range of middle tokens (+ the init rows
+//   for chunk 0, the local rows for the last chunk).  It first turns its
+//   range into ascending row ids in shared memory -- from the selection
+//   bitmap, or directly from the codes via the code-pair classes of
+//   tuple_select (no bitmap round trip) -- then every 16-lane half-warp
+//   gathers one 512 B K row and one V row per step with coalesced 128-bit
+//   loads, double-buffered (the next row is in flight while the current one
+//   is consumed), and folds it into an fp32 online softmax in the log2
+//   domain with lazy rescaling.  Half-warps, warps and CTAs are merged with
+//   (max, sum, acc) rescaling; the last CTA of a head to finish merges the
+//   per-CTA partials (atomic arrival counter), so a layer is one launch.
 //
 // Exact path (PQKV_PREC_F64, any d_h) -- the C++ API drop-in:
 //   exact_scores (attention.cpp:11-26) in fp64 with the same summation order
 //   (bit-identical f32 scores), max-subtracted fp64 exp, the serial fp64 total
 //   and the row-ordered fp64 accumulation of softmax_attention
 //   (attention.cpp:35-60).  Only exp() differs in implementation from libm.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -29,207 +34,315 @@ namespace {
 
 constexpr int AT_THREADS = 256;
 constexpr int AT_WARPS = AT_THREADS / 32;
-constexpr int CHUNK = 4096;  // middle rows per CTA (bitmap mode) / list positions (rows mode)
 constexpr int DH = 128;
+constexpr int LPR = 16;            // lanes per K/V row
+constexpr int VPL = DH / 4 / LPR;  // float4 per lane per row (2)
+
+enum { SRC_ROWS = 0, SRC_BITMAP = 1, SRC_TUPLE = 2 };
 
 struct AtArgs {
     const float* queries;  // [P][G][128]
     const float* keys;
     const float* values;
     long long kv_head_stride;
-    // bitmap mode
-    const uint32_t* bitmap;  // [P][words]
-    int words, s_mid, n_init, n_local, total;
-    // rows mode
-    const int64_t* rows;  // [P][t]
+    int src;
+    int n_init, n_local, total, s_mid;
+    int chunk;     // middle tokens (bitmap/tuple) or list positions (rows) per CTA
+    int n_chunks;  // CTAs per head
+    // SRC_BITMAP
+    const uint32_t* bitmap;
+    int words;
+    // SRC_TUPLE
+    const uint16_t* codes;
+    long long codes_head_stride;
+    int C;
+    const uint8_t* cls;  // [P][C*C]
+    const int* cut;      // [P][2]
+    // SRC_ROWS
+    const int64_t* rows;
     int t;
-    int n_chunks;          // chunks per head including the init/local chunk (bitmap mode)
-    float scale_log2;      // log2(e) / sqrt(d_h)
-    float* part;           // [P][n_chunks][G][DH + 2]
-    unsigned* arrivals;    // [P] zero on entry; reset by the combining CTA
-    float* out;            // [P][G][DH]
+    float scale_log2;    // log2(e) / sqrt(d_h)
+    float* part;         // [P][n_chunks][G][DH + 2]
+    unsigned* arrivals;  // [P] zero on entry; reset by the combining CTA
+    float* out;          // [P][G][DH]
 };
 
 __device__ __forceinline__ float safe_scale(float m_old, float m_new) {
     return m_old == -INFINITY ? 0.0f : exp2f(m_old - m_new);
 }
 
-template <int G, int RPI>
-__global__ void __launch_bounds__(AT_THREADS) attend_kernel(AtArgs a) {
-    __shared__ int rows_s[CHUNK + 128];
+// Shared memory: rows[rows_cap] | words[chunk/32] | cls[C*C] (tuple) | small.
+struct AtSmem {
+    int* rows;
+    uint32_t* words;
+    uint8_t* cls;
+};
+
+// Expands selection words (bit b of word w = middle token base + 32w + b) into
+// ascending token ids at rows[off...]; every warp owns a contiguous range of
+// words.  Returns the number of rows written (block-uniform).
+__device__ int expand_words(const uint32_t* words, int nwords, int token_base, int* rows, int off,
+                            uint32_t* wtot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (nwords + AT_WARPS - 1) / AT_WARPS;
+    const int w0 = warp * per, w1 = min(nwords, w0 + per);
+    uint32_t cnt = 0;
+    for (int w = w0 + lane; w < w1; w += 32) cnt += __popc(words[w]);
+    cnt = warp_sum(cnt);
+    if (lane == 0) wtot[warp] = cnt;
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < AT_WARPS; ++w) {
+        uint32_t v = wtot[w];
+        before += w < warp ? v : 0;
+        total += v;
+    }
+    __syncthreads();
+    uint32_t run = off + before;
+    for (int wb = w0; wb < w1; wb += 32) {
+        const int w = wb + lane;
+        uint32_t bits = w < w1 ? words[w] : 0u;
+        uint32_t c = __popc(bits), x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        uint32_t pos = run + x - c;
+        while (bits) {
+            int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            rows[pos++] = token_base + w * 32 + b;
+        }
+        run += __shfl_sync(FULL, x, 31);
+    }
+    __syncthreads();
+    return (int)total;
+}
+
+// Tuple classification of middle tokens [r0, r1) into selection words
+// (pq.cpp:128-140 pair score, topk.cpp tie rule via the tuple_select cut).
+// Warp segments never straddle a PQKV_TUPLE_CHUNK chunk (chunk % (8*32) and
+// PQKV_TUPLE_CHUNK % segment hold by construction).
+__device__ void classify_words(const AtArgs& a, int p, int r0, int r1, uint32_t* words,
+                               const uint8_t* cls, uint32_t* wtot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int seg = a.chunk / AT_WARPS;  // tokens per warp (multiple of 32)
+    const int s0 = r0 + warp * seg, s1 = min(r1, s0 + seg);
+    const int tc = s0 / PQKV_TUPLE_CHUNK;
+    const int cstar = a.cut[2 * p];
+    const uint32_t take = (uint32_t)a.cut[2 * p + 1];
+    const uint32_t* cd = reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride);
+    const bool boundary = tc == cstar && s0 < s1;
+    // pass 1 (boundary chunk only): equal-pair counts per warp, in id order
+    uint32_t eq_before = 0;
+    if (__syncthreads_or(boundary)) {
+        uint32_t neq = 0;
+        if (boundary)
+            for (int i0 = s0; i0 < s1; i0 += 32) {
+                const int i = i0 + lane;
+                uint8_t cl = 0;
+                if (i < s1) {
+                    uint32_t pr = cd[i];
+                    cl = cls[(pr & 0xffffu) * (uint32_t)a.C + (pr >> 16)];
+                }
+                neq += __popc(__ballot_sync(FULL, cl == 2));
+            }
+        if (lane == 0) wtot[warp] = boundary ? neq : 0;
+        __syncthreads();
+        // warps of the same tuple chunk precede in warp order
+        for (int w = 0; w < warp; ++w)
+            if ((r0 + w * seg) / PQKV_TUPLE_CHUNK == tc) eq_before += wtot[w];
+        __syncthreads();
+    }
+    // pass 2: selection words
+    uint32_t eq_run = eq_before;
+    for (int i0 = s0; i0 < s1; i0 += 32) {
+        const int i = i0 + lane;
+        uint8_t cl = 0;
+        if (i < s1) {
+            uint32_t pr = cd[i];
+            cl = cls[(pr & 0xffffu) * (uint32_t)a.C + (pr >> 16)];
+        }
+        const bool gt = cl == 1, eq = cl == 2;
+        bool sel;
+        if (tc < cstar) sel = gt || eq;
+        else if (tc > cstar) sel = gt;
+        else {
+            unsigned em = __ballot_sync(FULL, eq);
+            sel = gt || (eq && eq_run + __popc(em & lanemask_lt()) < take);
+            eq_run += __popc(em);
+        }
+        const unsigned word = __ballot_sync(FULL, sel);
+        if (lane == 0) words[(i0 - r0) >> 5] = word;
+    }
+    __syncthreads();
+}
+
+template <int G>
+__global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint32_t wtot[AT_WARPS];
     __shared__ int nrows_s;
-    __shared__ uint32_t wcnt[CHUNK / 32];
     __shared__ float wm[AT_WARPS][G], wl[AT_WARPS][G];
-    // wacc (warp partials) reuses rows_s once the gather loop is done
-    static_assert(AT_WARPS * G * DH <= CHUNK + 128, "warp partials must fit the row buffer");
 
     const int p = blockIdx.y, c = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int grp = lane >> 3, gl = lane & 7;
+    const int half = lane >> 4, hl = lane & 15;
+    const int nwords = a.chunk / 32;
+    int* rows = reinterpret_cast<int*>(smem_raw);
+    const int rows_cap = a.src == SRC_ROWS ? a.chunk : a.chunk + a.n_init + a.n_local;
+    uint32_t* words = reinterpret_cast<uint32_t*>(rows + rows_cap);
+    uint8_t* cls = reinterpret_cast<uint8_t*>(words + nwords);
 
-    // ---- 1. this CTA's row list ----
-    if (a.bitmap) {
-        const int last = a.n_chunks - 1;
-        if (c < last) {
-            const int w0 = c * (CHUNK / 32);
-            const int nw = min(CHUNK / 32, a.words - w0);
-            uint32_t bits = 0;
-            if (tid < CHUNK / 32) {
-                bits = tid < nw ? a.bitmap[(long long)p * a.words + w0 + tid] : 0u;
-                wcnt[tid] = __popc(bits);
-            }
-            __syncthreads();
-            if (tid == 0) {  // exclusive scan of 128 word counts
-                uint32_t run = 0;
-                for (int w = 0; w < CHUNK / 32; ++w) { uint32_t v = wcnt[w]; wcnt[w] = run; run += v; }
-                nrows_s = (int)run;
-            }
-            __syncthreads();
-            if (tid < CHUNK / 32) {
-                int off = (int)wcnt[tid];
-                int base = a.n_init + (w0 + tid) * 32;
-                while (bits) {
-                    int b = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    rows_s[off++] = base + b;
-                }
-            }
-        } else {
-            const int ni = a.n_init, nl = a.n_local;
-            for (int e = tid; e < ni + nl; e += AT_THREADS)
-                rows_s[e] = e < ni ? e : a.total - nl + (e - ni);
-            if (tid == 0) nrows_s = ni + nl;
-        }
+    // ---- 1. this CTA's row list (ascending token ids) ----
+    int nrows = 0;
+    if (a.src == SRC_ROWS) {
+        const int b0 = c * a.chunk, cnt = max(0, min(a.chunk, a.t - b0));
+        for (int e = tid; e < cnt; e += AT_THREADS) rows[e] = (int)a.rows[(long long)p * a.t + b0 + e];
+        nrows = cnt;
     } else {
-        const int b0 = c * CHUNK;
-        const int cnt = min(CHUNK, a.t - b0);
-        for (int e = tid; e < cnt; e += AT_THREADS) rows_s[e] = (int)a.rows[(long long)p * a.t + b0 + e];
-        if (tid == 0) nrows_s = max(cnt, 0);
+        if (c == 0)
+            for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
+        nrows = c == 0 ? a.n_init : 0;
+        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
+        const int nw = (max(0, r1 - r0) + 31) / 32;
+        if (a.src == SRC_BITMAP) {
+            for (int w = tid; w < nw; w += AT_THREADS) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
+        } else {
+            const int C2 = a.C * a.C;
+            if ((C2 & 3) == 0) {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(a.cls + (long long)p * C2);
+                for (int e = tid; e < C2 / 4; e += AT_THREADS) reinterpret_cast<uint32_t*>(cls)[e] = src[e];
+            } else {
+                for (int e = tid; e < C2; e += AT_THREADS) cls[e] = a.cls[(long long)p * C2 + e];
+            }
+            __syncthreads();
+            classify_words(a, p, r0, r1, words, cls, wtot);
+        }
+        __syncthreads();
+        nrows += expand_words(words, nw, a.n_init + r0, rows, nrows, wtot);
+        if (c == a.n_chunks - 1) {
+            for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
+            nrows += a.n_local;
+        }
     }
+    if (tid == 0) nrows_s = nrows;
     __syncthreads();
-    const int nrows = nrows_s;
+    nrows = nrows_s;
 
-    // ---- 2. queries in the lane layout: dims {32j + 4gl + e} ----
-    float q[G][16];
+    // ---- 2. queries in the lane layout: dims {64j + 4hl + e} ----
+    float q[G][4 * VPL];
 #pragma unroll
     for (int r = 0; r < G; ++r) {
         const float4* qp = reinterpret_cast<const float4*>(a.queries + ((long long)p * G + r) * DH);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            float4 v = __ldg(qp + j * 8 + gl);
+        for (int j = 0; j < VPL; ++j) {
+            float4 v = __ldg(qp + j * LPR + hl);
             q[r][4 * j + 0] = v.x * a.scale_log2;
             q[r][4 * j + 1] = v.y * a.scale_log2;
             q[r][4 * j + 2] = v.z * a.scale_log2;
             q[r][4 * j + 3] = v.w * a.scale_log2;
         }
     }
-    float m[G], l[G], acc[G][16];
+    float m[G], l[G], acc[G][4 * VPL];
 #pragma unroll
     for (int r = 0; r < G; ++r) {
         m[r] = -INFINITY;
         l[r] = 0.f;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) acc[r][e] = 0.f;
+        for (int e = 0; e < 4 * VPL; ++e) acc[r][e] = 0.f;
     }
 
-    const float* kbase = a.keys + (long long)p * a.kv_head_stride;
-    const float* vbase = a.values + (long long)p * a.kv_head_stride;
-    const int slot = warp * 4 + grp;        // 0..31
-    const int stride = AT_WARPS * 4 * RPI;  // rows per CTA step
-
-    // ---- 3. gather + online softmax ----
-    for (int base = 0; base < nrows; base += stride) {
-        float4 kr[RPI][4], vr[RPI][4];
-        bool valid[RPI];
+    // ---- 3. gather (double-buffered 128-bit loads) + online softmax ----
+    const float4* kb = reinterpret_cast<const float4*>(a.keys + (long long)p * a.kv_head_stride);
+    const float4* vb = reinterpret_cast<const float4*>(a.values + (long long)p * a.kv_head_stride);
+    const int slot = warp * 2 + half;          // 0..15
+    constexpr int STEP = AT_WARPS * 2;         // rows per CTA step
+    float4 kc[VPL], vc[VPL], kn[VPL], vn[VPL];
+    int ri = slot;
+    if (ri < nrows) {
+        const long long row = rows[ri];
 #pragma unroll
-        for (int u = 0; u < RPI; ++u) {
-            int ri = base + u * AT_WARPS * 4 + slot;
-            valid[u] = ri < nrows;
-            int row = valid[u] ? rows_s[ri] : rows_s[0];
-            const float4* kp = reinterpret_cast<const float4*>(kbase + (long long)row * DH);
-            const float4* vp = reinterpret_cast<const float4*>(vbase + (long long)row * DH);
+        for (int j = 0; j < VPL; ++j) {
+            kc[j] = __ldg(kb + row * (DH / 4) + j * LPR + hl);
+            vc[j] = __ldg(vb + row * (DH / 4) + j * LPR + hl);
+        }
+    }
+    for (; ri < nrows; ri += STEP) {  // half-warp uniform trip count
+        const int rn = ri + STEP;
+        if (rn < nrows) {  // prefetch the next row of this half-warp
+            const long long row = rows[rn];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                kr[u][j] = __ldg(kp + j * 8 + gl);
-                vr[u][j] = __ldg(vp + j * 8 + gl);
+            for (int j = 0; j < VPL; ++j) {
+                kn[j] = __ldg(kb + row * (DH / 4) + j * LPR + hl);
+                vn[j] = __ldg(vb + row * (DH / 4) + j * LPR + hl);
             }
         }
 #pragma unroll
         for (int r = 0; r < G; ++r) {
-            float s[RPI];
+            float d = 0.f;
 #pragma unroll
-            for (int u = 0; u < RPI; ++u) {
-                float d = 0.f;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    d = fmaf(q[r][4 * j + 0], kr[u][j].x, d);
-                    d = fmaf(q[r][4 * j + 1], kr[u][j].y, d);
-                    d = fmaf(q[r][4 * j + 2], kr[u][j].z, d);
-                    d = fmaf(q[r][4 * j + 3], kr[u][j].w, d);
-                }
-                d += __shfl_xor_sync(FULL, d, 1);
-                d += __shfl_xor_sync(FULL, d, 2);
-                d += __shfl_xor_sync(FULL, d, 4);
-                s[u] = valid[u] ? d : -INFINITY;
+            for (int j = 0; j < VPL; ++j) {
+                d = fmaf(q[r][4 * j + 0], kc[j].x, d);
+                d = fmaf(q[r][4 * j + 1], kc[j].y, d);
+                d = fmaf(q[r][4 * j + 2], kc[j].z, d);
+                d = fmaf(q[r][4 * j + 3], kc[j].w, d);
             }
-            float mn = m[r];
+            d += __shfl_xor_sync(0xffffu << (half * 16), d, 1, 16);
+            d += __shfl_xor_sync(0xffffu << (half * 16), d, 2, 16);
+            d += __shfl_xor_sync(0xffffu << (half * 16), d, 4, 16);
+            d += __shfl_xor_sync(0xffffu << (half * 16), d, 8, 16);
+            if (d > m[r]) {  // lazy rescale: only when the running max grows
+                const float alpha = safe_scale(m[r], d);
+                l[r] *= alpha;
 #pragma unroll
-            for (int u = 0; u < RPI; ++u) mn = fmaxf(mn, s[u]);
-            if (mn == -INFINITY) continue;
-            float alpha = safe_scale(m[r], mn);
-            float pw[RPI];
-            float lsum = 0.f;
-#pragma unroll
-            for (int u = 0; u < RPI; ++u) { pw[u] = exp2f(s[u] - mn); lsum += pw[u]; }
-            l[r] = l[r] * alpha + lsum;
-            m[r] = mn;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float o0 = acc[r][4 * j + 0] * alpha, o1 = acc[r][4 * j + 1] * alpha;
-                float o2 = acc[r][4 * j + 2] * alpha, o3 = acc[r][4 * j + 3] * alpha;
-#pragma unroll
-                for (int u = 0; u < RPI; ++u) {
-                    o0 = fmaf(pw[u], vr[u][j].x, o0);
-                    o1 = fmaf(pw[u], vr[u][j].y, o1);
-                    o2 = fmaf(pw[u], vr[u][j].z, o2);
-                    o3 = fmaf(pw[u], vr[u][j].w, o3);
-                }
-                acc[r][4 * j + 0] = o0;
-                acc[r][4 * j + 1] = o1;
-                acc[r][4 * j + 2] = o2;
-                acc[r][4 * j + 3] = o3;
+                for (int e = 0; e < 4 * VPL; ++e) acc[r][e] *= alpha;
+                m[r] = d;
             }
+            const float pw = exp2f(d - m[r]);
+            l[r] += pw;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                acc[r][4 * j + 0] = fmaf(pw, vc[j].x, acc[r][4 * j + 0]);
+                acc[r][4 * j + 1] = fmaf(pw, vc[j].y, acc[r][4 * j + 1]);
+                acc[r][4 * j + 2] = fmaf(pw, vc[j].z, acc[r][4 * j + 2]);
+                acc[r][4 * j + 3] = fmaf(pw, vc[j].w, acc[r][4 * j + 3]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            kc[j] = kn[j];
+            vc[j] = vn[j];
         }
     }
 
-    // ---- 4. merge the 4 groups of the warp (lanes gl, gl+8, gl+16, gl+24) ----
+    // ---- 4. merge the two half-warps (lanes hl and hl+16 hold the same dims) ----
 #pragma unroll
     for (int r = 0; r < G; ++r) {
+        float mo = __shfl_xor_sync(FULL, m[r], 16);
+        float lo = __shfl_xor_sync(FULL, l[r], 16);
+        float mn = fmaxf(m[r], mo);
+        float sa = safe_scale(m[r], mn), sb = safe_scale(mo, mn);
+        l[r] = l[r] * sa + lo * sb;
 #pragma unroll
-        for (int o = 8; o <= 16; o <<= 1) {
-            float mo = __shfl_xor_sync(FULL, m[r], o);
-            float lo = __shfl_xor_sync(FULL, l[r], o);
-            float mn = fmaxf(m[r], mo);
-            float sa = safe_scale(m[r], mn), sb = safe_scale(mo, mn);
-            l[r] = l[r] * sa + lo * sb;
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                float ao = __shfl_xor_sync(FULL, acc[r][e], o);
-                acc[r][e] = acc[r][e] * sa + ao * sb;
-            }
-            m[r] = mn;
+        for (int e = 0; e < 4 * VPL; ++e) {
+            float ao = __shfl_xor_sync(FULL, acc[r][e], 16);
+            acc[r][e] = acc[r][e] * sa + ao * sb;
         }
+        m[r] = mn;
     }
-    __syncthreads();  // every warp is past the gather loop: rows_s is free
-    float* wacc = reinterpret_cast<float*>(rows_s);
+    __syncthreads();  // every warp is past the gather loop: rows[] is free
+    float* wacc = reinterpret_cast<float*>(smem_raw);  // [AT_WARPS][G][DH]
 #pragma unroll
     for (int r = 0; r < G; ++r) {
-        if (grp == 0) {
+        if (half == 0) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < VPL; ++j)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) wacc[(warp * G + r) * DH + 32 * j + 4 * gl + e] = acc[r][4 * j + e];
-            if (gl == 0) { wm[warp][r] = m[r]; wl[warp][r] = l[r]; }
+                for (int e = 0; e < 4; ++e) wacc[(warp * G + r) * DH + 64 * j + 4 * hl + e] = acc[r][4 * j + e];
+            if (hl == 0) { wm[warp][r] = m[r]; wl[warp][r] = l[r]; }
         }
     }
     __syncthreads();
@@ -247,9 +360,9 @@ __global__ void __launch_bounds__(AT_THREADS) attend_kernel(AtArgs a) {
                 O += wacc[(w * G + r) * DH + d] * sc;
             }
         }
-        float* out = a.part + (((long long)p * a.n_chunks + c) * G + r) * (DH + 2);
-        out[2 + d] = O;
-        if (d == 0) { out[0] = M; out[1] = L; }
+        float* o = a.part + (((long long)p * a.n_chunks + c) * G + r) * (DH + 2);
+        o[2 + d] = O;
+        if (d == 0) { o[0] = M; o[1] = L; }
     }
 
     // ---- 6. the last CTA of this head merges all partials (no extra launch) ----
@@ -260,7 +373,7 @@ __global__ void __launch_bounds__(AT_THREADS) attend_kernel(AtArgs a) {
     __syncthreads();
     if (ticket != (unsigned)a.n_chunks - 1) return;
     __threadfence();
-    float* sc = reinterpret_cast<float*>(rows_s);  // [G][n_chunks] scale, then [G] sums
+    float* sc = reinterpret_cast<float*>(smem_raw) + AT_WARPS * G * DH;  // [G][n_chunks] + [G]
     const int nc = a.n_chunks;
     const float* pb = a.part + (long long)p * nc * G * (DH + 2);
     for (int r = warp; r < G; r += AT_WARPS) {
@@ -388,24 +501,6 @@ __global__ void bitmap_rows_kernel(const uint32_t* bitmap, int words, int n_init
     }
 }
 
-template <int G>
-void launch_fast(const AtArgs& a, dim3 grid, cudaStream_t st) {
-    if constexpr (G <= 2)
-        attend_kernel<G, 2><<<grid, AT_THREADS, 0, st>>>(a);
-    else
-        attend_kernel<G, 1><<<grid, AT_THREADS, 0, st>>>(a);
-    PQKV_LAUNCHED("attend_kernel");
-}
-
-bool launch_fast_any(int G, const AtArgs& a, dim3 grid, cudaStream_t st) {
-    switch (G) {
-        case 1: launch_fast<1>(a, grid, st); return true;
-        case 2: launch_fast<2>(a, grid, st); return true;
-        case 4: launch_fast<4>(a, grid, st); return true;
-        default: return false;
-    }
-}
-
 }  // namespace
 
 void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_t d_h,
@@ -428,6 +523,52 @@ void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_
     PQKV_LAUNCHED("softmax_exact_kernel");
 }
 
+// Chunk geometry: all CTAs resident in one wave where possible (the gather
+// reaches streaming bandwidth with ~1.6K rows per CTA, tools/microbench/
+// gather_probe.cu); middle chunks are multiples of PQKV_TUPLE_CHUNK so the
+// code-pair classification never splits a tuple chunk.
+static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
+    const size_t occ = G == 1 ? 4 : 2;
+    const size_t target = (size_t)ctx->sm_count * occ;
+    const size_t per_head = std::max<size_t>(1, target / std::max<size_t>(P, 1));
+    const size_t tcs = std::max<size_t>(1, ceil_div(s_mid, PQKV_TUPLE_CHUNK));
+    size_t q = std::min<size_t>(8, std::max<size_t>(1, ceil_div(tcs, per_head)));
+    return (int)(q * PQKV_TUPLE_CHUNK);
+}
+
+static size_t attend_smem(const AtArgs& a, int G) {
+    size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.chunk + a.n_init + a.n_local;
+    size_t bytes = rows_cap * 4 + (size_t)a.chunk / 32 * 4 + (a.src == SRC_TUPLE ? (size_t)a.C * a.C : 0);
+    size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
+    return round_up(std::max(bytes, merge), 16);
+}
+
+static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cudaStream_t st) {
+    Scratch sc(ctx);
+    size_t h_part = sc.plan<float>(P * a.n_chunks * G * (DH + 2));
+    sc.commit();
+    a.part = sc.get<float>(h_part);
+    a.arrivals = arrival_counters(ctx, P, st);
+    size_t smem = attend_smem(a, G);
+    dim3 grid((unsigned)a.n_chunks, (unsigned)P);
+    switch (G) {
+        case 1:
+            PQKV_CUDA(cudaFuncSetAttribute(attend_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attend_kernel<1><<<grid, AT_THREADS, smem, st>>>(a);
+            break;
+        case 2:
+            PQKV_CUDA(cudaFuncSetAttribute(attend_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attend_kernel<2><<<grid, AT_THREADS, smem, st>>>(a);
+            break;
+        case 4:
+            PQKV_CUDA(cudaFuncSetAttribute(attend_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attend_kernel<4><<<grid, AT_THREADS, smem, st>>>(a);
+            break;
+        default: fail(PQKV_EINVAL, "attend: g must be 1, 2 or 4 on the fast path");
+    }
+    PQKV_LAUNCHED("attend_kernel");
+}
+
 void launch_attend_rows(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_t d_h,
                         const float* keys, const float* values, size_t kv_head_stride,
                         const int64_t* rows, size_t t, int precision, float* out,
@@ -441,58 +582,54 @@ void launch_attend_rows(pqkv_ctx* ctx, const float* queries, size_t P, size_t G,
         launch_exact(ctx, queries, P, G, d_h, keys, values, kv_head_stride, rows, t, out, st);
         return;
     }
-    const int chunks = (int)ceil_div(t, CHUNK);
-    Scratch sc(ctx);
-    size_t h_part = sc.plan<float>(P * chunks * G * (DH + 2));
-    sc.commit();
     AtArgs a{};
     a.queries = queries;
     a.keys = keys;
     a.values = values;
     a.kv_head_stride = (long long)kv_head_stride;
+    a.src = SRC_ROWS;
     a.rows = rows;
     a.t = (int)t;
-    a.n_chunks = chunks;
+    const size_t target = (size_t)ctx->sm_count * (G == 1 ? 4 : 2);
+    const size_t per_head = std::max<size_t>(1, target / P);
+    a.chunk = (int)std::min<size_t>(8192, round_up(std::max<size_t>(32, ceil_div(t, per_head)), 32));
+    a.n_chunks = (int)ceil_div(t, (size_t)a.chunk);
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d_h));
-    a.part = sc.get<float>(h_part);
-    a.arrivals = arrival_counters(ctx, P, st);
     a.out = out;
-    launch_fast_any((int)G, a, dim3((unsigned)chunks, (unsigned)P), st);
+    launch_attend_kernel(ctx, a, P, (int)G, st);
 }
 
-bool launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
-                          const uint32_t* bitmap, float* out, cudaStream_t st, int* launches) {
+bool decode_fast_path(const pqkv_layer& L, size_t G) {
+    return L.d_h == DH && (G == 1 || G == 2 || G == 4) && L.kv_head_stride % 4 == 0;
+}
+
+void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
+                          const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
+                          cudaStream_t st) {
     bind_device(ctx);
     const size_t s_mid = L.total - L.n_init - L.n_local;
-    const size_t words = ceil_div(s_mid, 32);
-    bool fast = L.d_h == DH && (G == 1 || G == 2 || G == 4) && L.kv_head_stride % 4 == 0;
-    if (fast) {
-        const int mid_chunks = (int)ceil_div(s_mid, CHUNK);
-        const int chunks = mid_chunks + 1;
-        Scratch sc(ctx);
-        size_t h_part = sc.plan<float>(L.n_heads * chunks * G * (DH + 2));
-        sc.commit();
-        AtArgs a{};
-        a.queries = queries;
-        a.keys = L.keys;
-        a.values = L.values;
-        a.kv_head_stride = (long long)L.kv_head_stride;
-        a.bitmap = bitmap;
-        a.words = (int)words;
-        a.s_mid = (int)s_mid;
-        a.n_init = (int)L.n_init;
-        a.n_local = (int)L.n_local;
-        a.total = (int)L.total;
-        a.n_chunks = chunks;
-        a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
-        a.part = sc.get<float>(h_part);
-        a.arrivals = arrival_counters(ctx, L.n_heads, st);
-        a.out = out;
-        launch_fast_any((int)G, a, dim3((unsigned)chunks, (unsigned)L.n_heads), st);
-        if (launches) *launches = 1;
-        return true;
-    }
-    return false;  // caller materialises row lists and runs the exact kernels
+    AtArgs a{};
+    a.queries = queries;
+    a.keys = L.keys;
+    a.values = L.values;
+    a.kv_head_stride = (long long)L.kv_head_stride;
+    a.src = cls ? SRC_TUPLE : SRC_BITMAP;
+    a.n_init = (int)L.n_init;
+    a.n_local = (int)L.n_local;
+    a.total = (int)L.total;
+    a.s_mid = (int)s_mid;
+    a.chunk = plan_chunk_tokens(ctx, L.n_heads, G, s_mid);
+    a.n_chunks = (int)std::max<size_t>(1, ceil_div(s_mid, (size_t)a.chunk));
+    a.bitmap = bitmap;
+    a.words = (int)ceil_div(s_mid, 32);
+    a.codes = L.codes;
+    a.codes_head_stride = (long long)L.codes_head_stride;
+    a.C = 1 << L.b;
+    a.cls = cls;
+    a.cut = cut;
+    a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
+    a.out = out;
+    launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);
 }
 
 void launch_exact_scores(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_t d_h,

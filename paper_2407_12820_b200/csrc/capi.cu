@@ -235,41 +235,44 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         check_layer(L, g, k);
         if (L->n_heads == 0) return;
         cudaStream_t st = as_stream(stream);
-        const size_t s_mid = L->total - L->n_init - L->n_local;
-        const size_t words = ceil_div(s_mid, 32);
-        // the bitmap lives in the arena after the kernels' own scratch; keep a
-        // dedicated allocation so later Scratch plans cannot alias it
-        static thread_local uint32_t* bm = nullptr;
-        static thread_local size_t bm_words = 0;
-        static thread_local int bm_dev = -1;
-        if (L->n_heads * words > bm_words || bm_dev != ctx->device) {
-            if (bm) { cudaStreamSynchronize(st); cudaFree(bm); }
-            bm_words = L->n_heads * words;
-            PQKV_CUDA(cudaMalloc(&bm, bm_words * 4));
-            bm_dev = ctx->device;
-        }
+        const size_t P = L->n_heads, s_mid = L->total - L->n_init - L->n_local;
+        const size_t words = ceil_div(s_mid, 32), C = size_t{1} << L->b;
+        const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist);
+        const bool fast = decode_fast_path(*L, g);
         SelectSource src;
         src.queries = d_queries;
         src.g = g;
         src.d_h = L->d_h;
         src.m = L->m;
-        src.C = size_t{1} << L->b;
+        src.C = C;
         src.centroids = L->centroids;
         src.codes = L->codes;
         src.codes_head_stride = L->codes_head_stride;
-        if (tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist))
-            launch_select_tuple(ctx, src, L->tuple_hist, L->tuple_chunk_hist, L->n_heads, s_mid, k, bm, d_ids, st,
-                                nullptr);
+        if (tup && fast && !d_ids && k > 0) {
+            // pair-level select -> attention classifies its own codes
+            char* ws = static_cast<char*>(decode_workspace(ctx, round_up(P * C * C, 256) + P * 2 * sizeof(int)));
+            uint8_t* cls = reinterpret_cast<uint8_t*>(ws);
+            int* cut = reinterpret_cast<int*>(ws + round_up(P * C * C, 256));
+            launch_tuple_select(ctx, src, L->tuple_hist, L->tuple_chunk_hist, P, s_mid, k, cls, cut, nullptr,
+                                nullptr, st);
+            launch_decode_attend(ctx, *L, d_queries, g, nullptr, cls, cut, d_out, st);
+            return;
+        }
+        uint32_t* bm = static_cast<uint32_t*>(decode_workspace(ctx, P * words * 4));
+        if (tup)
+            launch_select_tuple(ctx, src, L->tuple_hist, L->tuple_chunk_hist, P, s_mid, k, bm, d_ids, st, nullptr);
         else
-            launch_select(ctx, src, L->n_heads, s_mid, k, bm, d_ids, st, nullptr);
-        if (launch_decode_attend(ctx, *L, d_queries, g, bm, d_out, st, nullptr)) return;
+            launch_select(ctx, src, P, s_mid, k, bm, d_ids, st, nullptr);
+        if (fast) {
+            launch_decode_attend(ctx, *L, d_queries, g, bm, nullptr, nullptr, d_out, st);
+            return;
+        }
         // generic geometry: ascending row lists, then the fp64 kernels
         const size_t T = L->n_init + k + L->n_local;
         int64_t* rows = nullptr;
-        PQKV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), L->n_heads * T * 8, st));
-        launch_bitmap_rows(ctx, bm, L->n_heads, words, L->n_init, L->n_local, L->total, T, rows, st);
-        launch_exact(ctx, d_queries, L->n_heads, g, L->d_h, L->keys, L->values, L->kv_head_stride, rows,
-                     T, d_out, st);
+        PQKV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), P * T * 8, st));
+        launch_bitmap_rows(ctx, bm, P, words, L->n_init, L->n_local, L->total, T, rows, st);
+        launch_exact(ctx, d_queries, P, g, L->d_h, L->keys, L->values, L->kv_head_stride, rows, T, d_out, st);
         PQKV_CUDA(cudaFreeAsync(rows, st));
     });
 }
@@ -280,8 +283,8 @@ int pqkv_decode_attend(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_querie
         need_ctx(ctx);
         check_layer(L, g, 0);
         if (L->n_heads == 0) return;
-        if (!launch_decode_attend(ctx, *L, d_queries, g, d_bitmap, d_out, as_stream(stream), nullptr))
-            fail(PQKV_EINVAL, "decode_attend: needs d_h == 128 and g in {1, 2, 4}");
+        if (!decode_fast_path(*L, g)) fail(PQKV_EINVAL, "decode_attend: needs d_h == 128 and g in {1, 2, 4}");
+        launch_decode_attend(ctx, *L, d_queries, g, d_bitmap, nullptr, nullptr, d_out, as_stream(stream));
     });
 }
 
@@ -312,8 +315,9 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
 int pqkv_decode_launches(const pqkv_layer* L, size_t g, int with_ids) {
     if (!L) return 0;
     bool fast = L->d_h == 128 && (g == 1 || g == 2 || g == 4) && L->kv_head_stride % 4 == 0;
-    int n = (L->m == 2 && L->b <= 7 && L->tuple_hist && L->tuple_chunk_hist) ? 2 /*pair select+bitmap*/
-                                                                             : 1 /*cluster select*/;
+    const bool tup = L->m == 2 && L->b <= 7 && L->tuple_hist && L->tuple_chunk_hist;
+    if (tup && fast && !with_ids) return 2;  // pair select + attention (classifies codes, fused combine)
+    int n = tup ? 2 /*pair select + bitmap*/ : 1 /*cluster select*/;
     n += with_ids ? 1 : 0 /*sort*/;
     n += fast ? 1 /*attend with fused combine*/ : 3 /*rows + scores + softmax*/;
     return n;

@@ -49,6 +49,20 @@ void* pinned_staging(pqkv_ctx* ctx, size_t bytes) {
     return ctx->pinned;
 }
 
+void* decode_workspace(pqkv_ctx* ctx, size_t bytes) {
+    if (bytes > ctx->ws_bytes) {
+        if (ctx->ws) {
+            PQKV_CUDA(cudaDeviceSynchronize());
+            PQKV_CUDA(cudaFree(ctx->ws));
+            ctx->ws = nullptr;
+        }
+        size_t want = round_up(bytes + bytes / 4, size_t(1) << 16);
+        PQKV_CUDA(cudaMalloc(&ctx->ws, want));
+        ctx->ws_bytes = want;
+    }
+    return ctx->ws;
+}
+
 unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st) {
     if (n > ctx->n_arrivals) {
         if (ctx->d_arrivals) {
@@ -97,6 +111,7 @@ int pqkv_ctx_destroy(pqkv_ctx* ctx) {
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
         if (ctx->d_stats) cudaFree(ctx->d_stats);
         if (ctx->d_arrivals) cudaFree(ctx->d_arrivals);
+        if (ctx->ws) cudaFree(ctx->ws);
         delete ctx;
     });
 }

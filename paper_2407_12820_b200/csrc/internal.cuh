@@ -23,6 +23,9 @@ struct pqkv_ctx {
     // between launches by the kernel itself).
     unsigned* d_arrivals = nullptr;
     size_t n_arrivals = 0;
+    // Decode workspace (selection bitmap / pair classes between kernels).
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
     // Device counters written by the build kernels (rechecked, total).
     unsigned long long* d_stats = nullptr;
     uint64_t last_rechecked = 0, last_total = 0;
@@ -138,10 +141,18 @@ void launch_attend_rows(pqkv_ctx* ctx, const float* queries, size_t n_heads, siz
                         size_t kv_head_stride, const int64_t* rows, size_t t, int precision,
                         float* out, cudaStream_t stream);
 
-// Fused fast path (d_h == 128, g in {1,2,4}); returns false for other shapes.
-bool launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t g,
-                          const uint32_t* bitmap, float* out, cudaStream_t stream,
-                          int* launches);
+// Fused fast path (d_h == 128, g in {1,2,4}): selection from a bitmap or from
+// the code-pair classes (cls, cut) of launch_tuple_select.
+bool decode_fast_path(const pqkv_layer& L, size_t g);
+void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t g,
+                          const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
+                          cudaStream_t stream);
+// Pair-level select only (writes cls [rows][C*C], cut [rows][2]).
+void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
+                         const uint16_t* chist, size_t rows, size_t n, size_t k, uint8_t* cls, int* cut,
+                         uint32_t* tkey, uint32_t* sel_before, cudaStream_t st);
+// Device buffer for decode-level intermediates (never aliases the arena).
+void* decode_workspace(pqkv_ctx* ctx, size_t bytes);
 void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_t d_h,
                   const float* keys, const float* values, size_t kv_head_stride,
                   const int64_t* rows, size_t t, float* out, cudaStream_t st);

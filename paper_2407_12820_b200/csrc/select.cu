@@ -64,27 +64,37 @@ struct SelArgs {
 };
 
 // Builds T[j][c] (pq.cpp:113-126, rows accumulated as in pq.cpp:157-159).
+// One thread per (j, c); the t-chain stays sequential (reference order) while
+// the centroid row is prefetched 16 floats at a time so the chain is not
+// serialised on L2 latency.
 __device__ void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
                           int C) {
     const int d_m = d_h / m;
     for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
         const int j = e / C;
         const float* cc = cen + (long long)e * d_m;
-        double acc[8];
         double t = 0.0;
-        for (int r0 = 0; r0 < g; r0 += 8) {
-            const int rn = min(8, g - r0);
+        for (int r0 = 0; r0 < g; r0 += 4) {
+            const int rn = min(4, g - r0);
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int t0 = 0; t0 < d_m; t0 += 16) {
+                float cv[16];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) acc[r] = 0.0;
-            for (int tt = 0; tt < d_m; ++tt) {
-                double cv = (double)__ldg(cc + tt);
+                for (int u = 0; u < 16; ++u) cv[u] = (t0 + u < d_m) ? __ldg(cc + t0 + u) : 0.0f;
 #pragma unroll
-                for (int r = 0; r < 8; ++r)
-                    if (r < rn)
-                        acc[r] = __fma_rn((double)__ldg(q + (long long)(r0 + r) * d_h + j * d_m + tt), cv, acc[r]);
+                for (int r = 0; r < 4; ++r) {
+                    if (r >= rn) break;
+                    const float* qq = q + (long long)(r0 + r) * d_h + j * d_m + t0;
+                    float qv[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) qv[u] = (t0 + u < d_m) ? __ldg(qq + u) : 0.0f;
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        if (t0 + u < d_m) acc[r] = __fma_rn((double)qv[u], (double)cv[u], acc[r]);
+                }
             }
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
+            for (int r = 0; r < 4; ++r)
                 if (r < rn) t = __dadd_rn(t, acc[r]);
         }
         lut[e] = t;
@@ -603,63 +613,78 @@ __global__ void __launch_bounds__(TB_THREADS) tuple_bitmap_kernel(
     uint32_t* tkey = reinterpret_cast<uint32_t*>(smem + ((C2 + 15) / 16) * 16);
     __shared__ uint32_t wc[TB_WARPS], ws[TB_WARPS];
     const bool ids = sel_key != nullptr;
-    for (int t = tid; t < C2; t += TB_THREADS) {
-        cls[t] = cls_g[(long long)p * C2 + t];
-        if (ids) tkey[t] = tkey_g[(long long)p * C2 + t];
+    if ((C2 & 3) == 0) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(cls_g + (long long)p * C2);
+        for (int t = tid; t < C2 / 4; t += TB_THREADS) reinterpret_cast<uint32_t*>(cls)[t] = src[t];
+    } else {
+        for (int t = tid; t < C2; t += TB_THREADS) cls[t] = cls_g[(long long)p * C2 + t];
     }
+    if (ids)
+        for (int t = tid; t < C2; t += TB_THREADS) tkey[t] = tkey_g[(long long)p * C2 + t];
     __syncthreads();
     const int cstar = cut[2 * p];
     const uint32_t take = (uint32_t)cut[2 * p + 1];
     const int r0 = c * PQKV_TUPLE_CHUNK, r1 = min(n, r0 + PQKV_TUPLE_CHUNK);
     const uint32_t* cd = reinterpret_cast<const uint32_t*>(codes + p * codes_head_stride);
     uint32_t eq_run = 0, sel_run = ids ? sel_before[(long long)p * n_chunks + c] : 0;
-    for (int base = r0; base < r1; base += TB_THREADS) {
-        const int i = base + tid;
-        uint32_t t = 0;
-        uint8_t cl = 0;
-        if (i < r1) {
-            uint32_t pr = cd[i];  // (c0, c1) little-endian u16 pair
-            t = (pr & 0xffffu) * (uint32_t)C + (pr >> 16);
-            cl = cls[t];
-        }
-        bool gt = cl == 1, eq = cl == 2;
-        bool sel;
-        if (c < cstar) sel = gt || eq;
-        else if (c > cstar) sel = gt;
-        else {  // the boundary chunk: equal pairs in id order, first `take`
-            unsigned em = __ballot_sync(FULL, eq);
-            if (lane == 0) wc[warp] = __popc(em);
-            __syncthreads();
-            uint32_t before = 0, tile = 0;
+    constexpr int U = 4;
+    for (int base0 = r0; base0 < r1; base0 += U * TB_THREADS) {
+        uint32_t prs[U];
 #pragma unroll
-            for (int w = 0; w < TB_WARPS; ++w) {
-                uint32_t v = wc[w];
-                before += w < warp ? v : 0;
-                tile += v;
-            }
-            __syncthreads();
-            sel = gt || (eq && eq_run + before + __popc(em & lanemask_lt()) < take);
-            eq_run += tile;
+        for (int u = 0; u < U; ++u) {
+            const int i = base0 + u * TB_THREADS + tid;
+            prs[u] = i < r1 ? cd[i] : 0u;  // (c0, c1) little-endian u16 pair
         }
-        unsigned sm = __ballot_sync(FULL, sel);
-        if (lane == 0 && base + warp * 32 < r1) bitmap[(long long)p * words + (base >> 5) + warp] = sm;
-        if (ids) {
-            if (lane == 0) ws[warp] = __popc(sm);
-            __syncthreads();
-            uint32_t before = 0, tile = 0;
 #pragma unroll
-            for (int w = 0; w < TB_WARPS; ++w) {
-                uint32_t v = ws[w];
-                before += w < warp ? v : 0;
-                tile += v;
+        for (int u = 0; u < U; ++u) {
+            const int base = base0 + u * TB_THREADS;
+            if (base >= r1) break;  // uniform
+            const int i = base + tid;
+            uint32_t t = 0;
+            uint8_t cl = 0;
+            if (i < r1) {
+                t = (prs[u] & 0xffffu) * (uint32_t)C + (prs[u] >> 16);
+                cl = cls[t];
             }
-            __syncthreads();
-            if (sel) {
-                uint32_t pos = sel_run + before + __popc(sm & lanemask_lt());
-                sel_key[(long long)p * k + pos] = tkey[t];
-                sel_id[(long long)p * k + pos] = (uint32_t)i;
+            bool gt = cl == 1, eq = cl == 2;
+            bool sel;
+            if (c < cstar) sel = gt || eq;
+            else if (c > cstar) sel = gt;
+            else {  // the boundary chunk: equal pairs in id order, first `take`
+                unsigned em = __ballot_sync(FULL, eq);
+                if (lane == 0) wc[warp] = __popc(em);
+                __syncthreads();
+                uint32_t before = 0, tile = 0;
+#pragma unroll
+                for (int w = 0; w < TB_WARPS; ++w) {
+                    uint32_t v = wc[w];
+                    before += w < warp ? v : 0;
+                    tile += v;
+                }
+                __syncthreads();
+                sel = gt || (eq && eq_run + before + __popc(em & lanemask_lt()) < take);
+                eq_run += tile;
             }
-            sel_run += tile;
+            unsigned sm = __ballot_sync(FULL, sel);
+            if (lane == 0 && base + warp * 32 < r1) bitmap[(long long)p * words + (base >> 5) + warp] = sm;
+            if (ids) {
+                if (lane == 0) ws[warp] = __popc(sm);
+                __syncthreads();
+                uint32_t before = 0, tile = 0;
+#pragma unroll
+                for (int w = 0; w < TB_WARPS; ++w) {
+                    uint32_t v = ws[w];
+                    before += w < warp ? v : 0;
+                    tile += v;
+                }
+                __syncthreads();
+                if (sel) {
+                    uint32_t pos = sel_run + before + __popc(sm & lanemask_lt());
+                    sel_key[(long long)p * k + pos] = tkey[t];
+                    sel_id[(long long)p * k + pos] = (uint32_t)i;
+                }
+                sel_run += tile;
+            }
         }
     }
 }
@@ -796,6 +821,33 @@ void launch_tuple_tables(pqkv_ctx* ctx, const uint16_t* codes, size_t P, size_t 
     PQKV_LAUNCHED("tuple_tables_kernel");
 }
 
+void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
+                         const uint16_t* chist, size_t rows, size_t n, size_t k, uint8_t* cls, int* cut,
+                         uint32_t* tkey, uint32_t* sel_before, cudaStream_t st) {
+    bind_device(ctx);
+    const size_t C = src.C, C2 = C * C, n_chunks = ceil_div(n, PQKV_TUPLE_CHUNK);
+    TupArgs a{};
+    a.queries = src.queries;
+    a.g = (int)src.g;
+    a.d_h = (int)src.d_h;
+    a.C = (int)C;
+    a.centroids = src.centroids;
+    a.thist = thist;
+    a.chist = chist;
+    a.n = (int)n;
+    a.k = (int)k;
+    a.n_chunks = (int)n_chunks;
+    a.cls = cls;
+    a.tkey = tkey;
+    a.cut = cut;
+    a.sel_before = sel_before;
+    size_t smem = 2 * C * 8 + (3 * C2 + NB + n_chunks + 40) * 4;
+    if (smem > 220 * 1024) fail(PQKV_EINVAL, "tuple select: table too large");
+    PQKV_CUDA(cudaFuncSetAttribute(tuple_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    tuple_select_kernel<<<(unsigned)rows, TUP_THREADS, smem, st>>>(a);
+    PQKV_LAUNCHED("tuple_select_kernel");
+}
+
 void launch_select_tuple(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
                          const uint16_t* chist, size_t rows, size_t n, size_t k, uint32_t* bitmap,
                          int64_t* ids, cudaStream_t st, int* launches) {
@@ -816,33 +868,18 @@ void launch_select_tuple(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
     size_t h_sk = sc.plan<uint32_t>(ids ? rows * k : 1), h_si = sc.plan<uint32_t>(ids ? rows * k : 1);
     size_t h_xk = sc.plan<uint32_t>(ids ? rows * k : 1), h_xi = sc.plan<uint32_t>(ids ? rows * k : 1);
     sc.commit();
-    TupArgs a{};
-    a.queries = src.queries;
-    a.g = (int)src.g;
-    a.d_h = (int)src.d_h;
-    a.C = (int)C;
-    a.centroids = src.centroids;
-    a.thist = thist;
-    a.chist = chist;
-    a.n = (int)n;
-    a.k = (int)k;
-    a.n_chunks = (int)n_chunks;
-    a.cls = sc.get<uint8_t>(h_cls);
-    a.tkey = ids ? sc.get<uint32_t>(h_tk) : nullptr;
-    a.cut = sc.get<int>(h_cut);
-    a.sel_before = ids ? sc.get<uint32_t>(h_sb) : nullptr;
-    size_t smem = 2 * C * 8 + (3 * C2 + NB + n_chunks + 40) * 4;
-    if (smem > 220 * 1024) fail(PQKV_EINVAL, "tuple select: table too large");
-    PQKV_CUDA(cudaFuncSetAttribute(tuple_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tuple_select_kernel<<<(unsigned)rows, TUP_THREADS, smem, st>>>(a);
-    PQKV_LAUNCHED("tuple_select_kernel");
+    uint8_t* cls = sc.get<uint8_t>(h_cls);
+    int* cut = sc.get<int>(h_cut);
+    uint32_t* tkey = ids ? sc.get<uint32_t>(h_tk) : nullptr;
+    uint32_t* sel_before = ids ? sc.get<uint32_t>(h_sb) : nullptr;
+    launch_tuple_select(ctx, src, thist, chist, rows, n, k, cls, cut, tkey, sel_before, st);
     ++nl;
     uint32_t* bm = bitmap ? bitmap : sc.get<uint32_t>(h_bm);
     size_t smem2 = round_up(C2, 16) + (ids ? C2 * 4 : 0);
     PQKV_CUDA(cudaFuncSetAttribute(tuple_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     tuple_bitmap_kernel<<<dim3((unsigned)n_chunks, (unsigned)rows), TB_THREADS, smem2, st>>>(
-        src.codes, (long long)src.codes_head_stride, (int)n, (int)C, a.cls, a.cut, bm, (int)words, a.tkey,
-        a.sel_before, ids ? sc.get<uint32_t>(h_sk) : nullptr, ids ? sc.get<uint32_t>(h_si) : nullptr, (int)k,
+        src.codes, (long long)src.codes_head_stride, (int)n, (int)C, cls, cut, bm, (int)words, tkey,
+        sel_before, ids ? sc.get<uint32_t>(h_sk) : nullptr, ids ? sc.get<uint32_t>(h_si) : nullptr, (int)k,
         (int)n_chunks);
     PQKV_LAUNCHED("tuple_bitmap_kernel");
     ++nl;
