@@ -156,26 +156,35 @@ __device__ void classify_words(const AtArgs& a, int p, int r0, int r1, uint32_t*
             if ((r0 + w * seg) / PQKV_TUPLE_CHUNK == tc) eq_before += wtot[w];
         __syncthreads();
     }
-    // pass 2: selection words
+    // pass 2: selection words; a warp's codes are fetched 8 words (256
+    // tokens) at a time so the loads overlap instead of serialising on L2.
     uint32_t eq_run = eq_before;
-    for (int i0 = s0; i0 < s1; i0 += 32) {
-        const int i = i0 + lane;
-        uint8_t cl = 0;
-        if (i < s1) {
-            uint32_t pr = cd[i];
-            cl = cls[(pr & 0xffffu) * (uint32_t)a.C + (pr >> 16)];
+    constexpr int PF = 8;
+    for (int b0 = s0; b0 < s1; b0 += 32 * PF) {
+        uint32_t prs[PF];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = b0 + 32 * u + lane;
+            prs[u] = i < s1 ? cd[i] : 0xffffffffu;
         }
-        const bool gt = cl == 1, eq = cl == 2;
-        bool sel;
-        if (tc < cstar) sel = gt || eq;
-        else if (tc > cstar) sel = gt;
-        else {
-            unsigned em = __ballot_sync(FULL, eq);
-            sel = gt || (eq && eq_run + __popc(em & lanemask_lt()) < take);
-            eq_run += __popc(em);
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i0 = b0 + 32 * u;
+            if (i0 >= s1) break;  // warp uniform
+            uint8_t cl = 0;
+            if (prs[u] != 0xffffffffu) cl = cls[(prs[u] & 0xffffu) * (uint32_t)a.C + (prs[u] >> 16)];
+            const bool gt = cl == 1, eq = cl == 2;
+            bool sel;
+            if (tc < cstar) sel = gt || eq;
+            else if (tc > cstar) sel = gt;
+            else {
+                unsigned em = __ballot_sync(FULL, eq);
+                sel = gt || (eq && eq_run + __popc(em & lanemask_lt()) < take);
+                eq_run += __popc(em);
+            }
+            const unsigned word = __ballot_sync(FULL, sel);
+            if (lane == 0) words[(i0 - r0) >> 5] = word;
         }
-        const unsigned word = __ballot_sync(FULL, sel);
-        if (lane == 0) words[(i0 - r0) >> 5] = word;
     }
     __syncthreads();
 }

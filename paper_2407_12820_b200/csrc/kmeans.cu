@@ -58,9 +58,12 @@ struct KmArgs {
     uint32_t* queue;  // [q][n]
     unsigned long long* stats;
     int counts_smem, sums_smem, cen64_smem, cenf_smem;
+    int vec4;  // point rows are 16-byte aligned
 };
 
 struct Smem {
+    double* gbuf;      // KM_THREADS*4 doubles (exact_running_sum replay buffer)
+    long long* lscr;   // 32 long longs
     uint32_t* counts;
     double* sums;
     double* cen64;   // authoritative fp64 centroids (smem copy or global)
@@ -214,6 +217,27 @@ __device__ int nearest_filtered(const float (&x)[D], const float* __restrict__ c
     return (b2 - e2 > b1 + e1) ? i1 : -1;
 }
 
+// Point row -> registers, 128-bit loads when the row is 16-byte aligned.
+template <int D>
+__device__ __forceinline__ void load_point(const float* xp, float (&x)[D], bool vec4) {
+    if constexpr (D % 4 == 0) {
+        if (vec4) {
+            const float4* x4 = reinterpret_cast<const float4*>(xp);
+#pragma unroll
+            for (int t = 0; t < D / 4; ++t) {
+                float4 v = __ldg(x4 + t);
+                x[4 * t] = v.x;
+                x[4 * t + 1] = v.y;
+                x[4 * t + 2] = v.z;
+                x[4 * t + 3] = v.w;
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < D; ++t) x[t] = __ldg(xp + t);
+}
+
 // ---- block helpers --------------------------------------------------------
 
 __device__ __forceinline__ void block_sync() { __syncthreads(); }
@@ -250,6 +274,98 @@ __device__ double warp_serial_sum(const double* v, int n, double* prefix) {
     return total;
 }
 
+// Exact, block-parallel reproduction of the serial fp64 running sum
+//   S_{-1} = +0.0,  S_i = fl(S_{i-1} + v_i),  v_i >= 0
+// of k-means++ (kmeans.cpp:64-65 total, 70-71 cum); S_i is stored in pre[i]
+// and S_{n-1} returned to every thread.  Processed in groups of
+// KM_THREADS*4 values.  While the running sum S stays inside one binade
+// [2^e, 2^(e+1)) every step is S + round_u(v_i) with u = ulp(S) (S is a
+// multiple of u, so round-to-nearest of S + v_i only rounds v_i), hence the
+// group is exact as S + u * (integer prefix of round_u(v_i)).  A group whose
+// sum leaves the binade, that contains a tie (v_i mod u == u/2, where the
+// even rule would depend on S), or that starts at 0/subnormal S is replayed
+// serially by one thread.  No approximation is ever accepted.
+__device__ double exact_running_sum(const double* v, int n, double* pre, double* gbuf,
+                                    long long* iscr, double* dsh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int E = 4, GROUP = KM_THREADS * E;
+    double S = 0.0;
+    for (int g0 = 0; g0 < n; g0 += GROUP) {
+        const int cnt = min(GROUP, n - g0);
+        double a[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = g0 + tid * E + e;
+            a[e] = i < n ? v[i] : 0.0;
+        }
+        const long long sb = __double_as_longlong(S);
+        const int expo = (int)((sb >> 52) & 0x7ff);
+        bool ok = S > 0.0 && expo > 52 && expo < 2046;  // normal, u normal, no overflow
+        long long dsum = 0;
+        long long d[E];
+        double u = 0.0, inv_u = 0.0, top = 0.0;
+        if (ok) {
+            u = __longlong_as_double((long long)(expo - 52) << 52);
+            inv_u = __longlong_as_double((long long)(2046 - expo + 52) << 52);  // 2^-(expo-1023-52)
+            top = __longlong_as_double((long long)(expo + 1) << 52);             // 2^(e+1)
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const double qv = a[e] * inv_u;  // exact (power-of-two scaling)
+                bool bad = !(qv < 4503599627370496.0);  // 2^52: a crosses anyway
+                const double fl = floor(qv), fr = qv - fl;
+                bad |= fr == 0.5;                        // tie: parity-dependent
+                d[e] = bad ? 0 : (long long)fl + (fr > 0.5 ? 1 : 0);
+                if (bad) ok = false;
+                dsum += d[e];
+            }
+        }
+        // block-wide: all ok? exclusive prefix of dsum
+        long long x = dsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) iscr[warp] = x;
+        const int all_ok = __syncthreads_and(ok);
+        long long before = x - dsum, total = 0;
+        for (int w = 0; w < KM_WARPS; ++w) {
+            long long t = iscr[w];
+            before += w < warp ? t : 0;
+            total += t;
+        }
+        bool fast = all_ok && (S + (double)total * u) < top;
+        if (fast) {
+            long long run = before;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                run += d[e];
+                const int i = g0 + tid * E + e;
+                if (i < n) pre[i] = S + (double)run * u;
+            }
+            S = S + (double)total * u;
+            __syncthreads();  // iscr reuse
+        } else {
+            // serial replay of this group (rare: start, binade crossings, ties)
+#pragma unroll
+            for (int e = 0; e < E; ++e) gbuf[tid * E + e] = a[e];
+            __syncthreads();
+            if (tid == 0) {
+                double s2 = S;
+                for (int j = 0; j < cnt; ++j) {
+                    s2 = __dadd_rn(s2, gbuf[j]);
+                    pre[g0 + j] = s2;
+                }
+                dsh[0] = s2;
+            }
+            __syncthreads();
+            S = dsh[0];
+            __syncthreads();
+        }
+    }
+    return S;
+}
+
 // ---- the per-problem kernel -------------------------------------------------
 
 // D > 0: compile-time subspace dim, point held in registers (fp32 for the
@@ -266,6 +382,10 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
     Smem s;
     {
         unsigned char* p = smem_raw;
+        s.gbuf = reinterpret_cast<double*>(p);
+        p += KM_THREADS * 4 * sizeof(double);
+        s.lscr = reinterpret_cast<long long*>(p);
+        p += 32 * sizeof(long long);
         s.iscratch = reinterpret_cast<int*>(p);
         p += 64 * sizeof(int);
         s.dscratch = reinterpret_cast<double*>(p);
@@ -325,9 +445,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
             float cmax = sh_cmax;
             for (int i = tid; i < n; i += KM_THREADS) {
                 float x[D > 0 ? D : 1];
-                const float* xp = point_ptr(a, q, i);
-#pragma unroll
-                for (int t = 0; t < (D > 0 ? D : 1); ++t) x[t] = __ldg(xp + t);
+                load_point<(D > 0 ? D : 1)>(point_ptr(a, q, i), x, a.vec4);
                 int c = nearest_filtered<(D > 0 ? D : 1)>(x, s.cenf, s.cnorm, cmax, K);
                 if (c >= 0) {
                     out[i] = (uint32_t)c;
@@ -353,10 +471,11 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
             for (int i = tid; i < n; i += KM_THREADS) {
                 uint32_t c;
                 if constexpr (D > 0) {
+                    float xf[D];
+                    load_point<D>(point_ptr(a, q, i), xf, a.vec4);
                     double x[D];
-                    const float* xp = point_ptr(a, q, i);
 #pragma unroll
-                    for (int t = 0; t < D; ++t) x[t] = (double)__ldg(xp + t);
+                    for (int t = 0; t < D; ++t) x[t] = (double)xf[t];
                     c = nearest_r<D>(x, s.cen64, K);
                 } else {
                     c = exact_nearest_g(i);
@@ -418,20 +537,57 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
     };
 
     // ---- update_means (kmeans.cpp:133-147), ordered per (cluster, dim) ----
+    // Warp w owns clusters c = w (mod KM_WARPS) and walks the assignment array
+    // in index order; member rows are fetched 8 at a time before the ordered
+    // fp64 accumulation so the chain does not wait on L2 per member.
     auto update_means = [&](const uint32_t* as) {
         for (long long e = tid; e < KD; e += KM_THREADS) s.sums[e] = 0.0;
         block_sync();
+        constexpr int MB = 8;   // members prefetched per batch
+        constexpr int DPL = 4;  // dims per lane handled by the prefetch path (dim <= 128)
+        const bool pre = dim <= 32 * DPL;
         for (int i0 = 0; i0 < n; i0 += 32) {
             int i = i0 + lane;
             uint32_t c = (i < n) ? as[i] : 0xffffffffu;
             unsigned mine = __ballot_sync(FULL, i < n && (int)(c % KM_WARPS) == warp);
             while (mine) {
-                int l = __ffs(mine) - 1;
-                mine &= mine - 1;
-                uint32_t cc = __shfl_sync(FULL, c, l);
-                const float* xp = point_ptr(a, q, i0 + l);
-                double* srow = s.sums + (long long)cc * dim;
-                for (int t = lane; t < dim; t += 32) srow[t] = __dadd_rn(srow[t], (double)__ldg(xp + t));
+                int ml[MB];
+                int cnt = 0;
+#pragma unroll
+                for (int u = 0; u < MB; ++u) {
+                    ml[u] = mine ? __ffs(mine) - 1 : -1;
+                    if (mine) { mine &= mine - 1; ++cnt; }
+                }
+                if (pre) {
+                    float xv[MB][DPL];
+#pragma unroll
+                    for (int u = 0; u < MB; ++u) {
+                        const float* xp = ml[u] >= 0 ? point_ptr(a, q, i0 + ml[u]) : nullptr;
+#pragma unroll
+                        for (int e = 0; e < DPL; ++e) {
+                            const int t = lane + 32 * e;
+                            xv[u][e] = (xp && t < dim) ? __ldg(xp + t) : 0.f;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < MB; ++u) {
+                        if (u >= cnt) break;
+                        uint32_t cc = __shfl_sync(FULL, c, ml[u]);
+                        double* srow = s.sums + (long long)cc * dim;
+#pragma unroll
+                        for (int e = 0; e < DPL; ++e) {
+                            const int t = lane + 32 * e;
+                            if (t < dim) srow[t] = __dadd_rn(srow[t], (double)xv[u][e]);
+                        }
+                    }
+                } else {
+                    for (int u = 0; u < cnt; ++u) {
+                        uint32_t cc = __shfl_sync(FULL, c, ml[u]);
+                        const float* xp = point_ptr(a, q, i0 + ml[u]);
+                        double* srow = s.sums + (long long)cc * dim;
+                        for (int t = lane; t < dim; t += 32) srow[t] = __dadd_rn(srow[t], (double)__ldg(xp + t));
+                    }
+                }
             }
         }
         block_sync();
@@ -483,10 +639,10 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
             aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64, dim);
         for (int c = 1; c < K; ++c) {
             block_sync();
-            if (warp == 0) {
-                double total = warp_serial_sum(aux0, n, aux1);
-                __syncwarp();
-                if (lane == 0) {
+            {
+                double total = exact_running_sum(aux0, n, aux1, s.gbuf, s.lscr, s.dscratch);
+                __syncthreads();  // aux1 (prefix) visible to thread 0's search
+                if (tid == 0) {
                     int chosen;
                     if (total > 0.0) {
                         double u = (double)(draws[c] >> 11) * 0x1.0p-53;
@@ -517,10 +673,12 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
                 cn = sqrtf(cn) * (1.0f + 9.6e-7f) + 1e-30f;
                 for (int i = tid; i < n; i += KM_THREADS) {
                     const float* xp = point_ptr(a, q, i);
+                    float xr[D > 0 ? D : 1];
+                    load_point<(D > 0 ? D : 1)>(xp, xr, a.vec4);
                     float acc = 0.f;
 #pragma unroll
                     for (int t = 0; t < (D > 0 ? D : 1); ++t) {
-                        float d = __ldg(xp + t) - cf[t];
+                        float d = xr[t] - cf[t];
                         acc = fmaf(d, d, acc);
                     }
                     double old = aux0[i];
@@ -657,7 +815,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     // shared-memory plan (same carve order as the kernel)
     const size_t KD = K * dim;
     const size_t budget = 200 * 1024;
-    size_t smem = 64 * 4 + 64 * 8;
+    size_t smem = KM_THREADS * 4 * 8 + 32 * 8 + 64 * 4 + 64 * 8;
     int counts_smem = 0, sums_smem = 0, cen64_smem = 0, cenf_smem = 0;
     auto take = [&](size_t bytes, int& flag) {
         bytes = round_up(bytes, 16);
@@ -732,6 +890,8 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     a.sums_smem = sums_smem;
     a.cen64_smem = cen64_smem;
     a.cenf_smem = cenf_smem;
+    a.vec4 = ((reinterpret_cast<uintptr_t>(b.points) & 15) == 0) && (b.row_stride % 4 == 0) &&
+             (b.problem_stride % 4 == 0) && (dim % 4 == 0);
 
     bind_device(ctx);
     int P = (int)Q;
