@@ -9,7 +9,7 @@ OBJDIR := build/obj
 LIB := paper_2407_12820_b200/lib/libpqkv.so
 CU := ctx capi kmeans select attend
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(OBJDIR)/api.o
-HDRS := include/pqkv_c.h $(CSRC)/common.cuh $(CSRC)/internal.cuh
+HDRS := include/pqkv_c.h $(CSRC)/common.cuh $(CSRC)/internal.cuh $(CSRC)/select_common.cuh
 
 .PHONY: all lib oracle clean
 all: lib oracle

@@ -63,7 +63,7 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled through NVML every 100 ms while the
+    """SM clocks + throttle reasons sampled through NVML every 10 ms while the
     timed region runs (the recipe's nvidia-smi clocks line, without pipes)."""
 
     def __init__(self, device):
@@ -98,7 +98,7 @@ class ClockSampler:
                 self.rows.append((mhz, reasons))
             except Exception:
                 pass
-            self.stop.wait(0.1)
+            self.stop.wait(0.01)
 
     def __exit__(self, *a):
         self.stop.set()
@@ -212,8 +212,8 @@ def cpu_baseline_leg(layer0, cen, codes, torch):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -28,6 +28,7 @@
 #include <cmath>
 
 #include "internal.cuh"
+#include "select_common.cuh"
 
 namespace pqkv_dev {
 namespace {
@@ -38,7 +39,7 @@ constexpr int DH = 128;
 constexpr int LPR = 16;            // lanes per K/V row
 constexpr int VPL = DH / 4 / LPR;  // float4 per lane per row (2)
 
-enum { SRC_ROWS = 0, SRC_BITMAP = 1, SRC_TUPLE = 2 };
+enum { SRC_ROWS = 0, SRC_BITMAP = 1, SRC_TUPLE = 2, SRC_PAIRS = 3 };
 
 struct AtArgs {
     const float* queries;  // [P][G][128]
@@ -58,6 +59,11 @@ struct AtArgs {
     int C;
     const uint8_t* cls;  // [P][C*C]
     const int* cut;      // [P][2]
+    // SRC_PAIRS (pair select fused into the prologue)
+    const float* centroids;       // [P][2][C][64]
+    const uint32_t* thist;        // [P][C*C]
+    const uint16_t* chist;        // [P][n_tchunks][C*C]
+    int n_tchunks, k, region;     // region: bytes of the aliased scratch area
     // SRC_ROWS
     const int64_t* rows;
     int t;
@@ -126,13 +132,11 @@ __device__ int expand_words(const uint32_t* words, int nwords, int token_base, i
 // Warp segments never straddle a PQKV_TUPLE_CHUNK chunk (chunk % (8*32) and
 // PQKV_TUPLE_CHUNK % segment hold by construction).
 __device__ void classify_words(const AtArgs& a, int p, int r0, int r1, uint32_t* words,
-                               const uint8_t* cls, uint32_t* wtot) {
+                               const uint8_t* cls, uint32_t* wtot, int cstar, uint32_t take) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int seg = a.chunk / AT_WARPS;  // tokens per warp (multiple of 32)
     const int s0 = r0 + warp * seg, s1 = min(r1, s0 + seg);
     const int tc = s0 / PQKV_TUPLE_CHUNK;
-    const int cstar = a.cut[2 * p];
-    const uint32_t take = (uint32_t)a.cut[2 * p + 1];
     const uint32_t* cd = reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride);
     const bool boundary = tc == cstar && s0 < s1;
     // pass 1 (boundary chunk only): equal-pair counts per warp, in id order
@@ -201,8 +205,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     const int half = lane >> 4, hl = lane & 15;
     const int nwords = a.chunk / 32;
     int* rows = reinterpret_cast<int*>(smem_raw);
-    const int rows_cap = a.src == SRC_ROWS ? a.chunk : a.chunk + a.n_init + a.n_local;
-    uint32_t* words = reinterpret_cast<uint32_t*>(rows + rows_cap);
+    uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + a.region);
     uint8_t* cls = reinterpret_cast<uint8_t*>(words + nwords);
 
     // ---- 1. this CTA's row list (ascending token ids) ----
@@ -219,6 +222,28 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         const int nw = (max(0, r1 - r0) + 31) / 32;
         if (a.src == SRC_BITMAP) {
             for (int w = tid; w < nw; w += AT_THREADS) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
+        } else if (a.src == SRC_PAIRS) {
+            // per-head pair-level top-k, recomputed by every CTA of the head
+            // (a few microseconds of latency instead of a separate launch)
+            const int C = a.C, C2 = C * C;
+            unsigned char* z = smem_raw;  // aliases rows[]: free until expansion
+            double* lut = reinterpret_cast<double*>(z);
+            uint32_t* key = reinterpret_cast<uint32_t*>(lut + 2 * C);
+            uint32_t* hist = key + C2;
+            uint32_t* eql = hist + NB;
+            uint32_t* ceq = eql + C2;
+            uint32_t* wsum = ceq + a.n_tchunks;
+            uint32_t* sh = wsum + 32;
+            pair_select<AT_THREADS>(a.queries + (long long)p * G * DH, G, DH,
+                                    a.centroids + (long long)p * 2 * C * (DH / 2), C,
+                                    a.thist + (long long)p * C2, a.chist + (long long)p * a.n_tchunks * C2,
+                                    a.n_tchunks, a.k, lut, key, hist, eql, ceq, wsum, sh, cls, nullptr);
+            const int cstar = (int)sh[3];
+            const uint32_t take = sh[4];
+            __syncthreads();  // scratch is rows[] again from here on
+            if (c == 0)
+                for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
+            classify_words(a, p, r0, r1, words, cls, wtot, cstar, take);
         } else {
             const int C2 = a.C * a.C;
             if ((C2 & 3) == 0) {
@@ -228,7 +253,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                 for (int e = tid; e < C2; e += AT_THREADS) cls[e] = a.cls[(long long)p * C2 + e];
             }
             __syncthreads();
-            classify_words(a, p, r0, r1, words, cls, wtot);
+            classify_words(a, p, r0, r1, words, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
         }
         __syncthreads();
         nrows += expand_words(words, nw, a.n_init + r0, rows, nrows, wtot);
@@ -545,11 +570,22 @@ static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
     return (int)(q * PQKV_TUPLE_CHUNK);
 }
 
-static size_t attend_smem(const AtArgs& a, int G) {
+static size_t pair_scratch_bytes(int C, int n_tchunks) {
+    return (size_t)16 * C + 4 * ((size_t)2 * C * C + NB + n_tchunks + 40);
+}
+
+// Shared memory: region (rows[] / merge partials / pair-select scratch)
+// followed by words[] and the pair classes.
+static size_t attend_smem(AtArgs& a, int G) {
     size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.chunk + a.n_init + a.n_local;
-    size_t bytes = rows_cap * 4 + (size_t)a.chunk / 32 * 4 + (a.src == SRC_TUPLE ? (size_t)a.C * a.C : 0);
     size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
-    return round_up(std::max(bytes, merge), 16);
+    size_t region = std::max(rows_cap * 4, merge);
+    if (a.src == SRC_PAIRS) region = std::max(region, pair_scratch_bytes(a.C, a.n_tchunks));
+    region = round_up(region, 16);
+    a.region = (int)region;
+    size_t tail = (size_t)a.chunk / 32 * 4 +
+                  ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
+    return round_up(region + tail, 16);
 }
 
 static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cudaStream_t st) {
@@ -612,9 +648,13 @@ bool decode_fast_path(const pqkv_layer& L, size_t G) {
     return L.d_h == DH && (G == 1 || G == 2 || G == 4) && L.kv_head_stride % 4 == 0;
 }
 
+bool decode_pairs_fused(const pqkv_layer& L, size_t G) {
+    return decode_fast_path(L, G) && L.m == 2 && L.b <= 6 && L.tuple_hist && L.tuple_chunk_hist;
+}
+
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
-                          cudaStream_t st) {
+                          cudaStream_t st, size_t k_pairs) {
     bind_device(ctx);
     const size_t s_mid = L.total - L.n_init - L.n_local;
     AtArgs a{};
@@ -622,7 +662,7 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     a.keys = L.keys;
     a.values = L.values;
     a.kv_head_stride = (long long)L.kv_head_stride;
-    a.src = cls ? SRC_TUPLE : SRC_BITMAP;
+    a.src = k_pairs ? SRC_PAIRS : (cls ? SRC_TUPLE : SRC_BITMAP);
     a.n_init = (int)L.n_init;
     a.n_local = (int)L.n_local;
     a.total = (int)L.total;
@@ -636,6 +676,11 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     a.C = 1 << L.b;
     a.cls = cls;
     a.cut = cut;
+    a.centroids = L.centroids;
+    a.thist = L.tuple_hist;
+    a.chist = L.tuple_chunk_hist;
+    a.n_tchunks = (int)ceil_div(s_mid, PQKV_TUPLE_CHUNK);
+    a.k = (int)k_pairs;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
     a.out = out;
     launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);

@@ -248,6 +248,12 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         src.centroids = L->centroids;
         src.codes = L->codes;
         src.codes_head_stride = L->codes_head_stride;
+        if (tup && fast && !d_ids && k > 0 && decode_pairs_fused(*L, g)) {
+            // one launch: every attention CTA selects its head's pairs, then
+            // classifies its own codes and gathers
+            launch_decode_attend(ctx, *L, d_queries, g, nullptr, nullptr, nullptr, d_out, st, k);
+            return;
+        }
         if (tup && fast && !d_ids && k > 0) {
             // pair-level select -> attention classifies its own codes
             char* ws = static_cast<char*>(decode_workspace(ctx, round_up(P * C * C, 256) + P * 2 * sizeof(int)));
@@ -316,7 +322,7 @@ int pqkv_decode_launches(const pqkv_layer* L, size_t g, int with_ids) {
     if (!L) return 0;
     bool fast = L->d_h == 128 && (g == 1 || g == 2 || g == 4) && L->kv_head_stride % 4 == 0;
     const bool tup = L->m == 2 && L->b <= 7 && L->tuple_hist && L->tuple_chunk_hist;
-    if (tup && fast && !with_ids) return 2;  // pair select + attention (classifies codes, fused combine)
+    if (tup && fast && !with_ids) return L->b <= 6 ? 1 : 2;  // [pair select +] attention
     int n = tup ? 2 /*pair select + bitmap*/ : 1 /*cluster select*/;
     n += with_ids ? 1 : 0 /*sort*/;
     n += fast ? 1 /*attend with fused combine*/ : 3 /*rows + scores + softmax*/;

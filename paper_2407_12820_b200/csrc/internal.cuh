@@ -144,9 +144,12 @@ void launch_attend_rows(pqkv_ctx* ctx, const float* queries, size_t n_heads, siz
 // Fused fast path (d_h == 128, g in {1,2,4}): selection from a bitmap or from
 // the code-pair classes (cls, cut) of launch_tuple_select.
 bool decode_fast_path(const pqkv_layer& L, size_t g);
+// k_pairs > 0: the per-head pair select runs in the attention prologue
+// (decode_pairs_fused geometry); cls/cut/bitmap are then unused.
+bool decode_pairs_fused(const pqkv_layer& L, size_t g);
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t g,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
-                          cudaStream_t stream);
+                          cudaStream_t stream, size_t k_pairs = 0);
 // Pair-level select only (writes cls [rows][C*C], cut [rows][2]).
 void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
                          const uint16_t* chist, size_t rows, size_t n, size_t k, uint8_t* cls, int* cut,

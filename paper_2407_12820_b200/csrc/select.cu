@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "select_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -39,7 +40,6 @@ namespace {
 constexpr int SEL_CL = 8;         // CTAs per head (portable cluster size)
 constexpr int SEL_THREADS = 512;  // 16 warps
 constexpr int SEL_WARPS = SEL_THREADS / 32;
-constexpr int NB = 2048;          // bins of the two 11-bit digit passes
 
 struct SelArgs {
     // ADC source
@@ -63,44 +63,6 @@ struct SelArgs {
     int* status;  // [rows]
 };
 
-// Builds T[j][c] (pq.cpp:113-126, rows accumulated as in pq.cpp:157-159).
-// One thread per (j, c); the t-chain stays sequential (reference order) while
-// the centroid row is prefetched 16 floats at a time so the chain is not
-// serialised on L2 latency.
-__device__ void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
-                          int C) {
-    const int d_m = d_h / m;
-    for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
-        const int j = e / C;
-        const float* cc = cen + (long long)e * d_m;
-        double t = 0.0;
-        for (int r0 = 0; r0 < g; r0 += 4) {
-            const int rn = min(4, g - r0);
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int t0 = 0; t0 < d_m; t0 += 16) {
-                float cv[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) cv[u] = (t0 + u < d_m) ? __ldg(cc + t0 + u) : 0.0f;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    if (r >= rn) break;
-                    const float* qq = q + (long long)(r0 + r) * d_h + j * d_m + t0;
-                    float qv[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) qv[u] = (t0 + u < d_m) ? __ldg(qq + u) : 0.0f;
-#pragma unroll
-                    for (int u = 0; u < 16; ++u)
-                        if (t0 + u < d_m) acc[r] = __fma_rn((double)qv[u], (double)cv[u], acc[r]);
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-                if (r < rn) t = __dadd_rn(t, acc[r]);
-        }
-        lut[e] = t;
-    }
-}
-
 __device__ __forceinline__ uint32_t adc_key(const double* lut, const uint16_t* code, int m, int C) {
     double acc = 0.0;
     for (int j = 0; j < m; ++j) acc = __dadd_rn(acc, lut[j * C + code[j]]);
@@ -112,59 +74,6 @@ __device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin) {
     unsigned peers = __match_any_sync(FULL, bin);
     int leader = __ffs(peers) - 1;
     if ((threadIdx.x & 31) == leader && bin != 0xffffffffu) atomicAdd(&hist[bin], __popc(peers));
-}
-
-// Block-wide exclusive scan (NT threads) of one u32 per thread.
-template <int NT = SEL_THREADS>
-__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* wsum, uint32_t* total) {
-    constexpr int NW = NT / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(FULL, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = lane < NW ? wsum[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(FULL, w, o);
-            if (lane >= o) w += y;
-        }
-        if (lane < NW) wsum[lane] = w;  // inclusive
-    }
-    __syncthreads();
-    uint32_t before = (warp ? wsum[warp - 1] : 0) + x - v;
-    if (total) *total = wsum[NW - 1];
-    __syncthreads();
-    return before;
-}
-
-// Finds the digit holding the k_rem-th largest element of hist[0..nb).
-// Returns (digit, count strictly above it) via out[0], out[1].
-template <int NT = SEL_THREADS>
-__device__ void find_digit(const uint32_t* hist, int nb, uint32_t k_rem, uint32_t* wsum,
-                           uint32_t* out) {
-    const int per = nb / NT;  // bins per thread (>= 1)
-    const int hi = nb - per * (int)threadIdx.x;  // this thread owns [hi-per, hi), from the top
-    uint32_t local = 0;
-    for (int b = hi - 1; b >= hi - per; --b) local += hist[b];
-    uint32_t above = block_excl_scan<NT>(local, wsum, nullptr);
-    if (above < k_rem && k_rem <= above + local) {
-        uint32_t acc = above;
-        for (int b = hi - 1; b >= hi - per; --b) {
-            if (k_rem <= acc + hist[b]) {
-                out[0] = (uint32_t)b;
-                out[1] = acc;
-                break;
-            }
-            acc += hist[b];
-        }
-    }
-    __syncthreads();
 }
 
 __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelArgs a) {
@@ -250,14 +159,14 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelArgs a) {
             uint32_t local = 0;
             for (int b = tid; b < NB; b += SEL_THREADS) local += tot[b];
             uint32_t total;
-            block_excl_scan(local, wsum, &total);
+            block_excl_scan<SEL_THREADS>(local, wsum, &total);
             if (total < k_rem) {
                 if (tid == 0 && rank == 0) a.status[row] = 1;
                 cluster.sync();
                 return;  // uniform across the cluster
             }
         }
-        find_digit(tot, nbins[p], k_rem, wsum, sh);
+        find_digit<SEL_THREADS>(tot, nbins[p], k_rem, wsum, sh);
         uint32_t digit = sh[0];
         k_rem -= sh[1];
         prefix = (prefix << (p == 0 ? 11 : (p == 1 ? 11 : 10))) | digit;
@@ -273,8 +182,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelArgs a) {
         neq += key == kstar;
     }
     uint32_t cta_gt, cta_eq;
-    block_excl_scan(ngt, wsum, &cta_gt);
-    block_excl_scan(neq, wsum, &cta_eq);
+    block_excl_scan<SEL_THREADS>(ngt, wsum, &cta_gt);
+    block_excl_scan<SEL_THREADS>(neq, wsum, &cta_eq);
     if (tid == 0) { pub[0] = cta_gt; pub[1] = cta_eq; }
     cluster.sync();
     // how many equal keys this CTA takes, and where its selections start
@@ -504,77 +413,21 @@ __global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a)
     const int p = blockIdx.x, tid = threadIdx.x, C = a.C, C2 = C * C;
     double* lut = reinterpret_cast<double*>(smem);                 // [2C]
     uint32_t* key = reinterpret_cast<uint32_t*>(lut + 2 * C);      // [C2]
-    uint32_t* w = key + C2;                                        // [C2]
-    uint32_t* hist = w + C2;                                       // [2048]
+    uint32_t* hist = key + C2;                                     // [2048]
     uint32_t* ceq = hist + NB;                                     // [n_chunks]
     uint32_t* eql = ceq + a.n_chunks;                              // [C2] equal pairs
     uint32_t* wsum = eql + C2;                                     // [32]
     uint32_t* sh = wsum + 32;                                      // [8]
-
-    build_lut(lut, a.queries + (long long)p * a.g * a.d_h,
-              a.centroids + (long long)p * 2 * C * (a.d_h / 2), a.g, a.d_h, 2, C);
-    for (int c = tid; c < a.n_chunks; c += TUP_THREADS) ceq[c] = 0;
-    if (tid == 0) sh[2] = 0;
-    __syncthreads();
-    const uint32_t* th = a.thist + (long long)p * C2;
-    for (int t = tid; t < C2; t += TUP_THREADS) {
-        double acc = __dadd_rn(0.0, lut[t / C]);
-        acc = __dadd_rn(acc, lut[C + t % C]);
-        key[t] = score_key((float)acc);
-        w[t] = th[t];
-    }
-    uint32_t k_rem = (uint32_t)a.k, prefix = 0;
-    const int shifts[3] = {21, 10, 0};
-    const int nbins[3] = {2048, 2048, 1024};
-    for (int pass = 0; pass < 3; ++pass) {
-        for (int b = tid; b < NB; b += TUP_THREADS) hist[b] = 0;
-        __syncthreads();
-        const uint32_t mask = (uint32_t)(nbins[pass] - 1);
-        for (int t = tid; t < C2; t += TUP_THREADS) {
-            uint32_t kk = key[t], ww = w[t];
-            if (!ww) continue;
-            if (pass > 0 && (kk >> shifts[pass - 1]) != prefix) continue;
-            atomicAdd(&hist[(kk >> shifts[pass]) & mask], ww);
-        }
-        __syncthreads();
-        find_digit<TUP_THREADS>(hist, nbins[pass], k_rem, wsum, sh);
-        k_rem -= sh[1];
-        prefix = (prefix << (pass == 2 ? 10 : 11)) | sh[0];
-        __syncthreads();
-    }
-    const uint32_t kstar = prefix;
-    // classify pairs, collect the equal ones
     uint8_t* cls = a.cls + (long long)p * C2;
-    for (int t = tid; t < C2; t += TUP_THREADS) {
-        uint32_t kk = key[t];
-        uint8_t c = kk > kstar ? 1 : (kk == kstar ? 2 : 0);
-        cls[t] = c;
-        if (c == 2 && w[t]) eql[atomicAdd(&sh[2], 1u)] = (uint32_t)t;
-        if (a.tkey) a.tkey[(long long)p * C2 + t] = kk;
-    }
-    __syncthreads();
-    const int neq = (int)sh[2];
     const uint16_t* ch = a.chist + (long long)p * a.n_chunks * C2;
-    for (int e = tid; e < neq * a.n_chunks; e += TUP_THREADS) {
-        int c = e / neq, t = (int)eql[e % neq];
-        uint32_t v = ch[(long long)c * C2 + t];
-        if (v) atomicAdd(&ceq[c], v);
+    pair_select<TUP_THREADS>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
+                             a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
+                             ch, a.n_chunks, a.k, lut, key, hist, eql, ceq, wsum, sh, cls,
+                             a.tkey ? a.tkey + (long long)p * C2 : nullptr);
+    if (tid == 0) {
+        a.cut[2 * p] = (int)sh[3];
+        a.cut[2 * p + 1] = (int)sh[4];
     }
-    __syncthreads();
-    if (tid == 0) {  // chunk holding the k_rem-th equal token in id order
-        uint32_t run = 0;
-        int cstar = a.n_chunks - 1;
-        uint32_t take = 0;
-        for (int c = 0; c < a.n_chunks; ++c) {
-            if (run + ceq[c] >= k_rem) { cstar = c; take = k_rem - run; break; }
-            run += ceq[c];
-        }
-        a.cut[2 * p] = cstar;
-        a.cut[2 * p + 1] = (int)take;
-        sh[3] = (uint32_t)cstar;
-        sh[4] = take;
-    }
-    __syncthreads();
     if (a.sel_before) {  // selected rows per chunk -> exclusive prefix (ordered ids)
         const int cstar = (int)sh[3];
         const uint32_t take = sh[4];
@@ -841,7 +694,7 @@ void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
     a.tkey = tkey;
     a.cut = cut;
     a.sel_before = sel_before;
-    size_t smem = 2 * C * 8 + (3 * C2 + NB + n_chunks + 40) * 4;
+    size_t smem = 2 * C * 8 + (2 * C2 + NB + n_chunks + 40) * 4;
     if (smem > 220 * 1024) fail(PQKV_EINVAL, "tuple select: table too large");
     PQKV_CUDA(cudaFuncSetAttribute(tuple_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tuple_select_kernel<<<(unsigned)rows, TUP_THREADS, smem, st>>>(a);
