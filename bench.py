@@ -22,7 +22,6 @@ import json
 import math
 import os
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -63,57 +62,66 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled through NVML every 10 ms while the
-    timed region runs (the recipe's nvidia-smi clocks line, without pipes)."""
+    """SM clocks + throttle reasons sampled every 10 ms by a separate process
+    (tools/clock_sampler.py, NVML) while the timed region runs; only samples
+    inside [enter, exit] are kept."""
 
     def __init__(self, device):
         self.device = device
-        self.rows = []
-        self.stop = threading.Event()
+        self.proc = None
+        self.out = None
 
-    def __enter__(self):
+    def start(self):
+        import subprocess
+        import tempfile
+
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".jsonl", delete=False)
         try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.thread = threading.Thread(target=self._run, daemon=True)
-            self.thread.start()
-        except Exception as e:  # no NVML: report unsampled
-            self.nv = None
-            self.err = str(e)
+            self.proc = subprocess.Popen([sys.executable, os.path.join(ROOT, "tools", "clock_sampler.py"),
+                                          str(self.device), "0.01"], stdout=self.out,
+                                         stderr=subprocess.DEVNULL)
+            time.sleep(1.0)  # sampler up before the timed region
+        except Exception:
+            self.proc = None
         return self
 
-    def _run(self):
-        nv = self.nv
-        while not self.stop.is_set():
-            try:
-                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                try:
-                    reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                except AttributeError:
-                    reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                self.rows.append((mhz, reasons))
-            except Exception:
-                pass
-            self.stop.wait(0.01)
+    def __enter__(self):
+        self.t0 = time.time()
+        return self
 
     def __exit__(self, *a):
-        self.stop.set()
-        if self.nv:
-            self.thread.join(timeout=2)
+        self.t1 = time.time()
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
 
     def summary(self):
-        if not self.nv or not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        rows, max_mhz = [], None
+        if self.out:
+            self.out.flush()
+            with open(self.out.name) as f:
+                for line in f:
+                    try:
+                        v = json.loads(line)
+                    except Exception:
+                        continue
+                    if isinstance(v, dict):
+                        max_mhz = v.get("max_mhz", max_mhz)
+                    elif self.t0 - 0.005 <= v[0] <= self.t1 + 0.005:
+                        rows.append(v)
+            os.unlink(self.out.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": max_mhz, "reasons": ["unsampled"], "samples": 0}
         bits = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                 0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
-        sm = sorted(r[0] for r in self.rows)
-        reasons = sorted({name for _, rs in self.rows for bit, name in bits.items() if rs & bit})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = sorted(r[1] for r in rows)
+        reasons = sorted({name for r in rows for bit, name in bits.items() if r[2] & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max_mhz, "reasons": reasons, "samples": len(rows)}
 
 
 def make_layer_inputs(torch, seed, device):
@@ -282,7 +290,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    clk = ClockSampler(local).start()
+    with clk:
         ev0.record(stream)
         for i in range(args.warmup, n_total):
             step(i)
@@ -378,8 +387,8 @@ def main():
                   "context_tokens_per_s": S_MID / build_layer_s, "layers": N_LAYERS,
                   "fp64_rechecked_points": rech, "points": tot},
     }
-    with_clk = clk.summary()
-    line["clocks"] = with_clk
+    clk.stop()
+    line["clocks"] = clk.summary()
     if rank == 0 and not args.no_cpu_baseline:
         dec, bld = cpu_baseline_leg(keep0[0], keep0[1], keep0[2], torch)
         line["cpu_baseline"] = dec

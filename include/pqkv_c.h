@@ -84,6 +84,11 @@ PQKV_API int pqkv_ctx_set_assign_mode(pqkv_ctx* ctx, int mode);
 /* Counters of the last build on this context: fp64 re-checked points. */
 PQKV_API int pqkv_ctx_last_build_stats(pqkv_ctx* ctx, uint64_t* rechecked_points, uint64_t* total_points);
 
+/* SM cycles per build phase of problem 0 of the last build (profiling):
+ * [0] k-means++ running sums + search, [1] k-means++ distances,
+ * [2] assign + repair, [4] ordered update, [5] other. */
+PQKV_API int pqkv_ctx_last_build_profile(pqkv_ctx* ctx, uint64_t cycles[8]);
+
 /* ---- device memory helpers (for FFI hosts without a CUDA runtime) ----- */
 PQKV_API int pqkv_device_alloc(pqkv_ctx* ctx, size_t bytes, void** out);
 PQKV_API int pqkv_device_free(pqkv_ctx* ctx, void* ptr);

@@ -45,6 +45,7 @@ _SIGS = {
     "pqkv_ctx_destroy": (_i, [_vp]),
     "pqkv_ctx_set_assign_mode": (_i, [_vp, _i]),
     "pqkv_ctx_last_build_stats": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
+    "pqkv_ctx_last_build_profile": (_i, [_vp, C.POINTER(_u64)]),
     "pqkv_device_alloc": (_i, [_vp, _sz, C.POINTER(_vp)]),
     "pqkv_device_free": (_i, [_vp, _vp]),
     "pqkv_copy": (_i, [_vp, _vp, _vp, _sz, _i]),
@@ -143,6 +144,13 @@ class Context:
         a, b = _u64(0), _u64(0)
         _check(lib().pqkv_ctx_last_build_stats(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def last_build_profile(self):
+        """SM cycles per phase of problem 0 of the last build."""
+        arr = (_u64 * 8)()
+        _check(lib().pqkv_ctx_last_build_profile(self.h, arr))
+        names = ["seed_chain", "seed_dist", "assign", "-", "update", "other"]
+        return {n: int(arr[i]) for i, n in enumerate(names) if n != "-"}
 
     # ---- (A) build ---------------------------------------------------------
     def kmeans_fit(self, points, k: int, max_iter: int, seeds, inertia: bool = False):

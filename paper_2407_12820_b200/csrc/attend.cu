@@ -228,16 +228,16 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             const int C = a.C, C2 = C * C;
             unsigned char* z = smem_raw;  // aliases rows[]: free until expansion
             double* lut = reinterpret_cast<double*>(z);
-            uint32_t* key = reinterpret_cast<uint32_t*>(lut + 2 * C);
-            uint32_t* hist = key + C2;
-            uint32_t* eql = hist + NB;
+            uint32_t* hist = reinterpret_cast<uint32_t*>(lut + 2 * C);
+            uint32_t* cnt = hist + NB;
+            uint32_t* eql = cnt + NB;
             uint32_t* ceq = eql + C2;
             uint32_t* wsum = ceq + a.n_tchunks;
-            uint32_t* sh = wsum + 32;
-            pair_select<AT_THREADS>(a.queries + (long long)p * G * DH, G, DH,
+            uint32_t* sh = wsum + 64;
+            pair_select<AT_THREADS, 16>(a.queries + (long long)p * G * DH, G, DH,
                                     a.centroids + (long long)p * 2 * C * (DH / 2), C,
                                     a.thist + (long long)p * C2, a.chist + (long long)p * a.n_tchunks * C2,
-                                    a.n_tchunks, a.k, lut, key, hist, eql, ceq, wsum, sh, cls, nullptr);
+                                    a.n_tchunks, a.k, lut, nullptr, hist, cnt, eql, ceq, wsum, sh, cls, nullptr);
             const int cstar = (int)sh[3];
             const uint32_t take = sh[4];
             __syncthreads();  // scratch is rows[] again from here on
@@ -571,7 +571,7 @@ static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
 }
 
 static size_t pair_scratch_bytes(int C, int n_tchunks) {
-    return (size_t)16 * C + 4 * ((size_t)2 * C * C + NB + n_tchunks + 40);
+    return (size_t)16 * C + 4 * ((size_t)C * C + 2 * NB + n_tchunks + 72);
 }
 
 // Shared memory: region (rows[] / merge partials / pair-select scratch)

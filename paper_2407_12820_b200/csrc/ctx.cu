@@ -169,6 +169,13 @@ int pqkv_stream_sync(pqkv_ctx* ctx, void* stream) {
     });
 }
 
+int pqkv_ctx_last_build_profile(pqkv_ctx* ctx, uint64_t cycles[8]) {
+    return guard([&] {
+        if (!ctx || !cycles) fail(PQKV_EINVAL, "NULL argument");
+        for (int i = 0; i < 8; ++i) cycles[i] = ctx->last_phase_cycles[i];
+    });
+}
+
 // PqConfig::create (pq.cpp:13-25): same rejection rules and messages.
 int pqkv_pq_config(size_t m, size_t b, size_t d_h, size_t* d_m, size_t* n_clusters) {
     return guard([&] {

@@ -29,6 +29,7 @@ struct pqkv_ctx {
     // Device counters written by the build kernels (rechecked, total).
     unsigned long long* d_stats = nullptr;
     uint64_t last_rechecked = 0, last_total = 0;
+    unsigned long long last_phase_cycles[8] = {};  // problem 0 of the last build
 };
 
 namespace pqkv_dev {

@@ -59,6 +59,7 @@ struct KmArgs {
     unsigned long long* stats;
     int counts_smem, sums_smem, cen64_smem, cenf_smem;
     int vec4;  // point rows are 16-byte aligned
+    unsigned long long* timers;  // [q][8] per-phase SM cycles (thread 0's view)
 };
 
 struct Smem {
@@ -408,6 +409,16 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
     uint32_t* queue = a.queue + (long long)q * n;
     __shared__ int sh_int[4];
     __shared__ float sh_cmax;
+    // phase timers: 0 seed chain, 1 seed distances, 2 assign+repair, 3 -, 4 update, 5 other
+    unsigned long long t_acc[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long t_last = clock64();
+    auto tick = [&](int ph) {
+        if (tid == 0) {
+            unsigned long long now = clock64();
+            t_acc[ph] += now - t_last;
+            t_last = now;
+        }
+    };
 
     // refresh the f32 copy + norms after the fp64 centroids change
     auto refresh_f32 = [&]() {
@@ -639,6 +650,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
             aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64, dim);
         for (int c = 1; c < K; ++c) {
             block_sync();
+            tick(1);
             {
                 double total = exact_running_sum(aux0, n, aux1, s.gbuf, s.lscr, s.dscratch);
                 __syncthreads();  // aux1 (prefix) visible to thread 0's search
@@ -661,6 +673,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
                 }
             }
             block_sync();
+            tick(0);
             set_centroid_from_point(c, sh_int[3]);
             block_sync();
             const double* cc = s.cen64 + (long long)c * dim;
@@ -694,16 +707,20 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
             }
         }
         block_sync();
+        tick(1);
     }
     refresh_f32();
+    tick(5);
 
     // =====================================================================
     // 2. Lloyd iterations (kmeans.cpp:174-183)
     // =====================================================================
     assign_with_repair(asg);
+    tick(2);
     int iters = 0;
     for (int iter = 1; iter <= T; ++iter) {
         update_means(asg);
+        tick(4);
         if (a.inertia) {
             for (int i = tid; i < n; i += KM_THREADS)
                 aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64 + (long long)asg[i] * dim, dim);
@@ -716,7 +733,9 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
         }
         iters = iter;
         refresh_f32();
+        tick(5);
         assign_with_repair(nxt);
+        tick(2);
         int changed = 0;
         for (int i = tid; i < n; i += KM_THREADS) changed |= (nxt[i] != asg[i]);
         if (!__syncthreads_or(changed)) break;
@@ -737,6 +756,9 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
         for (int i = tid; i < n; i += KM_THREADS) cd[(long long)i * a.m_sub] = (uint16_t)asg[i];
     }
     if (a.iterations && tid == 0) a.iterations[q] = (uint32_t)iters;
+    tick(5);
+    if (tid == 0 && a.timers)
+        for (int ph = 0; ph < 6; ++ph) a.timers[(long long)q * 8 + ph] = t_acc[ph];
 }
 
 // ---- pq_encode_one (pq.cpp:74-99): one CTA per head, one warp per subspace
@@ -847,6 +869,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     size_t h_sums = sc.plan<double>(sums_smem ? 1 : Q * KD);
     size_t h_cnt = sc.plan<uint32_t>(counts_smem ? 1 : Q * K);
     size_t h_q = sc.plan<uint32_t>(Q * n);
+    size_t h_tm = sc.plan<unsigned long long>(Q * 8);
     sc.commit();
 
     // mt19937_64 draws (rng.hpp:13-33): k-means++ consumes exactly K raw
@@ -886,6 +909,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     a.gcounts = sc.get<uint32_t>(h_cnt);
     a.queue = sc.get<uint32_t>(h_q);
     a.stats = ctx->d_stats;
+    a.timers = sc.get<unsigned long long>(h_tm);
     a.counts_smem = counts_smem;
     a.sums_smem = sums_smem;
     a.cen64_smem = cen64_smem;
@@ -919,6 +943,8 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     }
     unsigned long long stats[2] = {0, 0};
     PQKV_CUDA(cudaMemcpyAsync(stats, ctx->d_stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
+    PQKV_CUDA(cudaMemcpyAsync(ctx->last_phase_cycles, a.timers, 8 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
     PQKV_CUDA(cudaStreamSynchronize(st));
     ctx->last_rechecked = stats[0];
     ctx->last_total = stats[1];

@@ -412,17 +412,17 @@ __global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a)
     extern __shared__ __align__(16) unsigned char smem[];
     const int p = blockIdx.x, tid = threadIdx.x, C = a.C, C2 = C * C;
     double* lut = reinterpret_cast<double*>(smem);                 // [2C]
-    uint32_t* key = reinterpret_cast<uint32_t*>(lut + 2 * C);      // [C2]
-    uint32_t* hist = key + C2;                                     // [2048]
-    uint32_t* ceq = hist + NB;                                     // [n_chunks]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(lut + 2 * C);     // [NB]
+    uint32_t* cnt = hist + NB;                                     // [NB]
+    uint32_t* ceq = cnt + NB;                                      // [n_chunks]
     uint32_t* eql = ceq + a.n_chunks;                              // [C2] equal pairs
-    uint32_t* wsum = eql + C2;                                     // [32]
-    uint32_t* sh = wsum + 32;                                      // [8]
+    uint32_t* wsum = eql + C2;                                     // [64]
+    uint32_t* sh = wsum + 64;                                      // [8]
     uint8_t* cls = a.cls + (long long)p * C2;
     const uint16_t* ch = a.chist + (long long)p * a.n_chunks * C2;
-    pair_select<TUP_THREADS>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
+    pair_select<TUP_THREADS, 16>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
                              a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
-                             ch, a.n_chunks, a.k, lut, key, hist, eql, ceq, wsum, sh, cls,
+                             ch, a.n_chunks, a.k, lut, nullptr, hist, cnt, eql, ceq, wsum, sh, cls,
                              a.tkey ? a.tkey + (long long)p * C2 : nullptr);
     if (tid == 0) {
         a.cut[2 * p] = (int)sh[3];
@@ -694,7 +694,7 @@ void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
     a.tkey = tkey;
     a.cut = cut;
     a.sel_before = sel_before;
-    size_t smem = 2 * C * 8 + (2 * C2 + NB + n_chunks + 40) * 4;
+    size_t smem = 2 * C * 8 + (C2 + 2 * NB + n_chunks + 72) * 4;
     if (smem > 220 * 1024) fail(PQKV_EINVAL, "tuple select: table too large");
     PQKV_CUDA(cudaFuncSetAttribute(tuple_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tuple_select_kernel<<<(unsigned)rows, TUP_THREADS, smem, st>>>(a);

@@ -12,9 +12,46 @@ constexpr int NB = 2048;  // bins of the two 11-bit radix digits
 // One thread per (j, c); the t-chain stays sequential (reference order) while
 // the centroid row is prefetched 16 floats at a time so the chain is not
 // serialised on L2 latency.
+template <int DM>
+__device__ __forceinline__ void lut_entry_vec(double* lut, const float* q, const float* cen, int g, int d_h,
+                                              int e, int j) {
+    // centroid row and query slice as 128-bit loads, all issued before the
+    // sequential fp64 chain (t ascending, products exact => DFMA == mul+add)
+    const float4* cc4 = reinterpret_cast<const float4*>(cen + (long long)e * DM);
+    float4 cv[DM / 4];
+#pragma unroll
+    for (int u = 0; u < DM / 4; ++u) cv[u] = __ldg(cc4 + u);
+    double t = 0.0;
+    for (int r = 0; r < g; ++r) {
+        const float4* q4 = reinterpret_cast<const float4*>(q + (long long)r * d_h + j * DM);
+        float4 qv[DM / 4];
+#pragma unroll
+        for (int u = 0; u < DM / 4; ++u) qv[u] = __ldg(q4 + u);
+        double acc = 0.0;
+#pragma unroll
+        for (int u = 0; u < DM / 4; ++u) {
+            acc = __fma_rn((double)qv[u].x, (double)cv[u].x, acc);
+            acc = __fma_rn((double)qv[u].y, (double)cv[u].y, acc);
+            acc = __fma_rn((double)qv[u].z, (double)cv[u].z, acc);
+            acc = __fma_rn((double)qv[u].w, (double)cv[u].w, acc);
+        }
+        t = __dadd_rn(t, acc);
+    }
+    lut[e] = t;
+}
+
 __device__ inline void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
                           int C) {
     const int d_m = d_h / m;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(cen)) & 15) == 0 &&
+                         (d_h % 4) == 0;
+    if (aligned && (d_m == 64 || d_m == 32)) {
+        for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
+            if (d_m == 64) lut_entry_vec<64>(lut, q, cen, g, d_h, e, e / C);
+            else lut_entry_vec<32>(lut, q, cen, g, d_h, e, e / C);
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
         const int j = e / C;
         const float* cc = cen + (long long)e * d_m;
@@ -106,48 +143,129 @@ __device__ void find_digit(const uint32_t* hist, int nb, uint32_t k_rem, uint32_
 // cls[], and finds the PQKV_TUPLE_CHUNK chunk c* holding the k_rem-th equal
 // token in id order plus how many of c*'s equal tokens are taken.  On return
 // (after a barrier) sh[3] = c*, sh[4] = take, sh[5] = K*.  All scratch is
-// shared memory owned by the caller: lut[2C] f64, key[C*C], hist[NB],
-// eql[C*C], ceq[n_chunks], wsum[32], sh[8].
-template <int NT>
+// shared memory owned by the caller: lut[2C] f64, key[C*C] (nullable),
+// hist[NB], cnt[NB], eql[C*C], ceq[n_chunks], wsum[64], sh[8].
+template <int NT, int WMAX>
 __device__ void pair_select(const float* q, int g, int d_h, const float* cen, int C,
                             const uint32_t* thist, const uint16_t* chist, int n_chunks, int k,
-                            double* lut, uint32_t* key, uint32_t* hist, uint32_t* eql, uint32_t* ceq,
-                            uint32_t* wsum, uint32_t* sh, uint8_t* cls, uint32_t* tkey_out) {
+                            double* lut, uint32_t* key, uint32_t* hist, uint32_t* cnt, uint32_t* eql,
+                            uint32_t* ceq, uint32_t* wsum, uint32_t* sh, uint8_t* cls, uint32_t* tkey_out) {
     const int tid = threadIdx.x, C2 = C * C;
+    // pair weights: loaded once into registers (WMAX * NT >= C2), in flight
+    // while the ADC table is built
+    uint32_t w[WMAX];
+#pragma unroll
+    for (int u = 0; u < WMAX; ++u) {
+        const int t = tid + u * NT;
+        w[u] = t < C2 ? __ldg(thist + t) : 0u;
+    }
     build_lut(lut, q, cen, g, d_h, 2, C);
     for (int c = tid; c < n_chunks; c += NT) ceq[c] = 0;
-    if (tid == 0) sh[2] = 0;
     __syncthreads();
-    for (int t = tid; t < C2; t += NT) {
-        double acc = __dadd_rn(0.0, lut[t / C]);
-        acc = __dadd_rn(acc, lut[C + t % C]);
-        key[t] = score_key((float)acc);
+    uint32_t kr[WMAX];
+#pragma unroll
+    for (int u = 0; u < WMAX; ++u) {
+        const int t = tid + u * NT;
+        kr[u] = 0;
+        if (t < C2) {
+            double acc = __dadd_rn(0.0, lut[t / C]);
+            acc = __dadd_rn(acc, lut[C + t % C]);
+            kr[u] = score_key((float)acc);
+            if (key) key[t] = kr[u];
+        }
     }
-    uint32_t k_rem = (uint32_t)k, prefix = 0;
-    const int shifts[3] = {21, 10, 0};
-    const int nbins[3] = {2048, 2048, 1024};
-    for (int pass = 0; pass < 3; ++pass) {
-        for (int b = tid; b < NB; b += NT) hist[b] = 0;
+    // ---- weighted radix select over the pair keys ----
+    // Digit 0 spans [kmin, kmax] of the present pairs (f32 bit patterns of
+    // nearby scores share their top bits, so fixed top-bit digits would pile
+    // into a few bins); later digits refine the remaining low bits.  Each
+    // pass also counts pairs per bin: once the threshold bin holds a single
+    // pair its key is K* and the remaining passes are skipped.
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+    for (int u = 0; u < WMAX; ++u)
+        if (w[u]) { kmin = min(kmin, kr[u]); kmax = max(kmax, kr[u]); }
+    {
+        const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
+            kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+        }
+        if (lane == 0) { wsum[warp] = kmin; wsum[32 + warp] = kmax; }
+        for (int b = tid; b < NB; b += NT) { hist[b] = 0; cnt[b] = 0; }
         __syncthreads();
-        const uint32_t mask = (uint32_t)(nbins[pass] - 1);
-        for (int t = tid; t < C2; t += NT) {
-            uint32_t kk = key[t];
-            if (pass > 0 && (kk >> shifts[pass - 1]) != prefix) continue;
-            uint32_t ww = __ldg(thist + t);
-            if (ww) atomicAdd(&hist[(kk >> shifts[pass]) & mask], ww);
+        if (tid == 0) {
+            uint32_t a = 0xffffffffu, z = 0u;
+            for (int e = 0; e < NT / 32; ++e) { a = min(a, wsum[e]); z = max(z, wsum[32 + e]); }
+            sh[6] = a;
+            sh[7] = z;
         }
         __syncthreads();
-        find_digit<NT>(hist, nbins[pass], k_rem, wsum, sh);
-        k_rem -= sh[1];
-        prefix = (prefix << (pass == 2 ? 10 : 11)) | sh[0];
-        __syncthreads();
+        kmin = sh[6];
+        kmax = sh[7];
     }
-    const uint32_t kstar = prefix;
-    for (int t = tid; t < C2; t += NT) {
-        uint32_t kk = key[t];
+    uint32_t k_rem = (uint32_t)k;
+    const uint32_t range = kmax - kmin;
+    int shift = 32 - __clz(range | 1u);  // bits needed for (key - kmin)
+    shift = max(0, shift - 11);          // digit 0 = top 11 bits of (key - kmin)
+    uint32_t lo = kmin;                  // keys in the current candidate bin: [lo, lo + 2^shift... )
+    uint32_t prefix_val = 0;             // (key - kmin) >> (shift + width) of the chosen bins
+    int width = 11;
+    uint32_t kstar = 0;
+    bool done = false;
+    int cur_shift = shift;
+    for (int pass = 0; pass < 4 && !done; ++pass) {
+        const uint32_t nb = 1u << width;
+        const uint32_t mask = nb - 1;
+        // candidates: (key - kmin) >> (cur_shift + width) == prefix_val
+#pragma unroll
+        for (int u = 0; u < WMAX; ++u) {
+            const uint32_t rel = kr[u] - kmin;
+            const bool in = w[u] && (pass == 0 || (rel >> (cur_shift + width)) == prefix_val);
+            if (in) {
+                const uint32_t b = (rel >> cur_shift) & mask;
+                atomicAdd(&hist[b], w[u]);
+                atomicAdd(&cnt[b], 1u);
+            }
+        }
+        __syncthreads();
+        find_digit<NT>(hist, (int)nb < NT ? NT : (int)nb, k_rem, wsum, sh);
+        const uint32_t b = sh[0];
+        k_rem -= sh[1];
+        const uint32_t items = cnt[b];
+        __syncthreads();
+        prefix_val = (prefix_val << width) | b;
+        if (items == 1 || cur_shift == 0) {
+            // the bin holds one distinct pair (or one exact key): find it
+            if (tid == 0) sh[5] = 0xffffffffu;
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < WMAX; ++u) {
+                const uint32_t rel = kr[u] - kmin;
+                if (w[u] && (rel >> cur_shift) == prefix_val) atomicMin(&sh[5], kr[u]);
+            }
+            __syncthreads();
+            kstar = sh[5];
+            done = true;
+        } else {
+            // next digit: the low cur_shift bits, up to 11 at a time
+            width = min(11, cur_shift);
+            cur_shift -= width;
+            for (int e = tid; e < max(1 << width, NT); e += NT) { hist[e] = 0; cnt[e] = 0; }
+            __syncthreads();
+        }
+    }
+    (void)lo;
+    if (tid == 0) sh[2] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < WMAX; ++u) {
+        const int t = tid + u * NT;
+        if (t >= C2) break;
+        const uint32_t kk = kr[u];
         uint8_t c = kk > kstar ? 1 : (kk == kstar ? 2 : 0);
         cls[t] = c;
-        if (c == 2 && __ldg(thist + t)) eql[atomicAdd(&sh[2], 1u)] = (uint32_t)t;
+        if (c == 2 && w[u]) eql[atomicAdd(&sh[2], 1u)] = (uint32_t)t;
         if (tkey_out) tkey_out[t] = kk;
     }
     __syncthreads();
