@@ -23,6 +23,8 @@
 //   (bit-identical f32 scores), max-subtracted fp64 exp, the serial fp64 total
 //   and the row-ordered fp64 accumulation of softmax_attention
 //   (attention.cpp:35-60).  Only exp() differs in implementation from libm.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -223,9 +225,14 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         if (a.src == SRC_BITMAP) {
             for (int w = tid; w < nw; w += AT_THREADS) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
         } else if (a.src == SRC_PAIRS) {
-            // per-head pair-level top-k, recomputed by every CTA of the head
-            // (a few microseconds of latency instead of a separate launch)
+            // per-head pair-level top-k: computed by rank 0 of each thread-block
+            // cluster, shared with the cluster's other CTAs through DSMEM
+            namespace cg = cooperative_groups;
+            cg::cluster_group cluster = cg::this_cluster();
+            const unsigned crank = cluster.block_rank();
+            __shared__ uint32_t cut_s[2];
             const int C = a.C, C2 = C * C;
+            if (crank == 0) {
             unsigned char* z = smem_raw;  // aliases rows[]: free until expansion
             double* lut = reinterpret_cast<double*>(z);
             uint32_t* hist = reinterpret_cast<uint32_t*>(lut + 2 * C);
@@ -238,9 +245,17 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                                     a.centroids + (long long)p * 2 * C * (DH / 2), C,
                                     a.thist + (long long)p * C2, a.chist + (long long)p * a.n_tchunks * C2,
                                     a.n_tchunks, a.k, lut, nullptr, hist, cnt, eql, ceq, wsum, sh, cls, nullptr);
-            const int cstar = (int)sh[3];
-            const uint32_t take = sh[4];
-            __syncthreads();  // scratch is rows[] again from here on
+                if (tid == 0) { cut_s[0] = sh[3]; cut_s[1] = sh[4]; }
+            }
+            cluster.sync();
+            if (crank != 0) {
+                const uint32_t* rc = cluster.map_shared_rank(reinterpret_cast<const uint32_t*>(cls), 0);
+                for (int e = tid; e < (C2 + 3) / 4; e += AT_THREADS) reinterpret_cast<uint32_t*>(cls)[e] = rc[e];
+                if (tid < 2) cut_s[tid] = cluster.map_shared_rank(cut_s, 0)[tid];
+            }
+            cluster.sync();  // rank 0's tables are no longer read remotely
+            const int cstar = (int)cut_s[0];
+            const uint32_t take = cut_s[1];
             if (c == 0)
                 for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
             classify_words(a, p, r0, r1, words, cls, wtot, cstar, take);
@@ -588,7 +603,32 @@ static size_t attend_smem(AtArgs& a, int G) {
     return round_up(region + tail, 16);
 }
 
+template <int G>
+static void launch_attend_g(const AtArgs& a, dim3 grid, size_t smem, int cl, cudaStream_t st) {
+    PQKV_CUDA(cudaFuncSetAttribute(attend_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(AT_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PQKV_CUDA(cudaLaunchKernelEx(&cfg, attend_kernel<G>, a));
+}
+
 static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cudaStream_t st) {
+    // pair-select mode: 8-CTA clusters share one pair select (pad the chunk
+    // count to a multiple of the cluster; padded CTAs own empty ranges)
+    int cl = 1;
+    if (a.src == SRC_PAIRS && a.n_chunks >= 4) {
+        cl = 8;
+        a.n_chunks = (int)round_up((size_t)a.n_chunks, (size_t)cl);
+    }
     Scratch sc(ctx);
     size_t h_part = sc.plan<float>(P * a.n_chunks * G * (DH + 2));
     sc.commit();
@@ -597,18 +637,9 @@ static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cuda
     size_t smem = attend_smem(a, G);
     dim3 grid((unsigned)a.n_chunks, (unsigned)P);
     switch (G) {
-        case 1:
-            PQKV_CUDA(cudaFuncSetAttribute(attend_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attend_kernel<1><<<grid, AT_THREADS, smem, st>>>(a);
-            break;
-        case 2:
-            PQKV_CUDA(cudaFuncSetAttribute(attend_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attend_kernel<2><<<grid, AT_THREADS, smem, st>>>(a);
-            break;
-        case 4:
-            PQKV_CUDA(cudaFuncSetAttribute(attend_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attend_kernel<4><<<grid, AT_THREADS, smem, st>>>(a);
-            break;
+        case 1: launch_attend_g<1>(a, grid, smem, cl, st); break;
+        case 2: launch_attend_g<2>(a, grid, smem, cl, st); break;
+        case 4: launch_attend_g<4>(a, grid, smem, cl, st); break;
         default: fail(PQKV_EINVAL, "attend: g must be 1, 2 or 4 on the fast path");
     }
     PQKV_LAUNCHED("attend_kernel");

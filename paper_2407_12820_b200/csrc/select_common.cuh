@@ -8,6 +8,15 @@ namespace pqkv_dev {
 
 constexpr int NB = 2048;  // bins of the two 11-bit radix digits
 
+#ifdef PQKV_PROBE_TIMERS
+}  // namespace pqkv_dev
+__device__ unsigned long long g_t[64][16];  // probe builds only
+namespace pqkv_dev {
+#define PQKV_T(ph) do { if (threadIdx.x == 0) ::g_t[blockIdx.x][ph] = clock64(); } while (0)
+#else
+#define PQKV_T(ph) do { } while (0)
+#endif
+
 // Builds T[j][c] (pq.cpp:113-126, rows accumulated as in pq.cpp:157-159).
 // One thread per (j, c); the t-chain stays sequential (reference order) while
 // the centroid row is prefetched 16 floats at a time so the chain is not
@@ -153,6 +162,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
     const int tid = threadIdx.x, C2 = C * C;
     // pair weights: loaded once into registers (WMAX * NT >= C2), in flight
     // while the ADC table is built
+    PQKV_T(0);
     uint32_t w[WMAX];
 #pragma unroll
     for (int u = 0; u < WMAX; ++u) {
@@ -160,8 +170,10 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
         w[u] = t < C2 ? __ldg(thist + t) : 0u;
     }
     build_lut(lut, q, cen, g, d_h, 2, C);
+    PQKV_T(1);
     for (int c = tid; c < n_chunks; c += NT) ceq[c] = 0;
     __syncthreads();
+    PQKV_T(2);
     uint32_t kr[WMAX];
 #pragma unroll
     for (int u = 0; u < WMAX; ++u) {
@@ -204,6 +216,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
         kmin = sh[6];
         kmax = sh[7];
     }
+    PQKV_T(3);
     uint32_t k_rem = (uint32_t)k;
     const uint32_t range = kmax - kmin;
     int shift = 32 - __clz(range | 1u);  // bits needed for (key - kmin)
@@ -256,6 +269,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
         }
     }
     (void)lo;
+    PQKV_T(4);
     if (tid == 0) sh[2] = 0;
     __syncthreads();
 #pragma unroll
@@ -269,6 +283,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
         if (tkey_out) tkey_out[t] = kk;
     }
     __syncthreads();
+    PQKV_T(5);
     const int neq = (int)sh[2];
     for (int e = tid; e < neq * n_chunks; e += NT) {
         int c = e / neq, t = (int)eql[e % neq];
@@ -276,6 +291,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
         if (v) atomicAdd(&ceq[c], v);
     }
     __syncthreads();
+    PQKV_T(6);
     if (tid < 32) {  // chunk holding the k_rem-th equal token (warp scan over chunks)
         const int lane = tid;
         uint32_t run = 0;

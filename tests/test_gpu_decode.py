@@ -224,7 +224,8 @@ def _decode_case(orc, s, h, g, n_init, n_local, k, m=2, b=6, seed=3, T=6, tuple_
 
 @pytest.mark.parametrize("tup", [False, True])
 @pytest.mark.parametrize("s,h,g,n_init,n_local,k", [(4096, 3, 1, 4, 64, 819), (2000, 2, 4, 16, 64, 300),
-                                                    (700, 2, 2, 0, 1, 50), (9000, 2, 1, 4, 64, 1800)])
+                                                    (700, 2, 2, 0, 1, 50), (9000, 2, 1, 4, 64, 1800),
+                                                    (24000, 1, 1, 4, 64, 4800), (20000, 1, 4, 16, 64, 100)])
 def test_fused_decode_matches_reference_pipeline(ctx, orc, s, h, g, n_init, n_local, k, tup):
     kk, vv, qq, cen, codes, layer = _decode_case(orc, s, h, g, n_init, n_local, k, tuple_tables=tup, ctx=ctx)
     out, ids = ctx.decode(layer, _t(qq), k, want_ids=True)
