@@ -22,8 +22,11 @@
 // update_means (kmeans.cpp:133-147) accumulates in ascending point order per
 // (cluster, dim): warp w owns clusters c = w (mod W) and walks the assignment
 // array in order.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <vector>
@@ -278,93 +281,142 @@ __device__ double warp_serial_sum(const double* v, int n, double* prefix) {
 // Exact, block-parallel reproduction of the serial fp64 running sum
 //   S_{-1} = +0.0,  S_i = fl(S_{i-1} + v_i),  v_i >= 0
 // of k-means++ (kmeans.cpp:64-65 total, 70-71 cum); S_i is stored in pre[i]
-// and S_{n-1} returned to every thread.  Processed in groups of
-// KM_THREADS*4 values.  While the running sum S stays inside one binade
+// and S_{n-1} is returned to every thread.  While S stays inside one binade
 // [2^e, 2^(e+1)) every step is S + round_u(v_i) with u = ulp(S) (S is a
-// multiple of u, so round-to-nearest of S + v_i only rounds v_i), hence the
-// group is exact as S + u * (integer prefix of round_u(v_i)).  A group whose
-// sum leaves the binade, that contains a tie (v_i mod u == u/2, where the
-// even rule would depend on S), or that starts at 0/subnormal S is replayed
-// serially by one thread.  No approximation is ever accepted.
+// multiple of u, so round-to-nearest of S + v_i only rounds v_i), so a run
+// of such steps is exact as S + u * (integer prefix of round_u(v_i)).  The
+// first element that would leave the binade, that is a tie (v_i mod u ==
+// u/2, where round-half-even depends on S), or that meets S == 0 /
+// subnormal, is done serially by one thread; the parallel pass then resumes
+// after it.  No approximation is ever accepted.
 __device__ double exact_running_sum(const double* v, int n, double* pre, double* gbuf,
                                     long long* iscr, double* dsh) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int E = 4, GROUP = KM_THREADS * E;
+    int* ish = reinterpret_cast<int*>(iscr + 2 * KM_WARPS);
     double S = 0.0;
     for (int g0 = 0; g0 < n; g0 += GROUP) {
         const int cnt = min(GROUP, n - g0);
         double a[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const int i = g0 + tid * E + e;
-            a[e] = i < n ? v[i] : 0.0;
+            const int li = tid * E + e;
+            a[e] = g0 + li < n ? v[g0 + li] : 0.0;
+            gbuf[li] = a[e];
         }
-        const long long sb = __double_as_longlong(S);
-        const int expo = (int)((sb >> 52) & 0x7ff);
-        bool ok = S > 0.0 && expo > 52 && expo < 2046;  // normal, u normal, no overflow
-        long long dsum = 0;
-        long long d[E];
-        double u = 0.0, inv_u = 0.0, top = 0.0;
-        if (ok) {
-            u = __longlong_as_double((long long)(expo - 52) << 52);
-            inv_u = __longlong_as_double((long long)(2046 - expo + 52) << 52);  // 2^-(expo-1023-52)
-            top = __longlong_as_double((long long)(expo + 1) << 52);             // 2^(e+1)
+        __syncthreads();
+        int j = 0;  // first element of the group not yet summed (block uniform)
+        while (j < cnt) {
+            const long long sb = __double_as_longlong(S);
+            const int expo = (int)((sb >> 52) & 0x7ff);
+            const bool normal = S > 0.0 && expo > 52 && expo < 2046;
+            double u = 0.0, inv_u = 0.0, top = 0.0;
+            long long d[E];
+            bool bad[E];
+            long long dsum = 0;
+            if (normal) {
+                u = __longlong_as_double((long long)(expo - 52) << 52);
+                inv_u = __longlong_as_double((long long)(2098 - expo) << 52);  // 1/u, exact
+                top = __longlong_as_double((long long)(expo + 1) << 52);        // 2^(e+1)
+            }
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                const double qv = a[e] * inv_u;  // exact (power-of-two scaling)
-                bool bad = !(qv < 4503599627370496.0);  // 2^52: a crosses anyway
-                const double fl = floor(qv), fr = qv - fl;
-                bad |= fr == 0.5;                        // tie: parity-dependent
-                d[e] = bad ? 0 : (long long)fl + (fr > 0.5 ? 1 : 0);
-                if (bad) ok = false;
+                const int li = tid * E + e;
+                d[e] = 0;
+                bad[e] = false;
+                if (li >= j && li < cnt) {
+                    if (!normal) {
+                        bad[e] = true;
+                    } else {
+                        const double qv = a[e] * inv_u;  // exact power-of-two scaling
+                        const double fl = floor(qv), fr = qv - fl;
+                        bad[e] = !(qv < 4503599627370496.0) || fr == 0.5;
+                        d[e] = bad[e] ? 0 : (long long)fl + (fr > 0.5 ? 1 : 0);
+                    }
+                }
                 dsum += d[e];
             }
-        }
-        // block-wide: all ok? exclusive prefix of dsum
-        long long x = dsum;
+            long long x = dsum;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            long long y = __shfl_up_sync(FULL, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) iscr[warp] = x;
-        const int all_ok = __syncthreads_and(ok);
-        long long before = x - dsum, total = 0;
-        for (int w = 0; w < KM_WARPS; ++w) {
-            long long t = iscr[w];
-            before += w < warp ? t : 0;
-            total += t;
-        }
-        bool fast = all_ok && (S + (double)total * u) < top;
-        if (fast) {
-            long long run = before;
+            for (int o = 1; o < 32; o <<= 1) {
+                long long y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) iscr[warp] = x;
+            if (tid == 0) ish[0] = cnt;  // first stop index
+            __syncthreads();
+            long long run = x - dsum;
+            for (int w = 0; w < warp; ++w) run += iscr[w];
+            // first element that is bad or whose exact-in-binade sum reaches top
+            int stop = cnt;
+            long long r2 = run;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                run += d[e];
-                const int i = g0 + tid * E + e;
-                if (i < n) pre[i] = S + (double)run * u;
-            }
-            S = S + (double)total * u;
-            __syncthreads();  // iscr reuse
-        } else {
-            // serial replay of this group (rare: start, binade crossings, ties)
-#pragma unroll
-            for (int e = 0; e < E; ++e) gbuf[tid * E + e] = a[e];
-            __syncthreads();
-            if (tid == 0) {
-                double s2 = S;
-                for (int j = 0; j < cnt; ++j) {
-                    s2 = __dadd_rn(s2, gbuf[j]);
-                    pre[g0 + j] = s2;
+                const int li = tid * E + e;
+                if (li >= j && li < cnt && stop == cnt) {
+                    r2 += d[e];
+                    if (bad[e] || !(S + (double)r2 * u < top)) stop = li;
                 }
-                dsh[0] = s2;
+            }
+            if (stop < cnt) atomicMin(&ish[0], stop);
+            __syncthreads();
+            const int xs = ish[0];
+            // accept [j, xs)
+            r2 = run;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int li = tid * E + e;
+                if (li >= j && li < xs) {
+                    r2 += d[e];
+                    pre[g0 + li] = S + (double)r2 * u;
+                }
+            }
+            // new S = value at xs - 1 (held by the thread owning xs - 1)
+            if (xs > j && (xs - 1) / E == tid) {
+                long long r3 = run;
+                for (int e = 0; e <= (xs - 1) % E; ++e) r3 += d[e];
+                dsh[0] = S + (double)r3 * u;
             }
             __syncthreads();
-            S = dsh[0];
-            __syncthreads();
+            if (xs > j) S = dsh[0];
+            if (xs < cnt) {  // the stop element, serially
+                if (tid == 0) {
+                    const double s2 = __dadd_rn(S, gbuf[xs]);
+                    pre[g0 + xs] = s2;
+                    dsh[1] = s2;
+                }
+                __syncthreads();
+                S = dsh[1];
+                j = xs + 1;
+            } else {
+                j = cnt;
+            }
+            __syncthreads();  // iscr / ish / dsh reuse
         }
     }
     return S;
+}
+
+// First i in [0, n) with pre[i] >= target (pre non-decreasing; n-1 if none),
+// by one warp with 32-ary probing.
+__device__ int warp_lower_bound(const double* pre, int n, double target) {
+    const int lane = threadIdx.x & 31;
+    int lo = 0, hi = n - 1;  // answer in [lo, hi]
+    while (hi - lo >= 32) {
+        const int span = hi - lo + 1;
+        const int step = (span + 31) / 32;
+        const int pidx = min(lo + lane * step + step - 1, hi);  // last index of lane's bucket
+        const bool ge = pre[pidx] >= target;
+        const unsigned m = __ballot_sync(FULL, ge);
+        const int f = m ? __ffs(m) - 1 : 31;
+        const int nlo = lo + f * step;
+        hi = m ? min(lo + f * step + step - 1, hi) : hi;
+        lo = nlo;
+    }
+    const int idx = lo + lane;
+    const bool ge = idx <= hi && pre[idx] >= target;
+    const unsigned m = __ballot_sync(FULL, ge);
+    return m ? lo + __ffs(m) - 1 : n - 1;
 }
 
 // ---- the per-problem kernel -------------------------------------------------
@@ -653,23 +705,18 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_problem_kernel(KmArgs a)
             tick(1);
             {
                 double total = exact_running_sum(aux0, n, aux1, s.gbuf, s.lscr, s.dscratch);
-                __syncthreads();  // aux1 (prefix) visible to thread 0's search
-                if (tid == 0) {
+                __syncthreads();  // aux1 (prefix) visible to warp 0's search
+                if (warp == 0) {
                     int chosen;
                     if (total > 0.0) {
                         double u = (double)(draws[c] >> 11) * 0x1.0p-53;
                         double target = __dmul_rn(u, total);
-                        // first i with prefix[i] >= target (prefix is non-decreasing)
-                        int lo = 0, hi = n - 1;
-                        while (lo < hi) {
-                            int mid = (lo + hi) >> 1;
-                            if (aux1[mid] >= target) hi = mid; else lo = mid + 1;
-                        }
-                        chosen = (aux1[lo] >= target) ? lo : n - 1;
+                        // first i with cum >= target (kmeans.cpp:70-74): prefix is non-decreasing
+                        chosen = warp_lower_bound(aux1, n, target);
                     } else {
                         chosen = (int)(draws[c] % (unsigned long long)n);
                     }
-                    sh_int[3] = chosen;
+                    if (lane == 0) sh_int[3] = chosen;
                 }
             }
             block_sync();
@@ -812,6 +859,496 @@ __global__ void assign_nearest_kernel(const float* points, int n, int dim, const
     out[i] = best;
 }
 
+// =============================================================================
+// v2: one thread-block CLUSTER of R CTAs per problem (R = 1..8, so a batch of
+// few problems still fills the GPU).  CTA r owns the point slice
+// [r*ceil(n/R), ...).  Cluster-wide state: counts merged through DSMEM, the
+// k-means++ running sum and the rare repair run on rank 0, centroids
+// broadcast through global memory after each update.
+//
+// update_means (kmeans.cpp:133-147) without the sequential walk: the sum of
+// a (cluster, dim) chain of f32 values in fp64 never rounds -- in ANY order --
+// when sum|x| < 2^52 * ulp_min, ulp_min the smallest f32 ulp among its nonzero
+// members (every partial sum is then a multiple of ulp_min below 2^53 ulp_min,
+// hence representable).  Such chains are reduced in parallel over a stable
+// member list (counting sort by cluster); a chain that fails the check is
+// recomputed in point order.  Either way the means are bit-identical.
+// =============================================================================
+constexpr int V2_MG = 4;  // member groups per warp in the parallel reduction
+
+struct V2Smem {
+    double* gbuf;
+    long long* lscr;
+    int* iscratch;
+    double* dscratch;
+    uint32_t* cnt_loc;   // [K] this slice
+    uint32_t* cnt_all;   // [K] cluster total
+    uint32_t* moff;      // [K] member-list offsets
+    uint32_t* run;       // [K] scatter cursors
+    uint32_t* wcnt;      // [KM_WARPS][K]
+    float* cenf;         // [K*D]
+    float* cnorm;        // [K]
+    double* cen64;       // [K*D]
+};
+
+__host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
+    size_t b = (size_t)KM_THREADS * 4 * 8 + 32 * 8 + 64 * 4 + 64 * 8;
+    b += (size_t)4 * K * 4 + (size_t)KM_WARPS * K * 4;
+    b = (b + 15) / 16 * 16;
+    b += (size_t)K * D * 4 + (size_t)K * 4;
+    b = (b + 15) / 16 * 16;
+    b += (size_t)K * D * 8;
+    return b;
+}
+
+template <int D>
+__global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a, uint32_t* members_g) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int R = (int)cl.num_blocks();
+    const int r = (int)cl.block_rank();
+    const int q = blockIdx.x / R;
+    const int n = a.n, K = a.K, T = a.T;
+    const long long KD = (long long)K * D;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + R - 1) / R;
+    const int lo = min(n, r * per), hi = min(n, lo + per);
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V2Smem s;
+    {
+        unsigned char* p = smem_raw;
+        s.gbuf = reinterpret_cast<double*>(p); p += KM_THREADS * 4 * 8;
+        s.lscr = reinterpret_cast<long long*>(p); p += 32 * 8;
+        s.iscratch = reinterpret_cast<int*>(p); p += 64 * 4;
+        s.dscratch = reinterpret_cast<double*>(p); p += 64 * 8;
+        s.cnt_loc = reinterpret_cast<uint32_t*>(p); p += K * 4;
+        s.cnt_all = reinterpret_cast<uint32_t*>(p); p += K * 4;
+        s.moff = reinterpret_cast<uint32_t*>(p); p += K * 4;
+        s.run = reinterpret_cast<uint32_t*>(p); p += K * 4;
+        s.wcnt = reinterpret_cast<uint32_t*>(p); p += KM_WARPS * K * 4;
+        p = smem_raw + (p - smem_raw + 15) / 16 * 16;
+        s.cenf = reinterpret_cast<float*>(p); p += KD * 4;
+        s.cnorm = reinterpret_cast<float*>(p); p += K * 4;
+        p = smem_raw + (p - smem_raw + 15) / 16 * 16;
+        s.cen64 = reinterpret_cast<double*>(p);
+    }
+    uint32_t* asg = a.asg0 + (long long)q * n;
+    uint32_t* nxt = a.asg1 + (long long)q * n;
+    double* aux0 = a.aux0 + (long long)q * n;
+    double* aux1 = a.aux1 + (long long)q * n;
+    uint32_t* queue = a.queue + (long long)q * n;
+    uint32_t* mem = members_g + (long long)q * n;
+    double* gcen = a.cen64 + q * KD;
+    __shared__ int sh_int[8];
+    __shared__ float sh_cmax;
+    __shared__ int sh_flag;
+    unsigned long long t_acc[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long t_last = clock64();
+    auto tick = [&](int ph) {
+        if (tid == 0) {
+            unsigned long long now = clock64();
+            t_acc[ph] += now - t_last;
+            t_last = now;
+        }
+    };
+    auto cluster_or = [&](int v) -> int {
+        int mine = __syncthreads_or(v);
+        if (tid == 0) sh_flag = mine;
+        cl.sync();
+        int any = 0;
+        for (int rr = 0; rr < R; ++rr) any |= *cl.map_shared_rank(&sh_flag, rr);
+        cl.sync();  // sh_flag may be rewritten after this
+        return any;
+    };
+    auto refresh_f32 = [&]() {
+        for (long long e = tid; e < KD; e += KM_THREADS) s.cenf[e] = (float)s.cen64[e];
+        if (tid == 0) sh_cmax = 0.f;
+        __syncthreads();
+        for (int c = tid; c < K; c += KM_THREADS) {
+            float acc = 0.f;
+            for (int t = 0; t < D; ++t) acc = fmaf(s.cenf[c * D + t], s.cenf[c * D + t], acc);
+            float nrm = sqrtf(acc) * (1.0f + 9.6e-7f) + 1e-30f;
+            s.cnorm[c] = nrm;
+            atomicMax(reinterpret_cast<int*>(&sh_cmax), __float_as_int(nrm));
+        }
+        __syncthreads();
+    };
+    auto merge_counts = [&]() {
+        cl.sync();
+        for (int c = tid; c < K; c += KM_THREADS) {
+            uint32_t t = 0;
+            for (int rr = 0; rr < R; ++rr) t += cl.map_shared_rank(s.cnt_loc, rr)[c];
+            s.cnt_all[c] = t;
+        }
+        __syncthreads();
+    };
+
+    // ---- assignment pass over this CTA's slice (+ cluster-wide repair) ----
+    auto assign_pass = [&](uint32_t* out) {
+        for (int c = tid; c < K; c += KM_THREADS) s.cnt_loc[c] = 0;
+        if (tid == 0) sh_int[0] = 0;
+        __syncthreads();
+        const float cmax = sh_cmax;
+        for (int i = lo + tid; i < hi; i += KM_THREADS) {
+            float x[D];
+            load_point<D>(point_ptr(a, q, i), x, a.vec4);
+            int c = nearest_filtered<D>(x, s.cenf, s.cnorm, cmax, K);
+            if (c >= 0) {
+                out[i] = (uint32_t)c;
+                atomicAdd(&s.cnt_loc[c], 1u);
+            } else {
+                queue[lo + atomicAdd(&sh_int[0], 1)] = (uint32_t)i;
+            }
+        }
+        __syncthreads();
+        const int qn = sh_int[0];
+        for (int e = tid; e < qn; e += KM_THREADS) {
+            const int i = (int)queue[lo + e];
+            const uint32_t c = nearest_g(point_ptr(a, q, i), s.cen64, K, D);
+            out[i] = c;
+            atomicAdd(&s.cnt_loc[c], 1u);
+        }
+        if (tid == 0 && a.stats) {
+            atomicAdd(&a.stats[0], (unsigned long long)qn);
+            atomicAdd(&a.stats[1], (unsigned long long)(hi - lo));
+        }
+        merge_counts();
+        if (n < K) return;
+        int empty = 0;
+        for (int c = tid; c < K; c += KM_THREADS) empty |= (s.cnt_all[c] == 0);
+        if (!__syncthreads_or(empty)) return;  // uniform: cnt_all is identical in every CTA
+        // rare path (kmeans.cpp:111-127): rank 0 repairs over all points
+        if (r == 0) {
+            for (int i = tid; i < n; i += KM_THREADS)
+                aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64 + (long long)out[i] * D, D);
+            __syncthreads();
+            for (int c = 0; c < K; ++c) {
+                if (s.cnt_all[c] != 0) continue;
+                double best = -1.0;
+                int bi = n;
+                for (int i = tid; i < n; i += KM_THREADS) {
+                    if (s.cnt_all[out[i]] < 2) continue;
+                    double d = aux0[i];
+                    if (d > best) { best = d; bi = i; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    double ob = __shfl_xor_sync(FULL, best, o);
+                    int oi = __shfl_xor_sync(FULL, bi, o);
+                    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                }
+                if (lane == 0) { s.dscratch[warp] = best; s.iscratch[warp] = bi; }
+                __syncthreads();
+                if (tid == 0) {
+                    double b = s.dscratch[0];
+                    int ii = s.iscratch[0];
+                    for (int w = 1; w < KM_WARPS; ++w) {
+                        double ob = s.dscratch[w];
+                        int oi = s.iscratch[w];
+                        if (ob > b || (ob == b && oi < ii)) { b = ob; ii = oi; }
+                    }
+                    sh_int[1] = ii;
+                }
+                __syncthreads();
+                const int donor = sh_int[1];
+                if (donor >= n) break;
+                if (tid == 0) {
+                    s.cnt_all[out[donor]] -= 1;
+                    out[donor] = (uint32_t)c;
+                    s.cnt_all[c] += 1;
+                }
+                __syncthreads();
+            }
+        }
+        cl.sync();  // repaired assignment visible
+        for (int c = tid; c < K; c += KM_THREADS) s.cnt_loc[c] = 0;
+        __syncthreads();
+        for (int i = lo + tid; i < hi; i += KM_THREADS) atomicAdd(&s.cnt_loc[out[i]], 1u);
+        merge_counts();
+    };
+
+    // ---- update_means: member lists + certified order-free sums ----
+    auto update_means = [&](const uint32_t* as) {
+        // offsets: members of cluster c in point order, slices in rank order
+        if (tid == 0) {
+            uint32_t run = 0;
+            for (int c = 0; c < K; ++c) { s.moff[c] = run; run += s.cnt_all[c]; }
+        }
+        __syncthreads();
+        for (int c = tid; c < K; c += KM_THREADS) {
+            uint32_t before = 0;
+            for (int rr = 0; rr < r; ++rr) before += cl.map_shared_rank(s.cnt_loc, rr)[c];
+            s.run[c] = s.moff[c] + before;
+        }
+        for (int e = tid; e < KM_WARPS * K; e += KM_THREADS) s.wcnt[e] = 0;
+        __syncthreads();
+        // stable scatter of this slice
+        for (int b0 = lo; b0 < hi; b0 += KM_THREADS) {
+            const int i = b0 + tid;
+            const uint32_t c = i < hi ? as[i] : 0xffffffffu;
+            const unsigned peers = __match_any_sync(FULL, c);
+            const uint32_t wr = __popc(peers & lanemask_lt());
+            if (c != 0xffffffffu && wr == 0) s.wcnt[warp * K + c] = __popc(peers);
+            __syncthreads();
+            if (c != 0xffffffffu) {
+                uint32_t before = 0;
+                for (int w = 0; w < warp; ++w) before += s.wcnt[w * K + c];
+                mem[s.run[c] + before + wr] = (uint32_t)i;
+            }
+            __syncthreads();
+            for (int cc = tid; cc < K; cc += KM_THREADS) {
+                uint32_t tot = 0;
+                for (int w = 0; w < KM_WARPS; ++w) { tot += s.wcnt[w * K + cc]; s.wcnt[w * K + cc] = 0; }
+                s.run[cc] += tot;
+            }
+            __syncthreads();
+        }
+        cl.sync();  // every slice's member list is written
+        // sums: warp gw of the cluster owns clusters c = gw (mod KM_WARPS*R)
+        constexpr int DG = 32 / V2_MG;                       // lanes per member group (8)
+        constexpr int DPL = (D + DG - 1) / DG;               // dims per lane
+        const int mg = lane / DG, dl = lane % DG;            // member group, lane in group
+        const int gw = r * KM_WARPS + warp;
+        for (int c = gw; c < K; c += KM_WARPS * R) {
+            const uint32_t cnt = s.cnt_all[c];
+            if (cnt == 0) continue;  // empty cluster keeps its centroid
+            const uint32_t base = s.moff[c];
+            double acc[DPL], aabs[DPL];
+            int emin[DPL];
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) { acc[e] = 0.0; aabs[e] = 0.0; emin[e] = 0x7fffffff; }
+            // members mg, mg+4, ... ; 4 member rows per warp step, unrolled x4
+            for (uint32_t m0 = 0; m0 < cnt; m0 += V2_MG * 4) {
+                float xv[4][DPL];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t m = m0 + u * V2_MG + mg;
+                    const float* xp = m < cnt ? point_ptr(a, q, (int)mem[base + m]) : nullptr;
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e) {
+                        const int t = dl + DG * e;
+                        xv[u][e] = (xp && t < D) ? __ldg(xp + t) : 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e) {
+                        const float x = xv[u][e];
+                        acc[e] += (double)x;
+                        aabs[e] += (double)fabsf(x);
+                        if (x != 0.0f) emin[e] = min(emin[e], (int)((__float_as_uint(x) >> 23) & 0xff));
+                    }
+            }
+            // combine the member groups (lanes dl, dl+8, dl+16, dl+24)
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+#pragma unroll
+                for (int o = DG; o < 32; o <<= 1) {
+                    acc[e] += __shfl_xor_sync(FULL, acc[e], o);
+                    aabs[e] += __shfl_xor_sync(FULL, aabs[e], o);
+                    emin[e] = min(emin[e], __shfl_xor_sync(FULL, emin[e], o));
+                }
+            // certificate: sum|x| < 2^52 * ulp_min (ulp of the smallest-exponent
+            // member: 2^(e-150) for normal e, 2^-149 for subnormals)
+            bool ok = true;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) {
+                if (dl + DG * e >= D || emin[e] == 0x7fffffff) continue;
+                const int ue = emin[e] == 0 ? -149 : emin[e] - 150;
+                ok = ok && (aabs[e] * (1.0 + 1e-9) < ldexp(1.0, 52 + ue));
+            }
+            ok = __all_sync(FULL, ok);
+            if (!ok) {
+                // exact fallback: the reference's order (points ascending), lanes = dims
+                for (int t0 = 0; t0 < D; t0 += 32) {
+                    const int t = t0 + lane;
+                    double sacc = 0.0;
+                    for (uint32_t m = 0; m < cnt; ++m) {
+                        const float* xp = point_ptr(a, q, (int)mem[base + m]);
+                        if (t < D) sacc = __dadd_rn(sacc, (double)__ldg(xp + t));
+                    }
+                    if (t < D) gcen[(long long)c * D + t] = __ddiv_rn(sacc, (double)cnt);
+                }
+            } else if (mg == 0) {
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) {
+                    const int t = dl + DG * e;
+                    if (t < D) gcen[(long long)c * D + t] = __ddiv_rn(acc[e], (double)cnt);
+                }
+            }
+        }
+        cl.sync();  // new means visible in global memory
+        for (long long e = tid; e < KD; e += KM_THREADS) s.cen64[e] = gcen[e];
+        __syncthreads();
+    };
+
+    // =====================================================================
+    // 1. seeding
+    // =====================================================================
+    const unsigned long long* draws = a.draws + (long long)q * K;
+    if (n <= K) {
+        if (r == 0) {  // seed_from_distinct (kmeans.cpp:44-57), small
+            for (int i = tid; i < n; i += KM_THREADS) {
+                const uint32_t* xi = reinterpret_cast<const uint32_t*>(point_ptr(a, q, i));
+                int seen = 0;
+                for (int j = 0; j < i && !seen; ++j) {
+                    const uint32_t* xj = reinterpret_cast<const uint32_t*>(point_ptr(a, q, j));
+                    int eq = 1;
+                    for (int t = 0; t < D && eq; ++t) eq = (xi[t] == xj[t]);
+                    seen = eq;
+                }
+                asg[i] = seen ? 0u : 1u;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                int nd = 0;
+                for (int i = 0; i < n; ++i)
+                    if (asg[i]) nxt[nd++] = (uint32_t)i;
+                sh_int[2] = nd;
+            }
+            __syncthreads();
+            const int nd = sh_int[2];
+            for (long long e = tid; e < KD; e += KM_THREADS) {
+                const int c = (int)(e / D), t = (int)(e % D);
+                const int src = (int)nxt[c < nd - 1 ? c : nd - 1];
+                gcen[e] = (double)point_ptr(a, q, src)[t];
+            }
+        }
+        cl.sync();
+        for (long long e = tid; e < KD; e += KM_THREADS) s.cen64[e] = gcen[e];
+        __syncthreads();
+    } else {
+        const int c0 = (int)(draws[0] % (unsigned long long)n);
+        for (int t = tid; t < D; t += KM_THREADS) s.cen64[t] = (double)point_ptr(a, q, c0)[t];
+        __syncthreads();
+        for (int i = lo + tid; i < hi; i += KM_THREADS) aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64, D);
+        for (int c = 1; c < K; ++c) {
+            cl.sync();  // every slice's min_d2 is final for this step
+            tick(1);
+            if (r == 0) {
+                const double total = exact_running_sum(aux0, n, aux1, s.gbuf, s.lscr, s.dscratch);
+                __syncthreads();
+                if (warp == 0) {
+                    int chosen;
+                    if (total > 0.0) {
+                        const double u = (double)(draws[c] >> 11) * 0x1.0p-53;
+                        chosen = warp_lower_bound(aux1, n, __dmul_rn(u, total));
+                    } else {
+                        chosen = (int)(draws[c] % (unsigned long long)n);
+                    }
+                    if (lane == 0) sh_int[3] = chosen;
+                }
+            }
+            cl.sync();
+            const int chosen = *cl.map_shared_rank(&sh_int[3], 0);
+            tick(0);
+            for (int t = tid; t < D; t += KM_THREADS)
+                s.cen64[(long long)c * D + t] = (double)point_ptr(a, q, chosen)[t];
+            __syncthreads();
+            const double* cc = s.cen64 + (long long)c * D;
+            float cf[D];
+            float cn = 0.f;
+#pragma unroll
+            for (int t = 0; t < D; ++t) { cf[t] = (float)cc[t]; cn = fmaf(cf[t], cf[t], cn); }
+            cn = sqrtf(cn) * (1.0f + 9.6e-7f) + 1e-30f;
+            for (int i = lo + tid; i < hi; i += KM_THREADS) {
+                const float* xp = point_ptr(a, q, i);
+                float xr[D];
+                load_point<D>(xp, xr, a.vec4);
+                float acc = 0.f;
+#pragma unroll
+                for (int t = 0; t < D; ++t) {
+                    const float d = xr[t] - cf[t];
+                    acc = fmaf(d, d, acc);
+                }
+                const double old = aux0[i];
+                if (acc < 1e37f && (double)(acc - err_bound(acc, cn, D)) > old) continue;
+                const double d = dist2_g(xp, cc, D);
+                if (d < old) aux0[i] = d;
+            }
+        }
+        cl.sync();
+        tick(1);
+        if (r == 0)
+            for (long long e = tid; e < KD; e += KM_THREADS) gcen[e] = s.cen64[e];
+        // (no sync needed: gcen is read after the next cluster barrier)
+    }
+    refresh_f32();
+    tick(5);
+
+    // =====================================================================
+    // 2. Lloyd iterations (kmeans.cpp:174-183)
+    // =====================================================================
+    assign_pass(asg);
+    tick(2);
+    int iters = 0;
+    for (int iter = 1; iter <= T; ++iter) {
+        update_means(asg);
+        tick(4);
+        if (a.inertia) {
+            for (int i = lo + tid; i < hi; i += KM_THREADS)
+                aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64 + (long long)asg[i] * D, D);
+            cl.sync();
+            if (r == 0 && warp == 0) {
+                double tot = warp_serial_sum(aux0, n, nullptr);
+                if (lane == 0) a.inertia[(long long)q * T + iter - 1] = tot;
+            }
+            cl.sync();
+        }
+        iters = iter;
+        refresh_f32();
+        tick(5);
+        assign_pass(nxt);
+        tick(2);
+        int changed = 0;
+        for (int i = lo + tid; i < hi; i += KM_THREADS) changed |= (nxt[i] != asg[i]);
+        if (!cluster_or(changed)) break;
+        uint32_t* t = asg;
+        asg = nxt;
+        nxt = t;
+    }
+
+    // =====================================================================
+    // 3. emit
+    // =====================================================================
+    if (r == 0)
+        for (long long e = tid; e < KD; e += KM_THREADS) a.centroids_out[q * KD + e] = (float)s.cen64[e];
+    if (a.assign_out)
+        for (int i = lo + tid; i < hi; i += KM_THREADS) a.assign_out[(long long)q * n + i] = asg[i];
+    if (a.codes) {
+        const int head = q / a.m_sub, j = q % a.m_sub;
+        uint16_t* cd = a.codes + (long long)head * a.codes_head_stride + j;
+        for (int i = lo + tid; i < hi; i += KM_THREADS) cd[(long long)i * a.m_sub] = (uint16_t)asg[i];
+    }
+    if (a.iterations && tid == 0 && r == 0) a.iterations[q] = (uint32_t)iters;
+    tick(5);
+    if (tid == 0 && r == 0 && a.timers)
+        for (int ph = 0; ph < 6; ++ph) a.timers[(long long)q * 8 + ph] = t_acc[ph];
+    cl.sync();  // keep smem alive for remote readers
+}
+
+template <int D>
+void launch_cluster_v2(const KmArgs& a, uint32_t* members, int problems, int R, size_t smem, cudaStream_t st) {
+    auto kern = kmeans_cluster_kernel<D>;
+    PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(problems * R));
+    cfg.blockDim = dim3(KM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)R;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PQKV_CUDA(cudaLaunchKernelEx(&cfg, kern, a, members));
+    PQKV_LAUNCHED("kmeans_cluster_kernel");
+}
+
 template <int D, bool F>
 void launch_problem(const KmArgs& a, int problems, size_t smem, cudaStream_t st) {
     auto kern = kmeans_problem_kernel<D, F>;
@@ -861,7 +1398,19 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
         if (D > 0 && !cen64_smem) D = 0;  // register path reads smem centroids
     }
 
+    // v2 (cluster of R CTAs per problem) for the filtered path with smem tables
+    const bool v2 = filter && D >= 8 && K <= 1024 && v2_smem_bytes((int)K, D) <= 200 * 1024 &&
+                    std::getenv("PQKV_KMEANS_V1") == nullptr;
+    int R = 1;
+    if (v2) {
+        R = (int)std::max<size_t>(1, (size_t)ctx->sm_count / Q);
+        R = std::min(R, 8);
+        R = (int)std::min<size_t>((size_t)R, std::max<size_t>(1, ceil_div(n, 4096)));
+        while (R & (R - 1)) --R;  // power of two
+    }
+
     Scratch sc(ctx);
+    size_t h_mem = sc.plan<uint32_t>(v2 ? Q * n : 1);
     size_t h_draws = sc.plan<unsigned long long>(Q * K);
     size_t h_a0 = sc.plan<uint32_t>(Q * n), h_a1 = sc.plan<uint32_t>(Q * n);
     size_t h_x0 = sc.plan<double>(Q * n), h_x1 = sc.plan<double>(Q * n);
@@ -919,7 +1468,18 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
 
     bind_device(ctx);
     int P = (int)Q;
-    if (filter) {
+    if (v2) {
+        const size_t smem2 = v2_smem_bytes((int)K, D);
+        uint32_t* members = sc.get<uint32_t>(h_mem);
+        switch (D) {
+            case 8: launch_cluster_v2<8>(a, members, P, R, smem2, st); break;
+            case 16: launch_cluster_v2<16>(a, members, P, R, smem2, st); break;
+            case 32: launch_cluster_v2<32>(a, members, P, R, smem2, st); break;
+            case 64: launch_cluster_v2<64>(a, members, P, R, smem2, st); break;
+            case 128: launch_cluster_v2<128>(a, members, P, R, smem2, st); break;
+            default: fail(PQKV_ERUNTIME, "kmeans: bad v2 dim");
+        }
+    } else if (filter) {
         switch (D) {
             case 2: launch_problem<2, true>(a, P, smem, st); break;
             case 4: launch_problem<4, true>(a, P, smem, st); break;

@@ -9,7 +9,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-MODES = ["filtered", "exact"]
+MODES = ["filtered", "exact", "filtered_v1"]
 
 
 def _t(a):
@@ -20,10 +20,17 @@ def _t(a):
 
 @pytest.fixture(params=MODES)
 def mode_ctx(ctx, request):
+    """filtered: cluster-split v2 kernel (default); filtered_v1: one CTA per
+    problem; exact: fp64 assign everywhere (v1)."""
+    import os
+
     import paper_2407_12820_b200 as pq
 
-    ctx.set_assign_mode(pq.ASSIGN_FILTERED if request.param == "filtered" else pq.ASSIGN_EXACT)
+    ctx.set_assign_mode(pq.ASSIGN_EXACT if request.param == "exact" else pq.ASSIGN_FILTERED)
+    if request.param == "filtered_v1":
+        os.environ["PQKV_KMEANS_V1"] = "1"
     yield ctx
+    os.environ.pop("PQKV_KMEANS_V1", None)
     ctx.set_assign_mode(pq.ASSIGN_FILTERED)
 
 
@@ -84,6 +91,18 @@ def test_pq_construct_bit_exact(mode_ctx, orc, s, d_h, m, b, T):
         wc, wcd = orc.pq_construct(k[h], m, b, T, seeds[h])
         assert np.array_equal(codes[h], wcd)
         assert np.array_equal(cen[h].view(np.uint32), wc.view(np.uint32))
+
+
+@pytest.mark.parametrize("s,kind", [(32768, oracle.POWERLAW), (20000, oracle.GAUSSIAN)])
+def test_pq_construct_cluster_split_large(ctx, orc, s, kind):
+    """v2 with an 8-CTA cluster per problem on realistic keys (gaussian mixture
+    of the e2e workload and the powerlaw profile), m2b6 and m4b8."""
+    k, _, _ = orc.gen_workload(s, 128, 1, 1, kind, seed=s)
+    for m, b in [(2, 6), (4, 8)]:
+        cen, codes = ctx.pq_build(_t(k), m, b, 10, [s + m])
+        wc, wcd = orc.pq_construct(k[0], m, b, 10, s + m)
+        assert np.array_equal(codes[0].cpu().numpy().view(np.uint16), wcd)
+        assert np.array_equal(cen[0].cpu().numpy(), wc)
 
 
 def test_pq_construct_32k_powerlaw(ctx, orc):
