@@ -63,6 +63,7 @@ struct KmArgs {
     int counts_smem, sums_smem, cen64_smem, cenf_smem;
     int vec4;  // point rows are 16-byte aligned
     unsigned long long* timers;  // [q][8] per-phase SM cycles (thread 0's view)
+    uint16_t* nearseed;          // [q][n] v2: seed index achieving min_d2 (pruning only)
 };
 
 struct Smem {
@@ -295,14 +296,18 @@ __device__ double exact_running_sum(const double* v, int n, double* pre, double*
     constexpr int E = 4, GROUP = KM_THREADS * E;
     int* ish = reinterpret_cast<int*>(iscr + 2 * KM_WARPS);
     double S = 0.0;
+    double nx[E];  // next group's values, prefetched while this group runs
+#pragma unroll
+    for (int e = 0; e < E; ++e) nx[e] = tid * E + e < n ? v[tid * E + e] : 0.0;
     for (int g0 = 0; g0 < n; g0 += GROUP) {
         const int cnt = min(GROUP, n - g0);
         double a[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int li = tid * E + e;
-            a[e] = g0 + li < n ? v[g0 + li] : 0.0;
+            a[e] = nx[e];
             gbuf[li] = a[e];
+            nx[e] = g0 + GROUP + li < n ? v[g0 + GROUP + li] : 0.0;
         }
         __syncthreads();
         int j = 0;  // first element of the group not yet summed (block uniform)
@@ -889,6 +894,7 @@ struct V2Smem {
     float* cenf;         // [K*D]
     float* cnorm;        // [K]
     double* cen64;       // [K*D]
+    double* dseed2;      // [K] squared distance of seed j to the newest seed
 };
 
 __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
@@ -897,7 +903,7 @@ __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
     b = (b + 15) / 16 * 16;
     b += (size_t)K * D * 4 + (size_t)K * 4;
     b = (b + 15) / 16 * 16;
-    b += (size_t)K * D * 8;
+    b += (size_t)K * D * 8 + (size_t)K * 8;
     return b;
 }
 
@@ -931,7 +937,8 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
         s.cenf = reinterpret_cast<float*>(p); p += KD * 4;
         s.cnorm = reinterpret_cast<float*>(p); p += K * 4;
         p = smem_raw + (p - smem_raw + 15) / 16 * 16;
-        s.cen64 = reinterpret_cast<double*>(p);
+        s.cen64 = reinterpret_cast<double*>(p); p += KD * 8;
+        s.dseed2 = reinterpret_cast<double*>(p);
     }
     uint32_t* asg = a.asg0 + (long long)q * n;
     uint32_t* nxt = a.asg1 + (long long)q * n;
@@ -939,6 +946,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
     double* aux1 = a.aux1 + (long long)q * n;
     uint32_t* queue = a.queue + (long long)q * n;
     uint32_t* mem = members_g + (long long)q * n;
+    uint16_t* nears = a.nearseed + (long long)q * n;
     double* gcen = a.cen64 + q * KD;
     __shared__ int sh_int[8];
     __shared__ float sh_cmax;
@@ -1223,7 +1231,10 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
         const int c0 = (int)(draws[0] % (unsigned long long)n);
         for (int t = tid; t < D; t += KM_THREADS) s.cen64[t] = (double)point_ptr(a, q, c0)[t];
         __syncthreads();
-        for (int i = lo + tid; i < hi; i += KM_THREADS) aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64, D);
+        for (int i = lo + tid; i < hi; i += KM_THREADS) {
+            aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64, D);
+            nears[i] = 0;
+        }
         for (int c = 1; c < K; ++c) {
             cl.sync();  // every slice's min_d2 is final for this step
             tick(1);
@@ -1248,12 +1259,26 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
                 s.cen64[(long long)c * D + t] = (double)point_ptr(a, q, chosen)[t];
             __syncthreads();
             const double* cc = s.cen64 + (long long)c * D;
+            // triangle inequality: d(x, mu_c) >= d(mu_j, mu_c) - d(x, mu_j) with j the
+            // seed behind min_d2(x); if d(mu_j, mu_c)^2 >= 4 min_d2 (+ margin for
+            // fp64 rounding) then min(min_d2, dist2(x, mu_c)) == min_d2: skip x.
+            for (int j = tid; j < c; j += KM_THREADS) {
+                double acc = 0.0;
+                for (int t = 0; t < D; ++t) {
+                    const double df = s.cen64[(long long)j * D + t] - cc[t];
+                    acc = fma(df, df, acc);
+                }
+                s.dseed2[j] = acc * (1.0 - 1e-12);
+            }
             float cf[D];
             float cn = 0.f;
 #pragma unroll
             for (int t = 0; t < D; ++t) { cf[t] = (float)cc[t]; cn = fmaf(cf[t], cf[t], cn); }
             cn = sqrtf(cn) * (1.0f + 9.6e-7f) + 1e-30f;
+            __syncthreads();
             for (int i = lo + tid; i < hi; i += KM_THREADS) {
+                const double md = aux0[i];
+                if (s.dseed2[nears[i]] >= 4.0 * md * (1.0 + 1e-7) + 1e-300) continue;
                 const float* xp = point_ptr(a, q, i);
                 float xr[D];
                 load_point<D>(xp, xr, a.vec4);
@@ -1263,10 +1288,13 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
                     const float d = xr[t] - cf[t];
                     acc = fmaf(d, d, acc);
                 }
-                const double old = aux0[i];
+                const double old = md;
                 if (acc < 1e37f && (double)(acc - err_bound(acc, cn, D)) > old) continue;
                 const double d = dist2_g(xp, cc, D);
-                if (d < old) aux0[i] = d;
+                if (d < old) {
+                    aux0[i] = d;
+                    nears[i] = (uint16_t)c;
+                }
             }
         }
         cl.sync();
@@ -1399,7 +1427,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     }
 
     // v2 (cluster of R CTAs per problem) for the filtered path with smem tables
-    const bool v2 = filter && D >= 8 && K <= 1024 && v2_smem_bytes((int)K, D) <= 200 * 1024 &&
+    const bool v2 = filter && D >= 8 && K <= 1024 && K <= 65536 && v2_smem_bytes((int)K, D) <= 200 * 1024 &&
                     std::getenv("PQKV_KMEANS_V1") == nullptr;
     int R = 1;
     if (v2) {
@@ -1411,6 +1439,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
 
     Scratch sc(ctx);
     size_t h_mem = sc.plan<uint32_t>(v2 ? Q * n : 1);
+    size_t h_near = sc.plan<uint16_t>(v2 ? Q * n : 1);
     size_t h_draws = sc.plan<unsigned long long>(Q * K);
     size_t h_a0 = sc.plan<uint32_t>(Q * n), h_a1 = sc.plan<uint32_t>(Q * n);
     size_t h_x0 = sc.plan<double>(Q * n), h_x1 = sc.plan<double>(Q * n);
@@ -1459,6 +1488,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     a.queue = sc.get<uint32_t>(h_q);
     a.stats = ctx->d_stats;
     a.timers = sc.get<unsigned long long>(h_tm);
+    a.nearseed = sc.get<uint16_t>(h_near);
     a.counts_smem = counts_smem;
     a.sums_smem = sums_smem;
     a.cen64_smem = cen64_smem;
