@@ -149,8 +149,8 @@ class Context:
         """SM cycles per phase of problem 0 of the last build."""
         arr = (_u64 * 8)()
         _check(lib().pqkv_ctx_last_build_profile(self.h, arr))
-        names = ["seed_chain", "seed_dist", "assign", "-", "update", "other"]
-        return {n: int(arr[i]) for i, n in enumerate(names) if n != "-"}
+        names = ["seed_chain", "seed_dist", "assign", "update_scatter", "update", "other"]
+        return {n: int(arr[i]) for i, n in enumerate(names)}
 
     # ---- (A) build ---------------------------------------------------------
     def kmeans_fit(self, points, k: int, max_iter: int, seeds, inertia: bool = False):

@@ -64,6 +64,8 @@ struct KmArgs {
     int vec4;  // point rows are 16-byte aligned
     unsigned long long* timers;  // [q][8] per-phase SM cycles (thread 0's view)
     uint16_t* nearseed;          // [q][n] v2: seed index achieving min_d2 (pruning only)
+    float* ubound;               // [q][n] v2 Hamerly upper bound (distance to own centroid)
+    float* lbound;               // [q][n] v2 Hamerly lower bound (distance to any other)
 };
 
 struct Smem {
@@ -241,6 +243,55 @@ __device__ __forceinline__ void load_point(const float* xp, float (&x)[D], bool 
     }
 #pragma unroll
     for (int t = 0; t < D; ++t) x[t] = __ldg(xp + t);
+}
+
+// Filtered nearest that also returns Hamerly bounds for a certified point:
+// ub >= true distance to the returned centroid, lb <= true distance to every
+// other centroid (both rounded outward).  Returns -1 when not certified.
+template <int D>
+__device__ int nearest_filtered_b(const float (&x)[D], const float* __restrict__ cenf,
+                                  const float* __restrict__ cnorm, float cnorm_max, int K, float& ub,
+                                  float& lb) {
+    float b1 = FLT_MAX, b2 = FLT_MAX;
+    int i1 = 0;
+    int c = 0;
+    for (; c + 4 <= K; c += 4) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        const float* c0 = cenf + c * D;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            float d0 = x[t] - c0[t];
+            float d1 = x[t] - c0[D + t];
+            float d2 = x[t] - c0[2 * D + t];
+            float d3 = x[t] - c0[3 * D + t];
+            a0 = fmaf(d0, d0, a0);
+            a1 = fmaf(d1, d1, a1);
+            a2 = fmaf(d2, d2, a2);
+            a3 = fmaf(d3, d3, a3);
+        }
+        float av[4] = {a0, a1, a2, a3};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float v = av[e];
+            if (v < b1) { b2 = b1; b1 = v; i1 = c + e; }
+            else if (v < b2) { b2 = v; }
+        }
+    }
+    for (; c < K; ++c) {
+        float v = dist_f<D>(x, cenf + c * D);
+        if (v < b1) { b2 = b1; b1 = v; i1 = c; }
+        else if (v < b2) { b2 = v; }
+    }
+    if (!(b1 < 1e37f)) return -1;
+    const float e1 = err_bound(b1, cnorm[i1], D);
+    ub = __fsqrt_ru(__fmul_ru(__fadd_ru(b1, e1), 1.000001f));
+    if (K == 1) { lb = INFINITY; return 0; }
+    const float u = 5.9604645e-8f;
+    if (!(b2 < 1e37f) || !(b2 > 8.0f * u * u * cnorm_max * cnorm_max)) return -1;
+    const float e2 = err_bound(b2, cnorm_max, D);
+    if (!(b2 - e2 > b1 + e1)) return -1;
+    lb = __fsqrt_rd(fmaxf(0.f, __fmul_rd(__fsub_rd(b2, e2), 0.999999f)));
+    return i1;
 }
 
 // ---- block helpers --------------------------------------------------------
@@ -895,6 +946,7 @@ struct V2Smem {
     float* cnorm;        // [K]
     double* cen64;       // [K*D]
     double* dseed2;      // [K] squared distance of seed j to the newest seed
+    float* delta;        // [K] centroid movement of the last update (rounded up)
 };
 
 __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
@@ -903,7 +955,7 @@ __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
     b = (b + 15) / 16 * 16;
     b += (size_t)K * D * 4 + (size_t)K * 4;
     b = (b + 15) / 16 * 16;
-    b += (size_t)K * D * 8 + (size_t)K * 8;
+    b += (size_t)K * D * 8 + (size_t)K * 8 + (size_t)K * 4;
     return b;
 }
 
@@ -938,7 +990,8 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
         s.cnorm = reinterpret_cast<float*>(p); p += K * 4;
         p = smem_raw + (p - smem_raw + 15) / 16 * 16;
         s.cen64 = reinterpret_cast<double*>(p); p += KD * 8;
-        s.dseed2 = reinterpret_cast<double*>(p);
+        s.dseed2 = reinterpret_cast<double*>(p); p += K * 8;
+        s.delta = reinterpret_cast<float*>(p);
     }
     uint32_t* asg = a.asg0 + (long long)q * n;
     uint32_t* nxt = a.asg1 + (long long)q * n;
@@ -947,6 +1000,11 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
     uint32_t* queue = a.queue + (long long)q * n;
     uint32_t* mem = members_g + (long long)q * n;
     uint16_t* nears = a.nearseed + (long long)q * n;
+    float* ubd = a.ubound + (long long)q * n;
+    float* lbd = a.lbound + (long long)q * n;
+    __shared__ float sh_dmax1, sh_dmax2;
+    __shared__ int sh_dargmax;
+    bool bounds_valid = false;
     double* gcen = a.cen64 + q * KD;
     __shared__ int sh_int[8];
     __shared__ float sh_cmax;
@@ -993,18 +1051,39 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
     };
 
     // ---- assignment pass over this CTA's slice (+ cluster-wide repair) ----
-    auto assign_pass = [&](uint32_t* out) {
+    // Hamerly bounds (certified): a point whose moved upper bound stays below
+    // its moved lower bound keeps its centroid -- it is provably the unique
+    // nearest in exact arithmetic and the fp64 margins exceed rounding -- so
+    // neither its row nor any distance is touched.
+    auto assign_pass = [&](uint32_t* out, const uint32_t* prev) {
         for (int c = tid; c < K; c += KM_THREADS) s.cnt_loc[c] = 0;
         if (tid == 0) sh_int[0] = 0;
         __syncthreads();
         const float cmax = sh_cmax;
+        const float dm1 = sh_dmax1, dm2 = sh_dmax2;
+        const int dma = sh_dargmax;
         for (int i = lo + tid; i < hi; i += KM_THREADS) {
+            if (bounds_valid) {
+                const uint32_t ap = prev[i];
+                const float u = __fadd_ru(ubd[i], s.delta[ap]);
+                const float l = __fsub_rd(lbd[i], (int)ap == dma ? dm2 : dm1);
+                if (__fmul_ru(u, 1.000001f) < l) {
+                    out[i] = ap;
+                    atomicAdd(&s.cnt_loc[ap], 1u);
+                    ubd[i] = u;
+                    lbd[i] = l;
+                    continue;
+                }
+            }
             float x[D];
             load_point<D>(point_ptr(a, q, i), x, a.vec4);
-            int c = nearest_filtered<D>(x, s.cenf, s.cnorm, cmax, K);
+            float ub, lb;
+            int c = nearest_filtered_b<D>(x, s.cenf, s.cnorm, cmax, K, ub, lb);
             if (c >= 0) {
                 out[i] = (uint32_t)c;
                 atomicAdd(&s.cnt_loc[c], 1u);
+                ubd[i] = ub;
+                lbd[i] = lb;
             } else {
                 queue[lo + atomicAdd(&sh_int[0], 1)] = (uint32_t)i;
             }
@@ -1016,6 +1095,8 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             const uint32_t c = nearest_g(point_ptr(a, q, i), s.cen64, K, D);
             out[i] = c;
             atomicAdd(&s.cnt_loc[c], 1u);
+            ubd[i] = INFINITY;  // re-scan next pass
+            lbd[i] = 0.f;
         }
         if (tid == 0 && a.stats) {
             atomicAdd(&a.stats[0], (unsigned long long)qn);
@@ -1065,6 +1146,8 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
                     s.cnt_all[out[donor]] -= 1;
                     out[donor] = (uint32_t)c;
                     s.cnt_all[c] += 1;
+                    ubd[donor] = INFINITY;  // not at its nearest centroid any more
+                    lbd[donor] = 0.f;
                 }
                 __syncthreads();
             }
@@ -1113,6 +1196,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             __syncthreads();
         }
         cl.sync();  // every slice's member list is written
+        tick(3);
         // sums: warp gw of the cluster owns clusters c = gw (mod KM_WARPS*R)
         constexpr int DG = 32 / V2_MG;                       // lanes per member group (8)
         constexpr int DPL = (D + DG - 1) / DG;               // dims per lane
@@ -1188,6 +1272,33 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             }
         }
         cl.sync();  // new means visible in global memory
+        // centroid movement (Hamerly): delta_c >= |mu_c(new) - mu_c(old)|
+        for (int c = tid; c < K; c += KM_THREADS) {
+            double dd = 0.0;
+            for (int t = 0; t < D; ++t) {
+                const double df = gcen[(long long)c * D + t] - s.cen64[(long long)c * D + t];
+                dd = fma(df, df, dd);
+            }
+            s.delta[c] = __double2float_ru(__dsqrt_ru(dd * (1.0 + 1e-12)));
+        }
+        __syncthreads();
+        if (warp == 0) {  // largest and second largest movement
+            float m1 = 0.f, m2 = 0.f;
+            int i1 = -1;
+            for (int c = lane; c < K; c += 32) {
+                const float v = s.delta[c];
+                if (v > m1) { m2 = m1; m1 = v; i1 = c; }
+                else if (v > m2) m2 = v;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float om1 = __shfl_xor_sync(FULL, m1, o), om2 = __shfl_xor_sync(FULL, m2, o);
+                const int oi = __shfl_xor_sync(FULL, i1, o);
+                if (om1 > m1) { m2 = fmaxf(m1, om2); m1 = om1; i1 = oi; }
+                else m2 = fmaxf(m2, om1);
+            }
+            if (lane == 0) { sh_dmax1 = m1; sh_dmax2 = m2; sh_dargmax = i1; }
+        }
         for (long long e = tid; e < KD; e += KM_THREADS) s.cen64[e] = gcen[e];
         __syncthreads();
     };
@@ -1309,7 +1420,8 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
     // =====================================================================
     // 2. Lloyd iterations (kmeans.cpp:174-183)
     // =====================================================================
-    assign_pass(asg);
+    assign_pass(asg, nullptr);
+    bounds_valid = true;
     tick(2);
     int iters = 0;
     for (int iter = 1; iter <= T; ++iter) {
@@ -1328,7 +1440,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
         iters = iter;
         refresh_f32();
         tick(5);
-        assign_pass(nxt);
+        assign_pass(nxt, asg);
         tick(2);
         int changed = 0;
         for (int i = lo + tid; i < hi; i += KM_THREADS) changed |= (nxt[i] != asg[i]);
@@ -1440,6 +1552,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     Scratch sc(ctx);
     size_t h_mem = sc.plan<uint32_t>(v2 ? Q * n : 1);
     size_t h_near = sc.plan<uint16_t>(v2 ? Q * n : 1);
+    size_t h_ub = sc.plan<float>(v2 ? Q * n : 1), h_lb = sc.plan<float>(v2 ? Q * n : 1);
     size_t h_draws = sc.plan<unsigned long long>(Q * K);
     size_t h_a0 = sc.plan<uint32_t>(Q * n), h_a1 = sc.plan<uint32_t>(Q * n);
     size_t h_x0 = sc.plan<double>(Q * n), h_x1 = sc.plan<double>(Q * n);
@@ -1489,6 +1602,8 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     a.stats = ctx->d_stats;
     a.timers = sc.get<unsigned long long>(h_tm);
     a.nearseed = sc.get<uint16_t>(h_near);
+    a.ubound = sc.get<float>(h_ub);
+    a.lbound = sc.get<float>(h_lb);
     a.counts_smem = counts_smem;
     a.sums_smem = sums_smem;
     a.cen64_smem = cen64_smem;
