@@ -1057,7 +1057,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
     // neither its row nor any distance is touched.
     auto assign_pass = [&](uint32_t* out, const uint32_t* prev) {
         for (int c = tid; c < K; c += KM_THREADS) s.cnt_loc[c] = 0;
-        if (tid == 0) sh_int[0] = 0;
+        if (tid == 0) { sh_int[0] = 0; sh_int[4] = 0; }
         __syncthreads();
         const float cmax = sh_cmax;
         const float dm1 = sh_dmax1, dm2 = sh_dmax2;
@@ -1072,6 +1072,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
                     atomicAdd(&s.cnt_loc[ap], 1u);
                     ubd[i] = u;
                     lbd[i] = l;
+                    atomicAdd(&sh_int[4], 1);
                     continue;
                 }
             }
@@ -1101,6 +1102,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
         if (tid == 0 && a.stats) {
             atomicAdd(&a.stats[0], (unsigned long long)qn);
             atomicAdd(&a.stats[1], (unsigned long long)(hi - lo));
+            atomicAdd(&a.stats[2], (unsigned long long)sh_int[4]);
         }
         merge_counts();
         if (n < K) return;
@@ -1242,33 +1244,42 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
                     aabs[e] += __shfl_xor_sync(FULL, aabs[e], o);
                     emin[e] = min(emin[e], __shfl_xor_sync(FULL, emin[e], o));
                 }
-            // certificate: sum|x| < 2^52 * ulp_min (ulp of the smallest-exponent
+            // certificate per dim: sum|x| < 2^52 * ulp_min (ulp of the smallest-exponent
             // member: 2^(e-150) for normal e, 2^-149 for subnormals)
-            bool ok = true;
+            unsigned badm = 0;  // failing dims of this lane, bit e
 #pragma unroll
             for (int e = 0; e < DPL; ++e) {
                 if (dl + DG * e >= D || emin[e] == 0x7fffffff) continue;
                 const int ue = emin[e] == 0 ? -149 : emin[e] - 150;
-                ok = ok && (aabs[e] * (1.0 + 1e-9) < ldexp(1.0, 52 + ue));
+                if (!(aabs[e] * (1.0 + 1e-9) < ldexp(1.0, 52 + ue))) badm |= 1u << e;
             }
-            ok = __all_sync(FULL, ok);
-            if (!ok) {
-                // exact fallback: the reference's order (points ascending), lanes = dims
-                for (int t0 = 0; t0 < D; t0 += 32) {
-                    const int t = t0 + lane;
-                    double sacc = 0.0;
-                    for (uint32_t m = 0; m < cnt; ++m) {
-                        const float* xp = point_ptr(a, q, (int)mem[base + m]);
-                        if (t < D) sacc = __dadd_rn(sacc, (double)__ldg(xp + t));
-                    }
-                    if (t < D) gcen[(long long)c * D + t] = __ddiv_rn(sacc, (double)cnt);
-                }
-            } else if (mg == 0) {
+            if (mg == 0) {
 #pragma unroll
                 for (int e = 0; e < DPL; ++e) {
                     const int t = dl + DG * e;
-                    if (t < D) gcen[(long long)c * D + t] = __ddiv_rn(acc[e], (double)cnt);
+                    if (t < D && !((badm >> e) & 1u)) gcen[(long long)c * D + t] = __ddiv_rn(acc[e], (double)cnt);
                 }
+            }
+            // exact fallback for failing dims: the reference's order (points
+            // ascending), 32 members per step -- indices and values fetched in
+            // parallel, then folded serially through the warp
+            unsigned any = __ballot_sync(FULL, mg == 0 && badm != 0);
+            while (any) {
+                const int src = __ffs(any) - 1;
+                const unsigned bm = __shfl_sync(FULL, badm, src);
+                const int e = __ffs(bm) - 1;
+                const int t = (src % DG) + DG * e;
+                double sacc = 0.0;
+                for (uint32_t m0 = 0; m0 < cnt; m0 += 32) {
+                    const uint32_t m = m0 + lane;
+                    const float xv = m < cnt ? __ldg(point_ptr(a, q, (int)mem[base + m]) + t) : 0.0f;
+                    const int nb = (int)min(32u, cnt - m0);
+                    for (int l = 0; l < nb; ++l) sacc = __dadd_rn(sacc, (double)__shfl_sync(FULL, xv, l));
+                }
+                if (lane == 0) gcen[(long long)c * D + t] = __ddiv_rn(sacc, (double)cnt);
+                // clear (src, e) and continue with the next failing dim
+                if (lane == src) badm &= ~(1u << e);
+                any = __ballot_sync(FULL, mg == 0 && badm != 0);
             }
         }
         cl.sync();  // new means visible in global memory
@@ -1573,7 +1584,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     }
     PQKV_CUDA(cudaMemcpyAsync(sc.get<unsigned long long>(h_draws), draws.data(),
                               draws.size() * 8, cudaMemcpyHostToDevice, st));
-    PQKV_CUDA(cudaMemsetAsync(ctx->d_stats, 0, 2 * sizeof(unsigned long long), st));
+    PQKV_CUDA(cudaMemsetAsync(ctx->d_stats, 0, 4 * sizeof(unsigned long long), st));
 
     KmArgs a{};
     a.points = b.points;
@@ -1646,13 +1657,14 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
             default: launch_problem<0, false>(a, P, smem, st); break;
         }
     }
-    unsigned long long stats[2] = {0, 0};
+    unsigned long long stats[4] = {0, 0, 0, 0};
     PQKV_CUDA(cudaMemcpyAsync(stats, ctx->d_stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
     PQKV_CUDA(cudaMemcpyAsync(ctx->last_phase_cycles, a.timers, 8 * sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost, st));
     PQKV_CUDA(cudaStreamSynchronize(st));
     ctx->last_rechecked = stats[0];
     ctx->last_total = stats[1];
+    ctx->last_phase_cycles[6] = stats[2];  // Hamerly-skipped point visits
 }
 
 void launch_encode(pqkv_ctx* ctx, const float* keys, size_t n_heads, size_t key_stride,
