@@ -149,7 +149,8 @@ class Context:
         """SM cycles per phase of problem 0 of the last build."""
         arr = (_u64 * 8)()
         _check(lib().pqkv_ctx_last_build_profile(self.h, arr))
-        names = ["seed_chain", "seed_dist", "assign", "update_scatter", "update", "other", "skipped_points"]
+        names = ["seed_chain", "seed_dist", "assign", "update_scatter", "update", "other", "skipped_points",
+                 "seed_skipped_points"]
         return {n: int(arr[i]) for i, n in enumerate(names)}
 
     # ---- (A) build ---------------------------------------------------------

@@ -294,6 +294,70 @@ __device__ int nearest_filtered_b(const float (&x)[D], const float* __restrict__
     return i1;
 }
 
+// Expanded-form fp32 filter: S_e = fl(fl(|x|^2 + |cf|^2) - 2 fl(x.cf)) with
+// FMA chains -- one FFMA per (point, centroid, dim) instead of a sub and an
+// FMA.  Rigorous bound on |S_e - S64|: the dot and the norms carry
+// gamma_D (|x| + |cf|)^2, the two final roundings u*S_e, and the f32 rounding
+// of the fp64 centroid 2u sqrt(S)|c| + u^2|c|^2; E_exp doubles the sum (which
+// also covers gamma_D vs D*u and S vs S_e) and adds the subnormal slack.
+__device__ __forceinline__ float err_bound_exp(float s, float xn, float cn, int D) {
+    const float u = 5.9604645e-8f;
+    const float su = sqrtf(fmaxf(s, 0.0f));
+    const float xc = xn + cn;
+    return 2.0f * ((D + 4) * u * xc * xc + u * fabsf(s) + 2.0f * u * su * cn + u * u * cn * cn) +
+           D * 7.2e-43f;
+}
+
+template <int D>
+__device__ int nearest_filtered_exp(const float (&x)[D], const float* __restrict__ cenf,
+                                    const float* __restrict__ ncf, const float* __restrict__ cnorm,
+                                    float cnorm_max, int K, float& ub, float& lb) {
+    float nx = 0.f;
+#pragma unroll
+    for (int t = 0; t < D; ++t) nx = fmaf(x[t], x[t], nx);
+    const float xn = sqrtf(nx) * 1.000001f + 1e-30f;
+    float b1 = FLT_MAX, b2 = FLT_MAX;
+    int i1 = 0;
+    int c = 0;
+    for (; c + 4 <= K; c += 4) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        const float* c0 = cenf + c * D;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            a0 = fmaf(x[t], c0[t], a0);
+            a1 = fmaf(x[t], c0[D + t], a1);
+            a2 = fmaf(x[t], c0[2 * D + t], a2);
+            a3 = fmaf(x[t], c0[3 * D + t], a3);
+        }
+        float av[4] = {fmaf(-2.f, a0, nx + ncf[c]), fmaf(-2.f, a1, nx + ncf[c + 1]),
+                       fmaf(-2.f, a2, nx + ncf[c + 2]), fmaf(-2.f, a3, nx + ncf[c + 3])};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float v = av[e];
+            if (v < b1) { b2 = b1; b1 = v; i1 = c + e; }
+            else if (v < b2) { b2 = v; }
+        }
+    }
+    for (; c < K; ++c) {
+        float dd = 0.f;
+#pragma unroll
+        for (int t = 0; t < D; ++t) dd = fmaf(x[t], cenf[c * D + t], dd);
+        float v = fmaf(-2.f, dd, nx + ncf[c]);
+        if (v < b1) { b2 = b1; b1 = v; i1 = c; }
+        else if (v < b2) { b2 = v; }
+    }
+    if (!(b1 < 1e37f) || !(nx < 1e37f)) return -1;
+    const float e1 = err_bound_exp(b1, xn, cnorm[i1], D);
+    ub = __fsqrt_ru(fmaxf(0.f, __fmul_ru(__fadd_ru(b1, e1), 1.000001f)));
+    if (K == 1) { lb = INFINITY; return 0; }
+    const float u = 5.9604645e-8f;
+    if (!(b2 < 1e37f) || !(b2 > 8.0f * u * u * cnorm_max * cnorm_max)) return -1;
+    const float e2 = err_bound_exp(b2, xn, cnorm_max, D);
+    if (!(b2 - e2 > b1 + e1)) return -1;
+    lb = __fsqrt_rd(fmaxf(0.f, __fmul_rd(__fsub_rd(b2, e2), 0.999999f)));
+    return i1;
+}
+
 // ---- block helpers --------------------------------------------------------
 
 __device__ __forceinline__ void block_sync() { __syncthreads(); }
@@ -947,6 +1011,7 @@ struct V2Smem {
     double* cen64;       // [K*D]
     double* dseed2;      // [K] squared distance of seed j to the newest seed
     float* delta;        // [K] centroid movement of the last update (rounded up)
+    float* ncf;          // [K] |cf|^2 in fp32 (expanded-form filter)
 };
 
 __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
@@ -955,7 +1020,7 @@ __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
     b = (b + 15) / 16 * 16;
     b += (size_t)K * D * 4 + (size_t)K * 4;
     b = (b + 15) / 16 * 16;
-    b += (size_t)K * D * 8 + (size_t)K * 8 + (size_t)K * 4;
+    b += (size_t)K * D * 8 + (size_t)K * 8 + (size_t)K * 4 + (size_t)K * 4;
     return b;
 }
 
@@ -991,7 +1056,8 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
         p = smem_raw + (p - smem_raw + 15) / 16 * 16;
         s.cen64 = reinterpret_cast<double*>(p); p += KD * 8;
         s.dseed2 = reinterpret_cast<double*>(p); p += K * 8;
-        s.delta = reinterpret_cast<float*>(p);
+        s.delta = reinterpret_cast<float*>(p); p += K * 4;
+        s.ncf = reinterpret_cast<float*>(p);
     }
     uint32_t* asg = a.asg0 + (long long)q * n;
     uint32_t* nxt = a.asg1 + (long long)q * n;
@@ -1036,6 +1102,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             for (int t = 0; t < D; ++t) acc = fmaf(s.cenf[c * D + t], s.cenf[c * D + t], acc);
             float nrm = sqrtf(acc) * (1.0f + 9.6e-7f) + 1e-30f;
             s.cnorm[c] = nrm;
+            s.ncf[c] = acc;
             atomicMax(reinterpret_cast<int*>(&sh_cmax), __float_as_int(nrm));
         }
         __syncthreads();
@@ -1079,7 +1146,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             float x[D];
             load_point<D>(point_ptr(a, q, i), x, a.vec4);
             float ub, lb;
-            int c = nearest_filtered_b<D>(x, s.cenf, s.cnorm, cmax, K, ub, lb);
+            int c = nearest_filtered_exp<D>(x, s.cenf, s.ncf, s.cnorm, cmax, K, ub, lb);
             if (c >= 0) {
                 out[i] = (uint32_t)c;
                 atomicAdd(&s.cnt_loc[c], 1u);
@@ -1357,6 +1424,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             aux0[i] = dist2_g(point_ptr(a, q, i), s.cen64, D);
             nears[i] = 0;
         }
+        if (tid == 0) sh_int[5] = 0;
         for (int c = 1; c < K; ++c) {
             cl.sync();  // every slice's min_d2 is final for this step
             tick(1);
@@ -1400,7 +1468,10 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             __syncthreads();
             for (int i = lo + tid; i < hi; i += KM_THREADS) {
                 const double md = aux0[i];
-                if (s.dseed2[nears[i]] >= 4.0 * md * (1.0 + 1e-7) + 1e-300) continue;
+                if (s.dseed2[nears[i]] >= 4.0 * md * (1.0 + 1e-7) + 1e-300) {
+                    atomicAdd(&sh_int[5], 1);
+                    continue;
+                }
                 const float* xp = point_ptr(a, q, i);
                 float xr[D];
                 load_point<D>(xp, xr, a.vec4);
@@ -1421,6 +1492,7 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
         }
         cl.sync();
         tick(1);
+        if (tid == 0 && a.stats) atomicAdd(&a.stats[3], (unsigned long long)sh_int[5]);
         if (r == 0)
             for (long long e = tid; e < KD; e += KM_THREADS) gcen[e] = s.cen64[e];
         // (no sync needed: gcen is read after the next cluster barrier)
@@ -1665,6 +1737,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     ctx->last_rechecked = stats[0];
     ctx->last_total = stats[1];
     ctx->last_phase_cycles[6] = stats[2];  // Hamerly-skipped point visits
+    ctx->last_phase_cycles[7] = stats[3];  // k-means++ triangle-skipped point visits
 }
 
 void launch_encode(pqkv_ctx* ctx, const float* keys, size_t n_heads, size_t key_stride,

@@ -29,7 +29,8 @@ cen, codes = ctx.pq_build(keys, 2, 6, 10, list(range(P)))
 torch.cuda.synchronize()
 print(f"build P={P} s={S} exact={exact}: {time.perf_counter() - t0:.3f} s, rechecked/total={ctx.last_build_stats()}")
 prof = ctx.last_build_profile()
-print("hamerly skipped point-visits:", prof.pop("skipped_points"))
+print("hamerly skipped point-visits:", prof.pop("skipped_points"), "k-means++ triangle-skipped:",
+      prof.pop("seed_skipped_points"))
 tot = sum(prof.values()) or 1
 print("phase ms @1.965GHz:", {k: round(v / 1.965e6, 2) for k, v in prof.items()}, "share:",
       {k: round(v / tot, 3) for k, v in prof.items()})
