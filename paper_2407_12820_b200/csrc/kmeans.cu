@@ -189,16 +189,33 @@ __device__ int nearest_filtered(const float (&x)[D], const float* __restrict__ c
     for (; c + 4 <= K; c += 4) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
         const float* c0 = cenf + c * D;
+        if constexpr (D % 4 == 0) {  // 128-bit broadcast reads of the 4 centroid rows
+            const float4* q0 = reinterpret_cast<const float4*>(c0);
 #pragma unroll
-        for (int t = 0; t < D; ++t) {
-            float d0 = x[t] - c0[t];
-            float d1 = x[t] - c0[D + t];
-            float d2 = x[t] - c0[2 * D + t];
-            float d3 = x[t] - c0[3 * D + t];
-            a0 = fmaf(d0, d0, a0);
-            a1 = fmaf(d1, d1, a1);
-            a2 = fmaf(d2, d2, a2);
-            a3 = fmaf(d3, d3, a3);
+            for (int t4 = 0; t4 < D / 4; ++t4) {
+                const float4 v[4] = {q0[t4], q0[D / 4 + t4], q0[D / 2 + t4], q0[3 * D / 4 + t4]};
+                float* acc4[4] = {&a0, &a1, &a2, &a3};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float d;
+                    d = x[4 * t4 + 0] - v[e].x; *acc4[e] = fmaf(d, d, *acc4[e]);
+                    d = x[4 * t4 + 1] - v[e].y; *acc4[e] = fmaf(d, d, *acc4[e]);
+                    d = x[4 * t4 + 2] - v[e].z; *acc4[e] = fmaf(d, d, *acc4[e]);
+                    d = x[4 * t4 + 3] - v[e].w; *acc4[e] = fmaf(d, d, *acc4[e]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                float d0 = x[t] - c0[t];
+                float d1 = x[t] - c0[D + t];
+                float d2 = x[t] - c0[2 * D + t];
+                float d3 = x[t] - c0[3 * D + t];
+                a0 = fmaf(d0, d0, a0);
+                a1 = fmaf(d1, d1, a1);
+                a2 = fmaf(d2, d2, a2);
+                a3 = fmaf(d3, d3, a3);
+            }
         }
         float av[4] = {a0, a1, a2, a3};
 #pragma unroll
@@ -258,16 +275,33 @@ __device__ int nearest_filtered_b(const float (&x)[D], const float* __restrict__
     for (; c + 4 <= K; c += 4) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
         const float* c0 = cenf + c * D;
+        if constexpr (D % 4 == 0) {  // 128-bit broadcast reads of the 4 centroid rows
+            const float4* q0 = reinterpret_cast<const float4*>(c0);
 #pragma unroll
-        for (int t = 0; t < D; ++t) {
-            float d0 = x[t] - c0[t];
-            float d1 = x[t] - c0[D + t];
-            float d2 = x[t] - c0[2 * D + t];
-            float d3 = x[t] - c0[3 * D + t];
-            a0 = fmaf(d0, d0, a0);
-            a1 = fmaf(d1, d1, a1);
-            a2 = fmaf(d2, d2, a2);
-            a3 = fmaf(d3, d3, a3);
+            for (int t4 = 0; t4 < D / 4; ++t4) {
+                const float4 v[4] = {q0[t4], q0[D / 4 + t4], q0[D / 2 + t4], q0[3 * D / 4 + t4]};
+                float* acc4[4] = {&a0, &a1, &a2, &a3};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float d;
+                    d = x[4 * t4 + 0] - v[e].x; *acc4[e] = fmaf(d, d, *acc4[e]);
+                    d = x[4 * t4 + 1] - v[e].y; *acc4[e] = fmaf(d, d, *acc4[e]);
+                    d = x[4 * t4 + 2] - v[e].z; *acc4[e] = fmaf(d, d, *acc4[e]);
+                    d = x[4 * t4 + 3] - v[e].w; *acc4[e] = fmaf(d, d, *acc4[e]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                float d0 = x[t] - c0[t];
+                float d1 = x[t] - c0[D + t];
+                float d2 = x[t] - c0[2 * D + t];
+                float d3 = x[t] - c0[3 * D + t];
+                a0 = fmaf(d0, d0, a0);
+                a1 = fmaf(d1, d1, a1);
+                a2 = fmaf(d2, d2, a2);
+                a3 = fmaf(d3, d3, a3);
+            }
         }
         float av[4] = {a0, a1, a2, a3};
 #pragma unroll
@@ -321,13 +355,16 @@ __device__ int nearest_filtered_exp(const float (&x)[D], const float* __restrict
     int c = 0;
     for (; c + 4 <= K; c += 4) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-        const float* c0 = cenf + c * D;
+        // 128-bit broadcast reads of 4 centroid rows: 4 LDS.128 per 16 FFMA
+        const float4* c0 = reinterpret_cast<const float4*>(cenf + c * D);
 #pragma unroll
-        for (int t = 0; t < D; ++t) {
-            a0 = fmaf(x[t], c0[t], a0);
-            a1 = fmaf(x[t], c0[D + t], a1);
-            a2 = fmaf(x[t], c0[2 * D + t], a2);
-            a3 = fmaf(x[t], c0[3 * D + t], a3);
+        for (int t4 = 0; t4 < D / 4; ++t4) {
+            const float4 v0 = c0[t4], v1 = c0[D / 4 + t4], v2 = c0[D / 2 + t4], v3 = c0[3 * D / 4 + t4];
+            const float x0 = x[4 * t4], x1 = x[4 * t4 + 1], x2 = x[4 * t4 + 2], x3 = x[4 * t4 + 3];
+            a0 = fmaf(x0, v0.x, a0); a0 = fmaf(x1, v0.y, a0); a0 = fmaf(x2, v0.z, a0); a0 = fmaf(x3, v0.w, a0);
+            a1 = fmaf(x0, v1.x, a1); a1 = fmaf(x1, v1.y, a1); a1 = fmaf(x2, v1.z, a1); a1 = fmaf(x3, v1.w, a1);
+            a2 = fmaf(x0, v2.x, a2); a2 = fmaf(x1, v2.y, a2); a2 = fmaf(x2, v2.z, a2); a2 = fmaf(x3, v2.w, a2);
+            a3 = fmaf(x0, v3.x, a3); a3 = fmaf(x1, v3.y, a3); a3 = fmaf(x2, v3.z, a3); a3 = fmaf(x3, v3.w, a3);
         }
         float av[4] = {fmaf(-2.f, a0, nx + ncf[c]), fmaf(-2.f, a1, nx + ncf[c + 1]),
                        fmaf(-2.f, a2, nx + ncf[c + 2]), fmaf(-2.f, a3, nx + ncf[c + 3])};
@@ -1466,10 +1503,23 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             for (int t = 0; t < D; ++t) { cf[t] = (float)cc[t]; cn = fmaf(cf[t], cf[t], cn); }
             cn = sqrtf(cn) * (1.0f + 9.6e-7f) + 1e-30f;
             __syncthreads();
-            for (int i = lo + tid; i < hi; i += KM_THREADS) {
-                const double md = aux0[i];
-                if (s.dseed2[nears[i]] >= 4.0 * md * (1.0 + 1e-7) + 1e-300) {
-                    atomicAdd(&sh_int[5], 1);
+            int nskip = 0;
+            for (int i0 = lo + tid; i0 < hi; i0 += 4 * KM_THREADS) {
+              double mdv[4];
+              uint16_t nrv[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                  const int i = i0 + u * KM_THREADS;
+                  mdv[u] = i < hi ? aux0[i] : 0.0;
+                  nrv[u] = i < hi ? nears[i] : (uint16_t)0;
+              }
+#pragma unroll 1
+              for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * KM_THREADS;
+                if (i >= hi) break;
+                const double md = mdv[u];
+                if (s.dseed2[nrv[u]] >= 4.0 * md * (1.0 + 1e-7) + 1e-300) {
+                    ++nskip;
                     continue;
                 }
                 const float* xp = point_ptr(a, q, i);
@@ -1488,7 +1538,9 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
                     aux0[i] = d;
                     nears[i] = (uint16_t)c;
                 }
+              }
             }
+            if (nskip) atomicAdd(&sh_int[5], nskip);
         }
         cl.sync();
         tick(1);
