@@ -1183,7 +1183,10 @@ __global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a,
             float x[D];
             load_point<D>(point_ptr(a, q, i), x, a.vec4);
             float ub, lb;
-            int c = nearest_filtered_exp<D>(x, s.cenf, s.ncf, s.cnorm, cmax, K, ub, lb);
+            // direct form: its bound scales with the distance itself, the
+            // expanded form's with (|x| + |c|)^2 (kept for reference: on the
+            // powerlaw keys it re-checks most points)
+            int c = nearest_filtered_b<D>(x, s.cenf, s.cnorm, cmax, K, ub, lb);
             if (c >= 0) {
                 out[i] = (uint32_t)c;
                 atomicAdd(&s.cnt_loc[c], 1u);
