@@ -89,6 +89,13 @@ PQKV_API int pqkv_ctx_last_build_stats(pqkv_ctx* ctx, uint64_t* rechecked_points
  * [2] assign + repair, [4] ordered update, [5] other. */
 PQKV_API int pqkv_ctx_last_build_profile(pqkv_ctx* ctx, uint64_t cycles[8]);
 
+/* Profiling mode (off by default): the attention kernel records per-CTA
+ * phase timestamps; pqkv_ctx_last_decode_profile returns mean SM cycles per
+ * CTA: [0] row-list prologue (incl. pair select), [1] pair select + DSMEM
+ * share of [0], [2] gather + softmax, [3] number of CTAs. */
+PQKV_API int pqkv_ctx_set_profiling(pqkv_ctx* ctx, int on);
+PQKV_API int pqkv_ctx_last_decode_profile(pqkv_ctx* ctx, double out[4]);
+
 /* ---- device memory helpers (for FFI hosts without a CUDA runtime) ----- */
 PQKV_API int pqkv_device_alloc(pqkv_ctx* ctx, size_t bytes, void** out);
 PQKV_API int pqkv_device_free(pqkv_ctx* ctx, void* ptr);

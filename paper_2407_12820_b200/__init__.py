@@ -46,6 +46,8 @@ _SIGS = {
     "pqkv_ctx_set_assign_mode": (_i, [_vp, _i]),
     "pqkv_ctx_last_build_stats": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
     "pqkv_ctx_last_build_profile": (_i, [_vp, C.POINTER(_u64)]),
+    "pqkv_ctx_set_profiling": (_i, [_vp, _i]),
+    "pqkv_ctx_last_decode_profile": (_i, [_vp, C.POINTER(C.c_double)]),
     "pqkv_device_alloc": (_i, [_vp, _sz, C.POINTER(_vp)]),
     "pqkv_device_free": (_i, [_vp, _vp]),
     "pqkv_copy": (_i, [_vp, _vp, _vp, _sz, _i]),
@@ -144,6 +146,15 @@ class Context:
         a, b = _u64(0), _u64(0)
         _check(lib().pqkv_ctx_last_build_stats(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def set_profiling(self, on: bool) -> None:
+        _check(lib().pqkv_ctx_set_profiling(self.h, int(on)))
+
+    def last_decode_profile(self):
+        """Mean SM cycles per attention CTA of the last decode (profiling mode)."""
+        arr = (C.c_double * 4)()
+        _check(lib().pqkv_ctx_last_decode_profile(self.h, arr))
+        return {"prologue": arr[0], "pair_select": arr[1], "gather": arr[2], "ctas": int(arr[3])}
 
     def last_build_profile(self):
         """SM cycles per phase of problem 0 of the last build."""

@@ -73,6 +73,7 @@ struct AtArgs {
     float* part;         // [P][n_chunks][G][DH + 2]
     unsigned* arrivals;  // [P] zero on entry; reset by the combining CTA
     float* out;          // [P][G][DH]
+    unsigned long long* prof;  // [grid][4] phase timestamps (profiling mode) or null
 };
 
 __device__ __forceinline__ float safe_scale(float m_old, float m_new) {
@@ -210,6 +211,8 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + a.region);
     uint8_t* cls = reinterpret_cast<uint8_t*>(words + nwords);
 
+    const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+    if (a.prof && tid == 0) a.prof[cta * 4 + 0] = clock64();
     // ---- 1. this CTA's row list (ascending token ids) ----
     int nrows = 0;
     if (a.src == SRC_ROWS) {
@@ -254,6 +257,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                 if (tid < 2) cut_s[tid] = cluster.map_shared_rank(cut_s, 0)[tid];
             }
             cluster.sync();  // rank 0's tables are no longer read remotely
+            if (a.prof && tid == 0) a.prof[cta * 4 + 1] = clock64();
             const int cstar = (int)cut_s[0];
             const uint32_t take = cut_s[1];
             if (c == 0)
@@ -280,6 +284,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     if (tid == 0) nrows_s = nrows;
     __syncthreads();
     nrows = nrows_s;
+    if (a.prof && tid == 0) a.prof[cta * 4 + 2] = clock64();
 
     // ---- 2. queries in the lane layout: dims {64j + 4hl + e} ----
     float q[G][4 * VPL];
@@ -367,6 +372,10 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         }
     }
 
+    if (a.prof) {
+        __syncthreads();
+        if (tid == 0) a.prof[cta * 4 + 3] = clock64();
+    }
     // ---- 4. merge the two half-warps (lanes hl and hl+16 hold the same dims) ----
 #pragma unroll
     for (int r = 0; r < G; ++r) {
@@ -634,6 +643,14 @@ static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cuda
     sc.commit();
     a.part = sc.get<float>(h_part);
     a.arrivals = arrival_counters(ctx, P, st);
+    a.prof = nullptr;
+    if (ctx->profiling) {
+        if (ctx->d_prof) cudaFree(ctx->d_prof);
+        ctx->n_prof = (size_t)a.n_chunks * P;
+        PQKV_CUDA(cudaMalloc(&ctx->d_prof, ctx->n_prof * 4 * sizeof(unsigned long long)));
+        PQKV_CUDA(cudaMemsetAsync(ctx->d_prof, 0, ctx->n_prof * 4 * sizeof(unsigned long long), st));
+        a.prof = ctx->d_prof;
+    }
     size_t smem = attend_smem(a, G);
     dim3 grid((unsigned)a.n_chunks, (unsigned)P);
     switch (G) {

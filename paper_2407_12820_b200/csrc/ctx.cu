@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <new>
+#include <vector>
 #include <string>
 
 #include "internal.cuh"
@@ -112,6 +113,7 @@ int pqkv_ctx_destroy(pqkv_ctx* ctx) {
         if (ctx->d_stats) cudaFree(ctx->d_stats);
         if (ctx->d_arrivals) cudaFree(ctx->d_arrivals);
         if (ctx->ws) cudaFree(ctx->ws);
+        if (ctx->d_prof) cudaFree(ctx->d_prof);
         delete ctx;
     });
 }
@@ -166,6 +168,39 @@ int pqkv_stream_sync(pqkv_ctx* ctx, void* stream) {
         if (!ctx) fail(PQKV_EINVAL, "pqkv_stream_sync: NULL context");
         bind_device(ctx);
         PQKV_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+    });
+}
+
+int pqkv_ctx_set_profiling(pqkv_ctx* ctx, int on) {
+    return guard([&] {
+        if (!ctx) fail(PQKV_EINVAL, "NULL context");
+        ctx->profiling = on ? 1 : 0;
+    });
+}
+
+// Mean SM cycles per CTA of the last attention launch (profiling mode):
+// [0] row-list prologue incl. pair select, [1] of which pair select + DSMEM,
+// [2] gather + softmax, [3] CTAs measured.
+int pqkv_ctx_last_decode_profile(pqkv_ctx* ctx, double out[4]) {
+    return guard([&] {
+        if (!ctx || !out) fail(PQKV_EINVAL, "NULL argument");
+        for (int i = 0; i < 4; ++i) out[i] = 0.0;
+        if (!ctx->d_prof || !ctx->n_prof) return;
+        bind_device(ctx);
+        std::vector<unsigned long long> h(ctx->n_prof * 4);
+        PQKV_CUDA(cudaDeviceSynchronize());
+        PQKV_CUDA(cudaMemcpy(h.data(), ctx->d_prof, h.size() * 8, cudaMemcpyDeviceToHost));
+        double n = 0;
+        for (size_t c = 0; c < ctx->n_prof; ++c) {
+            const unsigned long long* t = &h[c * 4];
+            if (!t[0] || !t[2] || !t[3]) continue;
+            out[0] += (double)(t[2] - t[0]);
+            out[1] += t[1] ? (double)(t[1] - t[0]) : 0.0;
+            out[2] += (double)(t[3] - t[2]);
+            n += 1;
+        }
+        if (n > 0) for (int i = 0; i < 3; ++i) out[i] /= n;
+        out[3] = n;
     });
 }
 

@@ -23,6 +23,10 @@ struct pqkv_ctx {
     // between launches by the kernel itself).
     unsigned* d_arrivals = nullptr;
     size_t n_arrivals = 0;
+    // Profiling mode: attention-kernel phase timestamps of the last launch.
+    int profiling = 0;
+    unsigned long long* d_prof = nullptr;
+    size_t n_prof = 0;
     // Decode workspace (selection bitmap / pair classes between kernels).
     void* ws = nullptr;
     size_t ws_bytes = 0;

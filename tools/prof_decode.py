@@ -40,4 +40,16 @@ bm, _ = ctx.pq_search(q, cen, codes, B, K, s=SM, ordered=False, tables=tables)
 for i in range(reps):
     ctx.decode_attend(layer, q, bm)
 torch.cuda.synchronize()
+if os.environ.get("PQKV_PHASES"):
+    ctx.set_profiling(True)
+    for mode in ("fused", "bitmap"):
+        for i in range(3):
+            if mode == "fused":
+                ctx.decode(layer, q, K)
+            else:
+                ctx.decode_attend(layer, q, bm)
+        torch.cuda.synchronize()
+        prof = ctx.last_decode_profile()
+        print(mode, {k: (round(v / 1965.0, 2) if k != "ctas" else v) for k, v in prof.items()}, "(us)")
+    ctx.set_profiling(False)
 print("done", out.abs().sum().item())
