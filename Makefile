@@ -2,11 +2,12 @@
 # (and the test-only oracle via oracle/Makefile).
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC,-fvisibility=hidden -Iinclude \
+EXTRA ?=
+NVFLAGS := $(EXTRA) -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC,-fvisibility=hidden -Iinclude \
            -Ipaper_2407_12820_b200/csrc --expt-relaxed-constexpr -diag-suppress 128
 CSRC := paper_2407_12820_b200/csrc
-OBJDIR := build/obj
-LIB := paper_2407_12820_b200/lib/libpqkv.so
+OBJDIR ?= build/obj
+LIB ?= paper_2407_12820_b200/lib/libpqkv.so
 CU := ctx capi kmeans select attend
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(OBJDIR)/api.o
 HDRS := include/pqkv_c.h $(CSRC)/common.cuh $(CSRC)/internal.cuh $(CSRC)/select_common.cuh

@@ -64,6 +64,8 @@ typedef enum { PQKV_PREC_F32 = 0, PQKV_PREC_F64 = 1 } pqkv_precision;
 /* Middle rows per chunk of the code-pair chunk histogram (see
  * pqkv_pq_tuple_tables). */
 #define PQKV_TUPLE_CHUNK 4096
+/* u64 timestamps per attention CTA recorded in profiling mode */
+#define PQKV_PROF_SLOTS 24
 
 /* k-means assign-step arithmetic.  Both produce bit-identical assignments:
  * EXACT evaluates every distance in the reference's fp64 order;
@@ -95,6 +97,13 @@ PQKV_API int pqkv_ctx_last_build_profile(pqkv_ctx* ctx, uint64_t cycles[8]);
  * share of [0], [2] gather + softmax, [3] number of CTAs. */
 PQKV_API int pqkv_ctx_set_profiling(pqkv_ctx* ctx, int on);
 PQKV_API int pqkv_ctx_last_decode_profile(pqkv_ctx* ctx, double out[4]);
+/* Raw per-CTA timestamps of the last attention launch: PQKV_PROF_SLOTS u64 per CTA --
+ * clock64 at start / after pair select / after the row list / after the
+ * gather; globaltimer ns at start / after the row list / after the gather /
+ * at exit; clock64 at the pair-select phase marks 0..6 (cluster rank 0) and
+ * after the first cluster barrier; [16] SM id, [17] cluster rank.
+ * *n_ctas = CTAs; copies min(cap, PQKV_PROF_SLOTS*n). */
+PQKV_API int pqkv_ctx_decode_profile_raw(pqkv_ctx* ctx, uint64_t* out, size_t cap, size_t* n_ctas);
 
 /* ---- device memory helpers (for FFI hosts without a CUDA runtime) ----- */
 PQKV_API int pqkv_device_alloc(pqkv_ctx* ctx, size_t bytes, void** out);

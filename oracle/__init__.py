@@ -79,6 +79,8 @@ class _Lib:
             self.lib.ref_last_error.restype = C.c_char_p
             self.lib.ref_bench_decode.restype = _dbl
             self.lib.ref_bench_decode.argtypes = [_sz] * 9 + [_vp] * 6 + [C.c_int]
+            self.lib.ref_bench_decode_steps.restype = _dbl
+            self.lib.ref_bench_decode_steps.argtypes = [_sz] * 9 + [_vp] * 3 + [_sz] + [_vp] * 3 + [C.c_int, _vp]
             self.lib.ref_bench_build.restype = _dbl
             self.lib.ref_bench_build.argtypes = [_sz] * 6 + [_vp] * 4 + [C.c_int]
 
@@ -206,6 +208,22 @@ class _Lib:
                                          _p(np.ascontiguousarray(queries)),
                                          _p(np.ascontiguousarray(centroids)),
                                          _p(np.ascontiguousarray(codes)), _p(out), n_threads)
+        return secs, out
+
+    def bench_decode_steps(self, keys, values, queries, centroids, codes, n_init, n_local, k,
+                           n_threads=0):
+        """queries [n_steps][P][g][d_h]; HeadStates built once; returns per-step seconds."""
+        P, total, d_h = keys.shape
+        n_steps, g = queries.shape[0], queries.shape[2]
+        m, C_ = centroids.shape[1], centroids.shape[2]
+        out = np.zeros((P, g, d_h), np.float32)
+        secs = np.zeros(n_steps, np.float64)
+        self.lib.ref_bench_decode_steps(P, total, d_h, g, n_init, n_local, m, C_, k,
+                                        _p(np.ascontiguousarray(keys)),
+                                        _p(np.ascontiguousarray(values)),
+                                        _p(np.ascontiguousarray(queries)), n_steps,
+                                        _p(np.ascontiguousarray(centroids)),
+                                        _p(np.ascontiguousarray(codes)), _p(out), n_threads, _p(secs))
         return secs, out
 
     def bench_build(self, keys, m, b, max_iter, seeds, n_threads=0):

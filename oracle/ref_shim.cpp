@@ -211,13 +211,15 @@ int ref_selective_attention(const float* query, const float* keys, const float* 
 // Inputs are flat per head: keys/values [P][total][d_h], queries [P][g][d_h],
 // centroids [P][m][C][d_m], codes [P][s_mid][m].  Returns wall seconds.
 // ---------------------------------------------------------------------------
-double ref_bench_decode(size_t P, size_t total, size_t d_h, size_t g, size_t n_init,
-                        size_t n_local, size_t m, size_t C, size_t k, const float* keys,
-                        const float* values, const float* queries, const float* centroids,
-                        const uint16_t* codes, float* out, int n_threads) {
+double ref_bench_decode_steps(size_t P, size_t total, size_t d_h, size_t g, size_t n_init,
+                              size_t n_local, size_t m, size_t C, size_t k, const float* keys,
+                              const float* values, const float* queries, size_t n_steps,
+                              const float* centroids, const uint16_t* codes, float* out,
+                              int n_threads, double* step_secs) {
     size_t s_mid = total - n_init - n_local, d_m = d_h / m;
-    // HeadStates are built outside the timed region (the reference keeps them
-    // resident across decode steps, kv_store.cpp:32-74).
+    // HeadStates are built once, outside the timed steps (the reference keeps
+    // them resident across decode steps, kv_store.cpp:32-74).  queries holds
+    // n_steps x [P][g][d_h]; step t uses slice t.
     std::vector<KvStore> stores;
     std::vector<PqIndex> idx;
     stores.reserve(P);
@@ -228,25 +230,40 @@ double ref_bench_decode(size_t P, size_t total, size_t d_h, size_t g, size_t n_i
                                       SegmentConfig{n_init, n_local, k});
         idx.push_back(make_index(centroids + p * m * C * d_m, m, C, d_m, codes + p * s_mid * m, s_mid));
     }
-    std::atomic<size_t> next{0};
-    auto worker = [&] {
-        for (size_t p; (p = next.fetch_add(1)) < P;) {
-            TensorF32 q = grid(queries + p * g * d_h, g, d_h);
-            std::vector<float> scores = pq_score_gqa(q, idx[p]);
-            std::vector<std::size_t> sel = approx_topk(scores, k);
-            for (auto& r : sel) r += n_init;
-            for (size_t r = 0; r < g; ++r) {
-                std::vector<float> o = selective_attention({q.row(r), d_h}, stores[p].state(0, 0), sel);
-                std::copy(o.begin(), o.end(), out + (p * g + r) * d_h);
-            }
-        }
-    };
     int nt = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
-    auto t0 = std::chrono::steady_clock::now();
-    std::vector<std::thread> pool;
-    for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
-    for (auto& t : pool) t.join();
-    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double total_secs = 0.0;
+    for (size_t step = 0; step < n_steps; ++step) {
+        const float* qs = queries + step * P * g * d_h;
+        std::atomic<size_t> next{0};
+        auto worker = [&] {
+            for (size_t p; (p = next.fetch_add(1)) < P;) {
+                TensorF32 q = grid(qs + p * g * d_h, g, d_h);
+                std::vector<float> scores = pq_score_gqa(q, idx[p]);
+                std::vector<std::size_t> sel = approx_topk(scores, k);
+                for (auto& r : sel) r += n_init;
+                for (size_t r = 0; r < g; ++r) {
+                    std::vector<float> o = selective_attention({q.row(r), d_h}, stores[p].state(0, 0), sel);
+                    std::copy(o.begin(), o.end(), out + (p * g + r) * d_h);
+                }
+            }
+        };
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+        for (auto& t : pool) t.join();
+        double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (step_secs) step_secs[step] = secs;
+        total_secs += secs;
+    }
+    return total_secs;
+}
+
+double ref_bench_decode(size_t P, size_t total, size_t d_h, size_t g, size_t n_init,
+                        size_t n_local, size_t m, size_t C, size_t k, const float* keys,
+                        const float* values, const float* queries, const float* centroids,
+                        const uint16_t* codes, float* out, int n_threads) {
+    return ref_bench_decode_steps(P, total, d_h, g, n_init, n_local, m, C, k, keys, values, queries, 1,
+                                  centroids, codes, out, n_threads, nullptr);
 }
 
 // CPU baseline for the prefill build: pq_construct per head on a thread pool.

@@ -25,6 +25,7 @@ ASSIGN_FILTERED, ASSIGN_EXACT = 0, 1
 TUPLE_CHUNK = 4096  # PQKV_TUPLE_CHUNK
 
 _sz, _vp, _i, _u64 = C.c_size_t, C.c_void_p, C.c_int, C.c_uint64
+PROF_SLOTS = 24  # PQKV_PROF_SLOTS (pqkv_c.h)
 
 
 class pqkv_layer(C.Structure):
@@ -48,6 +49,7 @@ _SIGS = {
     "pqkv_ctx_last_build_profile": (_i, [_vp, C.POINTER(_u64)]),
     "pqkv_ctx_set_profiling": (_i, [_vp, _i]),
     "pqkv_ctx_last_decode_profile": (_i, [_vp, C.POINTER(C.c_double)]),
+    "pqkv_ctx_decode_profile_raw": (_i, [_vp, _vp, _sz, C.POINTER(_sz)]),
     "pqkv_device_alloc": (_i, [_vp, _sz, C.POINTER(_vp)]),
     "pqkv_device_free": (_i, [_vp, _vp]),
     "pqkv_copy": (_i, [_vp, _vp, _vp, _sz, _i]),
@@ -77,9 +79,10 @@ def lib() -> C.CDLL:
     """The loaded product library; raises if it was not built."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"pqkv CUDA library missing: {LIB_PATH} (run __graft_entry__.build())")
-        L = C.CDLL(LIB_PATH)
+        path = os.environ.get("PQKV_LIB", LIB_PATH)  # experiment builds (tools/) only
+        if not os.path.exists(path):
+            raise RuntimeError(f"pqkv CUDA library missing: {path} (run __graft_entry__.build())")
+        L = C.CDLL(path)
         for name, (res, args) in _SIGS.items():
             fn = getattr(L, name)
             fn.restype = res
@@ -155,6 +158,18 @@ class Context:
         arr = (C.c_double * 4)()
         _check(lib().pqkv_ctx_last_decode_profile(self.h, arr))
         return {"prologue": arr[0], "pair_select": arr[1], "gather": arr[2], "ctas": int(arr[3])}
+
+    def decode_profile_raw(self):
+        """Per-CTA timestamps of the last attention launch, numpy u64 [n_ctas][PROF_SLOTS]
+        (see pqkv_ctx_decode_profile_raw)."""
+        import numpy as np
+
+        n = _sz(0)
+        _check(lib().pqkv_ctx_decode_profile_raw(self.h, None, 0, C.byref(n)))
+        arr = np.zeros((n.value, PROF_SLOTS), np.uint64)
+        if n.value:
+            _check(lib().pqkv_ctx_decode_profile_raw(self.h, arr.ctypes.data, arr.size, C.byref(n)))
+        return arr
 
     def last_build_profile(self):
         """SM cycles per phase of problem 0 of the last build."""

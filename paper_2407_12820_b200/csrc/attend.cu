@@ -73,7 +73,7 @@ struct AtArgs {
     float* part;         // [P][n_chunks][G][DH + 2]
     unsigned* arrivals;  // [P] zero on entry; reset by the combining CTA
     float* out;          // [P][G][DH]
-    unsigned long long* prof;  // [grid][4] phase timestamps (profiling mode) or null
+    unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
 
 __device__ __forceinline__ float safe_scale(float m_old, float m_new) {
@@ -134,13 +134,15 @@ __device__ int expand_words(const uint32_t* words, int nwords, int token_base, i
 // (pq.cpp:128-140 pair score, topk.cpp tie rule via the tuple_select cut).
 // Warp segments never straddle a PQKV_TUPLE_CHUNK chunk (chunk % (8*32) and
 // PQKV_TUPLE_CHUNK % segment hold by construction).
-__device__ void classify_words(const AtArgs& a, int p, int r0, int r1, uint32_t* words,
-                               const uint8_t* cls, uint32_t* wtot, int cstar, uint32_t take) {
+// The code pair of middle row i is cd[i - cd_off] (global memory, or a copy
+// of this CTA's range staged in shared memory).
+__device__ void classify_words(const AtArgs& a, int r0, int r1, const uint32_t* cd_base, int cd_off,
+                               uint32_t* words, const uint8_t* cls, uint32_t* wtot, int cstar, uint32_t take) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int seg = a.chunk / AT_WARPS;  // tokens per warp (multiple of 32)
     const int s0 = r0 + warp * seg, s1 = min(r1, s0 + seg);
     const int tc = s0 / PQKV_TUPLE_CHUNK;
-    const uint32_t* cd = reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride);
+    const uint32_t* cd = cd_base - cd_off;
     const bool boundary = tc == cstar && s0 < s1;
     // pass 1 (boundary chunk only): equal-pair counts per warp, in id order
     uint32_t eq_before = 0;
@@ -212,7 +214,16 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     uint8_t* cls = reinterpret_cast<uint8_t*>(words + nwords);
 
     const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
-    if (a.prof && tid == 0) a.prof[cta * 4 + 0] = clock64();
+    if (a.prof && tid == 0) {
+        a.prof[cta * PQKV_PROF_SLOTS + 0] = clock64();
+        a.prof[cta * PQKV_PROF_SLOTS + 4] = globaltimer_ns();
+        unsigned smid, crk;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crk));
+        a.prof[cta * PQKV_PROF_SLOTS + 16] = smid;
+        a.prof[cta * PQKV_PROF_SLOTS + 17] = crk;
+        a.prof[cta * PQKV_PROF_SLOTS + 18] = a.src == SRC_PAIRS && crk == (cta / 8) % 8;
+    }
     // ---- 1. this CTA's row list (ascending token ids) ----
     int nrows = 0;
     if (a.src == SRC_ROWS) {
@@ -220,7 +231,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         for (int e = tid; e < cnt; e += AT_THREADS) rows[e] = (int)a.rows[(long long)p * a.t + b0 + e];
         nrows = cnt;
     } else {
-        if (c == 0)
+        if (c == 0 && a.src != SRC_PAIRS)  // pair mode: written after the classification
             for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
         nrows = c == 0 ? a.n_init : 0;
         const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
@@ -228,41 +239,71 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         if (a.src == SRC_BITMAP) {
             for (int w = tid; w < nw; w += AT_THREADS) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
         } else if (a.src == SRC_PAIRS) {
-            // per-head pair-level top-k: computed by rank 0 of each thread-block
-            // cluster, shared with the cluster's other CTAs through DSMEM
+            // per-head pair-level top-k: computed by one CTA of each thread-block
+            // cluster and shared with the others through DSMEM.  The selecting
+            // rank rotates with the cluster index: the scheduler places equal
+            // ranks of neighbouring clusters on the same SM, so a fixed rank
+            // would stack up to four latency-bound selects on one SM.
             namespace cg = cooperative_groups;
             cg::cluster_group cluster = cg::this_cluster();
             const unsigned crank = cluster.block_rank();
+            const unsigned ncl = cluster.num_blocks();
+            const unsigned sel = (unsigned)(cta / ncl) % ncl;
+            // this CTA's code pairs (4 B per token): the other CTAs stage them
+            // in shared memory (cp.async, rows[] region) while the selector
+            // works; the selector reads them from L2 (prefetched)
+            const uint32_t* cd_g = reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride);
+            const uint32_t* cd_src = cd_g;
+            int cd_off = 0;
+            {
+                const int n = max(0, r1 - r0);
+                const uint32_t* src = cd_g + r0;
+                if (crank == sel) {
+                    for (int o = tid * 32; o < n; o += AT_THREADS * 32) prefetch_l2(src + o);
+                } else {
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(smem_raw);
+                    int head = 0;
+                    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                        head = n & ~3;
+                        for (int e = tid * 4; e < head; e += AT_THREADS * 4) cp_async16(dst + e, src + e);
+                    }
+                    for (int e = head + tid; e < n; e += AT_THREADS) cp_async4(dst + e, src + e);
+                    cp_async_commit();
+                    cd_src = dst;
+                    cd_off = r0;
+                }
+            }
             __shared__ uint32_t cut_s[2];
             const int C = a.C, C2 = C * C;
-            if (crank == 0) {
-            unsigned char* z = smem_raw;  // aliases rows[]: free until expansion
-            double* lut = reinterpret_cast<double*>(z);
-            uint32_t* hist = reinterpret_cast<uint32_t*>(lut + 2 * C);
-            uint32_t* cnt = hist + NB;
-            uint32_t* eql = cnt + NB;
-            uint32_t* ceq = eql + C2;
-            uint32_t* wsum = ceq + a.n_tchunks;
-            uint32_t* sh = wsum + 64;
-            pair_select<AT_THREADS, 16>(a.queries + (long long)p * G * DH, G, DH,
-                                    a.centroids + (long long)p * 2 * C * (DH / 2), C,
-                                    a.thist + (long long)p * C2, a.chist + (long long)p * a.n_tchunks * C2,
-                                    a.n_tchunks, a.k, lut, nullptr, hist, cnt, eql, ceq, wsum, sh, cls, nullptr);
+            if (crank == sel) {
+                PairScratch ps(smem_raw, C, a.n_tchunks);  // aliases rows[]: free until expansion
+                pair_select<AT_THREADS, 16>(a.queries + (long long)p * G * DH, G, DH,
+                                            a.centroids + (long long)p * 2 * C * (DH / 2), C,
+                                            a.thist + (long long)p * C2, a.chist + (long long)p * a.n_tchunks * C2,
+                                            a.n_tchunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
+                                            nullptr, a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr);
+                const uint32_t* sh = ps.sh;
                 if (tid == 0) { cut_s[0] = sh[3]; cut_s[1] = sh[4]; }
             }
             cluster.sync();
-            if (crank != 0) {
-                const uint32_t* rc = cluster.map_shared_rank(reinterpret_cast<const uint32_t*>(cls), 0);
+            if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 15] = clock64();
+            if (crank != sel) {
+                const uint32_t* rc = cluster.map_shared_rank(reinterpret_cast<const uint32_t*>(cls), sel);
                 for (int e = tid; e < (C2 + 3) / 4; e += AT_THREADS) reinterpret_cast<uint32_t*>(cls)[e] = rc[e];
-                if (tid < 2) cut_s[tid] = cluster.map_shared_rank(cut_s, 0)[tid];
+                if (tid < 2) cut_s[tid] = cluster.map_shared_rank(cut_s, sel)[tid];
             }
-            cluster.sync();  // rank 0's tables are no longer read remotely
-            if (a.prof && tid == 0) a.prof[cta * 4 + 1] = clock64();
+            // the selector's cls[]/cut_s are never written again; its exit is
+            // held back by the matching cluster wait at the end of the kernel
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            __syncthreads();
+            if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 1] = clock64();
             const int cstar = (int)cut_s[0];
             const uint32_t take = cut_s[1];
-            if (c == 0)
+            cp_async_wait_all();
+            __syncthreads();
+            classify_words(a, r0, r1, cd_src, cd_off, words, cls, wtot, cstar, take);
+            if (c == 0)  // after the staged codes are consumed (they share rows[])
                 for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
-            classify_words(a, p, r0, r1, words, cls, wtot, cstar, take);
         } else {
             const int C2 = a.C * a.C;
             if ((C2 & 3) == 0) {
@@ -272,7 +313,8 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                 for (int e = tid; e < C2; e += AT_THREADS) cls[e] = a.cls[(long long)p * C2 + e];
             }
             __syncthreads();
-            classify_words(a, p, r0, r1, words, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
+            classify_words(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), 0,
+                           words, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
         }
         __syncthreads();
         nrows += expand_words(words, nw, a.n_init + r0, rows, nrows, wtot);
@@ -284,7 +326,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     if (tid == 0) nrows_s = nrows;
     __syncthreads();
     nrows = nrows_s;
-    if (a.prof && tid == 0) a.prof[cta * 4 + 2] = clock64();
+    if (a.prof && tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 2] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 5] = globaltimer_ns(); }
 
     // ---- 2. queries in the lane layout: dims {64j + 4hl + e} ----
     float q[G][4 * VPL];
@@ -314,14 +356,15 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     const float4* vb = reinterpret_cast<const float4*>(a.values + (long long)p * a.kv_head_stride);
     const int slot = warp * 2 + half;          // 0..15
     constexpr int STEP = AT_WARPS * 2;         // rows per CTA step
+    const uint64_t pol = l2_evict_first_policy();
     float4 kc[VPL], vc[VPL], kn[VPL], vn[VPL];
     int ri = slot;
     if (ri < nrows) {
         const long long row = rows[ri];
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
-            kc[j] = __ldg(kb + row * (DH / 4) + j * LPR + hl);
-            vc[j] = __ldg(vb + row * (DH / 4) + j * LPR + hl);
+            kc[j] = ldg_stream(kb + row * (DH / 4) + j * LPR + hl, pol);
+            vc[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
         }
     }
     for (; ri < nrows; ri += STEP) {  // half-warp uniform trip count
@@ -330,8 +373,8 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             const long long row = rows[rn];
 #pragma unroll
             for (int j = 0; j < VPL; ++j) {
-                kn[j] = __ldg(kb + row * (DH / 4) + j * LPR + hl);
-                vn[j] = __ldg(vb + row * (DH / 4) + j * LPR + hl);
+                kn[j] = ldg_stream(kb + row * (DH / 4) + j * LPR + hl, pol);
+                vn[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
             }
         }
 #pragma unroll
@@ -374,7 +417,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
 
     if (a.prof) {
         __syncthreads();
-        if (tid == 0) a.prof[cta * 4 + 3] = clock64();
+        if (tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 3] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 6] = globaltimer_ns(); }
     }
     // ---- 4. merge the two half-warps (lanes hl and hl+16 hold the same dims) ----
 #pragma unroll
@@ -428,7 +471,11 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     __threadfence();
     __syncthreads();
     if (tid == 0) ticket = atomicAdd(&a.arrivals[p], 1u);
+    // pair mode: pairs with the cluster arrive after the DSMEM reads (no CTA
+    // of the cluster exits while another may still read its shared memory)
+    if (a.src == SRC_PAIRS) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     __syncthreads();
+    if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
     if (ticket != (unsigned)a.n_chunks - 1) return;
     __threadfence();
     float* sc = reinterpret_cast<float*>(smem_raw) + AT_WARPS * G * DH;  // [G][n_chunks] + [G]
@@ -458,6 +505,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         a.out[((long long)p * G + r) * DH + d] = O / sc[G * nc + r];
     }
     if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
+    if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
 }
 
 // ---- exact (fp64) path ------------------------------------------------------
@@ -594,9 +642,6 @@ static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
     return (int)(q * PQKV_TUPLE_CHUNK);
 }
 
-static size_t pair_scratch_bytes(int C, int n_tchunks) {
-    return (size_t)16 * C + 4 * ((size_t)C * C + 2 * NB + n_tchunks + 72);
-}
 
 // Shared memory: region (rows[] / merge partials / pair-select scratch)
 // followed by words[] and the pair classes.
@@ -604,7 +649,7 @@ static size_t attend_smem(AtArgs& a, int G) {
     size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.chunk + a.n_init + a.n_local;
     size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
     size_t region = std::max(rows_cap * 4, merge);
-    if (a.src == SRC_PAIRS) region = std::max(region, pair_scratch_bytes(a.C, a.n_tchunks));
+    if (a.src == SRC_PAIRS) region = std::max(region, pair_select_scratch(a.C, a.n_tchunks));
     region = round_up(region, 16);
     a.region = (int)region;
     size_t tail = (size_t)a.chunk / 32 * 4 +
@@ -647,8 +692,8 @@ static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cuda
     if (ctx->profiling) {
         if (ctx->d_prof) cudaFree(ctx->d_prof);
         ctx->n_prof = (size_t)a.n_chunks * P;
-        PQKV_CUDA(cudaMalloc(&ctx->d_prof, ctx->n_prof * 4 * sizeof(unsigned long long)));
-        PQKV_CUDA(cudaMemsetAsync(ctx->d_prof, 0, ctx->n_prof * 4 * sizeof(unsigned long long), st));
+        PQKV_CUDA(cudaMalloc(&ctx->d_prof, ctx->n_prof * PQKV_PROF_SLOTS * sizeof(unsigned long long)));
+        PQKV_CUDA(cudaMemsetAsync(ctx->d_prof, 0, ctx->n_prof * PQKV_PROF_SLOTS * sizeof(unsigned long long), st));
         a.prof = ctx->d_prof;
     }
     size_t smem = attend_smem(a, G);

@@ -146,8 +146,10 @@ int pqkv_topk(pqkv_ctx* ctx, const float* d_scores, size_t n_rows, size_t n, siz
     });
 }
 
-static bool tuple_ok(size_t m, size_t b, const void* th, const void* ch) {
-    return m == 2 && b <= 7 && th && ch;
+// Code-pair path: m = 2, C^2 <= 16384 pairs, per-pair row counts below
+// 2^(32 - 2b) (pair_select packs (pair << (32 - 2b) | count)).
+static bool tuple_ok(size_t m, size_t b, const void* th, const void* ch, size_t n) {
+    return m == 2 && b >= 1 && b <= 7 && th && ch && n < (size_t{1} << (32 - 2 * b));
 }
 
 int pqkv_pq_tuple_tables(pqkv_ctx* ctx, size_t n_heads, size_t b, const uint16_t* d_codes,
@@ -181,7 +183,7 @@ int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t
         src.centroids = d_centroids;
         src.codes = d_codes;
         src.codes_head_stride = codes_head_stride;
-        if (tuple_ok(m, b, d_tuple_hist, d_tuple_chunk_hist))
+        if (tuple_ok(m, b, d_tuple_hist, d_tuple_chunk_hist, s))
             launch_select_tuple(ctx, src, d_tuple_hist, d_tuple_chunk_hist, n_heads, s, k, d_bitmap,
                                 k ? d_ids : nullptr, as_stream(stream), nullptr);
         else
@@ -237,7 +239,7 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         cudaStream_t st = as_stream(stream);
         const size_t P = L->n_heads, s_mid = L->total - L->n_init - L->n_local;
         const size_t words = ceil_div(s_mid, 32), C = size_t{1} << L->b;
-        const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist);
+        const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist, s_mid);
         const bool fast = decode_fast_path(*L, g);
         SelectSource src;
         src.queries = d_queries;
@@ -321,7 +323,7 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
 int pqkv_decode_launches(const pqkv_layer* L, size_t g, int with_ids) {
     if (!L) return 0;
     bool fast = L->d_h == 128 && (g == 1 || g == 2 || g == 4) && L->kv_head_stride % 4 == 0;
-    const bool tup = L->m == 2 && L->b <= 7 && L->tuple_hist && L->tuple_chunk_hist;
+    const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist, L->total - L->n_init - L->n_local);
     if (tup && fast && !with_ids) return L->b <= 6 ? 1 : 2;  // [pair select +] attention
     int n = tup ? 2 /*pair select + bitmap*/ : 1 /*cluster select*/;
     n += with_ids ? 1 : 0 /*sort*/;

@@ -187,12 +187,12 @@ int pqkv_ctx_last_decode_profile(pqkv_ctx* ctx, double out[4]) {
         for (int i = 0; i < 4; ++i) out[i] = 0.0;
         if (!ctx->d_prof || !ctx->n_prof) return;
         bind_device(ctx);
-        std::vector<unsigned long long> h(ctx->n_prof * 4);
+        std::vector<unsigned long long> h(ctx->n_prof * PQKV_PROF_SLOTS);
         PQKV_CUDA(cudaDeviceSynchronize());
         PQKV_CUDA(cudaMemcpy(h.data(), ctx->d_prof, h.size() * 8, cudaMemcpyDeviceToHost));
         double n = 0;
         for (size_t c = 0; c < ctx->n_prof; ++c) {
-            const unsigned long long* t = &h[c * 4];
+            const unsigned long long* t = &h[c * PQKV_PROF_SLOTS];
             if (!t[0] || !t[2] || !t[3]) continue;
             out[0] += (double)(t[2] - t[0]);
             out[1] += t[1] ? (double)(t[1] - t[0]) : 0.0;
@@ -201,6 +201,22 @@ int pqkv_ctx_last_decode_profile(pqkv_ctx* ctx, double out[4]) {
         }
         if (n > 0) for (int i = 0; i < 3; ++i) out[i] /= n;
         out[3] = n;
+    });
+}
+
+// Raw per-CTA timestamps of the last attention launch (profiling mode):
+// 16 u64 per CTA (clock64 at start / after pair select / after the row list /
+// after the gather; globaltimer ns at start / after the row list / after the
+// gather / at exit; clock64 at the pair_select phase marks 0..6 (rank 0) and
+// after the first cluster barrier).  *n_ctas = CTAs; copies min(cap, 16 n).
+int pqkv_ctx_decode_profile_raw(pqkv_ctx* ctx, uint64_t* out, size_t cap, size_t* n_ctas) {
+    return guard([&] {
+        if (!ctx || !n_ctas) fail(PQKV_EINVAL, "NULL argument");
+        *n_ctas = ctx->d_prof ? ctx->n_prof : 0;
+        if (!ctx->d_prof || !out) return;
+        bind_device(ctx);
+        PQKV_CUDA(cudaDeviceSynchronize());
+        PQKV_CUDA(cudaMemcpy(out, ctx->d_prof, std::min(cap, ctx->n_prof * PQKV_PROF_SLOTS) * 8, cudaMemcpyDeviceToHost));
     });
 }
 

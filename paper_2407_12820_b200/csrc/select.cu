@@ -411,19 +411,16 @@ struct TupArgs {
 __global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int p = blockIdx.x, tid = threadIdx.x, C = a.C, C2 = C * C;
-    double* lut = reinterpret_cast<double*>(smem);                 // [2C]
-    uint32_t* hist = reinterpret_cast<uint32_t*>(lut + 2 * C);     // [NB]
-    uint32_t* cnt = hist + NB;                                     // [NB]
-    uint32_t* ceq = cnt + NB;                                      // [n_chunks]
-    uint32_t* eql = ceq + a.n_chunks;                              // [C2] equal pairs
-    uint32_t* wsum = eql + C2;                                     // [64]
-    uint32_t* sh = wsum + 64;                                      // [8]
+    PairScratch ps(smem, C, a.n_chunks);
+    uint32_t* sh = ps.sh;
+    uint32_t* ceq = ps.ceq;
+    uint32_t* hist = ps.hist;  // per-chunk counts below (dead radix bins, 2*NB entries with cnt)
     uint8_t* cls = a.cls + (long long)p * C2;
     const uint16_t* ch = a.chist + (long long)p * a.n_chunks * C2;
     pair_select<TUP_THREADS, 16>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
-                             a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
-                             ch, a.n_chunks, a.k, lut, nullptr, hist, cnt, eql, ceq, wsum, sh, cls,
-                             a.tkey ? a.tkey + (long long)p * C2 : nullptr);
+                                 a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
+                                 ch, a.n_chunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
+                                 a.tkey ? a.tkey + (long long)p * C2 : nullptr);
     if (tid == 0) {
         a.cut[2 * p] = (int)sh[3];
         a.cut[2 * p + 1] = (int)sh[4];
@@ -694,8 +691,8 @@ void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
     a.tkey = tkey;
     a.cut = cut;
     a.sel_before = sel_before;
-    size_t smem = 2 * C * 8 + (C2 + 2 * NB + n_chunks + 72) * 4;
-    if (smem > 220 * 1024) fail(PQKV_EINVAL, "tuple select: table too large");
+    size_t smem = pair_select_scratch((int)C, (int)n_chunks);
+    if (smem > 220 * 1024 || n_chunks > 2 * (size_t)NB) fail(PQKV_EINVAL, "tuple select: table too large");
     PQKV_CUDA(cudaFuncSetAttribute(tuple_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tuple_select_kernel<<<(unsigned)rows, TUP_THREADS, smem, st>>>(a);
     PQKV_LAUNCHED("tuple_select_kernel");

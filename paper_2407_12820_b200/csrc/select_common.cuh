@@ -8,14 +8,8 @@ namespace pqkv_dev {
 
 constexpr int NB = 2048;  // bins of the two 11-bit radix digits
 
-#ifdef PQKV_PROBE_TIMERS
-}  // namespace pqkv_dev
-__device__ unsigned long long g_t[64][16];  // probe builds only
-namespace pqkv_dev {
-#define PQKV_T(ph) do { if (threadIdx.x == 0) ::g_t[blockIdx.x][ph] = clock64(); } while (0)
-#else
-#define PQKV_T(ph) do { } while (0)
-#endif
+// Phase timestamps (profiling): tp[ph] = clock64() from thread 0 when tp != null.
+#define PQKV_T(ph) do { if (tp && threadIdx.x == 0) tp[ph] = clock64(); } while (0)
 
 // Builds T[j][c] (pq.cpp:113-126, rows accumulated as in pq.cpp:157-159).
 // One thread per (j, c); the t-chain stays sequential (reference order) while
@@ -147,19 +141,27 @@ __device__ void find_digit(const uint32_t* hist, int nb, uint32_t k_rem, uint32_
 
 
 // Pair-level exact top-k for one head (m == 2): builds the ADC table, the
-// C*C pair keys, radix-selects the k-th largest key weighted by the pair
-// histogram thist, classifies every pair (0 below, 1 above, 2 equal) into
-// cls[], and finds the PQKV_TUPLE_CHUNK chunk c* holding the k_rem-th equal
-// token in id order plus how many of c*'s equal tokens are taken.  On return
-// (after a barrier) sh[3] = c*, sh[4] = take, sh[5] = K*.  All scratch is
-// shared memory owned by the caller: lut[2C] f64, key[C*C] (nullable),
-// hist[NB], cnt[NB], eql[C*C], ceq[n_chunks], wsum[64], sh[8].
+// keys of the code pairs that occur (thist > 0), radix-selects the k-th
+// largest key weighted by the pair histogram thist, classifies every pair
+// (0 below or absent, 1 above, 2 equal) into cls[], and finds the
+// PQKV_TUPLE_CHUNK chunk c* holding the k_rem-th equal token in id order plus
+// how many of c*'s equal tokens are taken.  Pairs that never occur are
+// compacted away first (block scan), so the select costs O(distinct pairs),
+// not O(C^2).  On return (after a barrier) sh[3] = c*, sh[4] = take,
+// sh[5] = K*.  All scratch is shared memory owned by the caller (see
+// pair_select_scratch): lut[2C] f64, hist[NB], cnt[NB], lst[C*C], ceq[n_chunks]
+// u32, wsum[64], sh[8].  Requires C*C <= NT*WMAX and thist entries below
+// 2^(32 - log2(C*C)) (a list entry packs pair << wbits | weight).
+// tkey_out (nullable) receives the key of every pair.
 template <int NT, int WMAX>
 __device__ void pair_select(const float* q, int g, int d_h, const float* cen, int C,
                             const uint32_t* thist, const uint16_t* chist, int n_chunks, int k,
-                            double* lut, uint32_t* key, uint32_t* hist, uint32_t* cnt, uint32_t* eql,
-                            uint32_t* ceq, uint32_t* wsum, uint32_t* sh, uint8_t* cls, uint32_t* tkey_out) {
-    const int tid = threadIdx.x, C2 = C * C;
+                            double* lut, uint32_t* hist, uint32_t* cnt, uint32_t* lst, uint32_t* ceq,
+                            uint32_t* wsum, uint32_t* sh, uint8_t* cls, uint32_t* tkey_out,
+                            unsigned long long* tp = nullptr) {
+    const int tid = threadIdx.x, C2 = C * C, lane = tid & 31, warp = tid >> 5;
+    const int wbits = 32 - (32 - __clz((unsigned)(C2 - 1) | 1u));  // weight bits of a list entry
+    const uint32_t wmask = (1u << wbits) - 1u;
     // pair weights: loaded once into registers (WMAX * NT >= C2), in flight
     // while the ADC table is built
     PQKV_T(0);
@@ -170,74 +172,92 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
         w[u] = t < C2 ? __ldg(thist + t) : 0u;
     }
     build_lut(lut, q, cen, g, d_h, 2, C);
-    PQKV_T(1);
     for (int c = tid; c < n_chunks; c += NT) ceq[c] = 0;
-    __syncthreads();
-    PQKV_T(2);
-    uint32_t kr[WMAX];
+    for (int e = tid; e < (C2 + 3) / 4; e += NT) reinterpret_cast<uint32_t*>(cls)[e] = 0u;
+    PQKV_T(1);
+    // ---- compaction: lst[] = (pair << wbits | weight) of the pairs present ----
+    uint32_t nz = 0;
 #pragma unroll
-    for (int u = 0; u < WMAX; ++u) {
-        const int t = tid + u * NT;
-        kr[u] = 0;
-        if (t < C2) {
-            double acc = __dadd_rn(0.0, lut[t / C]);
-            acc = __dadd_rn(acc, lut[C + t % C]);
-            kr[u] = score_key((float)acc);
-            if (key) key[t] = kr[u];
-        }
-    }
-    // ---- weighted radix select over the pair keys ----
-    // Digit 0 spans [kmin, kmax] of the present pairs (f32 bit patterns of
-    // nearby scores share their top bits, so fixed top-bit digits would pile
-    // into a few bins); later digits refine the remaining low bits.  Each
-    // pass also counts pairs per bin: once the threshold bin holds a single
-    // pair its key is K* and the remaining passes are skipped.
-    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (int u = 0; u < WMAX; ++u) nz += w[u] != 0u;
+    uint32_t nnz;
+    uint32_t pos = block_excl_scan<NT>(nz, wsum, &nnz);  // ends with a barrier
 #pragma unroll
     for (int u = 0; u < WMAX; ++u)
-        if (w[u]) { kmin = min(kmin, kr[u]); kmax = max(kmax, kr[u]); }
-    {
-        const int lane = tid & 31, warp = tid >> 5;
+        if (w[u]) lst[pos++] = (uint32_t)(tid + u * NT) << wbits | w[u];
+    for (int b = tid; b < NB; b += NT) { hist[b] = 0; cnt[b] = 0; }
+    __syncthreads();
+    PQKV_T(2);
+    // this thread's items: lst[tid + u*NT], u < per (block-uniform)
+    const int per = (int)((nnz + NT - 1) / NT);
+    uint32_t it[WMAX], kr[WMAX];
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+    for (int u = 0; u < WMAX; ++u) {
+        it[u] = 0u;
+        kr[u] = 0u;
+        if (u < per) {
+            const int i = tid + u * NT;
+            if (i < (int)nnz) {
+                it[u] = lst[i];
+                const int t = (int)(it[u] >> wbits);
+                double acc = __dadd_rn(0.0, lut[t / C]);
+                acc = __dadd_rn(acc, lut[C + t % C]);
+                kr[u] = score_key((float)acc);
+                kmin = min(kmin, kr[u]);
+                kmax = max(kmax, kr[u]);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+    }
+    if (lane == 0) { wsum[warp] = kmin; wsum[32 + warp] = kmax; }
+    if (tkey_out)
+        for (int t = tid; t < C2; t += NT) {
+            double acc = __dadd_rn(0.0, lut[t / C]);
+            acc = __dadd_rn(acc, lut[C + t % C]);
+            tkey_out[t] = score_key((float)acc);
+        }
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t a = lane < NT / 32 ? wsum[lane] : 0xffffffffu, z = lane < NT / 32 ? wsum[32 + lane] : 0u;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
-            kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+            a = min(a, __shfl_xor_sync(FULL, a, o));
+            z = max(z, __shfl_xor_sync(FULL, z, o));
         }
-        if (lane == 0) { wsum[warp] = kmin; wsum[32 + warp] = kmax; }
-        for (int b = tid; b < NB; b += NT) { hist[b] = 0; cnt[b] = 0; }
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t a = 0xffffffffu, z = 0u;
-            for (int e = 0; e < NT / 32; ++e) { a = min(a, wsum[e]); z = max(z, wsum[32 + e]); }
-            sh[6] = a;
-            sh[7] = z;
-        }
-        __syncthreads();
-        kmin = sh[6];
-        kmax = sh[7];
+        if (lane == 0) { sh[6] = a; sh[7] = z; }
     }
+    __syncthreads();
+    kmin = sh[6];
+    kmax = sh[7];
     PQKV_T(3);
+    // ---- weighted radix select over the present pair keys ----
+    // Digit 0 spans [kmin, kmax] (f32 bit patterns of nearby scores share
+    // their top bits, so fixed top-bit digits would pile into a few bins);
+    // later digits refine the remaining low bits.  Each pass also counts
+    // pairs per bin: once the threshold bin holds a single pair its key is K*
+    // and the remaining passes are skipped.
     uint32_t k_rem = (uint32_t)k;
     const uint32_t range = kmax - kmin;
-    int shift = 32 - __clz(range | 1u);  // bits needed for (key - kmin)
-    shift = max(0, shift - 11);          // digit 0 = top 11 bits of (key - kmin)
-    uint32_t lo = kmin;                  // keys in the current candidate bin: [lo, lo + 2^shift... )
-    uint32_t prefix_val = 0;             // (key - kmin) >> (shift + width) of the chosen bins
+    int cur_shift = max(0, (32 - __clz(range | 1u)) - 11);  // digit 0 = top 11 bits of (key - kmin)
     int width = 11;
+    uint32_t prefix_val = 0;  // (key - kmin) >> (cur_shift + width) of the chosen bins
     uint32_t kstar = 0;
-    bool done = false;
-    int cur_shift = shift;
-    for (int pass = 0; pass < 4 && !done; ++pass) {
+    for (int pass = 0; pass < 4; ++pass) {
         const uint32_t nb = 1u << width;
         const uint32_t mask = nb - 1;
-        // candidates: (key - kmin) >> (cur_shift + width) == prefix_val
 #pragma unroll
         for (int u = 0; u < WMAX; ++u) {
+            if (u >= per) break;
             const uint32_t rel = kr[u] - kmin;
-            const bool in = w[u] && (pass == 0 || (rel >> (cur_shift + width)) == prefix_val);
+            const uint32_t wt = it[u] & wmask;
+            const bool in = wt && (pass == 0 || (rel >> (cur_shift + width)) == prefix_val);
             if (in) {
                 const uint32_t b = (rel >> cur_shift) & mask;
-                atomicAdd(&hist[b], w[u]);
+                atomicAdd(&hist[b], wt);
                 atomicAdd(&cnt[b], 1u);
             }
         }
@@ -254,33 +274,33 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
             __syncthreads();
 #pragma unroll
             for (int u = 0; u < WMAX; ++u) {
+                if (u >= per) break;
                 const uint32_t rel = kr[u] - kmin;
-                if (w[u] && (rel >> cur_shift) == prefix_val) atomicMin(&sh[5], kr[u]);
+                if ((it[u] & wmask) && (rel >> cur_shift) == prefix_val) atomicMin(&sh[5], kr[u]);
             }
             __syncthreads();
             kstar = sh[5];
-            done = true;
-        } else {
-            // next digit: the low cur_shift bits, up to 11 at a time
-            width = min(11, cur_shift);
-            cur_shift -= width;
-            for (int e = tid; e < max(1 << width, NT); e += NT) { hist[e] = 0; cnt[e] = 0; }
-            __syncthreads();
+            break;
         }
+        // next digit: the low cur_shift bits, up to 11 at a time
+        width = min(11, cur_shift);
+        cur_shift -= width;
+        for (int e = tid; e < max(1 << width, NT); e += NT) { hist[e] = 0; cnt[e] = 0; }
+        __syncthreads();
     }
-    (void)lo;
     PQKV_T(4);
+    // ---- classification of the present pairs; equal pairs -> eql (= lst) ----
+    uint32_t* eql = lst;  // every thread has its items in registers
     if (tid == 0) sh[2] = 0;
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < WMAX; ++u) {
-        const int t = tid + u * NT;
-        if (t >= C2) break;
-        const uint32_t kk = kr[u];
-        uint8_t c = kk > kstar ? 1 : (kk == kstar ? 2 : 0);
+        if (u >= per) break;
+        if (!(it[u] & wmask)) continue;
+        const uint32_t t = it[u] >> wbits, kk = kr[u];
+        const uint8_t c = kk > kstar ? 1 : (kk == kstar ? 2 : 0);
         cls[t] = c;
-        if (c == 2 && w[u]) eql[atomicAdd(&sh[2], 1u)] = (uint32_t)t;
-        if (tkey_out) tkey_out[t] = kk;
+        if (c == 2) eql[atomicAdd(&sh[2], 1u)] = t;
     }
     __syncthreads();
     PQKV_T(5);
@@ -293,7 +313,6 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
     __syncthreads();
     PQKV_T(6);
     if (tid < 32) {  // chunk holding the k_rem-th equal token (warp scan over chunks)
-        const int lane = tid;
         uint32_t run = 0;
         int cstar = -1;
         uint32_t take = 0;
@@ -323,5 +342,26 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
     }
     __syncthreads();
 }
+
+// Shared-memory bytes of pair_select's scratch for C centroids and n_chunks
+// tuple chunks (lut | hist | cnt | lst | ceq | wsum | sh).
+__host__ __device__ constexpr size_t pair_select_scratch(int C, int n_chunks) {
+    return (size_t)16 * C + (size_t)4 * (2 * NB + (size_t)C * C + n_chunks + 72);
+}
+
+// Carves pair_select's scratch out of z (8-byte aligned).
+struct PairScratch {
+    double* lut;
+    uint32_t *hist, *cnt, *lst, *ceq, *wsum, *sh;
+    __device__ PairScratch(unsigned char* z, int C, int n_chunks) {
+        lut = reinterpret_cast<double*>(z);
+        hist = reinterpret_cast<uint32_t*>(lut + 2 * C);
+        cnt = hist + NB;
+        lst = cnt + NB;
+        ceq = lst + C * C;
+        wsum = ceq + n_chunks;
+        sh = wsum + 64;
+    }
+};
 
 }  // namespace pqkv_dev

@@ -7,8 +7,8 @@
 #include <random>
 #include <vector>
 #include <cuda_runtime.h>
-#define PQKV_PROBE_TIMERS 1
 #include "select_common.cuh"
+__device__ unsigned long long g_t[64][16];
 
 using namespace pqkv_dev;
 
@@ -17,21 +17,15 @@ __global__ void probe(const float* q, const float* cen, const uint32_t* thist, c
                       int k, uint8_t* cls_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int p = blockIdx.x, C = 64, C2 = C * C;
-    double* lut = reinterpret_cast<double*>(smem);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(lut + 2 * C);
-    uint32_t* cnt = hist + NB;
-    uint32_t* eql = cnt + NB;
-    uint32_t* ceq = eql + C2;
-    uint32_t* wsum = ceq + n_chunks;
-    uint32_t* sh = wsum + 64;
+    PairScratch ps(smem, C, n_chunks);
     __shared__ uint8_t cls[4096];
     unsigned long long t0 = clock64();
     pair_select<NT, 16>(q + p * 128, 1, 128, cen + (size_t)p * 2 * C * 64, C, thist + (size_t)p * C2,
-                        chist + (size_t)p * n_chunks * C2, n_chunks, k, lut, nullptr, hist, cnt, eql, ceq, wsum, sh,
-                        cls, nullptr);
+                        chist + (size_t)p * n_chunks * C2, n_chunks, k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh,
+                        cls, nullptr, ::g_t[p]);
     if (threadIdx.x == 0) {
         ::g_t[p][15] = clock64() - t0;
-        cls_out[p] = (uint8_t)sh[3];
+        cls_out[p] = (uint8_t)ps.sh[3];
     }
 }
 
@@ -58,7 +52,7 @@ int main() {
     cudaMemcpy(dc, cen.data(), cen.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dth, th.data(), th.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dch, ch.data(), ch.size() * 2, cudaMemcpyHostToDevice);
-    size_t smem = 2 * C * 8 + (2 * NB + C2 + NCH + 80) * 4;
+    size_t smem = pair_select_scratch(C, NCH);
     cudaFuncSetAttribute(probe<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(probe<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int nt : {256, 1024}) {

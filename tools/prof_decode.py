@@ -7,6 +7,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2407_12820_b200 as pq  # noqa: E402
@@ -51,5 +52,27 @@ if os.environ.get("PQKV_PHASES"):
         torch.cuda.synchronize()
         prof = ctx.last_decode_profile()
         print(mode, {k: (round(v / 1965.0, 2) if k != "ctas" else v) for k, v in prof.items()}, "(us)")
+        raw = ctx.decode_profile_raw().astype(np.int64)
+        raw = raw[raw[:, 4] > 0]
+        t0 = raw[:, 4].min()
+        pct = lambda v: [round(float(np.percentile(v, q)) / 1e3, 1) for q in (0, 10, 50, 90, 100)]
+        print(f"  {mode} timeline us (p0/p10/p50/p90/p100 over {len(raw)} CTAs):")
+        print("    start      ", pct(raw[:, 4] - t0))
+        print("    rows ready ", pct(raw[:, 5] - t0))
+        print("    gather done", pct(raw[:, 6] - t0))
+        print("    exit       ", pct(raw[:, 7] - t0))
+        print("    gather span", pct(raw[:, 6] - raw[:, 5]))
+        if mode == "fused":
+            from collections import Counter
+            r0sm = Counter(raw[raw[:, 18] == 1][:, 16].tolist())
+            allsm = Counter(raw[:, 16].tolist())
+            print("  SMs used", len(allsm), "CTAs/SM", sorted(Counter(allsm.values()).items()),
+                  "selector CTAs per SM", sorted(Counter(r0sm.values()).items()))
+        r0 = raw[raw[:, 8] > 0]
+        if len(r0):
+            cyc = lambda a, b: round(float(np.median(r0[:, b] - r0[:, a])) / 1965.0, 2)
+            print("  pair_select phases, median us over", len(r0), "rank-0 CTAs: start->w+lut", cyc(0, 9),
+                  "lut", cyc(8, 9), "keys", cyc(10, 11), "radix", cyc(11, 12), "classify", cyc(12, 13),
+                  "chist", cyc(13, 14), "-> cluster.sync", cyc(14, 15), "-> dsmem+sync", cyc(15, 1))
     ctx.set_profiling(False)
 print("done", out.abs().sum().item())
