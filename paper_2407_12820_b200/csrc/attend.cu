@@ -131,70 +131,98 @@ __device__ int expand_words(const uint32_t* words, int nwords, int token_base, i
 }
 
 // Tuple classification of middle tokens [r0, r1) into selection words
-// (pq.cpp:128-140 pair score, topk.cpp tie rule via the tuple_select cut).
-// Warp segments never straddle a PQKV_TUPLE_CHUNK chunk (chunk % (8*32) and
-// PQKV_TUPLE_CHUNK % segment hold by construction).
-// The code pair of middle row i is cd[i - cd_off] (global memory, or a copy
-// of this CTA's range staged in shared memory).
+// (pq.cpp:128-140 pair score, topk.cpp tie rule via the pair-select cut):
+// a token is selected when its pair class is "above", or "equal" and it is
+// among the first `take` equal tokens of tuple chunk c* (all equal tokens of
+// earlier chunks, none of later ones).  The code pair of middle row i is
+// cd[i - cd_off] (global memory, or this CTA's range staged in shared
+// memory).  Each lane classifies 4 consecutive tokens per 128-token group
+// (one 128-bit load); nibbles are OR-reduced over 8 lanes into 32-token
+// words of "above" (words[]) and "equal" (eqw[]) bits, then the equal bits
+// are resolved per chunk.  Warp segments never straddle a PQKV_TUPLE_CHUNK
+// chunk (chunk % (8*512) and PQKV_TUPLE_CHUNK % segment hold by construction).
 __device__ void classify_words(const AtArgs& a, int r0, int r1, const uint32_t* cd_base, int cd_off,
-                               uint32_t* words, const uint8_t* cls, uint32_t* wtot, int cstar, uint32_t take) {
+                               uint32_t* words, uint32_t* eqw, const uint8_t* cls, uint32_t* wtot, int cstar,
+                               uint32_t take) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int seg = a.chunk / AT_WARPS;  // tokens per warp (multiple of 32)
+    const int seg = a.chunk / AT_WARPS;  // tokens per warp (multiple of 128)
     const int s0 = r0 + warp * seg, s1 = min(r1, s0 + seg);
     const int tc = s0 / PQKV_TUPLE_CHUNK;
     const uint32_t* cd = cd_base - cd_off;
+    const uint32_t C = (uint32_t)a.C;
+    // ---- step 1: above / equal words ----
+    for (int g0 = s0; g0 < s1; g0 += 128) {
+        const int i = g0 + 4 * lane;
+        uint32_t pr[4];
+        if (i + 3 < s1 && (reinterpret_cast<uintptr_t>(cd + i) & 15) == 0) {
+            const uint4 v = *reinterpret_cast<const uint4*>(cd + i);
+            pr[0] = v.x; pr[1] = v.y; pr[2] = v.z; pr[3] = v.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pr[e] = i + e < s1 ? cd[i + e] : 0xffffffffu;
+        }
+        uint32_t ng = 0, ne = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (pr[e] == 0xffffffffu) continue;
+            const uint8_t cl = cls[(pr[e] & 0xffffu) * C + (pr[e] >> 16)];
+            ng |= (uint32_t)(cl == 1) << e;
+            ne |= (uint32_t)(cl == 2) << e;
+        }
+        const int sh = 4 * (lane & 7);
+        ng <<= sh;
+        ne <<= sh;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            ng |= __shfl_xor_sync(FULL, ng, o);
+            ne |= __shfl_xor_sync(FULL, ne, o);
+        }
+        const int w = ((g0 - r0) >> 5) + (lane >> 3);
+        if ((lane & 7) == 0 && g0 + 32 * (lane >> 3) < s1) {
+            words[w] = ng;
+            eqw[w] = ne;
+        }
+    }
+    __syncwarp();
+    const int w0 = (s0 - r0) >> 5, w1 = (max(s0, s1) - r0 + 31) >> 5;
+    // ---- step 2: resolve the equal tokens ----
     const bool boundary = tc == cstar && s0 < s1;
-    // pass 1 (boundary chunk only): equal-pair counts per warp, in id order
-    uint32_t eq_before = 0;
     if (__syncthreads_or(boundary)) {
+        // equal tokens of c* before this warp (warps of the chunk in id order)
         uint32_t neq = 0;
         if (boundary)
-            for (int i0 = s0; i0 < s1; i0 += 32) {
-                const int i = i0 + lane;
-                uint8_t cl = 0;
-                if (i < s1) {
-                    uint32_t pr = cd[i];
-                    cl = cls[(pr & 0xffffu) * (uint32_t)a.C + (pr >> 16)];
-                }
-                neq += __popc(__ballot_sync(FULL, cl == 2));
-            }
+            for (int w = w0 + lane; w < w1; w += 32) neq += __popc(eqw[w]);
+        neq = warp_sum(neq);
         if (lane == 0) wtot[warp] = boundary ? neq : 0;
         __syncthreads();
-        // warps of the same tuple chunk precede in warp order
-        for (int w = 0; w < warp; ++w)
-            if ((r0 + w * seg) / PQKV_TUPLE_CHUNK == tc) eq_before += wtot[w];
+        uint32_t run = 0;
+        for (int v = 0; v < warp; ++v)
+            if ((r0 + v * seg) / PQKV_TUPLE_CHUNK == tc) run += wtot[v];
         __syncthreads();
-    }
-    // pass 2: selection words; a warp's codes are fetched 8 words (256
-    // tokens) at a time so the loads overlap instead of serialising on L2.
-    uint32_t eq_run = eq_before;
-    constexpr int PF = 8;
-    for (int b0 = s0; b0 < s1; b0 += 32 * PF) {
-        uint32_t prs[PF];
+        if (boundary)
+            for (int wb = w0; wb < w1; wb += 32) {
+                const int w = wb + lane;
+                const uint32_t e = w < w1 ? eqw[w] : 0u;
+                const uint32_t c = __popc(e);
+                uint32_t x = c;
 #pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int i = b0 + 32 * u + lane;
-            prs[u] = i < s1 ? cd[i] : 0xffffffffu;
-        }
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int i0 = b0 + 32 * u;
-            if (i0 >= s1) break;  // warp uniform
-            uint8_t cl = 0;
-            if (prs[u] != 0xffffffffu) cl = cls[(prs[u] & 0xffffu) * (uint32_t)a.C + (prs[u] >> 16)];
-            const bool gt = cl == 1, eq = cl == 2;
-            bool sel;
-            if (tc < cstar) sel = gt || eq;
-            else if (tc > cstar) sel = gt;
-            else {
-                unsigned em = __ballot_sync(FULL, eq);
-                sel = gt || (eq && eq_run + __popc(em & lanemask_lt()) < take);
-                eq_run += __popc(em);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, x, o);
+                    if (lane >= o) x += y;
+                }
+                const uint32_t before = run + x - c;
+                uint32_t keep = 0;
+                if (before + c <= take) keep = e;
+                else if (before < take) {
+                    uint32_t m = e;
+                    for (uint32_t n = take - before; n; --n) { keep |= m & (0u - m); m &= m - 1; }
+                }
+                if (w < w1) words[w] |= keep;
+                run += __shfl_sync(FULL, x, 31);
             }
-            const unsigned word = __ballot_sync(FULL, sel);
-            if (lane == 0) words[(i0 - r0) >> 5] = word;
-        }
     }
+    if (tc < cstar)
+        for (int w = w0 + lane; w < w1; w += 32) words[w] |= eqw[w];
     __syncthreads();
 }
 
@@ -211,7 +239,8 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     const int nwords = a.chunk / 32;
     int* rows = reinterpret_cast<int*>(smem_raw);
     uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + a.region);
-    uint8_t* cls = reinterpret_cast<uint8_t*>(words + nwords);
+    uint32_t* eqw = words + nwords;
+    uint8_t* cls = reinterpret_cast<uint8_t*>(eqw + nwords);
 
     const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
     if (a.prof && tid == 0) {
@@ -301,7 +330,9 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             const uint32_t take = cut_s[1];
             cp_async_wait_all();
             __syncthreads();
-            classify_words(a, r0, r1, cd_src, cd_off, words, cls, wtot, cstar, take);
+            if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 19] = clock64();
+            classify_words(a, r0, r1, cd_src, cd_off, words, eqw, cls, wtot, cstar, take);
+            if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 20] = clock64();
             if (c == 0)  // after the staged codes are consumed (they share rows[])
                 for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
         } else {
@@ -314,7 +345,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             }
             __syncthreads();
             classify_words(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), 0,
-                           words, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
+                           words, eqw, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
         }
         __syncthreads();
         nrows += expand_words(words, nw, a.n_init + r0, rows, nrows, wtot);
@@ -652,7 +683,7 @@ static size_t attend_smem(AtArgs& a, int G) {
     if (a.src == SRC_PAIRS) region = std::max(region, pair_select_scratch(a.C, a.n_tchunks));
     region = round_up(region, 16);
     a.region = (int)region;
-    size_t tail = (size_t)a.chunk / 32 * 4 +
+    size_t tail = (size_t)a.chunk / 32 * 4 * 2 +
                   ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
     return round_up(region + tail, 16);
 }

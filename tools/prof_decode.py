@@ -68,6 +68,10 @@ if os.environ.get("PQKV_PHASES"):
             allsm = Counter(raw[:, 16].tolist())
             print("  SMs used", len(allsm), "CTAs/SM", sorted(Counter(allsm.values()).items()),
                   "selector CTAs per SM", sorted(Counter(r0sm.values()).items()))
+        if mode == "fused":
+            cy = lambda a, b: [round(float(np.percentile(raw[:, b] - raw[:, a], q)) / 1965.0, 2) for q in (10, 50, 90, 100)]
+            print("  non-selector phases us (p10/p50/p90/p100): sync->staged", cy(1, 19), "classify", cy(19, 20),
+                  "expand", cy(20, 2))
         r0 = raw[raw[:, 8] > 0]
         if len(r0):
             cyc = lambda a, b: round(float(np.median(r0[:, b] - r0[:, a])) / 1965.0, 2)
