@@ -130,57 +130,67 @@ __device__ int expand_words(const uint32_t* words, int nwords, int token_base, i
     return (int)total;
 }
 
+// Staged code layout: within every block of 256 16-byte chunks (1024
+// tokens = 32 selection words), chunk u of word w sits at u * 32 + w, so the
+// 32 lanes of a warp reading chunk u of 32 consecutive words hit 32
+// consecutive 16-byte slots (no bank conflicts).
+__device__ __forceinline__ int code_swz(int f) { return (f & ~255) | ((f & 7) << 5) | ((f >> 3) & 31); }
+
 // Tuple classification of middle tokens [r0, r1) into selection words
 // (pq.cpp:128-140 pair score, topk.cpp tie rule via the pair-select cut):
 // a token is selected when its pair class is "above", or "equal" and it is
 // among the first `take` equal tokens of tuple chunk c* (all equal tokens of
-// earlier chunks, none of later ones).  The code pair of middle row i is
-// cd[i - cd_off] (global memory, or this CTA's range staged in shared
-// memory).  Each lane classifies 4 consecutive tokens per 128-token group
-// (one 128-bit load); nibbles are OR-reduced over 8 lanes into 32-token
-// words of "above" (words[]) and "equal" (eqw[]) bits, then the equal bits
-// are resolved per chunk.  Warp segments never straddle a PQKV_TUPLE_CHUNK
-// chunk (chunk % (8*512) and PQKV_TUPLE_CHUNK % segment hold by construction).
-__device__ void classify_words(const AtArgs& a, int r0, int r1, const uint32_t* cd_base, int cd_off,
+// earlier chunks, none of later ones).  Each lane builds one 32-token word
+// of "above" bits (words[]) and of "equal" bits (eqw[]) from 8 128-bit code
+// loads -- from shared memory (`staged`: this CTA's range copied with the
+// code_swz layout) or from global memory (cd_g, absolute rows) -- then the
+// equal bits are resolved per chunk.  Warp segments never straddle a
+// PQKV_TUPLE_CHUNK chunk (chunk % (8*512) and PQKV_TUPLE_CHUNK % segment hold
+// by construction).
+__device__ void classify_words(const AtArgs& a, int r0, int r1, const uint32_t* cd_g, const uint32_t* staged,
                                uint32_t* words, uint32_t* eqw, const uint8_t* cls, uint32_t* wtot, int cstar,
                                uint32_t take) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int seg = a.chunk / AT_WARPS;  // tokens per warp (multiple of 128)
+    const int seg = a.chunk / AT_WARPS;  // tokens per warp (multiple of 512)
     const int s0 = r0 + warp * seg, s1 = min(r1, s0 + seg);
     const int tc = s0 / PQKV_TUPLE_CHUNK;
-    const uint32_t* cd = cd_base - cd_off;
     const uint32_t C = (uint32_t)a.C;
-    // ---- step 1: above / equal words ----
-    for (int g0 = s0; g0 < s1; g0 += 128) {
-        const int i = g0 + 4 * lane;
-        uint32_t pr[4];
-        if (i + 3 < s1 && (reinterpret_cast<uintptr_t>(cd + i) & 15) == 0) {
-            const uint4 v = *reinterpret_cast<const uint4*>(cd + i);
-            pr[0] = v.x; pr[1] = v.y; pr[2] = v.z; pr[3] = v.w;
-        } else {
+    const bool gvec = (reinterpret_cast<uintptr_t>(cd_g + r0) & 15) == 0;
+    // ---- step 1: above / equal words, one word per lane ----
+    {
+        const int w0 = (s0 - r0) >> 5, w1 = (max(s0, s1) - r0 + 31) >> 5;
+        for (int wb = w0; wb < w1; wb += 32) {
+            const int wi = wb + lane;
+            if (wi >= w1) continue;
+            const int nvalid = min(32, r1 - (r0 + 32 * wi));
+            uint32_t gt = 0, eq = 0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) pr[e] = i + e < s1 ? cd[i + e] : 0xffffffffu;
-        }
-        uint32_t ng = 0, ne = 0;
+            for (int u = 0; u < 8; ++u) {
+                uint4 v;
+                if (staged) {
+                    v = reinterpret_cast<const uint4*>(staged)[code_swz(wi * 8 + u)];
+                } else if (gvec && nvalid == 32) {
+                    v = *reinterpret_cast<const uint4*>(cd_g + r0 + 32 * wi + 4 * u);
+                } else {
+                    const uint32_t* c = cd_g + r0 + 32 * wi + 4 * u;
+                    v.x = 4 * u + 0 < nvalid ? c[0] : 0u;
+                    v.y = 4 * u + 1 < nvalid ? c[1] : 0u;
+                    v.z = 4 * u + 2 < nvalid ? c[2] : 0u;
+                    v.w = 4 * u + 3 < nvalid ? c[3] : 0u;
+                }
+                const uint32_t pv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (pr[e] == 0xffffffffu) continue;
-            const uint8_t cl = cls[(pr[e] & 0xffffu) * C + (pr[e] >> 16)];
-            ng |= (uint32_t)(cl == 1) << e;
-            ne |= (uint32_t)(cl == 2) << e;
-        }
-        const int sh = 4 * (lane & 7);
-        ng <<= sh;
-        ne <<= sh;
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            ng |= __shfl_xor_sync(FULL, ng, o);
-            ne |= __shfl_xor_sync(FULL, ne, o);
-        }
-        const int w = ((g0 - r0) >> 5) + (lane >> 3);
-        if ((lane & 7) == 0 && g0 + 32 * (lane >> 3) < s1) {
-            words[w] = ng;
-            eqw[w] = ne;
+                for (int e = 0; e < 4; ++e) {
+                    const int t = 4 * u + e;
+                    if (t < nvalid) {
+                        const uint32_t cl = cls[(pv[e] & 0xffffu) * C + (pv[e] >> 16)];
+                        gt |= (uint32_t)(cl == 1) << t;
+                        eq |= (uint32_t)(cl == 2) << t;
+                    }
+                }
+            }
+            words[wi] = gt;
+            eqw[wi] = eq;
         }
     }
     __syncwarp();
@@ -282,8 +292,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             // in shared memory (cp.async, rows[] region) while the selector
             // works; the selector reads them from L2 (prefetched)
             const uint32_t* cd_g = reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride);
-            const uint32_t* cd_src = cd_g;
-            int cd_off = 0;
+            const uint32_t* staged = nullptr;
             {
                 const int n = max(0, r1 - r0);
                 const uint32_t* src = cd_g + r0;
@@ -294,12 +303,11 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                     int head = 0;
                     if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
                         head = n & ~3;
-                        for (int e = tid * 4; e < head; e += AT_THREADS * 4) cp_async16(dst + e, src + e);
+                        for (int f = tid; f < head / 4; f += AT_THREADS) cp_async16(dst + 4 * code_swz(f), src + 4 * f);
                     }
-                    for (int e = head + tid; e < n; e += AT_THREADS) cp_async4(dst + e, src + e);
+                    for (int e = head + tid; e < n; e += AT_THREADS) cp_async4(dst + 4 * code_swz(e >> 2) + (e & 3), src + e);
                     cp_async_commit();
-                    cd_src = dst;
-                    cd_off = r0;
+                    staged = dst;
                 }
             }
             __shared__ uint32_t cut_s[2];
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             cp_async_wait_all();
             __syncthreads();
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 19] = clock64();
-            classify_words(a, r0, r1, cd_src, cd_off, words, eqw, cls, wtot, cstar, take);
+            classify_words(a, r0, r1, cd_g, staged, words, eqw, cls, wtot, cstar, take);
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 20] = clock64();
             if (c == 0)  // after the staged codes are consumed (they share rows[])
                 for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                 for (int e = tid; e < C2; e += AT_THREADS) cls[e] = a.cls[(long long)p * C2 + e];
             }
             __syncthreads();
-            classify_words(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), 0,
+            classify_words(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), nullptr,
                            words, eqw, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
         }
         __syncthreads();
