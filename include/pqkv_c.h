@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PQKV_ABI_VERSION 1
+#define PQKV_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define PQKV_API __attribute__((visibility("default")))
@@ -195,7 +195,7 @@ PQKV_API int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_head
                    size_t m, size_t b, const float* d_centroids, const uint16_t* d_codes,
                    size_t codes_head_stride, size_t s, size_t k, uint32_t* d_bitmap,
                    int64_t* d_ids, const uint32_t* d_tuple_hist,
-                   const uint16_t* d_tuple_chunk_hist, void* stream);
+                   const uint16_t* d_tuple_chunk_hist, size_t tuple_chunks, void* stream);
 
 /* Softmax attention over explicit row lists (softmax_attention,
  * gqa_group_attention, selective_attention: attention.cpp:35-104).  For head
@@ -231,6 +231,7 @@ typedef struct {
     /* optional code-pair tables (pqkv_pq_tuple_tables) for m == 2, b <= 7 */
     const uint32_t* tuple_hist;
     const uint16_t* tuple_chunk_hist;
+    size_t tuple_chunks;      /* chunks per head of tuple_chunk_hist (0 = ceil(s_mid/PQKV_TUPLE_CHUNK)) */
 } pqkv_layer;
 
 /* Fused decode retrieval + sparse attention for one layer (the hot path):
@@ -252,6 +253,21 @@ PQKV_API int pqkv_decode_attend(pqkv_ctx* ctx, const pqkv_layer* layer, const fl
  * fused layer, copies d_out back and synchronizes `stream`. */
 PQKV_API int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* layer, const float* h_queries,
                      size_t g, size_t k, float* h_out, void* stream);
+
+/* One decode step of the e2e loop (run_e2e, experiments.cpp:197-260) for every
+ * head: evict_local_append (kv_store.cpp:77-90) -- the fresh K/V rows
+ * d_new_keys / d_new_values [n_heads][d_h] become token `total` (the newest
+ * local token) and the oldest local token (total - n_local) joins the middle
+ * segment: its key is encoded against the head's centroids (pq_encode_one,
+ * pq.cpp:74-99), appended as code row s_mid (append_code, pq.cpp:101-108) and
+ * counted in the code-pair tables when present -- then pqkv_decode with the
+ * step's queries.  layer->total is incremented on success.  The K/V, code
+ * and chunk-table buffers must be writable with room for the new row
+ * (kv_head_stride >= (total+1)*d_h, codes_cap rows of codes per head,
+ * tuple_chunks covering s_mid+1 rows). */
+PQKV_API int pqkv_decode_step(pqkv_ctx* ctx, pqkv_layer* layer, size_t codes_cap, const float* d_new_keys,
+                              const float* d_new_values, const float* d_queries, size_t g, size_t k,
+                              float* d_out, int64_t* d_ids, void* stream);
 
 /* Number of kernels pqkv_decode launches for this geometry (for the bench's
  * gpu_launches accounting). */

@@ -35,7 +35,7 @@ class pqkv_layer(C.Structure):
         ("keys", _vp), ("values", _vp), ("kv_head_stride", _sz), ("n_heads", _sz),
         ("total", _sz), ("n_init", _sz), ("n_local", _sz), ("d_h", _sz), ("m", _sz),
         ("b", _sz), ("centroids", _vp), ("codes", _vp), ("codes_head_stride", _sz),
-        ("tuple_hist", _vp), ("tuple_chunk_hist", _vp),
+        ("tuple_hist", _vp), ("tuple_chunk_hist", _vp), ("tuple_chunks", _sz),
     ]
 
 
@@ -63,10 +63,12 @@ _SIGS = {
     "pqkv_pq_score": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
     "pqkv_topk": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _vp, _vp]),
     "pqkv_pq_tuple_tables": (_i, [_vp, _sz, _sz, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp]),
-    "pqkv_pq_search": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
+    "pqkv_pq_search": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _vp, _vp, _vp, _sz,
+                            _vp]),
     "pqkv_exact_scores": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp, _sz, _vp, _vp]),
     "pqkv_attend_rows": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp, _sz, _i, _vp, _vp]),
     "pqkv_decode": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp, _vp]),
+    "pqkv_decode_step": (_i, [_vp, C.POINTER(pqkv_layer), _sz, _vp, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
     "pqkv_decode_attend": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _vp, _vp, _vp]),
     "pqkv_decode_host": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp]),
     "pqkv_decode_launches": (_i, [C.POINTER(pqkv_layer), _sz, _i]),
@@ -276,7 +278,8 @@ class Context:
         ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device) if ordered else None
         th, ch = tables if tables is not None else (None, None)
         _check(lib().pqkv_pq_search(self.h, _ptr(queries), P, g, d_h, m, b, _ptr(centroids), _ptr(codes),
-                                    cap * m, s, k, _ptr(bm), _ptr(ids), _ptr(th), _ptr(ch), _stream()))
+                                    cap * m, s, k, _ptr(bm), _ptr(ids), _ptr(th), _ptr(ch),
+                                    ch.shape[1] if ch is not None else 0, _stream()))
         return bm, (ids[:, :k] if ids is not None else None)
 
     def exact_scores(self, queries, keys, rows):
@@ -308,6 +311,20 @@ class Context:
         ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device) if want_ids else None
         L = layer.struct()
         _check(lib().pqkv_decode(self.h, C.byref(L), _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
+        return (out, ids[:, :k]) if want_ids else out
+
+    def decode_step(self, layer: "DecodeLayer", new_keys, new_values, queries, k: int, want_ids: bool = False):
+        """One e2e step (evict_local_append + decode, pqkv_decode_step): new_keys /
+        new_values [P][d_h] become token layer.total; layer.total grows by one."""
+        import torch
+
+        P, g, d_h = queries.shape
+        out = torch.empty((P, g, d_h), dtype=torch.float32, device=queries.device)
+        ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device) if want_ids else None
+        L = layer.struct()
+        _check(lib().pqkv_decode_step(self.h, C.byref(L), layer.codes.shape[1], _ptr(new_keys), _ptr(new_values),
+                                      _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
+        layer.total = L.total
         return (out, ids[:, :k]) if want_ids else out
 
     def decode_attend(self, layer: "DecodeLayer", queries, bitmap, out=None):
@@ -358,6 +375,7 @@ class DecodeLayer:
             codes_head_stride=self.codes.shape[1] * m,
             tuple_hist=self.tables[0].data_ptr() if self.tables is not None else None,
             tuple_chunk_hist=self.tables[1].data_ptr() if self.tables is not None else None,
+            tuple_chunks=self.tables[1].shape[1] if self.tables is not None else 0,
         )
 
     def launches(self, g: int, with_ids: bool = False) -> int:

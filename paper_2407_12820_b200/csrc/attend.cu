@@ -66,6 +66,7 @@ struct AtArgs {
     const uint32_t* thist;        // [P][C*C]
     const uint16_t* chist;        // [P][n_tchunks][C*C]
     int n_tchunks, k, region;     // region: bytes of the aliased scratch area
+    long long tchunk_stride;      // chunks per head of chist
     // SRC_ROWS
     const int64_t* rows;
     int t;
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                 PairScratch ps(smem_raw, C, a.n_tchunks);  // aliases rows[]: free until expansion
                 pair_select<AT_THREADS, 16>(a.queries + (long long)p * G * DH, G, DH,
                                             a.centroids + (long long)p * 2 * C * (DH / 2), C,
-                                            a.thist + (long long)p * C2, a.chist + (long long)p * a.n_tchunks * C2,
+                                            a.thist + (long long)p * C2, a.chist + (long long)p * a.tchunk_stride * C2,
                                             a.n_tchunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
                                             nullptr, a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr);
                 const uint32_t* sh = ps.sh;
@@ -812,6 +813,7 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     a.thist = L.tuple_hist;
     a.chist = L.tuple_chunk_hist;
     a.n_tchunks = (int)ceil_div(s_mid, PQKV_TUPLE_CHUNK);
+    a.tchunk_stride = L.tuple_chunks ? (long long)L.tuple_chunks : a.n_tchunks;
     a.k = (int)k_pairs;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
     a.out = out;

@@ -167,7 +167,7 @@ int pqkv_pq_tuple_tables(pqkv_ctx* ctx, size_t n_heads, size_t b, const uint16_t
 int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
                    size_t m, size_t b, const float* d_centroids, const uint16_t* d_codes,
                    size_t codes_head_stride, size_t s, size_t k, uint32_t* d_bitmap,
-                   int64_t* d_ids, const uint32_t* d_tuple_hist, const uint16_t* d_tuple_chunk_hist,
+                   int64_t* d_ids, const uint32_t* d_tuple_hist, const uint16_t* d_tuple_chunk_hist, size_t tuple_chunks,
                    void* stream) {
     return guard([&] {
         need_ctx(ctx);
@@ -183,6 +183,7 @@ int pqkv_pq_search(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t
         src.centroids = d_centroids;
         src.codes = d_codes;
         src.codes_head_stride = codes_head_stride;
+        src.tuple_chunk_stride = tuple_chunks;
         if (tuple_ok(m, b, d_tuple_hist, d_tuple_chunk_hist, s))
             launch_select_tuple(ctx, src, d_tuple_hist, d_tuple_chunk_hist, n_heads, s, k, d_bitmap,
                                 k ? d_ids : nullptr, as_stream(stream), nullptr);
@@ -250,6 +251,7 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         src.centroids = L->centroids;
         src.codes = L->codes;
         src.codes_head_stride = L->codes_head_stride;
+        src.tuple_chunk_stride = L->tuple_chunks;
         if (tup && fast && !d_ids && k > 0 && decode_pairs_fused(*L, g)) {
             // one launch: every attention CTA selects its head's pairs, then
             // classifies its own codes and gathers
@@ -283,6 +285,30 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         launch_exact(ctx, d_queries, P, g, L->d_h, L->keys, L->values, L->kv_head_stride, rows, T, d_out, st);
         PQKV_CUDA(cudaFreeAsync(rows, st));
     });
+}
+
+int pqkv_decode_step(pqkv_ctx* ctx, pqkv_layer* L, size_t codes_cap, const float* d_new_keys,
+                     const float* d_new_values, const float* d_queries, size_t g, size_t k, float* d_out,
+                     int64_t* d_ids, void* stream) {
+    int rc = guard([&] {
+        need_ctx(ctx);
+        check_layer(L, g, 0);
+        if (!d_new_keys || !d_new_values) fail(PQKV_EINVAL, "decode_step: NULL fresh K/V rows");
+        // kv_store.cpp:81-83
+        if (L->n_local == 0) fail(PQKV_ESTATE, "kv_store: local segment is empty");
+        const size_t s_mid = L->total - L->n_init - L->n_local;
+        if (L->kv_head_stride < (L->total + 1) * L->d_h) fail(PQKV_EINVAL, "decode_step: no room for the new token");
+        if (codes_cap < s_mid + 1 || L->codes_head_stride < codes_cap * L->m)
+            fail(PQKV_EINVAL, "decode_step: no room for the new code row");
+        if (L->m == 2 && L->tuple_hist && L->tuple_chunk_hist &&
+            L->tuple_chunks < ceil_div(s_mid + 1, PQKV_TUPLE_CHUNK))
+            fail(PQKV_EINVAL, "decode_step: tuple_chunks must cover the grown middle segment");
+        if (L->n_heads == 0) return;
+        launch_evict_append(ctx, *L, d_new_keys, d_new_values, as_stream(stream));
+    });
+    if (rc != PQKV_OK) return rc;
+    L->total += 1;  // the step's mutation is on the stream; the layer now has one more token
+    return pqkv_decode(ctx, L, d_queries, g, k, d_out, d_ids, stream);
 }
 
 int pqkv_decode_attend(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size_t g,

@@ -103,6 +103,8 @@ struct KmeansBatch {
 };
 void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t stream);
 
+void launch_evict_append(pqkv_ctx* ctx, const pqkv_layer& L, const float* new_keys, const float* new_values,
+                         cudaStream_t st);
 void launch_encode(pqkv_ctx* ctx, const float* keys, size_t n_heads, size_t key_stride,
                    size_t d_h, size_t m, size_t C, const float* centroids, uint16_t* codes,
                    size_t codes_head_stride, size_t row, cudaStream_t stream);
@@ -123,6 +125,7 @@ struct SelectSource {
     const float* centroids = nullptr;
     const uint16_t* codes = nullptr;
     size_t codes_head_stride = 0;
+    size_t tuple_chunk_stride = 0;  // chunks per head of the code-pair chunk table (0 = ceil(n/4096))
     // score mode
     const float* scores = nullptr;
     size_t scores_stride = 0;

@@ -406,6 +406,7 @@ struct TupArgs {
     uint32_t* tkey;         // [P][C2] pair keys (ids mode) or null
     int* cut;               // [P][2]: c*, take
     uint32_t* sel_before;   // [P][n_chunks] exclusive prefix of selected rows (ids mode) or null
+    long long chunk_stride;  // chunks per head of chist
 };
 
 __global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a) {
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a)
     uint32_t* ceq = ps.ceq;
     uint32_t* hist = ps.hist;  // per-chunk counts below (dead radix bins, 2*NB entries with cnt)
     uint8_t* cls = a.cls + (long long)p * C2;
-    const uint16_t* ch = a.chist + (long long)p * a.n_chunks * C2;
+    const uint16_t* ch = a.chist + (long long)p * a.chunk_stride * C2;
     pair_select<TUP_THREADS, 16>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
                                  a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
                                  ch, a.n_chunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
@@ -691,6 +692,8 @@ void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
     a.tkey = tkey;
     a.cut = cut;
     a.sel_before = sel_before;
+    a.chunk_stride = (long long)(src.tuple_chunk_stride ? src.tuple_chunk_stride : n_chunks);
+    if (a.chunk_stride < (long long)n_chunks) fail(PQKV_EINVAL, "tuple select: chunk table smaller than the rows");
     size_t smem = pair_select_scratch((int)C, (int)n_chunks);
     if (smem > 220 * 1024 || n_chunks > 2 * (size_t)NB) fail(PQKV_EINVAL, "tuple select: table too large");
     PQKV_CUDA(cudaFuncSetAttribute(tuple_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
