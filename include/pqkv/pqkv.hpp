@@ -9,14 +9,16 @@
 // host side only validates arguments and moves the caller's host buffers.
 //
 // Not provided here (out of the hot-path scope): the cost
-// model, simulator/timeline, workload generator, experiments drivers, CLI and
-// the block-cache hit/miss accounting of KvStore::fetch_topk (FetchReport's
-// hits/misses/bytes fields stay 0).
+// model, simulator/timeline, workload generator, experiments drivers and CLI.
+// KvStore's block-cache accounting (fetch_topk hits/misses/bytes, LRU/LFU
+// cache, cache_stats, trace) follows kv_store.cpp:93-203, with the
+// per-request block counts and ranking computed on the GPU (pqkv_block_rank).
 #pragma once
 
 #include <cstddef>
 #include <cstdint>
 #include <deque>
+#include <map>
 #include <random>
 #include <span>
 #include <string>
@@ -153,13 +155,41 @@ struct OffloadReport {
     std::size_t bytes_offloaded = 0;
 };
 
+struct CacheStats {
+    std::size_t hits = 0;
+    std::size_t misses = 0;
+    std::size_t requests = 0;  // distinct block lookups
+    std::size_t occupancy_tokens = 0;
+    double hit_rate = 0.0;
+};
+
+struct TraceRow {
+    std::size_t step = 0;  // per-state fetch ordinal, 1-based
+    std::size_t layer = 0;
+    std::size_t kv_head = 0;
+    std::size_t block_id = 0;
+    bool hit = false;
+};
+
 /// One (layer, kv_head) slice: init segment, local ring (oldest first) and the
 /// middle tokens, with the reference's public members.
 struct HeadState {
+    struct CachedBlock {
+        std::map<std::size_t, KvEntry> snapshot;
+        std::size_t freq = 0;
+        std::uint64_t last_used = 0;
+    };
+
     std::vector<KvEntry> init_entries;
     std::deque<std::pair<std::size_t, KvEntry>> local;
     std::unordered_map<std::size_t, KvEntry> middle;
-    std::size_t total_tokens = 0;
+    std::map<std::size_t, CachedBlock> cache;
+
+    std::size_t total_tokens = 0;  // next fresh token id
+    std::size_t occupancy_tokens = 0;
+    std::size_t hits = 0, misses = 0, requests = 0;
+    std::size_t fetch_calls = 0;
+    std::uint64_t tick = 0;
     bool prefilled = false;
 };
 
@@ -173,16 +203,23 @@ public:
                                    PqIndex& index);
     FetchReport fetch_topk(std::size_t layer, std::size_t kv_head,
                            std::span<const std::size_t> token_ids, std::size_t k_cache);
+    CacheStats cache_stats(std::size_t layer, std::size_t kv_head) const;
     const HeadState& state(std::size_t layer, std::size_t kv_head) const;
     std::size_t block_size() const { return block_size_; }
     std::size_t cache_capacity() const { return cache_capacity_; }
+    void enable_trace() { trace_enabled_ = true; }
+    const std::vector<TraceRow>& trace() const { return trace_; }
 
 private:
     HeadState& state_mut(std::size_t layer, std::size_t kv_head);
+    void evict_until_fits(HeadState& st, std::size_t incoming_tokens);
+    std::size_t token_bytes() const { return 2 * 2 * head_dim_; }  // fp16 K + V
     std::size_t num_layers_, num_kv_heads_, block_size_, cache_capacity_;
     CachePolicy policy_;
     std::size_t head_dim_ = 0;
     std::vector<HeadState> states_;
+    bool trace_enabled_ = false;
+    std::vector<TraceRow> trace_;
 };
 
 // ---- attention -----------------------------------------------------------------

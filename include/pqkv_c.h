@@ -269,6 +269,19 @@ PQKV_API int pqkv_decode_step(pqkv_ctx* ctx, pqkv_layer* layer, size_t codes_cap
                               const float* d_new_values, const float* d_queries, size_t g, size_t k,
                               float* d_out, int64_t* d_ids, void* stream);
 
+/* Block-cache accounting of a fetch (kv_store.cpp:115-191), per head p:
+ * the distinct requested tokens among d_ids + p*ids_stride [0..n_ids) (ids
+ * outside [0, n_tokens) are ignored) -> d_bitmap [p][ceil(n_tokens/32)] u32
+ * (nullable), distinct tokens per block of block_size token ids ->
+ * d_counts [p][ceil(n_tokens/block_size)] u32, the k_cache most requested
+ * blocks, count desc then block id asc (kv_store.cpp:158-166) -> d_ranked
+ * [p][k_cache] i64 (-1 padded), and the number of distinct blocks touched
+ * -> d_touched [p] (nullable). */
+PQKV_API int pqkv_block_rank(pqkv_ctx* ctx, const int64_t* d_ids, size_t n_heads, size_t ids_stride,
+                             size_t n_ids, size_t n_tokens, size_t block_size, size_t k_cache,
+                             uint32_t* d_bitmap, uint32_t* d_counts, int64_t* d_ranked, uint32_t* d_touched,
+                             void* stream);
+
 /* Number of kernels pqkv_decode launches for this geometry (for the bench's
  * gpu_launches accounting). */
 PQKV_API int pqkv_decode_launches(const pqkv_layer* layer, size_t g, int with_ids);

@@ -288,4 +288,45 @@ double ref_bench_build(size_t P, size_t s, size_t d_h, size_t m, size_t b, size_
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// Block-cache replay (kv_store.cpp:93-203): offload one (s, d_h) head, then
+// for request r: if append_before[r], evict_local_append(fresh row r) against
+// a pq_construct index (m = 2, b = 3) of the middle keys; then fetch_topk of
+// ids[offs[r] .. offs[r+1]) with k_cache.  out[3r..3r+2] = hits, misses,
+// bytes_from_slow_tier; out[3n..3n+3] = cache_stats hits, misses, requests,
+// occupancy; cached block ids -> cache_out (up to cache_cap), count -> *n_cached.
+int ref_fetch_replay(size_t s, size_t d_h, const float* keys, const float* values, size_t n_init,
+                     size_t n_local, size_t block, size_t capacity, int lfu, size_t n_req,
+                     const uint64_t* offs, const uint64_t* ids, const uint8_t* append_before,
+                     const float* fresh, size_t k_cache, uint64_t* out, uint64_t* cache_out,
+                     size_t cache_cap, size_t* n_cached) {
+    return guard([&] {
+        KvStore store(1, 1, block, capacity, lfu ? CachePolicy::kLfu : CachePolicy::kLru);
+        store.offload_prefill(0, 0, grid(keys, s, d_h), grid(values, s, d_h), SegmentConfig{n_init, n_local, 0});
+        std::size_t s_mid = s - n_init - n_local;
+        PqIndex index = pq_construct(grid(keys + n_init * d_h, s_mid, d_h), PqConfig::create(2, 3, d_h), 4, 9);
+        for (size_t r = 0; r < n_req; ++r) {
+            if (append_before[r]) {
+                KvEntry e;
+                e.key.assign(fresh + r * 2 * d_h, fresh + r * 2 * d_h + d_h);
+                e.value.assign(fresh + r * 2 * d_h + d_h, fresh + (r + 1) * 2 * d_h);
+                store.evict_local_append(0, 0, std::move(e), index);
+            }
+            std::vector<std::size_t> req(ids + offs[r], ids + offs[r + 1]);
+            FetchReport rep = store.fetch_topk(0, 0, req, k_cache);
+            out[3 * r] = rep.hits;
+            out[3 * r + 1] = rep.misses;
+            out[3 * r + 2] = rep.bytes_from_slow_tier;
+        }
+        CacheStats cs = store.cache_stats(0, 0);
+        out[3 * n_req] = cs.hits;
+        out[3 * n_req + 1] = cs.misses;
+        out[3 * n_req + 2] = cs.requests;
+        out[3 * n_req + 3] = cs.occupancy_tokens;
+        size_t n = 0;
+        for (const auto& kv : store.state(0, 0).cache)
+            if (n < cache_cap) cache_out[n++] = kv.first;
+        *n_cached = store.state(0, 0).cache.size();
+    });
+}
+
 }  // extern "C"

@@ -69,6 +69,7 @@ _SIGS = {
     "pqkv_attend_rows": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp, _sz, _i, _vp, _vp]),
     "pqkv_decode": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp, _vp]),
     "pqkv_decode_step": (_i, [_vp, C.POINTER(pqkv_layer), _sz, _vp, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
+    "pqkv_block_rank": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
     "pqkv_decode_attend": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _vp, _vp, _vp]),
     "pqkv_decode_host": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp]),
     "pqkv_decode_launches": (_i, [C.POINTER(pqkv_layer), _sz, _i]),
@@ -326,6 +327,24 @@ class Context:
                                       _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
         layer.total = L.total
         return (out, ids[:, :k]) if want_ids else out
+
+    def block_rank(self, ids, n_tokens: int, block_size: int, k_cache: int):
+        """Block-cache accounting of a fetch (pqkv_block_rank): ids [P][n] int64 token
+        ids -> (bitmap [P][words] i32, counts [P][blocks] i32, ranked [P][k_cache] i64,
+        touched [P] i32)."""
+        import torch
+
+        P, n = ids.shape
+        words = (n_tokens + 31) // 32
+        nb = max(1, (n_tokens + block_size - 1) // block_size)
+        dev = ids.device
+        bm = torch.empty((P, max(words, 1)), dtype=torch.int32, device=dev)
+        counts = torch.empty((P, nb), dtype=torch.int32, device=dev)
+        ranked = torch.empty((P, max(k_cache, 1)), dtype=torch.int64, device=dev)
+        touched = torch.empty((P,), dtype=torch.int32, device=dev)
+        _check(lib().pqkv_block_rank(self.h, _ptr(ids), P, ids.stride(0), n, n_tokens, block_size, k_cache,
+                                     _ptr(bm), _ptr(counts), _ptr(ranked), _ptr(touched), _stream()))
+        return bm, counts, ranked[:, :k_cache], touched
 
     def decode_attend(self, layer: "DecodeLayer", queries, bitmap, out=None):
         """Attention half of decode for a selection bitmap from pq_search."""

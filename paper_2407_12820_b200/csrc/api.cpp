@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <map>
 #include <numeric>
 #include <set>
 #include <stdexcept>
@@ -480,18 +481,124 @@ std::size_t KvStore::evict_local_append(std::size_t layer, std::size_t kv_head, 
     return evicted_id;
 }
 
-FetchReport KvStore::fetch_topk(std::size_t layer, std::size_t kv_head,
-                                std::span<const std::size_t> token_ids, std::size_t /*k_cache*/) {
+// LRU evicts the stalest block; LFU the least frequent, ties by least recent
+// use, then the lower block id (kv_store.cpp:93-113).
+void KvStore::evict_until_fits(HeadState& st, std::size_t incoming_tokens) {
+    while (!st.cache.empty() && st.occupancy_tokens + incoming_tokens > cache_capacity_) {
+        auto victim = st.cache.begin();
+        for (auto it = std::next(st.cache.begin()); it != st.cache.end(); ++it) {
+            bool worse;
+            if (policy_ == CachePolicy::kLru) {
+                worse = it->second.last_used < victim->second.last_used;
+            } else {
+                worse = it->second.freq < victim->second.freq ||
+                        (it->second.freq == victim->second.freq && it->second.last_used < victim->second.last_used);
+            }
+            if (worse) victim = it;
+        }
+        st.occupancy_tokens -= victim->second.snapshot.size();
+        st.cache.erase(victim);
+    }
+}
+
+// fetch_topk (kv_store.cpp:115-191).  The per-request work -- distinct
+// tokens, distinct tokens per block and the top-k_cache block ranking -- runs
+// on the GPU (pqkv_block_rank); the lookups and the LRU/LFU cache refresh are
+// the reference's sequential state machine.
+FetchReport KvStore::fetch_topk(std::size_t layer, std::size_t kv_head, std::span<const std::size_t> token_ids,
+                                std::size_t k_cache) {
     HeadState& st = state_mut(layer, kv_head);
     for (std::size_t id : token_ids)
         if (!st.middle.contains(id))
             throw std::out_of_range("kv_store: token " + std::to_string(id) + " is not a middle token");
+    ++st.fetch_calls;
+
+    const std::size_t n_tokens = st.total_tokens, bs = block_size_;
+    const std::size_t n_blocks = std::max<std::size_t>(1, (n_tokens + bs - 1) / bs);
+    const std::size_t words = (n_tokens + 31) / 32;
+    const std::size_t k_rank = std::min(k_cache, n_blocks);
+    std::vector<std::int64_t> ids(token_ids.begin(), token_ids.end());
+    std::vector<std::uint32_t> bits(words), counts(n_blocks);
+    std::vector<std::int64_t> ranked(k_rank);
+    {
+        Dev<std::int64_t> d_ids(ids.data(), ids.size());
+        Dev<std::uint32_t> d_bits(words), d_counts(n_blocks);
+        Dev<std::int64_t> d_ranked(k_rank);
+        check(pqkv_block_rank(default_context(), d_ids.get(), 1, ids.size(), ids.size(), n_tokens, bs, k_rank,
+                              d_bits.get(), d_counts.get(), d_ranked.get(), nullptr, nullptr));
+        d_bits.download(bits.data(), words);
+        d_counts.download(counts.data(), n_blocks);
+        d_ranked.download(ranked.data(), k_rank);
+    }
+
     FetchReport rep;
+    std::size_t touched = 0;
+    for (std::size_t b = 0; b < n_blocks; ++b) {  // distinct blocks, ascending id (a std::map in the reference)
+        if (!counts[b]) continue;
+        ++touched;
+        auto it = st.cache.find(b);
+        const bool hit = it != st.cache.end();
+        if (hit) {
+            ++rep.hits;
+            it->second.freq += 1;
+            it->second.last_used = ++st.tick;
+            const std::size_t hi = std::min(n_tokens, (b + 1) * bs);
+            for (std::size_t id = b * bs; id < hi; ++id)
+                if (((bits[id >> 5] >> (id & 31)) & 1u) && !it->second.snapshot.contains(id))
+                    rep.bytes_from_slow_tier += token_bytes();  // appended after caching
+        } else {
+            ++rep.misses;
+            rep.bytes_from_slow_tier += counts[b] * token_bytes();
+        }
+        if (trace_enabled_) trace_.push_back({st.fetch_calls, layer, kv_head, b, hit});
+    }
+    st.hits += rep.hits;
+    st.misses += rep.misses;
+    st.requests += touched;
+
+    // the middle segment is authoritative; cached copies are bit-identical
     rep.entries.reserve(token_ids.size());
     for (std::size_t id : token_ids) rep.entries.push_back(st.middle.at(id));
-    (void)policy_;
-    (void)cache_capacity_;
+
+    // cache update: top-k_cache blocks of this request by requested-token count,
+    // ties toward the lower block id
+    for (std::int64_t rb : ranked) {
+        if (rb < 0) break;
+        const std::size_t block_id = static_cast<std::size_t>(rb);
+        std::map<std::size_t, KvEntry> snapshot;
+        for (std::size_t id = block_id * bs; id < (block_id + 1) * bs; ++id) {
+            auto mit = st.middle.find(id);
+            if (mit != st.middle.end()) snapshot.emplace(id, mit->second);
+        }
+        // a refresh re-inserts with its counters kept, so stale snapshots heal
+        std::size_t freq = 1;
+        std::uint64_t last = 0;
+        auto it = st.cache.find(block_id);
+        const bool was_cached = it != st.cache.end();
+        if (was_cached) {
+            freq = it->second.freq;
+            last = it->second.last_used;
+            st.occupancy_tokens -= it->second.snapshot.size();
+            st.cache.erase(it);
+        }
+        if (snapshot.size() > cache_capacity_) continue;  // cannot fit even alone
+        evict_until_fits(st, snapshot.size());
+        const std::size_t tokens = snapshot.size();
+        st.cache.emplace(block_id, HeadState::CachedBlock{std::move(snapshot), freq, was_cached ? last : ++st.tick});
+        st.occupancy_tokens += tokens;
+    }
     return rep;
+}
+
+CacheStats KvStore::cache_stats(std::size_t layer, std::size_t kv_head) const {
+    const HeadState& st = state(layer, kv_head);
+    CacheStats cs;
+    cs.hits = st.hits;
+    cs.misses = st.misses;
+    cs.requests = st.requests;
+    cs.occupancy_tokens = st.occupancy_tokens;
+    cs.hit_rate = st.requests ? static_cast<double>(st.hits) / st.requests : 0.0;
+    return cs;
 }
 
 }  // namespace pqkv

@@ -311,6 +311,17 @@ int pqkv_decode_step(pqkv_ctx* ctx, pqkv_layer* L, size_t codes_cap, const float
     return pqkv_decode(ctx, L, d_queries, g, k, d_out, d_ids, stream);
 }
 
+int pqkv_block_rank(pqkv_ctx* ctx, const int64_t* d_ids, size_t n_heads, size_t ids_stride, size_t n_ids,
+                    size_t n_tokens, size_t block_size, size_t k_cache, uint32_t* d_bitmap, uint32_t* d_counts,
+                    int64_t* d_ranked, uint32_t* d_touched, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if ((!d_ids && n_ids) || !d_counts || (!d_ranked && k_cache)) fail(PQKV_EINVAL, "block_rank: NULL buffer");
+        launch_block_rank(ctx, d_ids, n_heads, ids_stride, n_ids, n_tokens, block_size, k_cache, d_bitmap,
+                          d_counts, d_ranked, d_touched, as_stream(stream));
+    });
+}
+
 int pqkv_decode_attend(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size_t g,
                        const uint32_t* d_bitmap, float* d_out, void* stream) {
     return guard([&] {

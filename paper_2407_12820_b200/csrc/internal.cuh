@@ -103,6 +103,9 @@ struct KmeansBatch {
 };
 void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t stream);
 
+void launch_block_rank(pqkv_ctx* ctx, const int64_t* ids, size_t n_heads, size_t ids_stride, size_t n_ids,
+                       size_t n_tokens, size_t block_size, size_t k_cache, uint32_t* bitmap, uint32_t* counts,
+                       int64_t* ranked, uint32_t* touched, cudaStream_t st);
 void launch_evict_append(pqkv_ctx* ctx, const pqkv_layer& L, const float* new_keys, const float* new_values,
                          cudaStream_t st);
 void launch_encode(pqkv_ctx* ctx, const float* keys, size_t n_heads, size_t key_stride,

@@ -21,6 +21,9 @@ int ref_pq_score_gqa(const float*, size_t, size_t, const float*, size_t, size_t,
 int ref_top_k_desc(const float*, size_t, size_t, const uint8_t*, uint64_t*);
 int ref_selective_attention(const float*, const float*, const float*, size_t, size_t, size_t, size_t,
                             const uint64_t*, size_t, float*);
+int ref_fetch_replay(size_t, size_t, const float*, const float*, size_t, size_t, size_t, size_t, int, size_t,
+                     const uint64_t*, const uint64_t*, const uint8_t*, const float*, size_t, uint64_t*, uint64_t*,
+                     size_t, size_t*);
 }
 
 using namespace pqkv;
@@ -371,10 +374,133 @@ static void reference_equality() {
     for (int j = 0; j < 32; ++j) CHECK(approx(got[j], want[j], 1e-6));
 }
 
+// Block-cache accounting (test_kv_store.cpp cases + a randomized replay
+// against the reference library, appends included).
+static void kv_cache_cases() {
+    {  // tokens sharing a block count as one lookup
+        TensorF32 k = random_grid(4, 256, 4), v = random_grid(5, 256, 4);
+        KvStore store(1, 1, 128, 1024, CachePolicy::kLru);
+        store.offload_prefill(0, 0, k, v, SegmentConfig{8, 8, 0});
+        FetchReport rep = store.fetch_topk(0, 0, std::vector<std::size_t>{100, 101, 200, 100}, 4);
+        CHECK(rep.entries.size() == 4);
+        CHECK(rep.hits + rep.misses == 2);
+        CHECK(rep.bytes_from_slow_tier == 3 * 2 * 2 * 4);
+        CHECK(store.cache_stats(0, 0).requests == 2);
+    }
+    {  // a warm block hits on the second request
+        TensorF32 k = random_grid(6, 256, 4), v = random_grid(7, 256, 4);
+        KvStore store(1, 1, 32, 1024, CachePolicy::kLru);
+        store.offload_prefill(0, 0, k, v, SegmentConfig{8, 8, 0});
+        CHECK(store.fetch_topk(0, 0, std::vector<std::size_t>{40}, 1).misses == 1);
+        FetchReport again = store.fetch_topk(0, 0, std::vector<std::size_t>{40}, 1);
+        CHECK(again.hits == 1);
+        CHECK(again.bytes_from_slow_tier == 0);
+    }
+    {  // zero capacity never caches
+        TensorF32 k = random_grid(8, 128, 4), v = random_grid(9, 128, 4);
+        KvStore store(1, 1, 16, 0, CachePolicy::kLfu);
+        store.offload_prefill(0, 0, k, v, SegmentConfig{4, 4, 0});
+        for (int i = 0; i < 5; ++i) {
+            FetchReport rep = store.fetch_topk(0, 0, std::vector<std::size_t>{60}, 2);
+            CHECK(rep.hits == 0 && rep.misses == 1);
+        }
+        CHECK(store.cache_stats(0, 0).occupancy_tokens == 0);
+        CHECK(store.fetch_topk(0, 0, std::vector<std::size_t>{}, 1).entries.empty());
+    }
+    {  // the cache keeps the most requested blocks, ties toward the lower id
+        TensorF32 k = random_grid(10, 512, 4), v = random_grid(11, 512, 4);
+        KvStore store(1, 1, 64, 4096, CachePolicy::kLru);
+        store.offload_prefill(0, 0, k, v, SegmentConfig{8, 8, 0});
+        store.enable_trace();
+        store.fetch_topk(0, 0, std::vector<std::size_t>{130, 140, 70, 280}, 2);
+        const HeadState& st = store.state(0, 0);
+        CHECK(st.cache.size() == 2 && st.cache.contains(2) && st.cache.contains(1) && !st.cache.contains(4));
+        CHECK(store.trace().size() == 3 && store.trace()[0].block_id == 1 && store.trace()[2].block_id == 4);
+    }
+    {  // eviction follows the policy
+        auto run = [&](CachePolicy policy) {
+            TensorF32 k = random_grid(12, 10, 4), v = random_grid(13, 10, 4);
+            KvStore store(1, 1, 1, 2, policy);
+            store.offload_prefill(0, 0, k, v, SegmentConfig{0, 1, 0});
+            auto touch = [&](std::size_t id) {
+                return store.fetch_topk(0, 0, std::vector<std::size_t>{id}, 1).hits == 1;
+            };
+            touch(0);
+            touch(0);
+            touch(1);
+            touch(2);
+            return touch(0);
+        };
+        CHECK(run(CachePolicy::kLru) == false);
+        CHECK(run(CachePolicy::kLfu) == true);
+    }
+    // randomized replay against the reference library
+    for (int trial = 0; trial < 6; ++trial) {
+        const std::size_t s = 700, d = 8, n_init = 4, n_local = 16;
+        const std::size_t block = trial % 3 == 0 ? 16 : (trial % 3 == 1 ? 32 : 7);
+        const std::size_t cap = trial < 3 ? 96 : 200;
+        const bool lfu = trial & 1;
+        const std::size_t k_cache = 1 + trial % 4, n_req = 120;
+        TensorF32 k = random_grid(100 + trial, s, d), v = random_grid(200 + trial, s, d);
+        Rng rng(300 + trial);
+        std::vector<uint64_t> offs{0}, ids;
+        std::vector<uint8_t> app(n_req);
+        std::vector<float> fresh(n_req * 2 * d);
+        for (float& x : fresh) x = static_cast<float>(rng.normal());
+        KvStore store(1, 1, block, cap, lfu ? CachePolicy::kLfu : CachePolicy::kLru);
+        store.offload_prefill(0, 0, k, v, SegmentConfig{n_init, n_local, 0});
+        TensorF32 mid({s - n_init - n_local, d},
+                      std::vector<float>(k.data.begin() + n_init * d, k.data.begin() + (s - n_local) * d));
+        PqIndex index = pq_construct(mid, PqConfig::create(2, 3, d), 4, 9);
+        std::size_t mid_end = s - n_local;  // middle ids [n_init, mid_end)
+        std::vector<uint64_t> got;
+        for (std::size_t r = 0; r < n_req; ++r) {
+            app[r] = rng.index(4) == 0;
+            if (app[r]) {
+                KvEntry e;
+                e.key.assign(fresh.begin() + r * 2 * d, fresh.begin() + r * 2 * d + d);
+                e.value.assign(fresh.begin() + r * 2 * d + d, fresh.begin() + (r + 1) * 2 * d);
+                store.evict_local_append(0, 0, std::move(e), index);
+                ++mid_end;
+            }
+            std::size_t n = 1 + rng.index(12);
+            std::vector<std::size_t> req;
+            std::size_t hot = n_init + rng.index(mid_end - n_init);
+            for (std::size_t i = 0; i < n; ++i) {
+                // clustered around a hot token (repeats and the newest rows included)
+                std::size_t id = rng.index(3) == 0 ? mid_end - 1 - rng.index(std::min<std::size_t>(8, mid_end - n_init))
+                                                  : hot + rng.index(40);
+                req.push_back(std::min(id, mid_end - 1));
+            }
+            for (std::size_t id : req) ids.push_back(id);
+            offs.push_back(ids.size());
+            FetchReport rep = store.fetch_topk(0, 0, req, k_cache);
+            got.push_back(rep.hits);
+            got.push_back(rep.misses);
+            got.push_back(rep.bytes_from_slow_tier);
+        }
+        CacheStats cs = store.cache_stats(0, 0);
+        got.push_back(cs.hits);
+        got.push_back(cs.misses);
+        got.push_back(cs.requests);
+        got.push_back(cs.occupancy_tokens);
+        std::vector<uint64_t> want(3 * n_req + 4), cache_ids(4096);
+        size_t n_cached = 0;
+        CHECK(ref_fetch_replay(s, d, k.data.data(), v.data.data(), n_init, n_local, block, cap, lfu ? 1 : 0, n_req,
+                               offs.data(), ids.data(), app.data(), fresh.data(), k_cache, want.data(),
+                               cache_ids.data(), cache_ids.size(), &n_cached) == 0);
+        CHECK(got == want);
+        std::vector<uint64_t> mine;
+        for (const auto& kv : store.state(0, 0).cache) mine.push_back(kv.first);
+        CHECK(mine.size() == n_cached && std::equal(mine.begin(), mine.end(), cache_ids.begin()));
+        CHECK(cs.hit_rate == (cs.requests ? static_cast<double>(cs.hits) / cs.requests : 0.0));
+    }
+}
+
 int main() {
     struct { const char* name; void (*fn)(); } suites[] = {
         {"pq", pq_cases}, {"topk", topk_cases}, {"kmeans", kmeans_cases}, {"attention", attention_cases},
-        {"reference_equality", reference_equality}};
+        {"reference_equality", reference_equality}, {"kv_cache", kv_cache_cases}};
     for (auto& s : suites) {
         int before = g_fail;
         try {
