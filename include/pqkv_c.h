@@ -96,6 +96,10 @@ PQKV_API int pqkv_ctx_last_build_profile(pqkv_ctx* ctx, uint64_t cycles[8]);
  * CTA: [0] row-list prologue (incl. pair select), [1] pair select + DSMEM
  * share of [0], [2] gather + softmax, [3] number of CTAs. */
 PQKV_API int pqkv_ctx_set_profiling(pqkv_ctx* ctx, int on);
+/* Test hook: when d_bitmap != NULL, the fused single-launch decodes also
+ * write their selection words (bit r = middle row r selected) to
+ * d_bitmap [n_heads][ceil(s_mid/32)]. */
+PQKV_API int pqkv_ctx_set_selection_dump(pqkv_ctx* ctx, uint32_t* d_bitmap);
 PQKV_API int pqkv_ctx_last_decode_profile(pqkv_ctx* ctx, double out[4]);
 /* Raw per-CTA timestamps of the last attention launch: PQKV_PROF_SLOTS u64 per CTA --
  * clock64 at start / after pair select / after the row list / after the

@@ -48,6 +48,7 @@ _SIGS = {
     "pqkv_ctx_last_build_stats": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
     "pqkv_ctx_last_build_profile": (_i, [_vp, C.POINTER(_u64)]),
     "pqkv_ctx_set_profiling": (_i, [_vp, _i]),
+    "pqkv_ctx_set_selection_dump": (_i, [_vp, _vp]),
     "pqkv_ctx_last_decode_profile": (_i, [_vp, C.POINTER(C.c_double)]),
     "pqkv_ctx_decode_profile_raw": (_i, [_vp, _vp, _sz, C.POINTER(_sz)]),
     "pqkv_device_alloc": (_i, [_vp, _sz, C.POINTER(_vp)]),
@@ -173,6 +174,10 @@ class Context:
         if n.value:
             _check(lib().pqkv_ctx_decode_profile_raw(self.h, arr.ctypes.data, arr.size, C.byref(n)))
         return arr
+
+    def set_selection_dump(self, bitmap):
+        """Test hook: fused decodes write their selection words into bitmap (or None)."""
+        _check(lib().pqkv_ctx_set_selection_dump(self.h, _ptr(bitmap)))
 
     def last_build_profile(self):
         """SM cycles per phase of problem 0 of the last build."""

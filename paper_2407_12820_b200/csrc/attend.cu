@@ -28,6 +28,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "select_common.cuh"
@@ -41,7 +43,7 @@ constexpr int DH = 128;
 constexpr int LPR = 16;            // lanes per K/V row
 constexpr int VPL = DH / 4 / LPR;  // float4 per lane per row (2)
 
-enum { SRC_ROWS = 0, SRC_BITMAP = 1, SRC_TUPLE = 2, SRC_PAIRS = 3 };
+enum { SRC_ROWS = 0, SRC_BITMAP = 1, SRC_TUPLE = 2, SRC_PAIRS = 3, SRC_KEYS = 4 };
 
 struct AtArgs {
     const float* queries;  // [P][G][128]
@@ -66,6 +68,7 @@ struct AtArgs {
     const uint32_t* thist;        // [P][C*C]
     const uint16_t* chist;        // [P][n_tchunks][C*C]
     int n_tchunks, k, region;     // region: bytes of the aliased scratch area
+    int m;                        // SRC_KEYS: subspaces (any m, b with m * 2^b * 8 <= 16 KB)
     long long tchunk_stride;      // chunks per head of chist
     // SRC_ROWS
     const int64_t* rows;
@@ -74,6 +77,7 @@ struct AtArgs {
     float* part;         // [P][n_chunks][G][DH + 2]
     unsigned* arrivals;  // [P] zero on entry; reset by the combining CTA
     float* out;          // [P][G][DH]
+    uint32_t* sel_dump;        // [P][words] selection words of the fused modes (test hook) or null
     unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
 
@@ -237,8 +241,262 @@ __device__ void classify_words(const AtArgs& a, int r0, int r1, const uint32_t* 
     __syncthreads();
 }
 
+// ---- SRC_KEYS: fused exact top-k over per-token ADC scores (generic m, b) ----
+// The CTAs of one head form one thread-block cluster; CTA rank r owns the
+// middle tokens [r*chunk, ...), so rank order is id order.  Every CTA builds
+// the fp64 ADC table (pq.cpp:113-126), computes its tokens' keys
+// f32(((0.0 + T[0][c0]) + T[1][c1]) + ...) (pq.cpp:128-140) into shared
+// memory and histograms them; three radix digit passes (11/11/10 bits) find
+// the k-th largest key K*, each pass merging the cluster's histograms through
+// DSMEM (every CTA sums the same bins, so one cluster barrier per pass; two
+// histogram buffers alternate so a buffer is only cleared after everyone has
+// read it).  Ties at K* go to the lowest ids (topk.cpp:17-22): a cluster-wide
+// prefix of per-CTA equal counts gives each CTA its share.  Output: the
+// CTA's selection words (bit = middle row selected).
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Histogram increment; bin == ~0u is a no-op.
+__device__ __forceinline__ void hist_inc(uint32_t* h, uint32_t bin) {
+    if (bin != 0xffffffffu) atomicAdd(&h[bin], 1u);
+}
+
+__device__ __forceinline__ uint32_t dsmem_ld(const void* local_ptr, unsigned rank) {
+    uint32_t ra, v;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((unsigned)__cvta_generic_to_shared(local_ptr)), "r"(rank));
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra));
+    return v;
+}
+
 template <int G>
+__device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsigned char* region, uint32_t* words,
+                                  uint32_t* hbuf /*[2][NB] + own[NB]*/, uint32_t* pub /*[4]*/, uint32_t* wtot,
+                                  uint32_t* sh, unsigned long long* tp) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = max(0, r1 - r0), C = a.C, m = a.m;
+    uint32_t crank, ncl;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+    uint32_t* keys = reinterpret_cast<uint32_t*>(region);            // [chunk]
+    double* lut = reinterpret_cast<double*>(keys + a.chunk);          // [m][C]
+    for (int e = tid; e < 2 * NB; e += AT_THREADS) hbuf[e] = 0u;      // both buffers
+    build_lut(lut, a.queries + (long long)p * G * DH, a.centroids + (long long)p * m * C * (DH / m), G, DH, m, C);
+    __syncthreads();
+    PQKV_T(0);
+    // ---- keys (pq.cpp:128-140 in j order, one f32 rounding) + local range ----
+    const uint16_t* cd = a.codes + p * a.codes_head_stride + (long long)r0 * m;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    const bool v4 = m == 4 && (reinterpret_cast<uintptr_t>(cd) & 7) == 0;
+    for (int i0 = 0; i0 < n; i0 += 8 * AT_THREADS) {
+        uint2 cv[8];
+        if (v4) {  // eight code rows in flight per thread
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * AT_THREADS + tid;
+                cv[u] = i < n ? *reinterpret_cast<const uint2*>(cd + 4LL * i) : make_uint2(0u, 0u);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * AT_THREADS + tid;
+            if (i >= n) break;
+            double acc = 0.0;
+            if (v4) {
+                acc = __dadd_rn(acc, lut[0 * C + (cv[u].x & 0xffffu)]);
+                acc = __dadd_rn(acc, lut[1 * C + (cv[u].x >> 16)]);
+                acc = __dadd_rn(acc, lut[2 * C + (cv[u].y & 0xffffu)]);
+                acc = __dadd_rn(acc, lut[3 * C + (cv[u].y >> 16)]);
+            } else {
+                for (int j = 0; j < m; ++j) acc = __dadd_rn(acc, lut[j * C + cd[(long long)i * m + j]]);
+            }
+            const uint32_t key = score_key((float)acc);
+            keys[i] = key;
+            kmin = min(kmin, key);
+            kmax = max(kmax, key);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+    }
+    if (lane == 0) wtot[warp] = kmin;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t lo = 0xffffffffu;
+        for (int w = 0; w < AT_WARPS; ++w) lo = min(lo, wtot[w]);
+        pub[1] = lo;
+    }
+    __syncthreads();
+    if (lane == 0) wtot[warp] = kmax;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t hi = 0u;
+        for (int w = 0; w < AT_WARPS; ++w) hi = max(hi, wtot[w]);
+        pub[2] = hi;
+    }
+    __syncthreads();
+    PQKV_T(1);
+    cluster_barrier();  // every CTA's keys and range are published
+    PQKV_T(2);
+    kmin = 0xffffffffu;
+    kmax = 0u;
+    for (unsigned r = 0; r < ncl; ++r) {
+        kmin = min(kmin, dsmem_ld(pub + 1, r));
+        kmax = max(kmax, dsmem_ld(pub + 2, r));
+    }
+    // ---- radix digits over rel = key - kmin: the first spans [kmin, kmax]
+    // (nearby scores share their top bits), later ones refine 11 bits at a time.
+    // Per pass: local histograms -> barrier -> CTA r sums its share of the
+    // bins over the cluster (DSMEM) -> barrier -> every CTA locates the share
+    // holding the k_rem-th largest key and reads that share's merged bins.
+    const uint32_t range = kmax - kmin;
+    const int bits = 32 - __clz(range | 1u);
+    int shift = max(0, bits - 11), width = bits - shift;
+    uint32_t k_rem = (uint32_t)a.k, prefix = 0;
+    uint32_t* own = hbuf + 2 * NB;  // [NB] merged counts of this CTA's share
+    uint32_t neq_local = 0;         // this CTA's keys equal to K* (bin count of the last pass)
+    for (int pass = 0;; ++pass) {
+        const int nb = 1 << width;
+        uint32_t* h = hbuf + (pass & 1) * NB;
+        if (pass >= 2) {  // this buffer was last read before the previous pass's barriers
+            for (int e = tid; e < NB; e += AT_THREADS) h[e] = 0u;
+            __syncthreads();
+        }
+        for (int i0 = 0; i0 < n; i0 += AT_THREADS) {
+            const int i = i0 + tid;
+            uint32_t bin = 0xffffffffu;
+            if (i < n) {
+                const uint32_t rel = keys[i] - kmin;
+                if (pass == 0 || (rel >> (shift + width)) == prefix) bin = (rel >> shift) & (uint32_t)(nb - 1);
+            }
+            hist_inc(h, bin);
+        }
+        __syncthreads();
+        if (pass == 0) PQKV_T(3);
+        cluster_barrier();  // every CTA's histogram of this pass is complete
+        if (pass == 0) PQKV_T(4);
+        const int share = (nb + (int)ncl - 1) / (int)ncl;  // bins per CTA
+        {
+            const int o0 = (int)crank * share, o1 = min(nb, o0 + share);
+            uint32_t tot = 0;
+            for (int bn = o0 + tid; bn < o1; bn += AT_THREADS) {
+                uint32_t v = 0;
+                for (unsigned r = 0; r < ncl; ++r) v += dsmem_ld(h + bn, r);
+                own[bn - o0] = v;
+                tot += v;
+            }
+            tot = warp_sum(tot);
+            if (lane == 0) wtot[warp] = tot;
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t t = 0;
+                for (int w = 0; w < AT_WARPS; ++w) t += wtot[w];
+                pub[3] = t;
+            }
+            __syncthreads();
+        }
+        if (pass == 0) PQKV_T(5);
+        cluster_barrier();  // every share is merged
+        if (pass == 0) PQKV_T(6);
+        if (tid < 32) {  // the share holding the k_rem-th largest key (shares in descending bin order)
+            const unsigned r = ncl - 1 - (unsigned)lane;
+            const uint32_t t = lane < (int)ncl ? dsmem_ld(pub + 3, r) : 0u;
+            uint32_t x = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            const unsigned hit = __ballot_sync(FULL, lane < (int)ncl && x >= k_rem && x - t < k_rem);
+            const int l = __ffs(hit) - 1;
+            if (lane == l) { sh[2] = r; sh[3] = x - t; }
+        }
+        __syncthreads();
+        const unsigned rs = sh[2];
+        const uint32_t above_share = sh[3];
+        // digit inside share rs: thread t owns share bins [hi - per, hi), top down
+        const int o0 = (int)rs * share, cnt_bins = min(nb, o0 + share) - o0;
+        const int nbe = max(cnt_bins, AT_THREADS);
+        const int per = (nbe + AT_THREADS - 1) / AT_THREADS;  // 1..8
+        const int hi = nbe - per * tid;
+        uint32_t cnt[8];
+        uint32_t local = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int bn = hi - per + e;
+            cnt[e] = (e < per && bn >= 0 && bn < cnt_bins) ? dsmem_ld(own + bn, rs) : 0u;
+            local += cnt[e];
+        }
+        const uint32_t kk = k_rem - above_share;
+        const uint32_t above = block_excl_scan<AT_THREADS>(local, wtot, nullptr);
+        if (above < kk && kk <= above + local) {
+            uint32_t acc = above;
+#pragma unroll
+            for (int e = 7; e >= 0; --e) {  // bins from the top
+                if (e >= per) continue;
+                if (kk <= acc + cnt[e]) {
+                    sh[0] = (uint32_t)(o0 + hi - per + e);
+                    sh[1] = above_share + acc;
+                    break;
+                }
+                acc += cnt[e];
+            }
+        }
+        __syncthreads();
+        k_rem -= sh[1];
+        prefix = (prefix << width) | sh[0];
+        if (shift == 0) neq_local = h[sh[0]];  // local keys in the final bin == K*
+        __syncthreads();
+        if (shift == 0) break;
+        width = min(11, shift);
+        shift -= width;
+    }
+    PQKV_T(7);
+    const uint32_t kstar = kmin + prefix;  // the k-th largest key; k_rem of its ties are taken
+    // ---- ties: equal keys of lower ranks come first ----
+    const uint32_t cta_eq = neq_local;
+    if (tid == 0) pub[0] = cta_eq;
+    cluster_barrier();
+    uint32_t eq_before = 0;
+    for (unsigned r = 0; r < crank; ++r) eq_before += dsmem_ld(pub, r);
+    // no remote reads of this CTA's histograms / pub after this point; the
+    // matching wait is at the end of the kernel (no CTA leaves early)
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    const uint32_t take = k_rem > eq_before ? min(cta_eq, k_rem - eq_before) : 0u;
+    // ---- selection words in id order ----
+    const int seg = a.chunk / AT_WARPS;
+    const int s0 = warp * seg, s1 = min(n, s0 + seg);
+    uint32_t weq = 0;
+    for (int i0 = s0; i0 < s1; i0 += 32) {
+        const int i = i0 + lane;
+        weq += __popc(__ballot_sync(FULL, i < s1 && keys[i] == kstar));
+    }
+    if (lane == 0) wtot[warp] = weq;
+    __syncthreads();
+    uint32_t run = 0;
+    for (int v = 0; v < warp; ++v) run += wtot[v];
+    for (int i0 = s0; i0 < s1; i0 += 32) {
+        const int i = i0 + lane;
+        const uint32_t key = i < s1 ? keys[i] : 0u;
+        const bool gt = i < s1 && key > kstar, eq = i < s1 && key == kstar;
+        const unsigned em = __ballot_sync(FULL, eq);
+        const bool sel = gt || (eq && run + __popc(em & lanemask_lt()) < take);
+        const unsigned word = __ballot_sync(FULL, sel);
+        if (lane == 0) words[i0 >> 5] = word;
+        run += __popc(em);
+    }
+    __syncthreads();
+}
+
+// MODE: 0 = the list modes (rows / bitmap / tuple classes, a.src at run
+// time), SRC_PAIRS or SRC_KEYS -- the fused single-launch modes get their own
+// instantiation so their prologues do not perturb the others' code.
+template <int G, int MODE>
 __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtArgs a) {
+    const int src = MODE == 0 ? a.src : MODE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint32_t wtot[AT_WARPS];
     __shared__ int nrows_s;
@@ -262,23 +520,30 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crk));
         a.prof[cta * PQKV_PROF_SLOTS + 16] = smid;
         a.prof[cta * PQKV_PROF_SLOTS + 17] = crk;
-        a.prof[cta * PQKV_PROF_SLOTS + 18] = a.src == SRC_PAIRS && crk == (cta / 8) % 8;
+        a.prof[cta * PQKV_PROF_SLOTS + 18] = (MODE == SRC_PAIRS) && crk == (cta / 8) % 8;
     }
     // ---- 1. this CTA's row list (ascending token ids) ----
     int nrows = 0;
-    if (a.src == SRC_ROWS) {
+    if (src == SRC_ROWS) {
         const int b0 = c * a.chunk, cnt = max(0, min(a.chunk, a.t - b0));
         for (int e = tid; e < cnt; e += AT_THREADS) rows[e] = (int)a.rows[(long long)p * a.t + b0 + e];
         nrows = cnt;
     } else {
-        if (c == 0 && a.src != SRC_PAIRS)  // pair mode: written after the classification
+        if (c == 0 && (MODE != SRC_PAIRS) && (MODE != SRC_KEYS))  // written after the select (shared region)
             for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
         nrows = c == 0 ? a.n_init : 0;
         const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
         const int nw = (max(0, r1 - r0) + 31) / 32;
-        if (a.src == SRC_BITMAP) {
+        if (src == SRC_BITMAP) {
             for (int w = tid; w < nw; w += AT_THREADS) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
-        } else if (a.src == SRC_PAIRS) {
+        } else if ((MODE == SRC_KEYS)) {
+            __shared__ uint32_t pub_s[4], sh_s[4];
+            keys_select_words<G>(a, p, r0, r1, smem_raw, words, eqw /* [2][NB/2] in keys mode */, pub_s, wtot, sh_s,
+                                 a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr);
+            if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 1] = clock64();
+            if (c == 0)
+                for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
+        } else if ((MODE == SRC_PAIRS)) {
             // per-head pair-level top-k: computed by one CTA of each thread-block
             // cluster and shared with the others through DSMEM.  The selecting
             // rank rotates with the cluster index: the scheduler places equal
@@ -357,6 +622,8 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                            words, eqw, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
         }
         __syncthreads();
+        if (a.sel_dump && ((MODE == SRC_PAIRS) || (MODE == SRC_KEYS)))
+            for (int w = tid; w < nw; w += AT_THREADS) a.sel_dump[(long long)p * a.words + r0 / 32 + w] = words[w];
         nrows += expand_words(words, nw, a.n_init + r0, rows, nrows, wtot);
         if (c == a.n_chunks - 1) {
             for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
@@ -513,7 +780,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     if (tid == 0) ticket = atomicAdd(&a.arrivals[p], 1u);
     // pair mode: pairs with the cluster arrive after the DSMEM reads (no CTA
     // of the cluster exits while another may still read its shared memory)
-    if (a.src == SRC_PAIRS) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if ((MODE == SRC_PAIRS) || (MODE == SRC_KEYS)) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     __syncthreads();
     if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
     if (ticket != (unsigned)a.n_chunks - 1) return;
@@ -690,16 +957,19 @@ static size_t attend_smem(AtArgs& a, int G) {
     size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
     size_t region = std::max(rows_cap * 4, merge);
     if (a.src == SRC_PAIRS) region = std::max(region, pair_select_scratch(a.C, a.n_tchunks));
+    if (a.src == SRC_KEYS) region = std::max(region, (size_t)a.chunk * 4 + (size_t)a.m * a.C * 8);
     region = round_up(region, 16);
     a.region = (int)region;
-    size_t tail = (size_t)a.chunk / 32 * 4 * 2 +
+    size_t tail = (size_t)a.chunk / 32 * 4 + (a.src == SRC_KEYS ? (size_t)NB * 12 : (size_t)a.chunk / 32 * 4) +
                   ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
     return round_up(region + tail, 16);
 }
 
-template <int G>
-static void launch_attend_g(const AtArgs& a, dim3 grid, size_t smem, int cl, cudaStream_t st) {
-    PQKV_CUDA(cudaFuncSetAttribute(attend_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int G, int MODE>
+static void launch_attend_gm(const AtArgs& a, dim3 grid, size_t smem, int cl, cudaStream_t st) {
+    auto kern = attend_kernel<G, MODE>;
+    PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (cl > 8) PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(AT_THREADS);
@@ -712,7 +982,20 @@ static void launch_attend_g(const AtArgs& a, dim3 grid, size_t smem, int cl, cud
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    PQKV_CUDA(cudaLaunchKernelEx(&cfg, attend_kernel<G>, a));
+    if (std::getenv("PQKV_DEBUG_CLUSTERS")) {
+        int nc = -1;
+        cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
+        std::fprintf(stderr, "attend_kernel<%d>: grid %u x %u, cluster %d, smem %zu -> max active clusters %d\n", G,
+                     grid.x, grid.y, cl, smem, nc);
+    }
+    PQKV_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
+template <int G>
+static void launch_attend_g(const AtArgs& a, dim3 grid, size_t smem, int cl, cudaStream_t st) {
+    if (a.src == SRC_PAIRS) launch_attend_gm<G, SRC_PAIRS>(a, grid, smem, cl, st);
+    else if (a.src == SRC_KEYS) launch_attend_gm<G, SRC_KEYS>(a, grid, smem, cl, st);
+    else launch_attend_gm<G, 0>(a, grid, smem, cl, st);
 }
 
 static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cudaStream_t st) {
@@ -723,12 +1006,14 @@ static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cuda
         cl = 8;
         a.n_chunks = (int)round_up((size_t)a.n_chunks, (size_t)cl);
     }
+    if (a.src == SRC_KEYS) cl = a.n_chunks;  // one cluster per head (<= 16 CTAs)
     Scratch sc(ctx);
     size_t h_part = sc.plan<float>(P * a.n_chunks * G * (DH + 2));
     sc.commit();
     a.part = sc.get<float>(h_part);
     a.arrivals = arrival_counters(ctx, P, st);
     a.prof = nullptr;
+    a.sel_dump = ctx->sel_dump;
     if (ctx->profiling) {
         if (ctx->d_prof) cudaFree(ctx->d_prof);
         ctx->n_prof = (size_t)a.n_chunks * P;
@@ -785,9 +1070,29 @@ bool decode_pairs_fused(const pqkv_layer& L, size_t G) {
     return decode_fast_path(L, G) && L.m == 2 && L.b <= 6 && L.tuple_hist && L.tuple_chunk_hist;
 }
 
+// SRC_KEYS geometry: one portable cluster of n_chunks <= 8 CTAs per head
+// (16-CTA clusters do not all fit one wave), chunks of 1024-token multiples
+// up to 16K tokens, keys + ADC table in the shared region.
+static bool keys_geometry(const pqkv_layer& L, size_t G, int* chunk, int* n_chunks) {
+    (void)G;
+    const size_t s_mid = L.total - L.n_init - L.n_local;
+    const size_t C = size_t{1} << L.b;
+    if (L.m * C * 8 > 16 * 1024 || s_mid == 0) return false;
+    const size_t nc = std::min<size_t>(8, ceil_div(s_mid, 1024));
+    const size_t ch = round_up(ceil_div(s_mid, nc), 1024);
+    if (ch > 16384) return false;
+    if (chunk) *chunk = (int)ch;
+    if (n_chunks) *n_chunks = (int)ceil_div(s_mid, ch);
+    return true;
+}
+
+bool decode_keys_fused(const pqkv_layer& L, size_t G) {
+    return decode_fast_path(L, G) && keys_geometry(L, G, nullptr, nullptr);
+}
+
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
-                          cudaStream_t st, size_t k_pairs) {
+                          cudaStream_t st, size_t k_pairs, size_t k_keys) {
     bind_device(ctx);
     const size_t s_mid = L.total - L.n_init - L.n_local;
     AtArgs a{};
@@ -795,7 +1100,7 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     a.keys = L.keys;
     a.values = L.values;
     a.kv_head_stride = (long long)L.kv_head_stride;
-    a.src = k_pairs ? SRC_PAIRS : (cls ? SRC_TUPLE : SRC_BITMAP);
+    a.src = k_keys ? SRC_KEYS : (k_pairs ? SRC_PAIRS : (cls ? SRC_TUPLE : SRC_BITMAP));
     a.n_init = (int)L.n_init;
     a.n_local = (int)L.n_local;
     a.total = (int)L.total;
@@ -814,7 +1119,9 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     a.chist = L.tuple_chunk_hist;
     a.n_tchunks = (int)ceil_div(s_mid, PQKV_TUPLE_CHUNK);
     a.tchunk_stride = L.tuple_chunks ? (long long)L.tuple_chunks : a.n_tchunks;
-    a.k = (int)k_pairs;
+    a.k = (int)(k_keys ? k_keys : k_pairs);
+    a.m = (int)L.m;
+    if (k_keys) keys_geometry(L, G, &a.chunk, &a.n_chunks);
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
     a.out = out;
     launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);

@@ -258,6 +258,12 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
             launch_decode_attend(ctx, *L, d_queries, g, nullptr, nullptr, nullptr, d_out, st, k);
             return;
         }
+        if (fast && !d_ids && k > 0 && !(tup && L->b <= 6) && decode_keys_fused(*L, g)) {
+            // one launch: per-head cluster computes ADC keys, radix-selects
+            // through DSMEM, then gathers (generic m, b)
+            launch_decode_attend(ctx, *L, d_queries, g, nullptr, nullptr, nullptr, d_out, st, 0, k);
+            return;
+        }
         if (tup && fast && !d_ids && k > 0) {
             // pair-level select -> attention classifies its own codes
             char* ws = static_cast<char*>(decode_workspace(ctx, round_up(P * C * C, 256) + P * 2 * sizeof(int)));
@@ -361,7 +367,9 @@ int pqkv_decode_launches(const pqkv_layer* L, size_t g, int with_ids) {
     if (!L) return 0;
     bool fast = L->d_h == 128 && (g == 1 || g == 2 || g == 4) && L->kv_head_stride % 4 == 0;
     const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist, L->total - L->n_init - L->n_local);
-    if (tup && fast && !with_ids) return L->b <= 6 ? 1 : 2;  // [pair select +] attention
+    if (tup && fast && !with_ids && L->b <= 6) return 1;       // pair select fused into the attention
+    if (fast && !with_ids && decode_keys_fused(*L, g)) return 1;  // key select fused into the attention
+    if (tup && fast && !with_ids) return 2;                     // pair select + attention
     int n = tup ? 2 /*pair select + bitmap*/ : 1 /*cluster select*/;
     n += with_ids ? 1 : 0 /*sort*/;
     n += fast ? 1 /*attend with fused combine*/ : 3 /*rows + scores + softmax*/;

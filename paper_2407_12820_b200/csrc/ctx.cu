@@ -171,6 +171,13 @@ int pqkv_stream_sync(pqkv_ctx* ctx, void* stream) {
     });
 }
 
+int pqkv_ctx_set_selection_dump(pqkv_ctx* ctx, uint32_t* d_bitmap) {
+    return guard([&] {
+        if (!ctx) fail(PQKV_EINVAL, "NULL context");
+        ctx->sel_dump = d_bitmap;
+    });
+}
+
 int pqkv_ctx_set_profiling(pqkv_ctx* ctx, int on) {
     return guard([&] {
         if (!ctx) fail(PQKV_EINVAL, "NULL context");

@@ -25,6 +25,7 @@ struct pqkv_ctx {
     size_t n_arrivals = 0;
     // Profiling mode: attention-kernel phase timestamps of the last launch.
     int profiling = 0;
+    uint32_t* sel_dump = nullptr;  // test hook: fused decodes write their selection words here
     unsigned long long* d_prof = nullptr;
     size_t n_prof = 0;
     // Decode workspace (selection bitmap / pair classes between kernels).
@@ -158,9 +159,13 @@ bool decode_fast_path(const pqkv_layer& L, size_t g);
 // k_pairs > 0: the per-head pair select runs in the attention prologue
 // (decode_pairs_fused geometry); cls/cut/bitmap are then unused.
 bool decode_pairs_fused(const pqkv_layer& L, size_t g);
+// Generic m, b (m * 2^b * 8 <= 16 KB, s_mid <= 16 chunks): the exact top-k
+// over per-token ADC keys runs in the attention prologue, one thread-block
+// cluster per head (k_keys > 0).
+bool decode_keys_fused(const pqkv_layer& L, size_t g);
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t g,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
-                          cudaStream_t stream, size_t k_pairs = 0);
+                          cudaStream_t stream, size_t k_pairs = 0, size_t k_keys = 0);
 // Pair-level select only (writes cls [rows][C*C], cut [rows][2]).
 void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
                          const uint16_t* chist, size_t rows, size_t n, size_t k, uint8_t* cls, int* cut,
