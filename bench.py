@@ -124,20 +124,11 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max_mhz, "reasons": reasons, "samples": len(rows)}
 
 
-def make_layer_inputs(torch, seed, device):
+def make_layer_inputs(ctx, seed):
     """Gaussian-mixture keys (workload.cpp:39-51 distribution: 8 shared means,
-    spread 0.5), N(0,1) values and base queries, generated on the GPU."""
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    keys = torch.empty((H, S, DH), dtype=torch.float32, device=device)
-    vals = torch.empty((H, S, DH), dtype=torch.float32, device=device)
-    for h in range(H):
-        means = torch.randn((8, DH), generator=g, device=device)
-        comp = torch.randint(0, 8, (S,), generator=g, device=device)
-        keys[h] = means[comp] + 0.5 * torch.randn((S, DH), generator=g, device=device)
-        vals[h] = torch.randn((S, DH), generator=g, device=device)
-    base_q = torch.randn((H, G, DH), generator=g, device=device)
-    return keys, vals, base_q
+    spread 0.5), N(0,1) values and base queries, generated in HBM by the
+    library's counter-based generator (pqkv_gen_workload)."""
+    return ctx.gen_workload(S, DH, h_kv=H, g=G, kind="gaussian", n_components=8, spread=0.5, seed=seed)
 
 
 def run_reference(args, rank, world):
@@ -256,7 +247,7 @@ def main():
     layers, build_s = [], []
     keep0 = None
     for li in range(N_LAYERS):
-        keys, vals, base_q = make_layer_inputs(torch, 1000 * rank + li, dev)
+        keys, vals, base_q = make_layer_inputs(ctx, 1000 * rank + li)
         mids = keys[:, N_INIT:N_INIT + S_MID]  # middle rows, strided view of the cache
         mids = mids.contiguous()
         seeds = [7 + 100 * rank + 10 * li + h for h in range(H)]

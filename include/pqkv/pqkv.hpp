@@ -18,6 +18,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <deque>
+#include <iosfwd>
 #include <map>
 #include <random>
 #include <span>
@@ -54,6 +55,19 @@ struct PQKV_CXX_API TensorF32 {
     /// std::invalid_argument on a size mismatch or a non-finite value.
     void validate() const;
 };
+
+// ---- .pqt files (tensor.cpp:46-150; the code's header: magic "PQKV", u32
+// version, u8 dtype (0 f32, 1 u16), u8 ndim, u64 dims, little-endian payload)
+
+inline constexpr std::uint32_t kTensorFormatVersion = 1;
+PQKV_CXX_API void write_tensor(std::ostream& out, const TensorF32& t);
+PQKV_CXX_API TensorF32 read_tensor(std::istream& in);
+PQKV_CXX_API void write_grid_u16(std::ostream& out, const std::vector<std::size_t>& dims,
+                                 const std::vector<std::uint16_t>& data);
+PQKV_CXX_API void read_grid_u16(std::istream& in, std::vector<std::size_t>& dims,
+                                std::vector<std::uint16_t>& data);
+PQKV_CXX_API void save_tensor(const std::string& path, const TensorF32& t);
+PQKV_CXX_API TensorF32 load_tensor(const std::string& path);
 
 /// mt19937_64 with explicit draw math (bit-identical streams to the reference).
 class PQKV_CXX_API Rng {
@@ -126,6 +140,12 @@ PQKV_CXX_API std::vector<std::size_t> approx_topk(
     std::span<const float> scores, std::size_t k,
     const std::unordered_set<std::size_t>& excluded = {});
 PQKV_CXX_API double codes_memory_ratio(const PqConfig& cfg, std::size_t d_h);
+
+/// Index files (pq.cpp:184-222): the centroid tensor, then the [s, m] u16 code grid.
+PQKV_CXX_API void write_index(std::ostream& out, const PqIndex& index);
+PQKV_CXX_API PqIndex read_index(std::istream& in);
+PQKV_CXX_API void save_index(const std::string& path, const PqIndex& index);
+PQKV_CXX_API PqIndex load_index(const std::string& path);
 
 PQKV_CXX_API std::vector<std::size_t> top_k_desc(
     std::span<const float> scores, std::size_t k,

@@ -286,6 +286,18 @@ PQKV_API int pqkv_block_rank(pqkv_ctx* ctx, const int64_t* d_ids, size_t n_heads
                              uint32_t* d_bitmap, uint32_t* d_counts, int64_t* d_ranked, uint32_t* d_touched,
                              void* stream);
 
+/* Synthetic KV workloads on the device (workload.cpp:16-117 distributions,
+ * counter-based generator: every value is a function of (seed, head, token,
+ * dim), so it is not the reference's sequential mt19937_64 stream).  kind:
+ * PQKV_WORKLOAD_GAUSSIAN (n_components means, spread) or
+ * PQKV_WORKLOAD_POWERLAW (zipf exponent; scaled exact score of rank r =
+ * 8/(r+1)^zipf).  Outputs d_keys/d_values [h_kv][s][d_h], d_queries
+ * [h_kv][g][d_h] f32. */
+enum { PQKV_WORKLOAD_GAUSSIAN = 0, PQKV_WORKLOAD_POWERLAW = 1 };
+PQKV_API int pqkv_gen_workload(pqkv_ctx* ctx, int kind, size_t s, size_t d_h, size_t h_kv, size_t g,
+                               size_t n_components, double spread, double zipf_exponent, uint64_t seed,
+                               float* d_keys, float* d_values, float* d_queries, void* stream);
+
 /* Number of kernels pqkv_decode launches for this geometry (for the bench's
  * gpu_launches accounting). */
 PQKV_API int pqkv_decode_launches(const pqkv_layer* layer, size_t g, int with_ids);

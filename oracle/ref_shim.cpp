@@ -329,4 +329,34 @@ int ref_fetch_replay(size_t s, size_t d_h, const float* keys, const float* value
     });
 }
 
+// .pqt round trips through the reference's own writers / readers
+// (tensor.cpp:110-150, pq.cpp:184-222).
+int ref_save_index(const char* path, const float* centroids, size_t m, size_t C, size_t d_m,
+                   const uint16_t* codes, size_t s) {
+    return guard([&] { save_index(path, make_index(centroids, m, C, d_m, codes, s)); });
+}
+
+int ref_load_index(const char* path, size_t* m, size_t* C, size_t* d_m, size_t* s, float* centroids,
+                   uint16_t* codes, size_t cen_cap, size_t code_cap) {
+    return guard([&] {
+        PqIndex ix = load_index(path);
+        *m = ix.cfg.m;
+        *C = ix.cfg.n_clusters;
+        *d_m = ix.cfg.d_m;
+        *s = ix.size();
+        if (centroids && ix.centroids.data.size() <= cen_cap)
+            std::copy(ix.centroids.data.begin(), ix.centroids.data.end(), centroids);
+        if (codes && ix.codes.size() <= code_cap) std::copy(ix.codes.begin(), ix.codes.end(), codes);
+    });
+}
+
+int ref_save_tensor(const char* path, const float* data, const size_t* dims, size_t ndim) {
+    return guard([&] {
+        std::vector<std::size_t> d(dims, dims + ndim);
+        std::size_t n = 1;
+        for (std::size_t x : d) n *= x;
+        save_tensor(path, TensorF32(d, std::vector<float>(data, data + n)));
+    });
+}
+
 }  // extern "C"

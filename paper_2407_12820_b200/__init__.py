@@ -70,6 +70,8 @@ _SIGS = {
     "pqkv_attend_rows": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp, _sz, _i, _vp, _vp]),
     "pqkv_decode": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp, _vp]),
     "pqkv_decode_step": (_i, [_vp, C.POINTER(pqkv_layer), _sz, _vp, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
+    "pqkv_gen_workload": (_i, [_vp, _i, _sz, _sz, _sz, _sz, _sz, C.c_double, C.c_double, _u64, _vp, _vp, _vp,
+                              _vp]),
     "pqkv_block_rank": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
     "pqkv_decode_attend": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _vp, _vp, _vp]),
     "pqkv_decode_host": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp]),
@@ -332,6 +334,24 @@ class Context:
                                       _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
         layer.total = L.total
         return (out, ids[:, :k]) if want_ids else out
+
+    def gen_workload(self, s: int, d_h: int = 128, h_kv: int = 1, g: int = 1, kind: str = "gaussian",
+                     n_components: int = 8, spread: float = 0.5, zipf: float = 1.0, seed: int = 7, out=None):
+        """Device-generated synthetic workload (pqkv_gen_workload): (keys [h][s][d],
+        values [h][s][d], queries [h][g][d]) f32 on this context's device; `out` may
+        supply (keys, values, queries) tensors (e.g. views of a larger cache)."""
+        import torch
+
+        dev = torch.device("cuda", self.device)
+        if out is None:
+            out = (torch.empty((h_kv, s, d_h), dtype=torch.float32, device=dev),
+                   torch.empty((h_kv, s, d_h), dtype=torch.float32, device=dev),
+                   torch.empty((h_kv, g, d_h), dtype=torch.float32, device=dev))
+        k, v, q = out
+        kd = {"gaussian": 0, "powerlaw": 1}[kind]
+        _check(lib().pqkv_gen_workload(self.h, kd, s, d_h, h_kv, g, n_components, spread, zipf, seed, _ptr(k),
+                                       _ptr(v), _ptr(q), _stream()))
+        return k, v, q
 
     def block_rank(self, ids, n_tokens: int, block_size: int, k_cache: int):
         """Block-cache accounting of a fetch (pqkv_block_rank): ids [P][n] int64 token

@@ -8,6 +8,11 @@
 #include "pqkv/pqkv.hpp"
 
 #include <algorithm>
+#include <bit>
+#include <cstring>
+#include <fstream>
+#include <istream>
+#include <ostream>
 #include <cmath>
 #include <limits>
 #include <map>
@@ -599,6 +604,133 @@ CacheStats KvStore::cache_stats(std::size_t layer, std::size_t kv_head) const {
     cs.occupancy_tokens = st.occupancy_tokens;
     cs.hit_rate = st.requests ? static_cast<double>(st.hits) / st.requests : 0.0;
     return cs;
+}
+
+// ---- .pqt file format (tensor.cpp:46-150, pq.cpp:184-222) -----------------------
+
+static_assert(std::endian::native == std::endian::little, ".pqt I/O assumes a little-endian host");
+
+namespace {
+
+constexpr char kPqtMagic[4] = {'P', 'Q', 'K', 'V'};
+constexpr std::uint8_t kPqtF32 = 0, kPqtU16 = 1;
+
+template <typename T>
+void put(std::ostream& out, const T& v) {
+    out.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+template <typename T>
+T get(std::istream& in) {
+    T v{};
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (!in) throw std::runtime_error("tensor: truncated file");
+    return v;
+}
+
+void put_header(std::ostream& out, std::uint8_t dtype, const std::vector<std::size_t>& dims) {
+    if (dims.empty()) throw std::invalid_argument("tensor: ndim must be >= 1");
+    if (dims.size() > 255) throw std::invalid_argument("tensor: too many dimensions");
+    out.write(kPqtMagic, 4);
+    put(out, kTensorFormatVersion);
+    put(out, dtype);
+    put(out, static_cast<std::uint8_t>(dims.size()));
+    for (std::size_t d : dims) put(out, static_cast<std::uint64_t>(d));
+}
+
+std::vector<std::size_t> get_header(std::istream& in, std::uint8_t want) {
+    char magic[4];
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, kPqtMagic, 4) != 0) throw std::runtime_error("tensor: bad magic");
+    if (get<std::uint32_t>(in) != kTensorFormatVersion) throw std::runtime_error("tensor: unsupported format version");
+    if (get<std::uint8_t>(in) != want) throw std::runtime_error("tensor: unexpected dtype");
+    const auto ndim = get<std::uint8_t>(in);
+    if (ndim == 0) throw std::runtime_error("tensor: ndim must be >= 1");
+    std::vector<std::size_t> dims(ndim);
+    for (auto& d : dims) d = static_cast<std::size_t>(get<std::uint64_t>(in));
+    return dims;
+}
+
+}  // namespace
+
+void write_tensor(std::ostream& out, const TensorF32& t) {
+    t.validate();
+    put_header(out, kPqtF32, t.dims);
+    out.write(reinterpret_cast<const char*>(t.data.data()), static_cast<std::streamsize>(t.data.size() * 4));
+    if (!out) throw std::runtime_error("tensor: write failed");
+}
+
+TensorF32 read_tensor(std::istream& in) {
+    TensorF32 t;
+    t.dims = get_header(in, kPqtF32);
+    t.data.resize(checked_numel(t.dims));
+    in.read(reinterpret_cast<char*>(t.data.data()), static_cast<std::streamsize>(t.data.size() * 4));
+    if (!in) throw std::runtime_error("tensor: truncated payload");
+    t.validate();
+    return t;
+}
+
+void write_grid_u16(std::ostream& out, const std::vector<std::size_t>& dims, const std::vector<std::uint16_t>& data) {
+    if (checked_numel(dims) != data.size()) throw std::invalid_argument("grid: data size does not match product of dims");
+    put_header(out, kPqtU16, dims);
+    out.write(reinterpret_cast<const char*>(data.data()), static_cast<std::streamsize>(data.size() * 2));
+    if (!out) throw std::runtime_error("grid: write failed");
+}
+
+void read_grid_u16(std::istream& in, std::vector<std::size_t>& dims, std::vector<std::uint16_t>& data) {
+    dims = get_header(in, kPqtU16);
+    data.resize(checked_numel(dims));
+    in.read(reinterpret_cast<char*>(data.data()), static_cast<std::streamsize>(data.size() * 2));
+    if (!in) throw std::runtime_error("grid: truncated payload");
+}
+
+void save_tensor(const std::string& path, const TensorF32& t) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("tensor: cannot open " + path);
+    write_tensor(out, t);
+}
+
+TensorF32 load_tensor(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("tensor: cannot open " + path);
+    return read_tensor(in);
+}
+
+void write_index(std::ostream& out, const PqIndex& index) {
+    index.cfg.validate();
+    write_tensor(out, index.centroids);
+    write_grid_u16(out, {index.size(), index.cfg.m}, index.codes);
+}
+
+PqIndex read_index(std::istream& in) {
+    PqIndex index;
+    index.centroids = read_tensor(in);
+    if (index.centroids.ndim() != 3) throw std::runtime_error("pq: centroid tensor must be 3-d");
+    index.cfg.m = index.centroids.dims[0];
+    index.cfg.n_clusters = index.centroids.dims[1];
+    index.cfg.d_m = index.centroids.dims[2];
+    index.cfg.b = 0;
+    for (std::size_t b = 1; b <= 16; ++b)
+        if ((std::size_t{1} << b) == index.cfg.n_clusters) index.cfg.b = b;
+    index.cfg.validate();
+    std::vector<std::size_t> dims;
+    read_grid_u16(in, dims, index.codes);
+    if (dims.size() != 2 || dims[1] != index.cfg.m) throw std::runtime_error("pq: code grid shape mismatch");
+    for (std::uint16_t c : index.codes)
+        if (c >= index.cfg.n_clusters) throw std::runtime_error("pq: code entry out of range");
+    return index;
+}
+
+void save_index(const std::string& path, const PqIndex& index) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("pq: cannot open " + path);
+    write_index(out, index);
+}
+
+PqIndex load_index(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("pq: cannot open " + path);
+    return read_index(in);
 }
 
 }  // namespace pqkv

@@ -317,6 +317,17 @@ int pqkv_decode_step(pqkv_ctx* ctx, pqkv_layer* L, size_t codes_cap, const float
     return pqkv_decode(ctx, L, d_queries, g, k, d_out, d_ids, stream);
 }
 
+int pqkv_gen_workload(pqkv_ctx* ctx, int kind, size_t s, size_t d_h, size_t h_kv, size_t g, size_t n_components,
+                      double spread, double zipf_exponent, uint64_t seed, float* d_keys, float* d_values,
+                      float* d_queries, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!d_keys || !d_values || !d_queries) fail(PQKV_EINVAL, "workload: NULL buffer");
+        launch_workload(ctx, kind, s, d_h, h_kv, g, n_components, spread, zipf_exponent, seed, d_keys, d_values,
+                        d_queries, as_stream(stream));
+    });
+}
+
 int pqkv_block_rank(pqkv_ctx* ctx, const int64_t* d_ids, size_t n_heads, size_t ids_stride, size_t n_ids,
                     size_t n_tokens, size_t block_size, size_t k_cache, uint32_t* d_bitmap, uint32_t* d_counts,
                     int64_t* d_ranked, uint32_t* d_touched, void* stream) {

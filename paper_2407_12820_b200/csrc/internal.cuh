@@ -104,6 +104,9 @@ struct KmeansBatch {
 };
 void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t stream);
 
+void launch_workload(pqkv_ctx* ctx, int kind, size_t s, size_t d, size_t h, size_t g, size_t n_comp,
+                     double spread, double zipf, uint64_t seed, float* keys, float* values, float* queries,
+                     cudaStream_t st);
 void launch_block_rank(pqkv_ctx* ctx, const int64_t* ids, size_t n_heads, size_t ids_stride, size_t n_ids,
                        size_t n_tokens, size_t block_size, size_t k_cache, uint32_t* bitmap, uint32_t* counts,
                        int64_t* ranked, uint32_t* touched, cudaStream_t st);

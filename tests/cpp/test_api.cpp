@@ -21,6 +21,8 @@ int ref_pq_score_gqa(const float*, size_t, size_t, const float*, size_t, size_t,
 int ref_top_k_desc(const float*, size_t, size_t, const uint8_t*, uint64_t*);
 int ref_selective_attention(const float*, const float*, const float*, size_t, size_t, size_t, size_t,
                             const uint64_t*, size_t, float*);
+int ref_save_index(const char*, const float*, size_t, size_t, size_t, const uint16_t*, size_t);
+int ref_load_index(const char*, size_t*, size_t*, size_t*, size_t*, float*, uint16_t*, size_t, size_t);
 int ref_fetch_replay(size_t, size_t, const float*, const float*, size_t, size_t, size_t, size_t, int, size_t,
                      const uint64_t*, const uint64_t*, const uint8_t*, const float*, size_t, uint64_t*, uint64_t*,
                      size_t, size_t*);
@@ -374,6 +376,32 @@ static void reference_equality() {
     for (int j = 0; j < 32; ++j) CHECK(approx(got[j], want[j], 1e-6));
 }
 
+// .pqt index files: ours and the reference's are interchangeable
+static void io_cases() {
+    TensorF32 keys = random_grid(77, 600, 16);
+    PqIndex idx = pq_construct(keys, PqConfig::create(2, 3, 16), 5, 3);
+    const std::string a = "/tmp/pqkv_io_ours.pqt", b = "/tmp/pqkv_io_ref.pqt";
+    save_index(a, idx);
+    size_t m = 0, C = 0, d_m = 0, n = 0;
+    std::vector<float> cen(2 * 8 * 8);
+    std::vector<uint16_t> codes(600 * 2);
+    CHECK(ref_load_index(a.c_str(), &m, &C, &d_m, &n, cen.data(), codes.data(), cen.size(), codes.size()) == 0);
+    CHECK(m == 2 && C == 8 && d_m == 8 && n == 600);
+    CHECK(cen == idx.centroids.data && codes == idx.codes);
+    CHECK(ref_save_index(b.c_str(), idx.centroids.data.data(), 2, 8, 8, idx.codes.data(), 600) == 0);
+    PqIndex back = load_index(b);
+    CHECK(back.codes == idx.codes && back.centroids.data == idx.centroids.data && back.cfg.b == 3 &&
+          back.centroids.dims == idx.centroids.dims);
+    TensorF32 t = random_grid(78, 4, 9);
+    save_tensor(a, t);
+    TensorF32 t2 = load_tensor(a);
+    CHECK(t2.dims == t.dims && t2.data == t.data);
+    CHECK_THROWS_AS(load_index(a), std::runtime_error);  // a 2-d tensor is not a centroid grid
+    CHECK_THROWS_AS(load_tensor("/tmp/pqkv_io_missing.pqt"), std::runtime_error);
+    std::remove(a.c_str());
+    std::remove(b.c_str());
+}
+
 // Block-cache accounting (test_kv_store.cpp cases + a randomized replay
 // against the reference library, appends included).
 static void kv_cache_cases() {
@@ -500,7 +528,7 @@ static void kv_cache_cases() {
 int main() {
     struct { const char* name; void (*fn)(); } suites[] = {
         {"pq", pq_cases}, {"topk", topk_cases}, {"kmeans", kmeans_cases}, {"attention", attention_cases},
-        {"reference_equality", reference_equality}, {"kv_cache", kv_cache_cases}};
+        {"reference_equality", reference_equality}, {"kv_cache", kv_cache_cases}, {"io", io_cases}};
     for (auto& s : suites) {
         int before = g_fail;
         try {
