@@ -194,7 +194,7 @@ def cpu_baseline_leg(layer0, cen, codes, torch):
     if not oracle.has_ref():
         return None, None
     ref = oracle.ref()
-    P = 8
+    P = min(H, max(1, os.cpu_count() or 1))  # one head per host thread
     keys, vals, base_q = layer0
     k = keys[:P].cpu().numpy()
     v = vals[:P].cpu().numpy()
@@ -204,7 +204,7 @@ def cpu_baseline_leg(layer0, cen, codes, torch):
     cores = min(os.cpu_count() or 1, P)
     ts = [ref.bench_decode(k, v, q, c, cd, N_INIT, N_LOCAL, K_SEL, cores)[0] for _ in range(3)]
     dec = {"value": float(np.median(ts)) * 1e6 * (H / P), "unit": "us/layer", "cores": cores,
-           "kind": "reference", "sample": f"{P} of {H} heads of one 128K layer, x{H // P} to a layer, median of 3"}
+           "kind": "reference", "sample": f"{P} of {H} heads of one 128K layer, x{H / P:g} to a layer, median of 3"}
     sb = 32768
     secs, _, _ = ref.bench_build(np.ascontiguousarray(k[:1, N_INIT:N_INIT + sb]), M, B, T_ITERS,
                                  np.array([5], np.uint64), 1)
@@ -387,7 +387,14 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "build": {"layer_s": build_layer_s, "key_vectors_per_s": H * S_MID / build_layer_s,
                   "context_tokens_per_s": S_MID / build_layer_s, "layers": N_LAYERS,
-                  "fp64_rechecked_points": rech, "points": tot},
+                  "fp64_rechecked_points": rech, "points": tot,
+                  # W = (T+2) s C d_h 3 fp64 ops per head for the reference's
+                  # exact algorithm; the certified fp32 filter skips most of them, so the
+                  # reference-equivalent rate exceeds the FP64 pipe (18.11 T op/s measured,
+                  # profiles/r01_fp64_probe.txt)
+                  "ref_equiv_fp64_ops_per_s": (T_ITERS + 2) * S_MID * (1 << B) * DH * 3 * H / build_layer_s,
+                  "fp64_peak_ops_per_s": 18.11e12,
+                  "key_bytes_per_s": H * S_MID * DH * 4 / build_layer_s},
     }
     clk.stop()
     line["clocks"] = clk.summary()
