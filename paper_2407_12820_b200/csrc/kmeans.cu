@@ -1061,8 +1061,12 @@ __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
     return b;
 }
 
+// Two CTAs per SM for D <= 64: the seeding, update and assign loops are
+// latency-bound row gathers, so warps in flight matter more than registers
+// (D = 128 rows would spill).
+constexpr int km_v2_occ(int dim) { return dim >= 128 ? 1 : 2; }
 template <int D>
-__global__ void __launch_bounds__(KM_THREADS, 1) kmeans_cluster_kernel(KmArgs a, uint32_t* members_g) {
+__global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kernel(KmArgs a, uint32_t* members_g) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int R = (int)cl.num_blocks();
@@ -1681,7 +1685,7 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
                     std::getenv("PQKV_KMEANS_V1") == nullptr;
     int R = 1;
     if (v2) {
-        R = (int)std::max<size_t>(1, (size_t)ctx->sm_count / Q);
+        R = (int)std::max<size_t>(1, (size_t)ctx->sm_count * km_v2_occ(D) / Q);
         R = std::min(R, 8);
         R = (int)std::min<size_t>((size_t)R, std::max<size_t>(1, ceil_div(n, 4096)));
         while (R & (R - 1)) --R;  // power of two

@@ -143,3 +143,18 @@ def test_build_errors(ctx):
     pts = torch.zeros((1, 4, 2), device="cuda")
     with pytest.raises(ValueError):
         ctx.kmeans_fit(pts, 0, 5, [1])
+
+
+def test_pq_construct_many_heads_cluster_of_four(ctx, orc):
+    """The bench geometry's cluster split: 32 heads x 2 subspaces at 2 CTAs/SM
+    -> 4-CTA clusters per problem; sampled heads vs the oracle."""
+    import torch
+
+    P, s = 32, 16384
+    keys, _, _ = orc.gen_workload(s, 128, P, 1, oracle.GAUSSIAN, seed=31)
+    cen, codes = ctx.pq_build(torch.from_numpy(keys).cuda(), 2, 6, 6, [100 + p for p in range(P)])
+    cen, codes = cen.cpu().numpy(), codes.cpu().numpy().view(np.uint16)
+    for p in (0, 13, 31):
+        wc, wcd = orc.pq_construct(keys[p], 2, 6, 6, 100 + p)
+        assert np.array_equal(codes[p], wcd), f"head {p}: codes"
+        assert np.array_equal(cen[p], wc), f"head {p}: centroids"
