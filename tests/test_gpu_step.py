@@ -16,9 +16,9 @@ def _rel(got, want):
     return np.abs(got - want).max() / max(1.0, np.abs(want).max())
 
 
-@pytest.mark.parametrize("g,kind,tables", [(1, oracle.GAUSSIAN, True), (4, oracle.POWERLAW, True),
-                                           (2, oracle.GAUSSIAN, False)])
-def test_decode_step_matches_e2e_loop(ctx, orc, g, kind, tables):
+@pytest.mark.parametrize("g,kind,tables,m,b", [(1, oracle.GAUSSIAN, True, 2, 6), (4, oracle.POWERLAW, True, 2, 6),
+                                               (2, oracle.GAUSSIAN, False, 2, 6), (4, oracle.GAUSSIAN, False, 4, 8)])
+def test_decode_step_matches_e2e_loop(ctx, orc, g, kind, tables, m, b):
     import torch
 
     import paper_2407_12820_b200 as pq
@@ -34,12 +34,12 @@ def test_decode_step_matches_e2e_loop(ctx, orc, g, kind, tables):
     kh[:, :S0], vh[:, :S0] = keys, vals
     dk, dv = torch.from_numpy(kh).cuda(), torch.from_numpy(vh).cuda()
     cap = s_mid0 + steps
-    cen, codes0 = ctx.pq_build(dk[:, n_init:n_init + s_mid0].contiguous(), 2, 6, 10, [5, 6])
-    codes = torch.zeros((P, cap, 2), dtype=torch.int16, device="cuda")
+    cen, codes0 = ctx.pq_build(dk[:, n_init:n_init + s_mid0].contiguous(), m, b, 10, [5, 6])
+    codes = torch.zeros((P, cap, m), dtype=torch.int16, device="cuda")
     codes[:, :s_mid0] = codes0
-    tabs = ctx.tuple_tables(codes, 6, s=s_mid0) if tables else None
+    tabs = ctx.tuple_tables(codes, b, s=s_mid0) if tables else None
     layer = pq.DecodeLayer(keys=dk, values=dv, centroids=cen, codes=codes, total=S0, n_init=n_init,
-                           n_local=n_local, b=6, tables=tabs)
+                           n_local=n_local, b=b, tables=tabs)
     cen_h = cen.cpu().numpy()
     codes_h = [list(codes0[p].cpu().numpy().view(np.uint16)) for p in range(P)]
     total = S0
@@ -61,7 +61,7 @@ def test_decode_step_matches_e2e_loop(ctx, orc, g, kind, tables):
         assert layer.total == total
         got_codes = codes[:, :total - n_init - n_local].cpu().numpy().view(np.uint16)
         for p in range(P):
-            cd = np.asarray(codes_h[p], np.uint16).reshape(-1, 2)
+            cd = np.asarray(codes_h[p], np.uint16).reshape(-1, m)
             assert np.array_equal(got_codes[p], cd), f"step {step}: appended code differs"
             rows = orc.top_k_desc(orc.pq_score_gqa(q[p], cen_h[p], cd), k)
             if ids is not None:
@@ -71,7 +71,7 @@ def test_decode_step_matches_e2e_loop(ctx, orc, g, kind, tables):
                                                rows + n_init)
                 assert _rel(out[p, r].cpu().numpy(), want) < 1e-3, f"step {step}: attention"
     if tables:  # the incrementally counted tables equal a rebuild over the grown codes
-        th, ch = ctx.tuple_tables(codes, 6, s=total - n_init - n_local)
+        th, ch = ctx.tuple_tables(codes, b, s=total - n_init - n_local)
         assert torch.equal(th, tabs[0]) and torch.equal(ch, tabs[1])
 
 
