@@ -66,7 +66,20 @@ struct KmArgs {
     uint16_t* nearseed;          // [q][n] v2: seed index achieving min_d2 (pruning only)
     float* ubound;               // [q][n] v2 Hamerly upper bound (distance to own centroid)
     float* lbound;               // [q][n] v2 Hamerly lower bound (distance to any other)
+    float* glb;                  // [q][n][KG] v2 group lower bounds (Yinyang) or null
+    uint32_t* lmem;              // [q][n] v2: each CTA's points in assigned-centroid order
 };
+
+// Group lower bounds (Yinyang): after seeding the K centroids are grouped
+// into KG groups (a few Lloyd steps over the centroids; the grouping only
+// affects speed).  Per point: an upper bound on its distance to its own
+// centroid and, per group, a lower bound on its distance to every other
+// centroid of the group, moved by the largest centroid drift of the group
+// after each update (rounded outward).  The assign pass evaluates only the
+// groups whose bound does not exceed the point's upper bound (plus its own
+// centroid's group); the skipped groups' bounds join the certification of the
+// fp32 filter, so the result is still the reference's exact argmin.
+constexpr int KG = 8;
 
 struct Smem {
     double* gbuf;      // KM_THREADS*4 doubles (exact_running_sum replay buffer)
@@ -1049,6 +1062,11 @@ struct V2Smem {
     double* dseed2;      // [K] squared distance of seed j to the newest seed
     float* delta;        // [K] centroid movement of the last update (rounded up)
     float* ncf;          // [K] |cf|^2 in fp32 (expanded-form filter)
+    float* cenfg;        // [K*D] cenf in group order (Yinyang)
+    float* cnormg;       // [K] cnorm in group order
+    int* grp;            // [K] group of centroid c
+    int* gorder;         // [K] centroid at group-order position
+    uint32_t* lrun;      // [K] CTA-local member-list cursors
 };
 
 __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
@@ -1058,6 +1076,8 @@ __host__ __device__ inline size_t v2_smem_bytes(int K, int D) {
     b += (size_t)K * D * 4 + (size_t)K * 4;
     b = (b + 15) / 16 * 16;
     b += (size_t)K * D * 8 + (size_t)K * 8 + (size_t)K * 4 + (size_t)K * 4;
+    b = (b + 15) / 16 * 16;
+    b += (size_t)K * D * 4 + (size_t)K * 4 * 4;  // Yinyang tables
     return b;
 }
 
@@ -1098,8 +1118,21 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
         s.cen64 = reinterpret_cast<double*>(p); p += KD * 8;
         s.dseed2 = reinterpret_cast<double*>(p); p += K * 8;
         s.delta = reinterpret_cast<float*>(p); p += K * 4;
-        s.ncf = reinterpret_cast<float*>(p);
+        s.ncf = reinterpret_cast<float*>(p); p += K * 4;
+        p = smem_raw + (p - smem_raw + 15) / 16 * 16;
+        s.cenfg = reinterpret_cast<float*>(p); p += KD * 4;
+        s.cnormg = reinterpret_cast<float*>(p); p += K * 4;
+        s.grp = reinterpret_cast<int*>(p); p += K * 4;
+        s.gorder = reinterpret_cast<int*>(p); p += K * 4;
+        s.lrun = reinterpret_cast<uint32_t*>(p);
     }
+    const bool yy = a.glb != nullptr;  // group bounds active for this launch
+    __shared__ int g_start[KG + 1];
+    __shared__ float g_delta[KG];
+    bool groups_ready = false;
+    uint32_t* lmem = yy ? a.lmem + (long long)q * n : nullptr;
+    float* glbp = yy ? a.glb + (long long)q * n * KG : nullptr;
+    bool lists_ready = false;  // lmem holds this CTA's points in assigned-centroid order
     uint32_t* asg = a.asg0 + (long long)q * n;
     uint32_t* nxt = a.asg1 + (long long)q * n;
     double* aux0 = a.aux0 + (long long)q * n;
@@ -1147,6 +1180,58 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
             atomicMax(reinterpret_cast<int*>(&sh_cmax), __float_as_int(nrm));
         }
         __syncthreads();
+        if (groups_ready) {  // group-ordered copy for the Yinyang assign
+            for (long long e = tid; e < KD; e += KM_THREADS) {
+                const int pos = (int)(e / D), t = (int)(e % D);
+                s.cenfg[e] = s.cenf[(long long)s.gorder[pos] * D + t];
+            }
+            for (int pos = tid; pos < K; pos += KM_THREADS) s.cnormg[pos] = s.cnorm[s.gorder[pos]];
+            __syncthreads();
+        }
+    };
+    // Centroid groups (Yinyang): KG Lloyd steps over the K centroids from the
+    // first KG seeds (k-means++ spreads them); deterministic, CTA-local.
+    auto form_groups = [&]() {
+        __shared__ float gctr[KG][D];
+        __shared__ int gcnt[KG];
+        for (int e = tid; e < KG * D; e += KM_THREADS) gctr[e / D][e % D] = s.cenf[(e / D) * D + e % D];
+        __syncthreads();
+        for (int it = 0; it < 4; ++it) {
+            for (int c = tid; c < K; c += KM_THREADS) {
+                float best = FLT_MAX;
+                int bg = 0;
+                for (int g = 0; g < KG; ++g) {
+                    float acc = 0.f;
+                    for (int t = 0; t < D; ++t) {
+                        const float d = s.cenf[c * D + t] - gctr[g][t];
+                        acc = fmaf(d, d, acc);
+                    }
+                    if (acc < best) { best = acc; bg = g; }
+                }
+                s.grp[c] = bg;
+            }
+            __syncthreads();
+            if (it == 3) break;
+            for (int e = tid; e < KG * D; e += KM_THREADS) {
+                const int g = e / D, t = e % D;
+                float sum = 0.f;
+                int cnt = 0;
+                for (int c = 0; c < K; ++c)
+                    if (s.grp[c] == g) { sum += s.cenf[c * D + t]; ++cnt; }
+                if (cnt) gctr[g][t] = sum / (float)cnt;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {  // stable group order
+            for (int g = 0; g < KG; ++g) gcnt[g] = 0;
+            for (int c = 0; c < K; ++c) ++gcnt[s.grp[c]];
+            int run = 0;
+            for (int g = 0; g < KG; ++g) { g_start[g] = run; run += gcnt[g]; gcnt[g] = g_start[g]; }
+            g_start[KG] = run;
+            for (int c = 0; c < K; ++c) s.gorder[gcnt[s.grp[c]]++] = c;
+        }
+        __syncthreads();
+        groups_ready = true;
     };
     auto merge_counts = [&]() {
         cl.sync();
@@ -1170,6 +1255,102 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
         const float cmax = sh_cmax;
         const float dm1 = sh_dmax1, dm2 = sh_dmax2;
         const int dma = sh_dargmax;
+        if (groups_ready) {
+            // ---- Yinyang pass: points in assigned-centroid order (coherent warps) ----
+            for (int j = lo + tid; j < hi; j += KM_THREADS) {
+                const int i = lists_ready ? (int)lmem[j] : j;
+                float* gl = glbp + (long long)i * KG;
+                float lg[KG];
+                float u = INFINITY;
+                int ga = -1;
+                if (bounds_valid) {
+                    const uint32_t ap = prev[i];
+                    ga = s.grp[ap];
+                    u = __fadd_ru(ubd[i], s.delta[ap]);
+                    const float4 l0 = reinterpret_cast<const float4*>(gl)[0], l1 = reinterpret_cast<const float4*>(gl)[1];
+                    const float lv[KG] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+                    float lmin = INFINITY;
+#pragma unroll
+                    for (int g = 0; g < KG; ++g) {
+                        lg[g] = __fsub_rd(lv[g], g_delta[g]);
+                        lmin = fminf(lmin, lg[g]);
+                    }
+                    if (__fmul_ru(u, 1.000001f) < lmin) {  // keeps its centroid (Hamerly over groups)
+                        out[i] = ap;
+                        atomicAdd(&s.cnt_loc[ap], 1u);
+                        ubd[i] = u;
+                        reinterpret_cast<float4*>(gl)[0] = make_float4(lg[0], lg[1], lg[2], lg[3]);
+                        reinterpret_cast<float4*>(gl)[1] = make_float4(lg[4], lg[5], lg[6], lg[7]);
+                        atomicAdd(&sh_int[4], 1);
+                        continue;
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < KG; ++g) lg[g] = -INFINITY;
+                }
+                float x[D];
+                load_point<D>(point_ptr(a, q, i), x, a.vec4);
+                const float uu = __fmul_ru(u, 1.000001f);
+                float b1 = FLT_MAX, e1 = 0.f;
+                int i1 = -1;
+                float low1[KG], low2[KG];
+                int idx1[KG];
+                unsigned evald = 0;
+#pragma unroll
+                for (int g = 0; g < KG; ++g) {
+                    low1[g] = INFINITY;
+                    low2[g] = INFINITY;
+                    idx1[g] = -1;
+                    if (!(lg[g] <= uu) && g != ga) continue;  // every centroid of g is provably farther
+                    evald |= 1u << g;
+                    for (int pos = g_start[g]; pos < g_start[g + 1]; ++pos) {
+                        const float v = dist_f<D>(x, s.cenfg + (long long)pos * D);
+                        const float e = err_bound(v, s.cnormg[pos], D);
+                        const int c = s.gorder[pos];
+                        if (v < b1) { b1 = v; e1 = e; i1 = c; }
+                        const float lo_v = v - e;
+                        if (lo_v < low1[g]) { low2[g] = low1[g]; low1[g] = lo_v; idx1[g] = c; }
+                        else if (lo_v < low2[g]) low2[g] = lo_v;
+                    }
+                }
+                // certified iff every other centroid's lower bound exceeds the
+                // best's upper bound (evaluated ones: their own error bounds;
+                // skipped groups: the group bound)
+                bool ok = i1 >= 0 && b1 < 1e37f;
+                const float hi1 = b1 + e1;
+#pragma unroll
+                for (int g = 0; g < KG; ++g) {
+                    if ((evald >> g) & 1u) {
+                        const float ex = idx1[g] == i1 ? low2[g] : low1[g];
+                        ok = ok && ex > hi1;
+                    } else {
+                        ok = ok && __fmul_rd(__fmul_rd(lg[g], lg[g]), 0.999999f) > hi1;
+                    }
+                }
+                if (ok) {
+                    out[i] = (uint32_t)i1;
+                    atomicAdd(&s.cnt_loc[i1], 1u);
+                    ubd[i] = __fsqrt_ru(__fmul_ru(__fadd_ru(b1, e1), 1.000001f));
+                    float nl[KG];
+#pragma unroll
+                    for (int g = 0; g < KG; ++g) {
+                        if ((evald >> g) & 1u) {
+                            const float ex = idx1[g] == i1 ? low2[g] : low1[g];
+                            nl[g] = ex >= INFINITY ? INFINITY : __fsqrt_rd(fmaxf(0.f, __fmul_rd(ex, 0.999999f)));
+                        } else {
+                            nl[g] = lg[g];
+                        }
+                    }
+                    reinterpret_cast<float4*>(gl)[0] = make_float4(nl[0], nl[1], nl[2], nl[3]);
+                    reinterpret_cast<float4*>(gl)[1] = make_float4(nl[4], nl[5], nl[6], nl[7]);
+                } else {
+                    queue[lo + atomicAdd(&sh_int[0], 1)] = (uint32_t)i;
+                    ubd[i] = INFINITY;  // re-scan next pass
+                    reinterpret_cast<float4*>(gl)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    reinterpret_cast<float4*>(gl)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        } else
         for (int i = lo + tid; i < hi; i += KM_THREADS) {
             if (bounds_valid) {
                 const uint32_t ap = prev[i];
@@ -1276,8 +1457,13 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
     auto update_means = [&](const uint32_t* as) {
         // offsets: members of cluster c in point order, slices in rank order
         if (tid == 0) {
-            uint32_t run = 0;
-            for (int c = 0; c < K; ++c) { s.moff[c] = run; run += s.cnt_all[c]; }
+            uint32_t run = 0, lrun = (uint32_t)lo;
+            for (int c = 0; c < K; ++c) {
+                s.moff[c] = run;
+                run += s.cnt_all[c];
+                s.lrun[c] = lrun;  // this CTA's own list (Yinyang pass order)
+                lrun += s.cnt_loc[c];
+            }
         }
         __syncthreads();
         for (int c = tid; c < K; c += KM_THREADS) {
@@ -1299,12 +1485,14 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
                 uint32_t before = 0;
                 for (int w = 0; w < warp; ++w) before += s.wcnt[w * K + c];
                 mem[s.run[c] + before + wr] = (uint32_t)i;
+                if (yy) lmem[s.lrun[c] + before + wr] = (uint32_t)i;
             }
             __syncthreads();
             for (int cc = tid; cc < K; cc += KM_THREADS) {
                 uint32_t tot = 0;
                 for (int w = 0; w < KM_WARPS; ++w) { tot += s.wcnt[w * K + cc]; s.wcnt[w * K + cc] = 0; }
                 s.run[cc] += tot;
+                s.lrun[cc] += tot;
             }
             __syncthreads();
         }
@@ -1421,6 +1609,12 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
             }
             if (lane == 0) { sh_dmax1 = m1; sh_dmax2 = m2; sh_dargmax = i1; }
         }
+        if (groups_ready && tid < KG) {  // largest drift per group (already rounded up)
+            float mx = 0.f;
+            for (int pos = g_start[tid]; pos < g_start[tid + 1]; ++pos) mx = fmaxf(mx, s.delta[s.gorder[pos]]);
+            g_delta[tid] = mx;
+        }
+        if (yy) lists_ready = true;
         for (long long e = tid; e < KD; e += KM_THREADS) s.cen64[e] = gcen[e];
         __syncthreads();
     };
@@ -1562,6 +1756,10 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
     // =====================================================================
     // 2. Lloyd iterations (kmeans.cpp:174-183)
     // =====================================================================
+    if (yy) {
+        form_groups();
+        refresh_f32();
+    }
     assign_pass(asg, nullptr);
     bounds_valid = true;
     tick(2);
@@ -1627,6 +1825,12 @@ void launch_cluster_v2(const KmArgs& a, uint32_t* members, int problems, int R, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (std::getenv("PQKV_DEBUG_CLUSTERS")) {
+        int nc = -1;
+        cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
+        std::fprintf(stderr, "kmeans_cluster_kernel<%d>: %d problems x cluster %d, smem %zu -> max active clusters %d\n",
+                     D, problems, R, smem, nc);
+    }
     PQKV_CUDA(cudaLaunchKernelEx(&cfg, kern, a, members));
     PQKV_LAUNCHED("kmeans_cluster_kernel");
 }
@@ -1685,7 +1889,9 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
                     std::getenv("PQKV_KMEANS_V1") == nullptr;
     int R = 1;
     if (v2) {
-        R = (int)std::max<size_t>(1, (size_t)ctx->sm_count * km_v2_occ(D) / Q);
+        // CTAs per SM: two for D <= 64 when both fit in shared memory
+        const int occ = km_v2_occ(D) == 2 && 2 * (v2_smem_bytes((int)K, D) + 2048) <= 227 * 1024 ? 2 : 1;
+        R = (int)std::max<size_t>(1, (size_t)ctx->sm_count * occ / Q);
         R = std::min(R, 8);
         R = (int)std::min<size_t>((size_t)R, std::max<size_t>(1, ceil_div(n, 4096)));
         while (R & (R - 1)) --R;  // power of two
@@ -1695,6 +1901,9 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     size_t h_mem = sc.plan<uint32_t>(v2 ? Q * n : 1);
     size_t h_near = sc.plan<uint16_t>(v2 ? Q * n : 1);
     size_t h_ub = sc.plan<float>(v2 ? Q * n : 1), h_lb = sc.plan<float>(v2 ? Q * n : 1);
+    // group bounds (Yinyang) when there are enough centroids to group
+    const bool yy = v2 && K >= 4 * (size_t)KG && std::getenv("PQKV_KMEANS_NOGROUPS") == nullptr;
+    size_t h_glb = sc.plan<float>(yy ? Q * n * KG : 4), h_lmem = sc.plan<uint32_t>(yy ? Q * n : 1);
     size_t h_draws = sc.plan<unsigned long long>(Q * K);
     size_t h_a0 = sc.plan<uint32_t>(Q * n), h_a1 = sc.plan<uint32_t>(Q * n);
     size_t h_x0 = sc.plan<double>(Q * n), h_x1 = sc.plan<double>(Q * n);
@@ -1746,6 +1955,8 @@ void launch_kmeans(pqkv_ctx* ctx, const KmeansBatch& b, cudaStream_t st) {
     a.nearseed = sc.get<uint16_t>(h_near);
     a.ubound = sc.get<float>(h_ub);
     a.lbound = sc.get<float>(h_lb);
+    a.glb = yy ? sc.get<float>(h_glb) : nullptr;
+    a.lmem = yy ? sc.get<uint32_t>(h_lmem) : nullptr;
     a.counts_smem = counts_smem;
     a.sums_smem = sums_smem;
     a.cen64_smem = cen64_smem;

@@ -27,7 +27,14 @@ torch.cuda.synchronize()
 t0 = time.perf_counter()
 cen, codes = ctx.pq_build(keys, 2, 6, 10, list(range(P)))
 torch.cuda.synchronize()
-print(f"build P={P} s={S} exact={exact}: {time.perf_counter() - t0:.3f} s, rechecked/total={ctx.last_build_stats()}")
+first = time.perf_counter() - t0
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+cen, codes = ctx.pq_build(keys, 2, 6, 10, list(range(P)))
+e1.record()
+torch.cuda.synchronize()
+print(f"build P={P} s={S} exact={exact}: first {first:.3f} s, warm {e0.elapsed_time(e1) / 1e3:.4f} s (events), "
+      f"rechecked/total={ctx.last_build_stats()}")
 prof = ctx.last_build_profile()
 print("hamerly skipped point-visits:", prof.pop("skipped_points"), "k-means++ triangle-skipped:",
       prof.pop("seed_skipped_points"))
