@@ -1734,7 +1734,14 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
                 }
                 const double old = md;
                 if (acc < 1e37f && (double)(acc - err_bound(acc, cn, D)) > old) continue;
-                const double d = dist2_g(xp, cc, D);
+                // dist2 (kmeans.cpp:14-21) from the row already in registers:
+                // fp64, separate sub / mul / add, ascending t
+                double d = 0.0;
+#pragma unroll
+                for (int t = 0; t < D; ++t) {
+                    const double df = __dsub_rn((double)xr[t], cc[t]);
+                    d = __dadd_rn(d, __dmul_rn(df, df));
+                }
                 if (d < old) {
                     aux0[i] = d;
                     nears[i] = (uint16_t)c;
