@@ -311,14 +311,14 @@ class Context:
                                       keys[0].numel(), _ptr(rows), t, precision, _ptr(out), _stream()))
         return out
 
-    def decode(self, layer: "DecodeLayer", queries, k: int, want_ids: bool = False):
+    def decode(self, layer: "DecodeLayer", queries, k: int, want_ids: bool = False, out=None):
         import torch
 
         P, g, d_h = queries.shape
-        out = torch.empty((P, g, d_h), dtype=torch.float32, device=queries.device)
+        if out is None:
+            out = torch.empty((P, g, d_h), dtype=torch.float32, device=queries.device)
         ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device) if want_ids else None
-        L = layer.struct()
-        _check(lib().pqkv_decode(self.h, C.byref(L), _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
+        _check(lib().pqkv_decode(self.h, layer.ref(), _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
         return (out, ids[:, :k]) if want_ids else out
 
     def decode_step(self, layer: "DecodeLayer", new_keys, new_values, queries, k: int, want_ids: bool = False):
@@ -386,8 +386,7 @@ class Context:
     def decode_host(self, layer: "DecodeLayer", h_queries, h_out, k: int):
         """h_queries / h_out: pinned CPU tensors [P][g][d_h]; synchronous."""
         P, g, d_h = h_queries.shape
-        L = layer.struct()
-        _check(lib().pqkv_decode_host(self.h, C.byref(L), C.c_void_p(h_queries.data_ptr()), g, k,
+        _check(lib().pqkv_decode_host(self.h, layer.ref(), C.c_void_p(h_queries.data_ptr()), g, k,
                                       C.c_void_p(h_out.data_ptr()), _stream()))
 
 
@@ -421,6 +420,18 @@ class DecodeLayer:
             tuple_chunk_hist=self.tables[1].data_ptr() if self.tables is not None else None,
             tuple_chunks=self.tables[1].shape[1] if self.tables is not None else 0,
         )
+
+    def ref(self):
+        """ctypes reference to a cached pqkv_layer (rebuilt when the fields change)."""
+        key = (self.keys.data_ptr(), self.values.data_ptr(), self.centroids.data_ptr(), self.codes.data_ptr(),
+               self.total, self.n_init, self.n_local, self.b,
+               None if self.tables is None else (self.tables[0].data_ptr(), self.tables[1].data_ptr()))
+        cache = self.__dict__.get("_ref_cache")
+        if cache is None or cache[0] != key:
+            L = self.struct()
+            cache = (key, L, C.byref(L))
+            self.__dict__["_ref_cache"] = cache
+        return cache[2]
 
     def launches(self, g: int, with_ids: bool = False) -> int:
         L = self.struct()

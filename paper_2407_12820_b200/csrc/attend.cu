@@ -968,8 +968,25 @@ static size_t attend_smem(AtArgs& a, int G) {
 template <int G, int MODE>
 static void launch_attend_gm(const AtArgs& a, dim3 grid, size_t smem, int cl, cudaStream_t st) {
     auto kern = attend_kernel<G, MODE>;
-    PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (cl > 8) PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    // attributes only grow: set once per (instantiation, device, thread) and
+    // new size instead of on every decode
+    static thread_local int smem_set[64], np_set[64];
+    static thread_local bool init = false;
+    if (!init) {
+        for (int d = 0; d < 64; ++d) { smem_set[d] = -1; np_set[d] = 0; }
+        init = true;
+    }
+    int dev = 0;
+    PQKV_CUDA(cudaGetDevice(&dev));
+    dev &= 63;
+    if ((int)smem > smem_set[dev]) {
+        PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set[dev] = (int)smem;
+    }
+    if (cl > 8 && !np_set[dev]) {
+        PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        np_set[dev] = 1;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(AT_THREADS);
