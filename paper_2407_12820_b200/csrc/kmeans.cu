@@ -456,11 +456,11 @@ __device__ double warp_serial_sum(const double* v, int n, double* prefix) {
 // subnormal, is done serially by one thread; the parallel pass then resumes
 // after it.  No approximation is ever accepted.
 __device__ double exact_running_sum(const double* v, int n, double* pre, double* gbuf,
-                                    long long* iscr, double* dsh) {
+                                    long long* iscr, double* dsh, double S_init = 0.0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int E = 4, GROUP = KM_THREADS * E;
     int* ish = reinterpret_cast<int*>(iscr + 2 * KM_WARPS);
-    double S = 0.0;
+    double S = S_init;
     double nx[E];  // next group's values, prefetched while this group runs
 #pragma unroll
     for (int e = 0; e < E; ++e) nx[e] = tid * E + e < n ? v[tid * E + e] : 0.0;
@@ -565,6 +565,76 @@ __device__ double exact_running_sum(const double* v, int n, double* pre, double*
         }
     }
     return S;
+}
+
+// Speculative part of a cluster-split running sum: the slice v[0..m) will be
+// entered with an exact S that is only known later, but within 1e-9
+// relative of P (the fp64 sum of the earlier slices; the serial sum differs
+// from it by << 1e-9 relative for any realistic n).  When P is safely inside
+// one binade [2^e, 2^(e+1)) the exact S is a multiple of u = ulp(2^e), every
+// step is S + round_u(v_j), and the slice is an integer prefix sum: the
+// inclusive prefix I_j (as a double, exact) goes to pre[j].  Returns false
+// when P is near a binade edge, an element is a rounding tie / out of range,
+// or the slice could leave the binade (the caller then runs the serial
+// exact sum for the slice).  *u_out, *iend_out on success.
+__device__ bool slice_increments(const double* v, int m, double P, double* pre, long long* iscr, double* u_out,
+                                 long long* iend_out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int E = 4, GROUP = KM_THREADS * E;
+    __shared__ int bad_s;
+    const long long pb = __double_as_longlong(P);
+    const int expo = (int)((pb >> 52) & 0x7ff);
+    if (!(P > 0.0) || expo <= 52 || expo >= 2045) return false;  // uniform
+    const double lo_edge = __longlong_as_double((long long)expo << 52);
+    const double top = __longlong_as_double((long long)(expo + 1) << 52);
+    if (!(P * (1.0 - 1e-9) >= lo_edge) || !(P * (1.0 + 1e-9) < top)) return false;
+    const double u = __longlong_as_double((long long)(expo - 52) << 52);
+    const double inv_u = __longlong_as_double((long long)(2098 - expo) << 52);
+    if (tid == 0) bad_s = 0;
+    __syncthreads();
+    long long carry = 0;
+    for (int g0 = 0; g0 < m; g0 += GROUP) {
+        long long d[E], dsum = 0;
+        int bad = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = g0 + tid * E + e;
+            d[e] = 0;
+            if (j < m) {
+                const double qv = v[j] * inv_u;
+                const double fl = floor(qv), fr = qv - fl;
+                if (!(qv < 4503599627370496.0) || fr == 0.5 || !(qv >= 0.0)) bad = 1;
+                else d[e] = (long long)fl + (fr > 0.5 ? 1 : 0);
+            }
+            dsum += d[e];
+        }
+        if (bad) bad_s = 1;
+        long long x = dsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) iscr[warp] = x;
+        __syncthreads();
+        long long run = carry + x - dsum, tile = 0;
+        for (int w = 0; w < KM_WARPS; ++w) {
+            if (w < warp) run += iscr[w];
+            tile += iscr[w];
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = g0 + tid * E + e;
+            run += d[e];
+            if (j < m) pre[j] = (double)run;
+        }
+        carry += tile;
+        __syncthreads();
+    }
+    const bool ok = !bad_s && carry < (1ll << 53) && P * (1.0 + 1e-9) + (double)carry * u < top;
+    *u_out = u;
+    *iend_out = carry;
+    return ok;
 }
 
 // First i in [0, n) with pre[i] >= target (pre non-decreasing; n-1 if none),
@@ -1666,9 +1736,77 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
         for (int c = 1; c < K; ++c) {
             cl.sync();  // every slice's min_d2 is final for this step
             tick(1);
+            // k-means++ running sums (kmeans.cpp:64-65, 70-71), split over the
+            // cluster: rank 0 runs the serial-exact sum over its slice while
+            // every other rank turns its slice into an integer prefix in the
+            // binade its entry value must lie in (slice_increments); the
+            // entries are then chained exactly, slices that cannot be
+            // certified are summed serially from their exact entry.
+            double total;
+            if (R == 1) {
+                total = exact_running_sum(aux0, n, aux1, s.gbuf, s.lscr, s.dscratch);
+                __syncthreads();  // aux1 (prefix) visible to warp 0's search
+            } else {
+                __shared__ double rs_pub[4];  // [0] approx slice sum, [1] u, [2] exit S (rank 0)
+                __shared__ long long rs_iend;
+                __shared__ int rs_ok;
+                {
+                    double part = 0.0;
+                    for (int i = lo + tid; i < hi; i += KM_THREADS) part += aux0[i];
+                    part = warp_sum(part);
+                    if (lane == 0) s.dscratch[warp] = part;
+                    __syncthreads();
+                    if (tid == 0) {
+                        double t = 0.0;
+                        for (int w = 0; w < KM_WARPS; ++w) t += s.dscratch[w];
+                        rs_pub[0] = t;
+                    }
+                }
+                cl.sync();  // approximate slice sums published
+                double P = 0.0;
+                for (int rr = 0; rr < r; ++rr) P += *cl.map_shared_rank(&rs_pub[0], rr);
+                if (r == 0) {
+                    const double ex = exact_running_sum(aux0, hi, aux1, s.gbuf, s.lscr, s.dscratch);
+                    if (tid == 0) rs_pub[2] = ex;
+                } else {
+                    double u;
+                    long long iend;
+                    const bool ok = slice_increments(aux0 + lo, hi - lo, P, aux1 + lo, s.lscr, &u, &iend);
+                    if (tid == 0) { rs_ok = ok ? 1 : 0; rs_pub[1] = u; rs_iend = iend; }
+                }
+                cl.sync();  // rank 0's exit and the speculative slices are ready
+                // chain the exact entries in rank order (identical in every CTA)
+                double S = *cl.map_shared_rank(&rs_pub[2], 0);
+                double my_entry = 0.0;
+                bool my_serial = false;
+                for (int rr = 1; rr < R; ++rr) {
+                    const int okr = *cl.map_shared_rank(&rs_ok, rr);
+                    const double ur = *cl.map_shared_rank(&rs_pub[1], rr);
+                    const long long ir = *cl.map_shared_rank(&rs_iend, rr);
+                    const int lor = min(n, rr * per), hir = min(n, lor + per);
+                    const double lo_edge = __longlong_as_double(__double_as_longlong(ur) + (52ll << 52));
+                    const bool fits = okr && S >= lo_edge && S + (double)ir * ur < 2.0 * lo_edge;
+                    if (rr == r) { my_entry = S; my_serial = !fits; }
+                    if (fits) {
+                        S = S + (double)ir * ur;
+                    } else {  // rare: rank rr sums its slice serially from the exact entry
+                        if (rr == r) {
+                            const double ex = exact_running_sum(aux0 + lor, hir - lor, aux1 + lor, s.gbuf, s.lscr,
+                                                                s.dscratch, S);
+                            if (tid == 0) rs_pub[2] = ex;
+                        }
+                        cl.sync();
+                        S = *cl.map_shared_rank(&rs_pub[2], rr);
+                    }
+                }
+                total = S;
+                if (r > 0 && !my_serial) {  // integer prefix -> exact running sums
+                    const double ur = rs_pub[1];
+                    for (int i = lo + tid; i < hi; i += KM_THREADS) aux1[i] = my_entry + aux1[i] * ur;
+                }
+                cl.sync();  // every slice's running sums are written
+            }
             if (r == 0) {
-                const double total = exact_running_sum(aux0, n, aux1, s.gbuf, s.lscr, s.dscratch);
-                __syncthreads();
                 if (warp == 0) {
                     int chosen;
                     if (total > 0.0) {
