@@ -78,6 +78,7 @@ struct AtArgs {
     unsigned* arrivals;  // [P] zero on entry; reset by the combining CTA
     float* out;          // [P][G][DH]
     uint32_t* sel_dump;        // [P][words] selection words of the fused modes (test hook) or null
+    uint32_t* sel_only;        // SRC_KEYS: write the selection bitmap [P][words] here and stop (split launch)
     unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
 
@@ -541,6 +542,14 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             keys_select_words<G>(a, p, r0, r1, smem_raw, words, eqw /* [2][NB/2] in keys mode */, pub_s, wtot, sh_s,
                                  a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr);
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 1] = clock64();
+            if (a.sel_only) {  // select-only launch: the bitmap-mode attention follows
+                for (int w = tid; w < nw; w += AT_THREADS) {
+                    a.sel_only[(long long)p * a.words + r0 / 32 + w] = words[w];
+                    if (a.sel_dump) a.sel_dump[(long long)p * a.words + r0 / 32 + w] = words[w];
+                }
+                asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+                return;
+            }
             if (c == 0)
                 for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
         } else if ((MODE == SRC_PAIRS)) {
@@ -1138,7 +1147,18 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     a.tchunk_stride = L.tuple_chunks ? (long long)L.tuple_chunks : a.n_tchunks;
     a.k = (int)(k_keys ? k_keys : k_pairs);
     a.m = (int)L.m;
-    if (k_keys) keys_geometry(L, G, &a.chunk, &a.n_chunks);
+    a.sel_only = nullptr;
+    if (k_keys) {
+        keys_geometry(L, G, &a.chunk, &a.n_chunks);
+        // g > 1 (1 CTA/SM per key cluster): select in one launch, gather in a
+        // second bitmap-mode launch with its own (finer) chunking
+        if (G > 1 && bitmap) {
+            a.sel_only = const_cast<uint32_t*>(bitmap);
+            launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);
+            launch_decode_attend(ctx, L, queries, G, bitmap, nullptr, nullptr, out, st, 0, 0);
+            return;
+        }
+    }
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
     a.out = out;
     launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);

@@ -36,9 +36,11 @@ def _run(ctx, orc, cen, codes, keys, vals, qs, b, n_init, n_local, k, tables):
         out = ctx.decode(layer, torch.from_numpy(qs).cuda(), k).cpu().numpy()
     finally:
         ctx.set_selection_dump(None)
-    assert layer.launches(qs.shape[1]) == 1
-    bits = dump.cpu().numpy().view(np.uint32)
+    pair_path = m == 2 and b <= 6 and tables
     g = qs.shape[1]
+    # pair path and g = 1 key path: one launch; g > 1 key path: select + attention
+    assert layer.launches(g) == (1 if pair_path or g == 1 else 2)
+    bits = dump.cpu().numpy().view(np.uint32)
     for p in range(P):
         rows = orc.top_k_desc(orc.pq_score_gqa(qs[p], cen[p], codes[p]), k)
         got = np.flatnonzero(np.unpackbits(bits[p].view(np.uint8), bitorder="little")[:s_mid])
