@@ -264,6 +264,37 @@ __device__ __forceinline__ void hist_inc(uint32_t* h, uint32_t bin) {
     if (bin != 0xffffffffu) atomicAdd(&h[bin], 1u);
 }
 
+__device__ __forceinline__ double dsmem_ld64(const double* local_ptr, unsigned rank) {
+    uint32_t ra;
+    double v;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((unsigned)__cvta_generic_to_shared(local_ptr)), "r"(rank));
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+    return v;
+}
+
+// ADC table entries [e0, e1) (pq.cpp:113-126 per entry; lut_entry_vec for
+// d_m = 32 / 64, the generic sequential chain otherwise).
+__device__ void build_lut_range(double* lut, const float* q, const float* cen, int g, int d_h, int m, int C,
+                                int e0, int e1) {
+    const int d_m = d_h / m;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(cen)) & 15) == 0 &&
+                         (d_h % 4) == 0;
+    for (int e = e0 + (int)threadIdx.x; e < e1; e += blockDim.x) {
+        const int j = e / C;
+        if (aligned && d_m == 64) { lut_entry_vec<64>(lut, q, cen, g, d_h, e, j); continue; }
+        if (aligned && d_m == 32) { lut_entry_vec<32>(lut, q, cen, g, d_h, e, j); continue; }
+        const float* cc = cen + (long long)e * d_m;
+        double t = 0.0;
+        for (int r = 0; r < g; ++r) {
+            const float* qq = q + (long long)r * d_h + j * d_m;
+            double acc = 0.0;
+            for (int u = 0; u < d_m; ++u) acc = __fma_rn((double)__ldg(qq + u), (double)__ldg(cc + u), acc);
+            t = __dadd_rn(t, acc);
+        }
+        lut[e] = t;
+    }
+}
+
 __device__ __forceinline__ uint32_t dsmem_ld(const void* local_ptr, unsigned rank) {
     uint32_t ra, v;
     asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((unsigned)__cvta_generic_to_shared(local_ptr)), "r"(rank));
@@ -283,7 +314,18 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     uint32_t* keys = reinterpret_cast<uint32_t*>(region);            // [chunk]
     double* lut = reinterpret_cast<double*>(keys + a.chunk);          // [m][C]
     for (int e = tid; e < 2 * NB; e += AT_THREADS) hbuf[e] = 0u;      // both buffers
-    build_lut(lut, a.queries + (long long)p * G * DH, a.centroids + (long long)p * m * C * (DH / m), G, DH, m, C);
+    // ADC table split over the cluster: rank r computes its share of the
+    // m*C entries, then copies the others' through DSMEM
+    {
+        const int ME = m * C, share = (ME + (int)ncl - 1) / (int)ncl;
+        const int e0 = min(ME, (int)crank * share), e1 = min(ME, e0 + share);
+        build_lut_range(lut, a.queries + (long long)p * G * DH, a.centroids + (long long)p * m * C * (DH / m), G, DH,
+                        m, C, e0, e1);
+        __syncthreads();
+        cluster_barrier();
+        for (int e = tid; e < ME; e += AT_THREADS)
+            if (e < e0 || e >= e1) lut[e] = dsmem_ld64(lut + e, (unsigned)(e / share));
+    }
     __syncthreads();
     PQKV_T(0);
     // ---- keys (pq.cpp:128-140 in j order, one f32 rounding) + local range ----
