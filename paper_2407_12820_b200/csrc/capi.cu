@@ -368,10 +368,28 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
         }
         float* d_q = dq;
         float* d_o = dq + L->n_heads * g * L->d_h;
+        // page-locked, device-mapped output buffer (cudaHostAlloc / pinned
+        // tensors under UVA): the combining CTAs write the outputs straight
+        // into host memory, so no D2H copy sits between the kernel and the
+        // synchronize
+        static thread_local const float* last_out = nullptr;
+        static thread_local float* last_mapped = nullptr;
+        float* mapped = nullptr;
+        if (h_out == last_out) {
+            mapped = last_mapped;
+        } else {
+            cudaPointerAttributes pa{};
+            if (cudaPointerGetAttributes(&pa, h_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                pa.devicePointer != nullptr)
+                mapped = static_cast<float*>(pa.devicePointer);
+            cudaGetLastError();
+            last_out = h_out;
+            last_mapped = mapped;
+        }
         PQKV_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, st));
-        int rc = pqkv_decode(ctx, L, d_q, g, k, d_o, nullptr, stream);
+        int rc = pqkv_decode(ctx, L, d_q, g, k, mapped ? mapped : d_o, nullptr, stream);
         if (rc != PQKV_OK) fail(rc, pqkv_last_error());
-        PQKV_CUDA(cudaMemcpyAsync(h_out, d_o, qbytes, cudaMemcpyDeviceToHost, st));
+        if (!mapped) PQKV_CUDA(cudaMemcpyAsync(h_out, d_o, qbytes, cudaMemcpyDeviceToHost, st));
         PQKV_CUDA(cudaStreamSynchronize(st));
     });
 }
