@@ -123,8 +123,13 @@ def _ptr(t):
 
 
 def _stream():
+    """The caller's current CUDA stream (torch's raw accessor: ~0.2 us instead of
+    ~3.5 us for torch.cuda.current_stream() on the per-decode path)."""
     import torch
 
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return C.c_void_p(raw(torch.cuda.current_device()))
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
