@@ -214,6 +214,21 @@ __device__ void classify_words(const AtArgs& a, int r0, int r1, const uint32_t* 
         uint32_t run = 0;
         for (int v = 0; v < warp; ++v)
             if ((r0 + v * seg) / PQKV_TUPLE_CHUNK == tc) run += wtot[v];
+        // a CTA that starts inside chunk c* (chunks below PQKV_TUPLE_CHUNK for
+        // few heads) also counts the equal tokens of c* before its range
+        const int a0 = cstar * PQKV_TUPLE_CHUNK;
+        if (r0 > a0 && r0 < a0 + PQKV_TUPLE_CHUNK) {
+            uint32_t pre = 0;
+            for (int i = a0 + tid; i < r0; i += AT_THREADS) {
+                const uint32_t pr = cd_g[i];
+                pre += cls[(pr & 0xffffu) * C + (pr >> 16)] == 2;
+            }
+            pre = warp_sum(pre);
+            __syncthreads();  // wtot reads above are done
+            if (lane == 0) wtot[warp] = pre;
+            __syncthreads();
+            for (int v = 0; v < AT_WARPS; ++v) run += wtot[v];
+        }
         __syncthreads();
         if (boundary)
             for (int wb = w0; wb < w1; wb += 32) {
@@ -996,6 +1011,10 @@ static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
     const size_t target = (size_t)ctx->sm_count * occ;
     const size_t per_head = std::max<size_t>(1, target / std::max<size_t>(P, 1));
     const size_t tcs = std::max<size_t>(1, ceil_div(s_mid, PQKV_TUPLE_CHUNK));
+    if (per_head >= 2 * tcs) {  // few heads: 1/2 or 1/4 code-pair chunks per CTA
+        const size_t sub = per_head >= 4 * tcs ? 4 : 2;
+        return (int)(PQKV_TUPLE_CHUNK / sub);
+    }
     size_t q = std::min<size_t>(8, std::max<size_t>(1, ceil_div(tcs, per_head)));
     return (int)(q * PQKV_TUPLE_CHUNK);
 }

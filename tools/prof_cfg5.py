@@ -1,7 +1,9 @@
-"""cfg5 per-GPU shape (BASELINE.json configs[4] at 8 GPUs): 16 (request, kv
-head) units x 128K context, m=4 b=8 (256 centroids), GQA g=4, top-k 1/10 +
-4 init + 64 local.  Prints build time and decode us/step (CUDA events).
-  python tools/prof_cfg5.py [units] [s]"""
+"""Decode / build timing for a BASELINE config.  Default: cfg5 per-GPU shape
+(configs[4] at 8 GPUs): 16 (request, kv head) units x 128K context, m=4 b=8
+(256 centroids), GQA g=4, top-k 1/10 + 4 init + 64 local.  cfg3 (one
+Llama-3-8B layer): `8 131072 4 2 6 5 tables`.  Prints build time and decode
+us/step (CUDA events).
+  python tools/prof_cfg5.py [units] [s] [g] [m] [b] [ratio] [tables]"""
 import os
 import sys
 import time
@@ -14,8 +16,13 @@ import paper_2407_12820_b200 as pq  # noqa: E402
 
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 131072
-DH, G, M, B, NI, NL = 128, 4, 4, 8, 4, 64
-K = round(S / 10)
+G = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+M = int(sys.argv[4]) if len(sys.argv) > 4 else 4
+B = int(sys.argv[5]) if len(sys.argv) > 5 else 8
+RATIO = int(sys.argv[6]) if len(sys.argv) > 6 else 10
+TABLES = len(sys.argv) > 7 and sys.argv[7] == "tables"
+DH, NI, NL = 128, 4, 64
+K = round(S / RATIO)
 SM = S - NI - NL
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev)
@@ -32,7 +39,9 @@ t0 = time.perf_counter()
 cen, codes = ctx.pq_build(keys[:, NI:NI + SM].contiguous(), M, B, 10, list(range(P)))
 torch.cuda.synchronize()
 print(f"build {P}x{SM} m{M}b{B}: {time.perf_counter() - t0:.3f} s")
-layer = pq.DecodeLayer(keys=keys, values=vals, centroids=cen, codes=codes, total=S, n_init=NI, n_local=NL, b=B)
+tabs = ctx.tuple_tables(codes, B) if TABLES else None
+layer = pq.DecodeLayer(keys=keys, values=vals, centroids=cen, codes=codes, total=S, n_init=NI, n_local=NL, b=B,
+                       tables=tabs)
 for i in range(3):
     ctx.decode(layer, q, K)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
