@@ -1581,13 +1581,26 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
             int emin[DPL];
 #pragma unroll
             for (int e = 0; e < DPL; ++e) { acc[e] = 0.0; aabs[e] = 0.0; emin[e] = 0x7fffffff; }
-            // members mg, mg+4, ... ; 4 member rows per warp step, unrolled x4
+            // members mg, mg+4, ... ; 4 member rows per warp step, unrolled x4;
+            // the next step's member indices are loaded one step ahead
+            uint32_t idn[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t m = u * V2_MG + mg;
+                idn[u] = m < cnt ? mem[base + m] : 0xffffffffu;
+            }
             for (uint32_t m0 = 0; m0 < cnt; m0 += V2_MG * 4) {
                 float xv[4][DPL];
+                uint32_t idc[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const uint32_t m = m0 + u * V2_MG + mg;
-                    const float* xp = m < cnt ? point_ptr(a, q, (int)mem[base + m]) : nullptr;
+                    idc[u] = idn[u];
+                    const uint32_t m = m0 + V2_MG * 4 + u * V2_MG + mg;
+                    idn[u] = m < cnt ? mem[base + m] : 0xffffffffu;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float* xp = idc[u] != 0xffffffffu ? point_ptr(a, q, (int)idc[u]) : nullptr;
 #pragma unroll
                     for (int e = 0; e < DPL; ++e) {
                         const int t = dl + DG * e;
