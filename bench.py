@@ -347,6 +347,33 @@ def main():
         e2e_s = float(t.item())
     e2e_us = e2e_s * 1e6 / (args.steps * world)
 
+    # ---- cfg4: one layer's heads sharded over the ranks + NCCL all-gather ----
+    # (BASELINE configs[3]; the path itself has no exchange, the gathered
+    # outputs are what the next layer's projection needs)
+    from paper_2407_12820_b200 import shard
+
+    hr = shard.partition(H, world, rank)
+    l0 = layers[0][0]
+    th, ch = l0.tables
+    sub = pq.DecodeLayer(keys=l0.keys[hr.start:hr.stop], values=l0.values[hr.start:hr.stop],
+                         centroids=l0.centroids[hr.start:hr.stop], codes=l0.codes[hr.start:hr.stop], total=S,
+                         n_init=N_INIT, n_local=N_LOCAL, b=B, tables=(th[hr.start:hr.stop], ch[hr.start:hr.stop]))
+    qsub = [queries[i][hr.start:hr.stop].contiguous() for i in range(N_LAYERS)]
+    for i in range(3):
+        shard.gather_heads(ctx.decode(sub, qsub[i % N_LAYERS], K_SEL), H)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    hs0, hs1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hs_steps = max(20, min(args.steps, 200))
+    hs0.record(stream)
+    for i in range(hs_steps):
+        full = shard.gather_heads(ctx.decode(sub, qsub[i % N_LAYERS], K_SEL), H)
+    hs1.record(stream)
+    torch.cuda.synchronize()
+    hs_us = shard.max_over_ranks(hs0.elapsed_time(hs1) * 1e3 / hs_steps, dev)
+    assert full.shape[0] == H
+
     # ---- numbers ----
     # The step is ONE launch of attend_kernel (pair select + classification +
     # gather + softmax + combine fused), so the dominant
@@ -385,6 +412,11 @@ def main():
         "e2e": {"value": e2e_us, "unit": "us/layer", "h2d_bytes_per_step": H * G * DH * 4,
                 "d2h_bytes_per_step": H * G * DH * 4},
         "gpu_launches": launches_per_step * args.steps,
+        "head_sharded": {"config": "cfg4: one layer's 32 heads split over the ranks, per-head outputs "
+                                   "all-gathered (NCCL all_gather_into_tensor) every step",
+                         "us_per_layer": hs_us, "heads_per_rank": len(hr), "steps": hs_steps,
+                         "note": "device-timed, max over ranks; the same K/V layer every step (L2-warm rows "
+                                 "possible at high rank counts)"},
         "build": {"layer_s": build_layer_s, "key_vectors_per_s": H * S_MID / build_layer_s,
                   "context_tokens_per_s": S_MID / build_layer_s, "layers": N_LAYERS,
                   "fp64_rechecked_points": rech, "points": tot,
