@@ -341,73 +341,6 @@ __device__ int nearest_filtered_b(const float (&x)[D], const float* __restrict__
     return i1;
 }
 
-// Expanded-form fp32 filter: S_e = fl(fl(|x|^2 + |cf|^2) - 2 fl(x.cf)) with
-// FMA chains -- one FFMA per (point, centroid, dim) instead of a sub and an
-// FMA.  Rigorous bound on |S_e - S64|: the dot and the norms carry
-// gamma_D (|x| + |cf|)^2, the two final roundings u*S_e, and the f32 rounding
-// of the fp64 centroid 2u sqrt(S)|c| + u^2|c|^2; E_exp doubles the sum (which
-// also covers gamma_D vs D*u and S vs S_e) and adds the subnormal slack.
-__device__ __forceinline__ float err_bound_exp(float s, float xn, float cn, int D) {
-    const float u = 5.9604645e-8f;
-    const float su = sqrtf(fmaxf(s, 0.0f));
-    const float xc = xn + cn;
-    return 2.0f * ((D + 4) * u * xc * xc + u * fabsf(s) + 2.0f * u * su * cn + u * u * cn * cn) +
-           D * 7.2e-43f;
-}
-
-template <int D>
-__device__ int nearest_filtered_exp(const float (&x)[D], const float* __restrict__ cenf,
-                                    const float* __restrict__ ncf, const float* __restrict__ cnorm,
-                                    float cnorm_max, int K, float& ub, float& lb) {
-    float nx = 0.f;
-#pragma unroll
-    for (int t = 0; t < D; ++t) nx = fmaf(x[t], x[t], nx);
-    const float xn = sqrtf(nx) * 1.000001f + 1e-30f;
-    float b1 = FLT_MAX, b2 = FLT_MAX;
-    int i1 = 0;
-    int c = 0;
-    for (; c + 4 <= K; c += 4) {
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-        // 128-bit broadcast reads of 4 centroid rows: 4 LDS.128 per 16 FFMA
-        const float4* c0 = reinterpret_cast<const float4*>(cenf + c * D);
-#pragma unroll
-        for (int t4 = 0; t4 < D / 4; ++t4) {
-            const float4 v0 = c0[t4], v1 = c0[D / 4 + t4], v2 = c0[D / 2 + t4], v3 = c0[3 * D / 4 + t4];
-            const float x0 = x[4 * t4], x1 = x[4 * t4 + 1], x2 = x[4 * t4 + 2], x3 = x[4 * t4 + 3];
-            a0 = fmaf(x0, v0.x, a0); a0 = fmaf(x1, v0.y, a0); a0 = fmaf(x2, v0.z, a0); a0 = fmaf(x3, v0.w, a0);
-            a1 = fmaf(x0, v1.x, a1); a1 = fmaf(x1, v1.y, a1); a1 = fmaf(x2, v1.z, a1); a1 = fmaf(x3, v1.w, a1);
-            a2 = fmaf(x0, v2.x, a2); a2 = fmaf(x1, v2.y, a2); a2 = fmaf(x2, v2.z, a2); a2 = fmaf(x3, v2.w, a2);
-            a3 = fmaf(x0, v3.x, a3); a3 = fmaf(x1, v3.y, a3); a3 = fmaf(x2, v3.z, a3); a3 = fmaf(x3, v3.w, a3);
-        }
-        float av[4] = {fmaf(-2.f, a0, nx + ncf[c]), fmaf(-2.f, a1, nx + ncf[c + 1]),
-                       fmaf(-2.f, a2, nx + ncf[c + 2]), fmaf(-2.f, a3, nx + ncf[c + 3])};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            float v = av[e];
-            if (v < b1) { b2 = b1; b1 = v; i1 = c + e; }
-            else if (v < b2) { b2 = v; }
-        }
-    }
-    for (; c < K; ++c) {
-        float dd = 0.f;
-#pragma unroll
-        for (int t = 0; t < D; ++t) dd = fmaf(x[t], cenf[c * D + t], dd);
-        float v = fmaf(-2.f, dd, nx + ncf[c]);
-        if (v < b1) { b2 = b1; b1 = v; i1 = c; }
-        else if (v < b2) { b2 = v; }
-    }
-    if (!(b1 < 1e37f) || !(nx < 1e37f)) return -1;
-    const float e1 = err_bound_exp(b1, xn, cnorm[i1], D);
-    ub = __fsqrt_ru(fmaxf(0.f, __fmul_ru(__fadd_ru(b1, e1), 1.000001f)));
-    if (K == 1) { lb = INFINITY; return 0; }
-    const float u = 5.9604645e-8f;
-    if (!(b2 < 1e37f) || !(b2 > 8.0f * u * u * cnorm_max * cnorm_max)) return -1;
-    const float e2 = err_bound_exp(b2, xn, cnorm_max, D);
-    if (!(b2 - e2 > b1 + e1)) return -1;
-    lb = __fsqrt_rd(fmaxf(0.f, __fmul_rd(__fsub_rd(b2, e2), 0.999999f)));
-    return i1;
-}
-
 // ---- block helpers --------------------------------------------------------
 
 __device__ __forceinline__ void block_sync() { __syncthreads(); }
@@ -1131,7 +1064,7 @@ struct V2Smem {
     double* cen64;       // [K*D]
     double* dseed2;      // [K] squared distance of seed j to the newest seed
     float* delta;        // [K] centroid movement of the last update (rounded up)
-    float* ncf;          // [K] |cf|^2 in fp32 (expanded-form filter)
+    float* ncf;          // [K] |cf|^2 in fp32
     float* cenfg;        // [K*D] cenf in group order (Yinyang)
     float* cnormg;       // [K] cnorm in group order
     int* grp;            // [K] group of centroid c
@@ -1438,9 +1371,9 @@ __global__ void __launch_bounds__(KM_THREADS, km_v2_occ(D)) kmeans_cluster_kerne
             float x[D];
             load_point<D>(point_ptr(a, q, i), x, a.vec4);
             float ub, lb;
-            // direct form: its bound scales with the distance itself, the
-            // expanded form's with (|x| + |c|)^2 (kept for reference: on the
-            // powerlaw keys it re-checks most points)
+            // direct form: its bound scales with the distance itself; the
+            // expanded form's (|x|^2 + |c|^2 - 2 x.c) scales with (|x| + |c|)^2,
+            // which re-checked most points of the powerlaw keys
             int c = nearest_filtered_b<D>(x, s.cenf, s.cnorm, cmax, K, ub, lb);
             if (c >= 0) {
                 out[i] = (uint32_t)c;

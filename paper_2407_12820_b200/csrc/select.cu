@@ -676,7 +676,7 @@ void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
                          const uint16_t* chist, size_t rows, size_t n, size_t k, uint8_t* cls, int* cut,
                          uint32_t* tkey, uint32_t* sel_before, cudaStream_t st) {
     bind_device(ctx);
-    const size_t C = src.C, C2 = C * C, n_chunks = ceil_div(n, PQKV_TUPLE_CHUNK);
+    const size_t C = src.C, n_chunks = ceil_div(n, PQKV_TUPLE_CHUNK);
     TupArgs a{};
     a.queries = src.queries;
     a.g = (int)src.g;
