@@ -372,19 +372,13 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
         // tensors under UVA): the combining CTAs write the outputs straight
         // into host memory, so no D2H copy sits between the kernel and the
         // synchronize
-        static thread_local const float* last_out = nullptr;
-        static thread_local float* last_mapped = nullptr;
         float* mapped = nullptr;
-        if (h_out == last_out) {
-            mapped = last_mapped;
-        } else {
+        {
             cudaPointerAttributes pa{};
             if (cudaPointerGetAttributes(&pa, h_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
                 pa.devicePointer != nullptr)
                 mapped = static_cast<float*>(pa.devicePointer);
             cudaGetLastError();
-            last_out = h_out;
-            last_mapped = mapped;
         }
         PQKV_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, st));
         int rc = pqkv_decode(ctx, L, d_q, g, k, mapped ? mapped : d_o, nullptr, stream);
