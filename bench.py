@@ -182,7 +182,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_leg(layer0, cen, codes, torch):
+def cpu_baseline_leg(layer0, cen, codes, torch, gpu_out=None):
     """The reference (oracle/_ref) on this box's host cores for a bounded sample
     (8 heads of layer 0, same GPU-built index -- bit-identical to the
     reference's), extrapolated x4 to the 32-head layer; plus a 1-head 32K-token
@@ -202,9 +202,17 @@ def cpu_baseline_leg(layer0, cen, codes, torch):
     c = cen[:P].cpu().numpy()
     cd = codes[:P].cpu().numpy().view(np.uint16)
     cores = min(os.cpu_count() or 1, P)
-    ts = [ref.bench_decode(k, v, q, c, cd, N_INIT, N_LOCAL, K_SEL, cores)[0] for _ in range(3)]
+    runs = [ref.bench_decode(k, v, q, c, cd, N_INIT, N_LOCAL, K_SEL, cores) for _ in range(3)]
+    ts = [r[0] for r in runs]
     dec = {"value": float(np.median(ts)) * 1e6 * (H / P), "unit": "us/layer", "cores": cores,
            "kind": "reference", "sample": f"{P} of {H} heads of one 128K layer, x{H / P:g} to a layer, median of 3"}
+    # parity on the benchmark's own inputs: the fused GPU decode of these heads
+    # (same base queries, same index) against the reference library's outputs
+    if gpu_out is not None:
+        want = runs[0][1]
+        got = gpu_out[:P].cpu().numpy()
+        rel = float(np.abs(got - want).max() / max(1.0, float(np.abs(want).max())))
+        dec["parity"] = {"heads": P, "max_rel_err": rel, "tolerance": 1e-3, "ok": rel < 1e-3}
     sb = 32768
     secs, _, _ = ref.bench_build(np.ascontiguousarray(k[:1, N_INIT:N_INIT + sb]), M, B, T_ITERS,
                                  np.array([5], np.uint64), 1)
@@ -431,7 +439,8 @@ def main():
     clk.stop()
     line["clocks"] = clk.summary()
     if rank == 0 and not args.no_cpu_baseline:
-        dec, bld = cpu_baseline_leg(keep0[0], keep0[1], keep0[2], torch)
+        gpu_out = ctx.decode(layers[0][0], layers[0][1], K_SEL)  # layer 0, base queries
+        dec, bld = cpu_baseline_leg(keep0[0], keep0[1], keep0[2], torch, gpu_out)
         line["cpu_baseline"] = dec
         line["cpu_baseline_build"] = bld
     if rank == 0:
