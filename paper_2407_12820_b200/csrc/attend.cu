@@ -78,6 +78,7 @@ struct AtArgs {
     unsigned* arrivals;  // [P] zero on entry; reset by the combining CTA
     float* out;          // [P][G][DH]
     uint32_t* sel_dump;        // [P][words] selection words of the fused modes (test hook) or null
+    int ring_off;              // g > 1: byte offset of the cp.async row ring in dynamic smem
     uint32_t* sel_only;        // SRC_KEYS: write the selection bitmap [P][words] here and stop (split launch)
     unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
@@ -731,8 +732,27 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     constexpr int STEP = AT_WARPS * 2;         // rows per CTA step
     const uint64_t pol = l2_evict_first_policy();
     float4 kc[VPL], vc[VPL], kn[VPL], vn[VPL];
+    // g > 1: a RING-deep cp.async pipeline per half-warp in shared memory
+    // (each lane copies and later reads back only its own 16-byte chunks, so
+    // no barrier is needed); g = 1: two rows in registers
+    constexpr int RING = 4;
+    float4* ring = G > 1 ? reinterpret_cast<float4*>(smem_raw + a.ring_off) + (size_t)slot * RING * 64 : nullptr;
+    auto issue = [&](int rr, int u) {
+        if (rr < nrows) {
+            const long long row = rows[rr];
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                cp_async16_hint(ring + u * 64 + j * LPR + hl, kb + row * (DH / 4) + j * LPR + hl, pol);
+                cp_async16_hint(ring + u * 64 + 32 + j * LPR + hl, vb + row * (DH / 4) + j * LPR + hl, pol);
+            }
+        }
+        cp_async_commit();
+    };
     int ri = slot;
-    if (ri < nrows) {
+    if constexpr (G > 1) {
+#pragma unroll
+        for (int u = 0; u < RING; ++u) issue(slot + u * STEP, u);
+    } else if (ri < nrows) {
         const long long row = rows[ri];
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
@@ -740,14 +760,25 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             vc[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
         }
     }
-    for (; ri < nrows; ri += STEP) {  // half-warp uniform trip count
-        const int rn = ri + STEP;
-        if (rn < nrows) {  // prefetch the next row of this half-warp
-            const long long row = rows[rn];
+    for (int it = 0; ri < nrows; ri += STEP, ++it) {  // half-warp uniform trip count
+        if constexpr (G > 1) {
+            cp_async_wait_group<RING - 1>();  // this half-warp's oldest row has landed
+            const int u = it % RING;
 #pragma unroll
             for (int j = 0; j < VPL; ++j) {
-                kn[j] = ldg_stream(kb + row * (DH / 4) + j * LPR + hl, pol);
-                vn[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
+                kc[j] = ring[u * 64 + j * LPR + hl];
+                vc[j] = ring[u * 64 + 32 + j * LPR + hl];
+            }
+            issue(ri + RING * STEP, u);
+        } else {
+            const int rn = ri + STEP;
+            if (rn < nrows) {  // prefetch the next row of this half-warp
+                const long long row = rows[rn];
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) {
+                    kn[j] = ldg_stream(kb + row * (DH / 4) + j * LPR + hl, pol);
+                    vn[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
+                }
             }
         }
 #pragma unroll
@@ -781,12 +812,15 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
                 acc[r][4 * j + 3] = fmaf(pw, vc[j].w, acc[r][4 * j + 3]);
             }
         }
+        if constexpr (G == 1) {
 #pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-            kc[j] = kn[j];
-            vc[j] = vn[j];
+            for (int j = 0; j < VPL; ++j) {
+                kc[j] = kn[j];
+                vc[j] = vn[j];
+            }
         }
     }
+    if constexpr (G > 1) cp_async_wait_all();
 
     if (a.prof) {
         __syncthreads();
@@ -1032,7 +1066,11 @@ static size_t attend_smem(AtArgs& a, int G) {
     a.region = (int)region;
     size_t tail = (size_t)a.chunk / 32 * 4 + (a.src == SRC_KEYS ? (size_t)NB * 12 : (size_t)a.chunk / 32 * 4) +
                   ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
-    return round_up(region + tail, 16);
+    a.ring_off = (int)round_up(region + tail, 16);
+    // g > 1: 16 half-warps x 4 rows x (K + V) of cp.async ring (not for the
+    // key path, whose g > 1 launch only selects)
+    const bool ring = G > 1 && a.src != SRC_KEYS;
+    return (size_t)a.ring_off + (ring ? (size_t)AT_WARPS * 2 * 4 * 2 * DH * 4 : 0);
 }
 
 template <int G, int MODE>
