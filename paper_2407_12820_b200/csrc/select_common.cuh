@@ -141,7 +141,7 @@ __device__ void find_digit(const uint32_t* hist, int nb, uint32_t k_rem, uint32_
 
 
 // Pair-level exact top-k for one head (m == 2): builds the ADC table, the
-// keys of the code pairs that occur (thist > 0), radix-selects the k-th
+// keys of the code pairs that occur (thist > 0), selects the k-th
 // largest key weighted by the pair histogram thist, classifies every pair
 // (0 below or absent, 1 above, 2 equal) into cls[], and finds the
 // PQKV_TUPLE_CHUNK chunk c* holding the k_rem-th equal token in id order plus
@@ -234,59 +234,109 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
     kmin = sh[6];
     kmax = sh[7];
     PQKV_T(3);
-    // ---- weighted radix select over the present pair keys ----
-    // Digit 0 spans [kmin, kmax] (f32 bit patterns of nearby scores share
-    // their top bits, so fixed top-bit digits would pile into a few bins);
-    // later digits refine the remaining low bits.  Each pass also counts
-    // pairs per bin: once the threshold bin holds a single pair its key is K*
-    // and the remaining passes are skipped.
+    // ---- weighted select over the present pair keys ----
+    // Each pass bins the candidate pairs linearly by score value over the
+    // candidates' [lo, hi] (a monotone map, so bins are ordered like keys;
+    // score-value bins spread the bulk of a score distribution, where the
+    // k-th largest sits, far better than key-bit digits, which split it by
+    // sign and exponent), finds the bin holding the k_rem-th largest weight
+    // and keeps its pairs.  It ends when one pair is left, when all the
+    // candidates share one key, or -- usually after the first pass -- when
+    // at most 32 pairs are left: one warp sorts them and walks their weights.
+    // On exit k_rem is the rank of the threshold among tokens with key K*.
     uint32_t k_rem = (uint32_t)k;
-    const uint32_t range = kmax - kmin;
-    int cur_shift = max(0, (32 - __clz(range | 1u)) - 11);  // digit 0 = top 11 bits of (key - kmin)
-    int width = 11;
-    uint32_t prefix_val = 0;  // (key - kmin) >> (cur_shift + width) of the chosen bins
     uint32_t kstar = 0;
-    for (int pass = 0; pass < 4; ++pass) {
-        const uint32_t nb = 1u << width;
-        const uint32_t mask = nb - 1;
+    uint32_t alive = 0;  // bit u: item u is still a candidate
+#pragma unroll
+    for (int u = 0; u < WMAX; ++u)
+        if (u < per && (it[u] & wmask)) alive |= 1u << u;
+    double lo = (double)key_score(kmin), hi = (double)key_score(kmax);
+    for (int pass = 0;; ++pass) {
+        if (lo == hi) {  // every candidate has the same key
+            kstar = score_key((float)lo);
+            break;
+        }
+        const double scale = (double)NB / (hi - lo);
 #pragma unroll
         for (int u = 0; u < WMAX; ++u) {
             if (u >= per) break;
-            const uint32_t rel = kr[u] - kmin;
-            const uint32_t wt = it[u] & wmask;
-            const bool in = wt && (pass == 0 || (rel >> (cur_shift + width)) == prefix_val);
-            if (in) {
-                const uint32_t b = (rel >> cur_shift) & mask;
-                atomicAdd(&hist[b], wt);
+            if ((alive >> u) & 1u) {
+                const int b = min(NB - 1, (int)(((double)key_score(kr[u]) - lo) * scale));
+                atomicAdd(&hist[b], it[u] & wmask);
                 atomicAdd(&cnt[b], 1u);
             }
         }
         __syncthreads();
-        find_digit<NT>(hist, (int)nb < NT ? NT : (int)nb, k_rem, wsum, sh);
-        const uint32_t b = sh[0];
+        find_digit<NT>(hist, NB, k_rem, wsum, sh);
+        const int bsel = (int)sh[0];
         k_rem -= sh[1];
-        const uint32_t items = cnt[b];
-        __syncthreads();
-        prefix_val = (prefix_val << width) | b;
-        if (items == 1 || cur_shift == 0) {
-            // the bin holds one distinct pair (or one exact key): find it
-            if (tid == 0) sh[5] = 0xffffffffu;
+        const uint32_t items = cnt[bsel];
+        float vmin = INFINITY, vmax = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < WMAX; ++u) {
+            if (u >= per) break;
+            if ((alive >> u) & 1u) {
+                const float f = key_score(kr[u]);
+                const int b = min(NB - 1, (int)(((double)f - lo) * scale));
+                if (b != bsel) alive &= ~(1u << u);
+                else { vmin = fminf(vmin, f); vmax = fmaxf(vmax, f); }
+            }
+        }
+        __syncthreads();  // hist / cnt / sh reads done
+        if (items <= 32) {
+            // one warp sorts the (key, weight) of the survivors, descending
+            unsigned long long* small = reinterpret_cast<unsigned long long*>(hist);
+            if (tid == 0) sh[2] = 0;
             __syncthreads();
 #pragma unroll
             for (int u = 0; u < WMAX; ++u) {
                 if (u >= per) break;
-                const uint32_t rel = kr[u] - kmin;
-                if ((it[u] & wmask) && (rel >> cur_shift) == prefix_val) atomicMin(&sh[5], kr[u]);
+                if ((alive >> u) & 1u) small[atomicAdd(&sh[2], 1u)] = (unsigned long long)kr[u] << 32 | (it[u] & wmask);
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const int n = (int)sh[2];
+                unsigned long long v = lane < n ? small[lane] : 0ull;
+#pragma unroll
+                for (int sz = 2; sz <= 32; sz <<= 1)
+#pragma unroll
+                    for (int st = sz >> 1; st > 0; st >>= 1) {
+                        const unsigned long long o = __shfl_xor_sync(FULL, v, st);
+                        const bool keep_max = ((lane & sz) == 0) == ((lane & st) == 0);
+                        v = keep_max ? (v > o ? v : o) : (v < o ? v : o);
+                    }
+                const uint32_t key = (uint32_t)(v >> 32), wt = (uint32_t)v;
+                uint32_t x = wt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, x, o);
+                    if (lane >= o) x += y;
+                }
+                const unsigned hm = __ballot_sync(FULL, lane < n && x >= k_rem);
+                const uint32_t ks = __shfl_sync(FULL, key, __ffs(hm) - 1);
+                const uint32_t above = warp_sum(lane < n && key > ks ? wt : 0u);
+                if (lane == 0) { sh[5] = ks; sh[6] = above; }
             }
             __syncthreads();
             kstar = sh[5];
+            k_rem -= sh[6];
             break;
         }
-        // next digit: the low cur_shift bits, up to 11 at a time
-        width = min(11, cur_shift);
-        cur_shift -= width;
-        for (int e = tid; e < max(1 << width, NT); e += NT) { hist[e] = 0; cnt[e] = 0; }
+        // more than 32 pairs left: next pass over their [min, max]
+        vmin = warp_min(vmin);
+        vmax = warp_max(vmax);
+        if (lane == 0) { reinterpret_cast<float*>(wsum)[warp] = vmin; reinterpret_cast<float*>(wsum)[32 + warp] = vmax; }
+        for (int e = tid; e < NB; e += NT) { hist[e] = 0; cnt[e] = 0; }
         __syncthreads();
+        float a = INFINITY, z = -INFINITY;
+#pragma unroll
+        for (int w2 = 0; w2 < NT / 32; ++w2) {
+            a = fminf(a, reinterpret_cast<float*>(wsum)[w2]);
+            z = fmaxf(z, reinterpret_cast<float*>(wsum)[32 + w2]);
+        }
+        lo = (double)a;
+        hi = (double)z;
+        __syncthreads();  // wsum reads done before find_digit reuses it
     }
     PQKV_T(4);
     // ---- classification of the present pairs; equal pairs -> eql (= lst) ----
