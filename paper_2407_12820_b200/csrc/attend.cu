@@ -581,6 +581,26 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         a.prof[cta * PQKV_PROF_SLOTS + 17] = crk;
         a.prof[cta * PQKV_PROF_SLOTS + 18] = (MODE == SRC_PAIRS) && crk == (cta / 8) % 8;
     }
+    // ---- 0. programmatic dependent launch ----
+    // Launched with programmatic stream serialization, this grid may start
+    // while the previous kernel on the stream is still draining.  Until
+    // griddepcontrol.wait returns it only warms L2 and the TLBs with
+    // prefetches of what its prologue reads (no loads: the previous kernel
+    // may still be writing them); it then lets the next decode launch early.
+    if (MODE == SRC_PAIRS) {
+        const int C2 = a.C * a.C;
+        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
+        const char* cd = reinterpret_cast<const char*>(a.codes + p * a.codes_head_stride + 2 * (long long)r0);
+        for (int o = tid * 128; o < 4 * (r1 - r0); o += AT_THREADS * 128) prefetch_l2(cd + o);
+        if ((c & 7) == 0) {  // one CTA per cluster: the head's select tables
+            const char* ce = reinterpret_cast<const char*>(a.centroids + (long long)p * 2 * a.C * (DH / 2));
+            for (int o = tid * 128; o < 4 * a.C * DH; o += AT_THREADS * 128) prefetch_l2(ce + o);
+            const char* th = reinterpret_cast<const char*>(a.thist + (long long)p * C2);
+            for (int o = tid * 128; o < 4 * C2; o += AT_THREADS * 128) prefetch_l2(th + o);
+        }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     // ---- 1. this CTA's row list (ascending token ids) ----
     int nrows = 0;
     if (src == SRC_ROWS) {
@@ -1100,13 +1120,17 @@ static void launch_attend_gm(const AtArgs& a, dim3 grid, size_t smem, int cl, cu
     cfg.blockDim = dim3(AT_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = (unsigned)cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch (see the kernel's step 0)
+    static const bool pdl = std::getenv("PQKV_NO_PDL") == nullptr;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     if (std::getenv("PQKV_DEBUG_CLUSTERS")) {
         int nc = -1;
         cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
