@@ -924,11 +924,22 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         if (lane == 0) sc[G * nc + r] = L;
     }
     __syncthreads();
+    // the partial rows are L2-resident but the merge sits on the kernel's
+    // critical tail: 16 loads in flight per thread (same cc order)
     for (int e = tid; e < G * DH; e += AT_THREADS) {
         const int r = e / DH, d = e % DH;
+        const float* pr = pb + (long long)r * (DH + 2) + 2 + d;
+        const long long cstr = (long long)G * (DH + 2);
         float O = 0.f;
-#pragma unroll 4
-        for (int cc = 0; cc < nc; ++cc) O = fmaf(__ldcg(pb + ((long long)cc * G + r) * (DH + 2) + 2 + d), sc[r * nc + cc], O);
+        int cc = 0;
+        for (; cc + 16 <= nc; cc += 16) {
+            float v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = __ldcg(pr + (cc + u) * cstr);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) O = fmaf(v[u], sc[r * nc + cc + u], O);
+        }
+        for (; cc < nc; ++cc) O = fmaf(__ldcg(pr + cc * cstr), sc[r * nc + cc], O);
         a.out[((long long)p * G + r) * DH + d] = O / sc[G * nc + r];
     }
     if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
