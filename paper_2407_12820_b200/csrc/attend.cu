@@ -79,6 +79,7 @@ struct AtArgs {
     float* out;          // [P][G][DH]
     uint32_t* sel_dump;        // [P][words] selection words of the fused modes (test hook) or null
     int ring_off;              // g > 1: byte offset of the cp.async row ring in dynamic smem
+    int ring4;                 // g > 1: ring depth 4 (else 2: large chunks keep 2 CTAs/SM)
     uint32_t* sel_only;        // SRC_KEYS: write the selection bitmap [P][words] here and stop (split launch)
     unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
@@ -755,7 +756,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     // g > 1: a RING-deep cp.async pipeline per half-warp in shared memory
     // (each lane copies and later reads back only its own 16-byte chunks, so
     // no barrier is needed); g = 1: two rows in registers
-    constexpr int RING = 4;
+    const int RING = a.ring4 ? 4 : 2;
     float4* ring = G > 1 ? reinterpret_cast<float4*>(smem_raw + a.ring_off) + (size_t)slot * RING * 64 : nullptr;
     auto issue = [&](int rr, int u) {
         if (rr < nrows) {
@@ -771,7 +772,8 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     int ri = slot;
     if constexpr (G > 1) {
 #pragma unroll
-        for (int u = 0; u < RING; ++u) issue(slot + u * STEP, u);
+        for (int u = 0; u < 4; ++u)
+            if (u < RING) issue(slot + u * STEP, u);
     } else if (ri < nrows) {
         const long long row = rows[ri];
 #pragma unroll
@@ -782,8 +784,9 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     }
     for (int it = 0; ri < nrows; ri += STEP, ++it) {  // half-warp uniform trip count
         if constexpr (G > 1) {
-            cp_async_wait_group<RING - 1>();  // this half-warp's oldest row has landed
-            const int u = it % RING;
+            if (a.ring4) cp_async_wait_group<3>();  // this half-warp's oldest row has landed
+            else cp_async_wait_group<1>();
+            const int u = it & (RING - 1);
 #pragma unroll
             for (int j = 0; j < VPL; ++j) {
                 kc[j] = ring[u * 64 + j * LPR + hl];
@@ -1100,8 +1103,12 @@ static size_t attend_smem(AtArgs& a, int G) {
     a.ring_off = (int)round_up(region + tail, 16);
     // g > 1: 16 half-warps x 4 rows x (K + V) of cp.async ring (not for the
     // key path, whose g > 1 launch only selects)
+    // depth 4 unless that costs the second CTA per SM (227 KB / 2 less the
+    // 1 KB per-CTA reservation): then depth 2
     const bool ring = G > 1 && a.src != SRC_KEYS;
-    return (size_t)a.ring_off + (ring ? (size_t)AT_WARPS * 2 * 4 * 2 * DH * 4 : 0);
+    const size_t ring4 = (size_t)AT_WARPS * 2 * 4 * 2 * DH * 4;
+    a.ring4 = !ring || (size_t)a.ring_off + ring4 <= 110 * 1024;
+    return (size_t)a.ring_off + (ring ? (a.ring4 ? ring4 : ring4 / 2) : 0);
 }
 
 template <int G, int MODE>
@@ -1136,8 +1143,12 @@ static void launch_attend_gm(const AtArgs& a, dim3 grid, size_t smem, int cl, cu
     attr[0].val.clusterDim.x = (unsigned)cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    // programmatic dependent launch (see the kernel's step 0)
-    static const bool pdl = std::getenv("PQKV_NO_PDL") == nullptr;
+    // programmatic dependent launch (see the kernel's step 0).  Not for
+    // clustered g > 1 grids (2 heavy CTAs per SM): placed early, while the
+    // previous grid drains, their 8-CTA clusters pack onto the SMs that free
+    // first (cfg3 73.5 -> 84 us, 32 heads g = 2 155 -> 193 us with it on)
+    static const bool pdl_env = std::getenv("PQKV_NO_PDL") == nullptr;
+    const bool pdl = pdl_env && !(G > 1 && cl > 1);
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
