@@ -298,6 +298,8 @@ __device__ void build_lut_range(double* lut, const float* q, const float* cen, i
                          (d_h % 4) == 0;
     for (int e = e0 + (int)threadIdx.x; e < e1; e += blockDim.x) {
         const int j = e / C;
+        if (aligned && d_m == 64 && g > 1) { lut_entry_multi<64>(lut, q, cen, g, d_h, e, j); continue; }
+        if (aligned && d_m == 32 && g > 1) { lut_entry_multi<32>(lut, q, cen, g, d_h, e, j); continue; }
         if (aligned && d_m == 64) { lut_entry_vec<64>(lut, q, cen, g, d_h, e, j); continue; }
         if (aligned && d_m == 32) { lut_entry_vec<32>(lut, q, cen, g, d_h, e, j); continue; }
         const float* cc = cen + (long long)e * d_m;

@@ -43,6 +43,38 @@ __device__ __forceinline__ void lut_entry_vec(double* lut, const float* q, const
     lut[e] = t;
 }
 
+// g > 1: the per-query dot products are independent chains (only their sum
+// t = ((0 + d_0) + d_1) + ... is ordered), so up to four run interleaved --
+// the serial latency is one d_m-long chain instead of g of them.
+template <int DM>
+__device__ __forceinline__ void lut_entry_multi(double* lut, const float* q, const float* cen, int g, int d_h,
+                                                int e, int j) {
+    const float4* cc4 = reinterpret_cast<const float4*>(cen + (long long)e * DM);
+    double t = 0.0;
+    for (int r0 = 0; r0 < g; r0 += 4) {
+        const int rn = min(4, g - r0);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+        for (int u = 0; u < DM / 4; ++u) {
+            const float4 cv = __ldg(cc4 + u);
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                if (rr < rn) {
+                    const float4 qv = __ldg(reinterpret_cast<const float4*>(q + (long long)(r0 + rr) * d_h + j * DM) + u);
+                    acc[rr] = __fma_rn((double)qv.x, (double)cv.x, acc[rr]);
+                    acc[rr] = __fma_rn((double)qv.y, (double)cv.y, acc[rr]);
+                    acc[rr] = __fma_rn((double)qv.z, (double)cv.z, acc[rr]);
+                    acc[rr] = __fma_rn((double)qv.w, (double)cv.w, acc[rr]);
+                }
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+            if (rr < rn) t = __dadd_rn(t, acc[rr]);
+    }
+    lut[e] = t;
+}
+
 __device__ inline void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
                           int C) {
     const int d_m = d_h / m;
@@ -50,8 +82,14 @@ __device__ inline void build_lut(double* lut, const float* q, const float* cen, 
                          (d_h % 4) == 0;
     if (aligned && (d_m == 64 || d_m == 32)) {
         for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
-            if (d_m == 64) lut_entry_vec<64>(lut, q, cen, g, d_h, e, e / C);
-            else lut_entry_vec<32>(lut, q, cen, g, d_h, e, e / C);
+            if (g > 1) {
+                if (d_m == 64) lut_entry_multi<64>(lut, q, cen, g, d_h, e, e / C);
+                else lut_entry_multi<32>(lut, q, cen, g, d_h, e, e / C);
+            } else if (d_m == 64) {
+                lut_entry_vec<64>(lut, q, cen, g, d_h, e, e / C);
+            } else {
+                lut_entry_vec<32>(lut, q, cen, g, d_h, e, e / C);
+            }
         }
         return;
     }
