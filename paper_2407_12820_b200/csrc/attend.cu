@@ -80,6 +80,8 @@ struct AtArgs {
     uint32_t* sel_dump;        // [P][words] selection words of the fused modes (test hook) or null
     int ring_off;              // g > 1: byte offset of the cp.async row ring in dynamic smem
     int ring4;                 // g > 1: ring depth 4 (else 2: large chunks keep 2 CTAs/SM)
+    int win;                   // selected middle rows expanded per gather window (list modes: chunk)
+    int stage;                 // pair mode: stage the CTA's codes in shared memory
     uint32_t* sel_only;        // SRC_KEYS: write the selection bitmap [P][words] here and stop (split launch)
     unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
@@ -136,6 +138,53 @@ __device__ int expand_words(const uint32_t* words, int nwords, int token_base, i
     }
     __syncthreads();
     return (int)total;
+}
+
+// expand_words restricted to the selected bits of rank [lo, hi) (rank = the
+// bit's position among all set bits of words[0..nwords) in id order); the
+// row of rank j goes to rows[off + j - lo].  Returns the number written.
+__device__ int expand_words_range(const uint32_t* words, int nwords, int token_base, int* rows, int off, uint32_t lo,
+                                  uint32_t hi, uint32_t* wtot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (nwords + AT_WARPS - 1) / AT_WARPS;
+    const int w0 = warp * per, w1 = min(nwords, w0 + per);
+    uint32_t cnt = 0;
+    for (int w = w0 + lane; w < w1; w += 32) cnt += __popc(words[w]);
+    cnt = warp_sum(cnt);
+    if (lane == 0) wtot[warp] = cnt;
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < AT_WARPS; ++w) {
+        uint32_t v = wtot[w];
+        before += w < warp ? v : 0;
+        total += v;
+    }
+    __syncthreads();
+    if (before < hi && before + cnt > lo) {
+        uint32_t run = before;
+        for (int wb = w0; wb < w1; wb += 32) {
+            const int w = wb + lane;
+            uint32_t bits = w < w1 ? words[w] : 0u;
+            uint32_t c = __popc(bits), x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            uint32_t pos = run + x - c;
+            if (pos < hi && pos + c > lo)
+                while (bits) {
+                    const int b = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    if (pos >= lo && pos < hi) rows[off + (int)(pos - lo)] = token_base + w * 32 + b;
+                    ++pos;
+                }
+            run += __shfl_sync(FULL, x, 31);
+        }
+    }
+    __syncthreads();
+    return (int)(min(total, hi) > lo ? min(total, hi) - lo : 0u);
 }
 
 // Staged code layout: within every block of 256 16-byte chunks (1024
@@ -606,6 +655,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     asm volatile("griddepcontrol.launch_dependents;");
     // ---- 1. this CTA's row list (ascending token ids) ----
     int nrows = 0;
+    int sel_total = 0;  // windowed list: selected middle rows of this CTA (0: one window)
     if (src == SRC_ROWS) {
         const int b0 = c * a.chunk, cnt = max(0, min(a.chunk, a.t - b0));
         for (int e = tid; e < cnt; e += AT_THREADS) rows[e] = (int)a.rows[(long long)p * a.t + b0 + e];
@@ -652,7 +702,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
             {
                 const int n = max(0, r1 - r0);
                 const uint32_t* src = cd_g + r0;
-                if (crank == sel) {
+                if (crank == sel || !a.stage) {
                     for (int o = tid * 32; o < n; o += AT_THREADS * 32) prefetch_l2(src + o);
                 } else {
                     uint32_t* dst = reinterpret_cast<uint32_t*>(smem_raw);
@@ -714,8 +764,23 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         __syncthreads();
         if (a.sel_dump && ((MODE == SRC_PAIRS) || (MODE == SRC_KEYS)))
             for (int w = tid; w < nw; w += AT_THREADS) a.sel_dump[(long long)p * a.words + r0 / 32 + w] = words[w];
-        nrows += expand_words(words, nw, a.n_init + r0, rows, nrows, wtot);
-        if (c == a.n_chunks - 1) {
+        if (a.win >= a.chunk) {
+            nrows += expand_words(words, nw, a.n_init + r0, rows, nrows, wtot);
+            sel_total = 0;
+        } else {  // windowed: the first a.win selected middle rows now, the rest after each gather window
+            uint32_t t = 0;
+            for (int w = tid; w < nw; w += AT_THREADS) t += __popc(words[w]);
+            t = warp_sum(t);
+            if (lane == 0) wtot[warp] = t;
+            __syncthreads();
+            t = 0;
+#pragma unroll
+            for (int w = 0; w < AT_WARPS; ++w) t += wtot[w];
+            __syncthreads();
+            sel_total = (int)t;
+            nrows += expand_words_range(words, nw, a.n_init + r0, rows, nrows, 0u, (uint32_t)a.win, wtot);
+        }
+        if (c == a.n_chunks - 1 && sel_total <= a.win) {
             for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
             nrows += a.n_local;
         }
@@ -771,6 +836,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         }
         cp_async_commit();
     };
+    for (int win_base = 0;; win_base += a.win) {
     int ri = slot;
     if constexpr (G > 1) {
 #pragma unroll
@@ -846,6 +912,21 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
         }
     }
     if constexpr (G > 1) cp_async_wait_all();
+    if (win_base + a.win >= sel_total) break;
+    // next window of this CTA's selected middle rows (+ the local rows after the last)
+    __syncthreads();
+    {
+        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
+        const int nw = (max(0, r1 - r0) + 31) / 32;
+        const int nb = win_base + a.win;
+        nrows = expand_words_range(words, nw, a.n_init + r0, rows, 0, (uint32_t)nb, (uint32_t)(nb + a.win), wtot);
+        if (c == a.n_chunks - 1 && nb + a.win >= sel_total) {
+            for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
+            nrows += a.n_local;
+        }
+        __syncthreads();
+    }
+    }
 
     if (a.prof) {
         __syncthreads();
@@ -1093,7 +1174,13 @@ static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
 // Shared memory: region (rows[] / merge partials / pair-select scratch)
 // followed by words[] and the pair classes.
 static size_t attend_smem(AtArgs& a, int G) {
-    size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.chunk + a.n_init + a.n_local;
+    // chunks above 8192 tokens (many heads: one wave of CTAs needs few, large
+    // chunks) expand and gather their rows in windows of 4096 and, in pair
+    // mode, classify codes straight from L2 instead of staging them, so the
+    // shared memory stays at the 8192-token footprint
+    a.win = (a.src == SRC_ROWS || a.chunk <= 8192) ? a.chunk : 4096;
+    a.stage = a.chunk <= 8192;
+    size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.win + a.n_init + a.n_local;
     size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
     size_t region = std::max(rows_cap * 4, merge);
     if (a.src == SRC_PAIRS) region = std::max(region, pair_select_scratch(a.C, a.n_tchunks));
@@ -1176,7 +1263,7 @@ static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cuda
     // count to a multiple of the cluster; padded CTAs own empty ranges)
     int cl = 1;
     if (a.src == SRC_PAIRS && a.n_chunks >= 4) {
-        cl = 8;
+        cl = a.n_chunks >= 8 ? 8 : 4;  // 4 chunks per head (many heads): no empty padded CTAs
         a.n_chunks = (int)round_up((size_t)a.n_chunks, (size_t)cl);
     }
     if (a.src == SRC_KEYS) cl = a.n_chunks;  // one cluster per head (<= 16 CTAs)

@@ -84,3 +84,46 @@ def test_fused_decode_heavy_ties(ctx, orc, m, b, c_used):
     vals = rng.standard_normal((P, s, 128)).astype(np.float32)
     qs = rng.standard_normal((P, 1, 128)).astype(np.float32)
     _run(ctx, orc, cen, codes, keys, vals, qs, b, n_init, n_local, k, m == 2)
+
+
+@pytest.mark.parametrize("g", [1, 2])
+def test_fused_decode_many_heads_windowed(ctx, orc, g):
+    """Many heads (80 x 64K): the plan picks chunks above 8192 tokens, so the
+    pair path classifies from L2 and expands + gathers its rows in windows."""
+    import torch
+
+    import paper_2407_12820_b200 as pq
+
+    P, S, n_init, n_local, m, b = 80, 65536, 4, 64, 2, 6
+    k = S // 5
+    s_mid = S - n_init - n_local
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    keys = torch.randn((P, S, 128), generator=gen, device="cuda")
+    keys[:, :, :8] += 2.0 * torch.randn((P, 1, 8), generator=gen, device="cuda")
+    vals = torch.randn((P, S, 128), generator=gen, device="cuda")
+    qs = torch.randn((P, g, 128), generator=gen, device="cuda")
+    cen, codes = ctx.pq_build(keys[:, n_init:n_init + s_mid].contiguous(), m, b, 4, list(range(P)))
+    tabs = ctx.tuple_tables(codes, b)
+    layer = pq.DecodeLayer(keys=keys, values=vals, centroids=cen, codes=codes, total=S, n_init=n_init,
+                           n_local=n_local, b=b, tables=tabs)
+    words = (s_mid + 31) // 32
+    dump = torch.zeros((P, words), dtype=torch.int32, device="cuda")
+    ctx.set_selection_dump(dump)
+    try:
+        out = ctx.decode(layer, qs, k).cpu().numpy()
+    finally:
+        ctx.set_selection_dump(None)
+    assert layer.launches(g) == 1
+    bits = dump.cpu().numpy().view(np.uint32)
+    cen_h = cen.cpu().numpy()
+    codes_h = codes.cpu().numpy().view(np.uint16)
+    q_h = qs.cpu().numpy()
+    for p in (0, 41, P - 1):
+        rows = orc.top_k_desc(orc.pq_score_gqa(q_h[p], cen_h[p], codes_h[p]), k)
+        got = np.flatnonzero(np.unpackbits(bits[p].view(np.uint8), bitorder="little")[:s_mid])
+        assert np.array_equal(got, np.sort(rows).astype(np.int64)), f"head {p}: selection differs"
+        kh, vh = keys[p].cpu().numpy(), vals[p].cpu().numpy()
+        for r in range(g):
+            want = orc.selective_attention(q_h[p, r], kh, vh, n_init, n_local, rows + n_init)
+            assert _rel(out[p, r], want) < 1e-3
