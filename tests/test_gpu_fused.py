@@ -58,6 +58,7 @@ def _run(ctx, orc, cen, codes, keys, vals, qs, b, n_init, n_local, k, tables):
     (8, 4, False, 5000, 2, 1, 700),      # m = 8
     (4, 8, False, 131072, 1, 4, 13107),  # 16-CTA cluster, 128K
     (4, 8, False, 800, 2, 1, 5),         # one CTA per head, tiny k
+    (4, 8, False, 131072, 2, 1, 65536),  # key path g = 1, 16K chunks: two gather windows per CTA
 ])
 def test_fused_decode_selection_exact(ctx, orc, m, b, tables, s, P, g, k):
     import torch
@@ -86,8 +87,8 @@ def test_fused_decode_heavy_ties(ctx, orc, m, b, c_used):
     _run(ctx, orc, cen, codes, keys, vals, qs, b, n_init, n_local, k, m == 2)
 
 
-@pytest.mark.parametrize("g", [1, 2])
-def test_fused_decode_many_heads_windowed(ctx, orc, g):
+@pytest.mark.parametrize("g,ratio", [(1, 5), (2, 5), (1, 2)])
+def test_fused_decode_many_heads_windowed(ctx, orc, g, ratio):
     """Many heads (80 x 64K): the plan picks chunks above 8192 tokens, so the
     pair path classifies from L2 and expands + gathers its rows in windows."""
     import torch
@@ -95,7 +96,7 @@ def test_fused_decode_many_heads_windowed(ctx, orc, g):
     import paper_2407_12820_b200 as pq
 
     P, S, n_init, n_local, m, b = 80, 65536, 4, 64, 2, 6
-    k = S // 5
+    k = S // ratio  # ratio 2: more selected rows per CTA than one window holds
     s_mid = S - n_init - n_local
     gen = torch.Generator(device="cuda")
     gen.manual_seed(7)
