@@ -580,21 +580,27 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     // ---- selection words in id order ----
     const int seg = a.chunk / AT_WARPS;
     const int s0 = warp * seg, s1 = min(n, s0 + seg);
-    uint32_t weq = 0;
-    for (int i0 = s0; i0 < s1; i0 += 32) {
-        const int i = i0 + lane;
-        weq += __popc(__ballot_sync(FULL, i < s1 && keys[i] == kstar));
-    }
-    if (lane == 0) wtot[warp] = weq;
-    __syncthreads();
+    // this CTA's ties are all taken or none is (the usual case): no per-warp
+    // tie prefix needed
+    const bool all_or_none = take == 0 || take == cta_eq;
     uint32_t run = 0;
-    for (int v = 0; v < warp; ++v) run += wtot[v];
+    if (!all_or_none) {
+        uint32_t weq = 0;
+        for (int i0 = s0; i0 < s1; i0 += 32) {
+            const int i = i0 + lane;
+            weq += __popc(__ballot_sync(FULL, i < s1 && keys[i] == kstar));
+        }
+        if (lane == 0) wtot[warp] = weq;
+        __syncthreads();
+        for (int v = 0; v < warp; ++v) run += wtot[v];
+    }
+    const uint32_t take_eff = all_or_none ? (take ? 0xffffffffu : 0u) : take;
     for (int i0 = s0; i0 < s1; i0 += 32) {
         const int i = i0 + lane;
         const uint32_t key = i < s1 ? keys[i] : 0u;
         const bool gt = i < s1 && key > kstar, eq = i < s1 && key == kstar;
         const unsigned em = __ballot_sync(FULL, eq);
-        const bool sel = gt || (eq && run + __popc(em & lanemask_lt()) < take);
+        const bool sel = gt || (eq && run + __popc(em & lanemask_lt()) < take_eff);
         const unsigned word = __ballot_sync(FULL, sel);
         if (lane == 0) words[i0 >> 5] = word;
         run += __popc(em);
