@@ -1356,6 +1356,29 @@ bool decode_keys_fused(const pqkv_layer& L, size_t G) {
     return decode_fast_path(L, G) && keys_geometry(L, G, nullptr, nullptr);
 }
 
+// Key path in two launches (cluster select -> bitmap, then a finer bitmap-mode
+// gather): always for g > 1 (one 8-CTA cluster per head leaves 1 CTA/SM for
+// a gather that needs 2); for g = 1 unless the cluster grid fills the GPU in
+// one wave with at least two CTAs per SM (16 units x 128K: fused 127 us,
+// split 99.5 us; 64 units: the 98 KB key CTAs need two waves fused).
+bool decode_keys_split(const pqkv_layer& L, size_t G) {
+    if (G > 1) return true;
+    int chunk = 0, n_chunks = 0;
+    if (!keys_geometry(L, G, &chunk, &n_chunks)) return false;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+            sms = 148;
+    }
+    const size_t ctas = L.n_heads * (size_t)n_chunks;
+    const size_t C = (size_t)1 << L.b;
+    const size_t smem = (size_t)chunk * 4 + L.m * C * 8 + (size_t)chunk / 32 * 4 + (size_t)NB * 12 + 3072;
+    const size_t per_sm = std::min<size_t>(4, (size_t)227 * 1024 / smem);
+    return ctas < 2 * (size_t)sms || ctas > per_sm * (size_t)sms;
+}
+
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
                           cudaStream_t st, size_t k_pairs, size_t k_keys) {
@@ -1392,7 +1415,7 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
         keys_geometry(L, G, &a.chunk, &a.n_chunks);
         // g > 1 (1 CTA/SM per key cluster): select in one launch, gather in a
         // second bitmap-mode launch with its own (finer) chunking
-        if (G > 1 && bitmap) {
+        if (bitmap && decode_keys_split(L, G)) {
             a.sel_only = const_cast<uint32_t*>(bitmap);
             launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);
             launch_decode_attend(ctx, L, queries, G, bitmap, nullptr, nullptr, out, st, 0, 0);

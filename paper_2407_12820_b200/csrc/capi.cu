@@ -262,7 +262,8 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
             // per-head cluster computes ADC keys and radix-selects through
             // DSMEM, then gathers (g = 1: same launch; g > 1: the selection
             // bitmap feeds a second, finer-grained attention launch)
-            uint32_t* bm = g > 1 ? static_cast<uint32_t*>(decode_workspace(ctx, P * words * 4)) : nullptr;
+            uint32_t* bm = decode_keys_split(*L, g) ? static_cast<uint32_t*>(decode_workspace(ctx, P * words * 4))
+                                                    : nullptr;
             launch_decode_attend(ctx, *L, d_queries, g, bm, nullptr, nullptr, d_out, st, 0, k);
             return;
         }
@@ -393,7 +394,7 @@ int pqkv_decode_launches(const pqkv_layer* L, size_t g, int with_ids) {
     bool fast = L->d_h == 128 && (g == 1 || g == 2 || g == 4) && L->kv_head_stride % 4 == 0;
     const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist, L->total - L->n_init - L->n_local);
     if (tup && fast && !with_ids && L->b <= 6) return 1;       // pair select fused into the attention
-    if (fast && !with_ids && decode_keys_fused(*L, g)) return g > 1 ? 2 : 1;  // key select [+] attention
+    if (fast && !with_ids && decode_keys_fused(*L, g)) return decode_keys_split(*L, g) ? 2 : 1;  // key select [+] attention
     if (tup && fast && !with_ids) return 2;                     // pair select + attention
     int n = tup ? 2 /*pair select + bitmap*/ : 1 /*cluster select*/;
     n += with_ids ? 1 : 0 /*sort*/;

@@ -166,6 +166,7 @@ bool decode_pairs_fused(const pqkv_layer& L, size_t g);
 // over per-token ADC keys runs in the attention prologue, one thread-block
 // cluster per head (k_keys > 0).
 bool decode_keys_fused(const pqkv_layer& L, size_t g);
+bool decode_keys_split(const pqkv_layer& L, size_t g);
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t g,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
                           cudaStream_t stream, size_t k_pairs = 0, size_t k_keys = 0);

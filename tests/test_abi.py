@@ -40,7 +40,11 @@ def test_pq_config_rules():
 
 def test_decode_launch_accounting():
     L = pq.pqkv_layer(d_h=128, kv_head_stride=128 * 10, n_heads=1, total=10, n_init=1, n_local=1, m=2, b=6)
-    assert pq.lib().pqkv_decode_launches(C.byref(L), 1, 0) == 1  # key select fused
+    # one head: the per-head cluster grid is too small to gather -> select + attention
+    assert pq.lib().pqkv_decode_launches(C.byref(L), 1, 0) == 2
+    L.n_heads = 400  # >= 2 CTAs per SM: key select fused into the gather
+    assert pq.lib().pqkv_decode_launches(C.byref(L), 1, 0) == 1
+    L.n_heads = 1
     assert pq.lib().pqkv_decode_launches(C.byref(L), 3, 1) == 5
 
 
