@@ -1180,12 +1180,22 @@ static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
 // Shared memory: region (rows[] / merge partials / pair-select scratch)
 // followed by words[] and the pair classes.
 static size_t attend_smem(AtArgs& a, int G) {
-    // chunks above 8192 tokens (many heads: one wave of CTAs needs few, large
-    // chunks) expand and gather their rows in windows of 4096 and, in pair
-    // mode, classify codes straight from L2 instead of staging them, so the
-    // shared memory stays at the 8192-token footprint
-    a.win = (a.src == SRC_ROWS || a.chunk <= 8192) ? a.chunk : 4096;
-    a.stage = a.chunk <= 8192;
+    // Chunks whose full row list + staged codes would cost CTAs per SM (many
+    // heads: one wave of CTAs needs few, large chunks) expand and gather their
+    // rows in windows of 4096 and, in pair mode, classify codes straight from
+    // L2 instead of staging them, so the shared memory stays at the
+    // 8192-token footprint.  Measured: g = 1, 64 units x 128K (16K chunks):
+    // windowed 285 us vs 468; g = 2, 32 heads (16K chunks, 2 CTAs/SM either
+    // way): staged 156 us vs windowed 194.
+    {
+        const size_t full_rows = ((size_t)a.chunk + a.n_init + a.n_local) * 4;
+        const size_t tail_est = (size_t)a.chunk / 32 * 8 + ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
+        const size_t ring2 = (G > 1 && a.src != SRC_KEYS) ? (size_t)AT_WARPS * 2 * 2 * 2 * DH * 4 : 0;
+        const size_t budget = (G == 1 ? 55 : 110) * 1024;
+        const bool full = a.src == SRC_ROWS || a.chunk <= 8192 || full_rows + tail_est + ring2 <= budget;
+        a.win = full ? a.chunk : 4096;
+        a.stage = full;
+    }
     size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.win + a.n_init + a.n_local;
     size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
     size_t region = std::max(rows_cap * 4, merge);
