@@ -36,11 +36,66 @@ N_LAYERS = 8
 METRIC = "decode PQ-retrieve+attend us/layer @128K ctx"
 WORKLOAD = "northstar-1layer-32h-128d-128Kctx-m2b6-top1/5+4init+64local-bs1"
 
+# BASELINE.json configs as decode units (one unit = one (request, layer,
+# kv_head) K/V set shared by g query heads).  "northstar" is the headline;
+# the others are reported beside it (device-timed, rotating layers) and are
+# the geometries tests/test_gpu_plans.py pins token for token.
+CONFIGS = {
+    "northstar": dict(units=32, g=1, s=131072, m=2, b=6, ratio=5, tables=True, layers=N_LAYERS,
+                      what="configs[1] geometry at 128K: 32 heads x 128 dim, m2b6, top 1/5 + 4 + 64, bs1"),
+    "cfg1": dict(units=8, g=1, s=4096, m=2, b=6, ratio=5, tables=True, layers=16,
+                 what="configs[0]: 8 heads x 4K, m2b6, top 1/5 (the CPU reference's own case)"),
+    "cfg2": dict(units=32, g=1, s=32768, m=2, b=6, ratio=5, tables=True, layers=4,
+                 what="configs[1]: 32 heads x 32K, m2b6, top 1/5 + 4 + 64, bs1"),
+    "cfg3_layer": dict(units=8, g=4, s=131072, m=2, b=6, ratio=5, tables=True, layers=4,
+                       what="configs[2] per layer: Llama-3-8B shape, 8 kv heads x g4 x 128K, m2b6, top 1/5"),
+    "cfg5_per_gpu": dict(units=16, g=4, s=131072, m=4, b=8, ratio=10, tables=False, layers=4,
+                         what="configs[4] per GPU at 8 GPUs: 16 (request, kv head) units x g4 x 128K, m4b8, "
+                              "top 1/10"),
+}
+
+
+def cfg_k(c):
+    return round(c["s"] / c["ratio"])
+
+
+def cfg_bytes(c):
+    """B = units * [s_mid m b/8 + C d_h 4 + T_att d_h 4 2 + 2 g d_h 4]."""
+    s_mid = c["s"] - N_INIT - N_LOCAL
+    t_att = N_INIT + cfg_k(c) + N_LOCAL
+    return c["units"] * (s_mid * c["m"] * c["b"] / 8 + (1 << c["b"]) * DH * 4 + t_att * DH * 4 * 2
+                         + 2 * c["g"] * DH * 4)
+
+
+def make_layer(ctx, name, kind="gaussian", seed=0):
+    """One layer of config `name`: device-generated K/V/queries (pqkv_gen_workload,
+    the reference's gaussian-mixture / powerlaw distributions) and its PQ index
+    built on the GPU (pq_construct semantics, T = 10) plus the code-pair tables.
+    Returns (DecodeLayer, base queries [units][g][d_h], build seconds)."""
+    import torch
+
+    import paper_2407_12820_b200 as pq
+
+    c = CONFIGS[name]
+    s, s_mid = c["s"], c["s"] - N_INIT - N_LOCAL
+    keys, vals, base_q = ctx.gen_workload(s, DH, h_kv=c["units"], g=c["g"], kind=kind, n_components=8,
+                                          spread=0.5, seed=seed)
+    mids = keys[:, N_INIT:N_INIT + s_mid].contiguous()
+    seeds = [7 + 131 * seed + h for h in range(c["units"])]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cen, codes = ctx.pq_build(mids, c["m"], c["b"], T_ITERS, seeds)
+    tables = ctx.tuple_tables(codes, c["b"]) if c["tables"] else None
+    torch.cuda.synchronize()
+    secs = time.perf_counter() - t0
+    del mids
+    layer = pq.DecodeLayer(keys=keys, values=vals, centroids=cen, codes=codes, total=s, n_init=N_INIT,
+                           n_local=N_LOCAL, b=c["b"], tables=tables)
+    return layer, base_q, secs
+
 
 def algorithmic_bytes_per_layer():
-    """B = h_kv [s_mid m b/8 + C d_h 4 + T_att d_h 4 2 + 2 g d_h 4]."""
-    t_att = N_INIT + K_SEL + N_LOCAL
-    return H * (S_MID * M * B / 8 + (1 << B) * DH * 4 + t_att * DH * 4 * 2 + 2 * G * DH * 4)
+    return cfg_bytes(CONFIGS["northstar"])
 
 
 def attend_bytes_per_launch():
@@ -86,11 +141,12 @@ class ClockSampler:
         return self
 
     def __enter__(self):
-        self.t0 = time.time()
+        self.windows = getattr(self, "windows", [])
+        self.windows.append([time.time(), None])
         return self
 
     def __exit__(self, *a):
-        self.t1 = time.time()
+        self.windows[-1][1] = time.time()
 
     def stop(self):
         if self.proc:
@@ -112,7 +168,7 @@ class ClockSampler:
                         continue
                     if isinstance(v, dict):
                         max_mhz = v.get("max_mhz", max_mhz)
-                    elif self.t0 - 0.005 <= v[0] <= self.t1 + 0.005:
+                    elif any(t0 - 0.005 <= v[0] <= t1 + 0.005 for t0, t1 in getattr(self, "windows", [])):
                         rows.append(v)
             os.unlink(self.out.name)
         if not rows:
@@ -122,13 +178,6 @@ class ClockSampler:
         sm = sorted(r[1] for r in rows)
         reasons = sorted({name for r in rows for bit, name in bits.items() if r[2] & bit})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max_mhz, "reasons": reasons, "samples": len(rows)}
-
-
-def make_layer_inputs(ctx, seed):
-    """Gaussian-mixture keys (workload.cpp:39-51 distribution: 8 shared means,
-    spread 0.5), N(0,1) values and base queries, generated in HBM by the
-    library's counter-based generator (pqkv_gen_workload)."""
-    return ctx.gen_workload(S, DH, h_kv=H, g=G, kind="gaussian", n_components=8, spread=0.5, seed=seed)
 
 
 def run_reference(args, rank, world):
@@ -182,11 +231,14 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_leg(layer0, cen, codes, torch, gpu_out=None):
-    """The reference (oracle/_ref) on this box's host cores for a bounded sample
-    (8 heads of layer 0, same GPU-built index -- bit-identical to the
-    reference's), extrapolated x4 to the 32-head layer; plus a 1-head 32K-token
-    pq_construct sample for the build."""
+def cpu_baseline_leg(layer, base_q, gpu_out, gpu_words):
+    """The reference (oracle/_ref, the unmodified library) on this box's host
+    cores for a bounded sample: P = min(32, cores) heads of headline layer 0
+    (same GPU-built index -- bit-identical to the reference's), one head per
+    host thread, 1 warm-up + 3 timed steps, median extrapolated x32/P to the
+    layer.  Parity on the same inputs: the GPU's selection words equal the
+    reference's approx_topk set, and the outputs are within 1e-3 relative.
+    Plus a build sample: pq_construct over P heads x 32K tokens on P threads."""
     import numpy as np
 
     import oracle
@@ -194,31 +246,76 @@ def cpu_baseline_leg(layer0, cen, codes, torch, gpu_out=None):
     if not oracle.has_ref():
         return None, None
     ref = oracle.ref()
-    P = min(H, max(1, os.cpu_count() or 1))  # one head per host thread
-    keys, vals, base_q = layer0
-    k = keys[:P].cpu().numpy()
-    v = vals[:P].cpu().numpy()
+    cores = os.cpu_count() or 1
+    P = min(H, max(1, cores))
+    k = layer.keys[:P].cpu().numpy()
+    v = layer.values[:P].cpu().numpy()
     q = base_q[:P].cpu().numpy()
-    c = cen[:P].cpu().numpy()
-    cd = codes[:P].cpu().numpy().view(np.uint16)
-    cores = min(os.cpu_count() or 1, P)
-    runs = [ref.bench_decode(k, v, q, c, cd, N_INIT, N_LOCAL, K_SEL, cores) for _ in range(3)]
-    ts = [r[0] for r in runs]
-    dec = {"value": float(np.median(ts)) * 1e6 * (H / P), "unit": "us/layer", "cores": cores,
-           "kind": "reference", "sample": f"{P} of {H} heads of one 128K layer, x{H / P:g} to a layer, median of 3"}
-    # parity on the benchmark's own inputs: the fused GPU decode of these heads
-    # (same base queries, same index) against the reference library's outputs
-    if gpu_out is not None:
-        want = runs[0][1]
-        got = gpu_out[:P].cpu().numpy()
-        rel = float(np.abs(got - want).max() / max(1.0, float(np.abs(want).max())))
-        dec["parity"] = {"heads": P, "max_rel_err": rel, "tolerance": 1e-3, "ok": rel < 1e-3}
+    c = layer.centroids[:P].cpu().numpy()
+    cd = layer.codes[:P].cpu().numpy().view(np.uint16)
+    qs = np.repeat(q[None], 4, axis=0)
+    secs, want = ref.bench_decode_steps(k, v, qs, c, cd, N_INIT, N_LOCAL, K_SEL, P)
+    dec = {"value": float(np.median(secs[1:])) * 1e6 * (H / P), "unit": "us/layer", "cores": P,
+           "kind": "reference",
+           "sample": f"{P} of {H} heads of one 128K layer (gaussian), one head per thread, median of 3 warm "
+                     f"steps, x{H / P:g} to a layer"}
+    got = gpu_out[:P].cpu().numpy()
+    rel = float(np.abs(got - want).max() / np.abs(want).max())
+    words = gpu_words[:P].cpu().numpy().view(np.uint32)
+    sel_ok = True
+    for p in range(min(P, 4)):  # selection sets of 4 heads against the reference's approx_topk
+        rows = ref.top_k_desc(ref.pq_score_gqa(q[p], c[p], cd[p]), K_SEL)
+        got_rows = np.flatnonzero(np.unpackbits(words[p].view(np.uint8), bitorder="little")[:S_MID])
+        sel_ok = sel_ok and np.array_equal(got_rows, np.sort(rows).astype(np.int64))
+    dec["parity"] = {"heads": P, "max_rel_err": rel, "tolerance": 1e-3, "selection_heads": min(P, 4),
+                     "selection_equal": bool(sel_ok), "ok": bool(rel < 1e-3 and sel_ok)}
     sb = 32768
-    secs, _, _ = ref.bench_build(np.ascontiguousarray(k[:1, N_INIT:N_INIT + sb]), M, B, T_ITERS,
-                                 np.array([5], np.uint64), 1)
-    bld = {"value": sb / secs, "unit": "key vectors/s", "cores": 1, "kind": "reference",
-           "sample": f"pq_construct m2b6 T={T_ITERS} on 1 head x {sb} tokens"}
+    mids = np.ascontiguousarray(k[:, N_INIT:N_INIT + sb])
+    bsecs, _, _ = ref.bench_build(mids, M, B, T_ITERS, np.arange(P, dtype=np.uint64) + 5, P)
+    bld = {"value": P * sb / bsecs, "unit": "key vectors/s", "cores": P, "kind": "reference",
+           "sample": f"pq_construct m2b6 T={T_ITERS} on {P} heads x {sb} tokens, one head per thread"}
     return dec, bld
+
+
+def time_steps(ctx, layers, queries, k, n_warm, n_steps, dist=None, dev=None, clk=None):
+    """Device time (ms) of n_steps decodes rotating over `layers` (CUDA events on
+    the launching stream, barrier + synchronize on both sides, max over ranks)."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    nl = len(layers)
+    for i in range(n_warm):
+        ctx.decode(layers[i % nl], queries[i % len(queries)], k)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk:
+        clk.__enter__()
+    ev0.record(stream)
+    for i in range(n_warm, n_warm + n_steps):
+        ctx.decode(layers[i % nl], queries[i % len(queries)], k)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def drift_queries(base, n, sigma, gen):
+    """Per-step query drift of run_e2e (experiments.cpp:212-216)."""
+    import torch
+
+    return [base + sigma * torch.randn(base.shape, generator=gen, device=base.device) for _ in range(n)]
 
 
 def main():
@@ -228,6 +325,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="headline only (skip cfg1/2/3/5 lines)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -250,104 +348,80 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
     ctx = pq.Context(local)
-
-    # ---- per-rank layers: inputs + GPU PQ build (timed separately) ----
-    layers, build_s = [], []
-    keep0 = None
-    for li in range(N_LAYERS):
-        keys, vals, base_q = make_layer_inputs(ctx, 1000 * rank + li)
-        mids = keys[:, N_INIT:N_INIT + S_MID]  # middle rows, strided view of the cache
-        mids = mids.contiguous()
-        seeds = [7 + 100 * rank + 10 * li + h for h in range(H)]
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        cen, codes = ctx.pq_build(mids, M, B, T_ITERS, seeds)
-        tables = ctx.tuple_tables(codes, B)  # code-pair histograms (part of the build)
-        torch.cuda.synchronize()
-        build_s.append(time.perf_counter() - t0)
-        rech, tot = ctx.last_build_stats()
-        del mids
-        layer = pq.DecodeLayer(keys=keys, values=vals, centroids=cen, codes=codes, total=S,
-                               n_init=N_INIT, n_local=N_LOCAL, b=B, tables=tables)
-        layers.append((layer, base_q))
-        if li == 0:
-            keep0 = ((keys, vals, base_q), cen, codes)
-    # per-step query drift (experiments.cpp:212-216)
-    gq = torch.Generator(device=dev)
-    gq.manual_seed(99 + rank)
     n_total = args.warmup + args.steps
     sigma = 0.25 / math.sqrt(DH)
-    queries = [layers[i % N_LAYERS][1] + sigma * torch.randn((H, G, DH), generator=gq, device=dev)
-               for i in range(n_total)]
-    out = torch.empty((H, G, DH), dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream()
+    gq = torch.Generator(device=dev)
+    gq.manual_seed(99 + rank)
 
-    def step(i):
-        layer = layers[i % N_LAYERS][0]
-        return ctx.decode(layer, queries[i], K_SEL)
+    # ---- headline: both of the reference's key distributions, 8 rotating layers each ----
+    heads = {}
+    build_s = []
+    rech_tot = [0, 0]
+    for kind in ("gaussian", "powerlaw"):
+        layers, qs = [], []
+        for li in range(N_LAYERS):
+            layer, base_q, secs = make_layer(ctx, "northstar", kind, seed=1000 * rank + 16 * li + (kind == "powerlaw"))
+            if kind == "gaussian":
+                build_s.append(secs)
+                r, t = ctx.last_build_stats()
+                rech_tot[0] += r
+                rech_tot[1] += t
+            layers.append(layer)
+            qs.append(base_q)
+        queries = [qs[i % N_LAYERS] + sigma * torch.randn(qs[0].shape, generator=gq, device=dev)
+                   for i in range(max(n_total, N_LAYERS))]
+        heads[kind] = (layers, qs, queries)
 
-    # ---- device-resident timing ----
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk = ClockSampler(local).start()
-    with clk:
-        ev0.record(stream)
-        for i in range(args.warmup, n_total):
-            step(i)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    if dist:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    timed = {}
+    for kind in ("gaussian", "powerlaw"):
+        layers, _, queries = heads[kind]
+        timed[kind] = time_steps(ctx, layers, queries, K_SEL, args.warmup, args.steps, dist, dev, clk)
+    worst = max(timed, key=lambda kd: timed[kd])
+    ms = timed[worst]
     ms_per_step = ms / args.steps
-    layers_done = args.steps * world
-    us_per_layer = ms * 1e3 / layers_done
+    us_per_layer = ms * 1e3 / (args.steps * world)
+    layers, base_qs, queries = heads[worst]
+    plan = ctx.decode_plan(layers[0], G, K_SEL)
 
     # ---- dominant kernel (attention gather + combine) timed alone ----
+    stream = torch.cuda.current_stream()
     bms = []
     for i in range(N_LAYERS):
-        bm, _ = ctx.pq_search(queries[i], layers[i][0].centroids, layers[i][0].codes, B, K_SEL, s=S_MID,
-                              bitmap=True, ordered=False, tables=layers[i][0].tables)
+        bm, _ = ctx.pq_search(queries[i], layers[i].centroids, layers[i].codes, B, K_SEL, s=S_MID,
+                              bitmap=True, ordered=False, tables=layers[i].tables)
         bms.append(bm)
+    out = torch.empty((H, G, DH), dtype=torch.float32, device=dev)
     sel_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
     reps = max(args.steps, 8)
     for i in range(3):
-        ctx.decode_attend(layers[i % N_LAYERS][0], queries[i], bms[i % N_LAYERS], out)
+        ctx.decode_attend(layers[i % N_LAYERS], queries[i], bms[i % N_LAYERS], out)
     torch.cuda.synchronize()
     sel_ev[0][0].record(stream)
     for i in range(reps):
-        ctx.decode_attend(layers[i % N_LAYERS][0], queries[i % N_LAYERS], bms[i % N_LAYERS], out)
+        ctx.decode_attend(layers[i % N_LAYERS], queries[i % N_LAYERS], bms[i % N_LAYERS], out)
     sel_ev[0][1].record(stream)
     sel_ev[1][0].record(stream)
     for i in range(reps):
-        ctx.pq_search(queries[i % N_LAYERS], layers[i % N_LAYERS][0].centroids, layers[i % N_LAYERS][0].codes,
-                      B, K_SEL, s=S_MID, bitmap=True, ordered=False, tables=layers[i % N_LAYERS][0].tables)
+        li = i % N_LAYERS
+        ctx.pq_search(queries[li], layers[li].centroids, layers[li].codes, B, K_SEL, s=S_MID, bitmap=True,
+                      ordered=False, tables=layers[li].tables)
     sel_ev[1][1].record(stream)
     torch.cuda.synchronize()
     attend_ms = sel_ev[0][0].elapsed_time(sel_ev[0][1]) / reps
     select_ms = sel_ev[1][0].elapsed_time(sel_ev[1][1]) / reps
 
-    # ---- end to end through the C ABI with HOST buffers ----
+    # ---- end to end through the C ABI with HOST buffers (pinned in, pinned out) ----
     hq = [q.cpu().pin_memory() for q in queries[:N_LAYERS]]
     ho = torch.empty((H, G, DH), dtype=torch.float32).pin_memory()
     for i in range(3):
-        ctx.decode_host(layers[i % N_LAYERS][0], hq[i % N_LAYERS], ho, K_SEL)
+        ctx.decode_host(layers[i % N_LAYERS], hq[i % N_LAYERS], ho, K_SEL)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for i in range(args.steps):
-        ctx.decode_host(layers[i % N_LAYERS][0], hq[i % N_LAYERS], ho, K_SEL)
+        ctx.decode_host(layers[i % N_LAYERS], hq[i % N_LAYERS], ho, K_SEL)
     e2e_s = time.perf_counter() - t0
     if dist:
         t = torch.tensor([e2e_s], device=dev)
@@ -357,18 +431,20 @@ def main():
 
     # ---- cfg4: one layer's heads sharded over the ranks + NCCL all-gather ----
     # (BASELINE configs[3]; the path itself has no exchange, the gathered
-    # outputs are what the next layer's projection needs)
+    # outputs are what the next layer's projection needs).  Layers rotate.
     from paper_2407_12820_b200 import shard
 
     hr = shard.partition(H, world, rank)
-    l0 = layers[0][0]
-    th, ch = l0.tables
-    sub = pq.DecodeLayer(keys=l0.keys[hr.start:hr.stop], values=l0.values[hr.start:hr.stop],
-                         centroids=l0.centroids[hr.start:hr.stop], codes=l0.codes[hr.start:hr.stop], total=S,
-                         n_init=N_INIT, n_local=N_LOCAL, b=B, tables=(th[hr.start:hr.stop], ch[hr.start:hr.stop]))
+    subs = []
+    for l0 in layers:
+        th, ch = l0.tables
+        subs.append(pq.DecodeLayer(keys=l0.keys[hr.start:hr.stop], values=l0.values[hr.start:hr.stop],
+                                   centroids=l0.centroids[hr.start:hr.stop], codes=l0.codes[hr.start:hr.stop],
+                                   total=S, n_init=N_INIT, n_local=N_LOCAL, b=B,
+                                   tables=(th[hr.start:hr.stop], ch[hr.start:hr.stop])))
     qsub = [queries[i][hr.start:hr.stop].contiguous() for i in range(N_LAYERS)]
     for i in range(3):
-        shard.gather_heads(ctx.decode(sub, qsub[i % N_LAYERS], K_SEL), H)
+        shard.gather_heads(ctx.decode(subs[i % N_LAYERS], qsub[i % N_LAYERS], K_SEL), H)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -376,17 +452,40 @@ def main():
     hs_steps = max(20, min(args.steps, 200))
     hs0.record(stream)
     for i in range(hs_steps):
-        full = shard.gather_heads(ctx.decode(sub, qsub[i % N_LAYERS], K_SEL), H)
+        full = shard.gather_heads(ctx.decode(subs[i % N_LAYERS], qsub[i % N_LAYERS], K_SEL), H)
     hs1.record(stream)
     torch.cuda.synchronize()
     hs_us = shard.max_over_ranks(hs0.elapsed_time(hs1) * 1e3 / hs_steps, dev)
     assert full.shape[0] == H
+    del subs, qsub
+
+    # ---- the other BASELINE configs, device-timed (rotating layers) ----
+    peak, peak_kind = peaks()
+    extra = {}
+    if not args.no_extra:
+        for name in ("cfg1", "cfg2", "cfg3_layer", "cfg5_per_gpu"):
+            c = CONFIGS[name]
+            made = [make_layer(ctx, name, "gaussian", seed=5000 + 1000 * rank + li) for li in range(c["layers"])]
+            ls = [m_[0] for m_ in made]
+            qx = [made[i % len(made)][1] + sigma * torch.randn(made[0][1].shape, generator=gq, device=dev)
+                  for i in range(len(made) * 4)]
+            kx = cfg_k(c)
+            n_steps = max(20, min(args.steps, 200))
+            ms_x = time_steps(ctx, ls, qx, kx, max(3, args.warmup), n_steps, dist, dev)
+            us = ms_x * 1e3 / n_steps
+            byts = cfg_bytes(c)
+            extra[name] = {"what": c["what"], "us_per_layer": us, "algorithmic_bytes": byts,
+                           "gbs": byts / (us * 1e-6) / 1e9, "frac": byts / (us * 1e-6) / 1e9 / peak,
+                           "k": kx, "build_s_per_layer": float(np.median([m_[2] for m_ in made])),
+                           "plan": ctx.decode_plan(ls[0], c["g"], kx), "steps": n_steps,
+                           "layers_rotated": len(ls)}
+            del made, ls, qx
+            torch.cuda.empty_cache()
 
     # ---- numbers ----
     # The step is ONE launch of attend_kernel (pair select + classification +
     # gather + softmax + combine fused), so the dominant
     # kernel's average launch duration is the device-timed step itself.
-    peak, peak_kind = peaks()
     layer_bytes = algorithmic_bytes_per_layer()
     achieved = layer_bytes / (ms_per_step * 1e-3) / 1e9
     attend_bytes = attend_bytes_per_launch()
@@ -399,7 +498,7 @@ def main():
         except Exception:
             traffic = None
     build_layer_s = float(np.median(build_s))
-    launches_per_step = layers[0][0].launches(G)
+    launches_per_step = layers[0].launches(G)
     line = {
         "metric": METRIC, "value": us_per_layer, "unit": "us/layer", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -408,26 +507,29 @@ def main():
         "config": {"workload": WORKLOAD, "global_batch": 1, "seq_len": S, "heads": H, "head_dim": DH,
                    "m": M, "b": B, "k": K_SEL, "n_init": N_INIT, "n_local": N_LOCAL,
                    "layers_rotated": N_LAYERS, "parallelism": f"dp{world} (independent layers per GPU)",
-                   "l2": "inputs larger than L2: 8 rotating layers x 4.3 GB K/V (+26 MB codes and pair tables each: 206 MB > L2), 0.86 GB gathered per step"},
+                   "key_distributions": {kd: timed[kd] * 1e3 / (args.steps * world) for kd in timed},
+                   "value_is": f"the slower distribution ({worst}); each timed over its own {args.steps} steps",
+                   "plan": plan,
+                   "l2": "inputs larger than L2: 8 rotating layers x 4.3 GB K/V per distribution (+26 MB codes "
+                         "and pair tables each: 206 MB > L2), 0.86 GB gathered per step"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "attend_kernel<1> pair mode (the whole fused decode step, 1 launch/layer)",
+                     "kernel": "attend_kernel<1,3> pair mode (the whole fused decode step, 1 launch/layer)",
                      "kernel_ms": ms_per_step, "algorithmic_bytes": layer_bytes,
                      "bytes_basis": "SURVEY 8(d): h_kv*(s_mid*m*b/8 + C*d_h*4 + T_att*d_h*4*2 + 2*g*d_h*4)"},
         "attend_only": {"kernel": "attend_kernel bitmap mode (gather + softmax + combine, selection precomputed)",
                         "ms": attend_ms, "gbs": attend_only_gbs, "frac": attend_only_gbs / peak,
                         "bytes": attend_bytes, "select_ms": select_ms},
         "e2e": {"value": e2e_us, "unit": "us/layer", "h2d_bytes_per_step": H * G * DH * 4,
-                "d2h_bytes_per_step": H * G * DH * 4},
-        "gpu_launches": launches_per_step * args.steps,
+                "d2h_bytes_per_step": H * G * DH * 4, "api": "pqkv_decode_host (C ABI, pinned host buffers)"},
+        "gpu_launches": launches_per_step * args.steps * 2,
+        "configs": extra,
         "head_sharded": {"config": "cfg4: one layer's 32 heads split over the ranks, per-head outputs "
-                                   "all-gathered (NCCL all_gather_into_tensor) every step",
-                         "us_per_layer": hs_us, "heads_per_rank": len(hr), "steps": hs_steps,
-                         "note": "device-timed, max over ranks; the same K/V layer every step (L2-warm rows "
-                                 "possible at high rank counts)"},
+                                   "all-gathered (NCCL all_gather_into_tensor) every step, 8 rotating layers",
+                         "us_per_layer": hs_us, "heads_per_rank": len(hr), "steps": hs_steps},
         "build": {"layer_s": build_layer_s, "key_vectors_per_s": H * S_MID / build_layer_s,
                   "context_tokens_per_s": S_MID / build_layer_s, "layers": N_LAYERS,
-                  "fp64_rechecked_points": rech, "points": tot,
+                  "fp64_rechecked_points": rech_tot[0], "points": rech_tot[1],
                   # W = (T+2) s C d_h 3 fp64 ops per head for the reference's
                   # exact algorithm; the certified fp32 filter skips most of them, so the
                   # reference-equivalent rate exceeds the FP64 pipe (18.11 T op/s measured,
@@ -439,8 +541,14 @@ def main():
     clk.stop()
     line["clocks"] = clk.summary()
     if rank == 0 and not args.no_cpu_baseline:
-        gpu_out = ctx.decode(layers[0][0], layers[0][1], K_SEL)  # layer 0, base queries
-        dec, bld = cpu_baseline_leg(keep0[0], keep0[1], keep0[2], torch, gpu_out)
+        gl, gqs, _ = heads["gaussian"]
+        words = torch.zeros((H, (S_MID + 31) // 32), dtype=torch.int32, device=dev)
+        ctx.set_selection_dump(words)
+        try:
+            gpu_out = ctx.decode(gl[0], gqs[0], K_SEL)  # layer 0, base queries
+        finally:
+            ctx.set_selection_dump(None)
+        dec, bld = cpu_baseline_leg(gl[0], gqs[0], gpu_out, words)
         line["cpu_baseline"] = dec
         line["cpu_baseline_build"] = bld
     if rank == 0:

@@ -302,6 +302,32 @@ PQKV_API int pqkv_gen_workload(pqkv_ctx* ctx, int kind, size_t s, size_t d_h, si
  * gpu_launches accounting). */
 PQKV_API int pqkv_decode_launches(const pqkv_layer* layer, size_t g, int with_ids);
 
+/* The launch plan pqkv_decode picks for this layer, g, k (on ctx's device):
+ * which fused mode runs, how the middle tokens are split over attention CTAs
+ * and how those CTAs are grouped.  Used by tests to pin a parity case to the
+ * exact geometry a benchmark runs, and by tools for reporting. */
+enum {
+    PQKV_MODE_PAIRS_FUSED = 1, /* m == 2, b <= 6 + pair tables: select fused into the attention (1 launch) */
+    PQKV_MODE_KEYS_FUSED = 2,  /* per-token ADC keys, cluster radix select fused into the attention */
+    PQKV_MODE_KEYS_SPLIT = 3,  /* cluster key select -> bitmap, then a bitmap-mode attention launch */
+    PQKV_MODE_PAIRS_SPLIT = 4, /* pair select launch -> attention classifies its codes */
+    PQKV_MODE_BITMAP = 5,      /* separate select (+ ordered ids) -> bitmap-mode attention */
+    PQKV_MODE_GENERIC = 6      /* d_h != 128 or g not in {1,2,4}: row lists + the fp64 kernels */
+};
+typedef struct {
+    int mode;               /* PQKV_MODE_* */
+    int launches;           /* kernels per call (pqkv_decode_launches) */
+    int chunk_tokens;       /* middle tokens per attention CTA (fused / bitmap modes) */
+    int ctas_per_head;      /* attention CTAs per head (after cluster padding) */
+    int cluster;            /* CTAs per thread-block cluster of the attention launch */
+    int staged;             /* pair modes: the CTA's codes are staged in shared memory */
+    int window;             /* selected rows expanded per gather window (== chunk_tokens: one window) */
+    int ring_depth;         /* g > 1: rows in flight per gather slot */
+    size_t smem_bytes;      /* dynamic shared memory per attention CTA */
+} pqkv_decode_plan_t;
+PQKV_API int pqkv_decode_plan(pqkv_ctx* ctx, const pqkv_layer* layer, size_t g, size_t k, int with_ids,
+                              pqkv_decode_plan_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,17 @@ class pqkv_layer(C.Structure):
     ]
 
 
+class pqkv_decode_plan_t(C.Structure):
+    """Mirror of pqkv_decode_plan_t (pqkv_c.h)."""
+
+    _fields_ = [
+        ("mode", _i), ("launches", _i), ("chunk_tokens", _i), ("ctas_per_head", _i), ("cluster", _i),
+        ("staged", _i), ("window", _i), ("ring_depth", _i), ("smem_bytes", _sz),
+    ]
+
+
+PLAN_MODES = {1: "pairs_fused", 2: "keys_fused", 3: "keys_split", 4: "pairs_split", 5: "bitmap", 6: "generic"}
+
 _SIGS = {
     "pqkv_abi_version": (_i, []),
     "pqkv_last_error": (C.c_char_p, []),
@@ -76,6 +87,7 @@ _SIGS = {
     "pqkv_decode_attend": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _vp, _vp, _vp]),
     "pqkv_decode_host": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp]),
     "pqkv_decode_launches": (_i, [C.POINTER(pqkv_layer), _sz, _i]),
+    "pqkv_decode_plan": (_i, [_vp, C.POINTER(pqkv_layer), _sz, _sz, _i, C.POINTER(pqkv_decode_plan_t)]),
 }
 
 _lib = None
@@ -326,6 +338,15 @@ class Context:
         _check(lib().pqkv_decode(self.h, layer.ref(), _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
         return (out, ids[:, :k]) if want_ids else out
 
+    def decode_plan(self, layer: "DecodeLayer", g: int, k: int, want_ids: bool = False) -> dict:
+        """The launch plan pqkv_decode picks for this layer / g / k (pqkv_decode_plan)."""
+        out = pqkv_decode_plan_t()
+        L = layer.struct()
+        _check(lib().pqkv_decode_plan(self.h, C.byref(L), g, k, int(want_ids), C.byref(out)))
+        d = {name: getattr(out, name) for name, _ in pqkv_decode_plan_t._fields_}
+        d["mode"] = PLAN_MODES.get(d["mode"], d["mode"])
+        return d
+
     def decode_step(self, layer: "DecodeLayer", new_keys, new_values, queries, k: int, want_ids: bool = False):
         """One e2e step (evict_local_append + decode, pqkv_decode_step): new_keys /
         new_values [P][d_h] become token layer.total; layer.total grows by one."""
@@ -335,9 +356,11 @@ class Context:
         out = torch.empty((P, g, d_h), dtype=torch.float32, device=queries.device)
         ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device) if want_ids else None
         L = layer.struct()
-        _check(lib().pqkv_decode_step(self.h, C.byref(L), layer.codes.shape[1], _ptr(new_keys), _ptr(new_values),
-                                      _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
-        layer.total = L.total
+        try:
+            _check(lib().pqkv_decode_step(self.h, C.byref(L), layer.codes.shape[1], _ptr(new_keys),
+                                          _ptr(new_values), _ptr(queries), g, k, _ptr(out), _ptr(ids), _stream()))
+        finally:
+            layer.total = L.total  # the C side grows total only once the token is appended
         return (out, ids[:, :k]) if want_ids else out
 
     def gen_workload(self, s: int, d_h: int = 128, h_kv: int = 1, g: int = 1, kind: str = "gaussian",

@@ -1274,7 +1274,9 @@ static void launch_attend_g(const AtArgs& a, dim3 grid, size_t smem, int cl, cud
     else launch_attend_gm<G, 0>(a, grid, smem, cl, st);
 }
 
-static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cudaStream_t st) {
+// Cluster size and dynamic shared memory of an attention launch; pads
+// a.n_chunks to a multiple of the cluster.
+static int plan_attend_launch(AtArgs& a, int G, size_t* smem) {
     // pair-select mode: 8-CTA clusters share one pair select (pad the chunk
     // count to a multiple of the cluster; padded CTAs own empty ranges)
     int cl = 1;
@@ -1283,6 +1285,13 @@ static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cuda
         a.n_chunks = (int)round_up((size_t)a.n_chunks, (size_t)cl);
     }
     if (a.src == SRC_KEYS) cl = a.n_chunks;  // one cluster per head (<= 16 CTAs)
+    *smem = attend_smem(a, G);
+    return cl;
+}
+
+static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cudaStream_t st) {
+    size_t smem = 0;
+    const int cl = plan_attend_launch(a, G, &smem);
     Scratch sc(ctx);
     size_t h_part = sc.plan<float>(P * a.n_chunks * G * (DH + 2));
     sc.commit();
@@ -1297,7 +1306,6 @@ static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cuda
         PQKV_CUDA(cudaMemsetAsync(ctx->d_prof, 0, ctx->n_prof * PQKV_PROF_SLOTS * sizeof(unsigned long long), st));
         a.prof = ctx->d_prof;
     }
-    size_t smem = attend_smem(a, G);
     dim3 grid((unsigned)a.n_chunks, (unsigned)P);
     switch (G) {
         case 1: launch_attend_g<1>(a, grid, smem, cl, st); break;
@@ -1375,13 +1383,7 @@ bool decode_keys_split(const pqkv_layer& L, size_t G) {
     if (G > 1) return true;
     int chunk = 0, n_chunks = 0;
     if (!keys_geometry(L, G, &chunk, &n_chunks)) return false;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-            sms = 148;
-    }
+    const int sms = current_sm_count();
     const size_t ctas = L.n_heads * (size_t)n_chunks;
     const size_t C = (size_t)1 << L.b;
     const size_t smem = (size_t)chunk * 4 + L.m * C * 8 + (size_t)chunk / 32 * 4 + (size_t)NB * 12 + 3072;
@@ -1389,30 +1391,26 @@ bool decode_keys_split(const pqkv_layer& L, size_t G) {
     return ctas < 2 * (size_t)sms || ctas > per_sm * (size_t)sms;
 }
 
-void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
-                          const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
-                          cudaStream_t st, size_t k_pairs, size_t k_keys) {
-    bind_device(ctx);
+// AtArgs of a decode attention launch (everything but queries, out and the
+// selection inputs).
+static void decode_args(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_pairs, size_t k_keys, bool bitmap,
+                        bool tuple_cls, AtArgs& a) {
     const size_t s_mid = L.total - L.n_init - L.n_local;
-    AtArgs a{};
-    a.queries = queries;
     a.keys = L.keys;
     a.values = L.values;
     a.kv_head_stride = (long long)L.kv_head_stride;
-    a.src = k_keys ? SRC_KEYS : (k_pairs ? SRC_PAIRS : (cls ? SRC_TUPLE : SRC_BITMAP));
+    a.src = k_keys ? SRC_KEYS : (k_pairs ? SRC_PAIRS : (tuple_cls ? SRC_TUPLE : SRC_BITMAP));
+    (void)bitmap;
     a.n_init = (int)L.n_init;
     a.n_local = (int)L.n_local;
     a.total = (int)L.total;
     a.s_mid = (int)s_mid;
     a.chunk = plan_chunk_tokens(ctx, L.n_heads, G, s_mid);
     a.n_chunks = (int)std::max<size_t>(1, ceil_div(s_mid, (size_t)a.chunk));
-    a.bitmap = bitmap;
     a.words = (int)ceil_div(s_mid, 32);
     a.codes = L.codes;
     a.codes_head_stride = (long long)L.codes_head_stride;
     a.C = 1 << L.b;
-    a.cls = cls;
-    a.cut = cut;
     a.centroids = L.centroids;
     a.thist = L.tuple_hist;
     a.chist = L.tuple_chunk_hist;
@@ -1421,18 +1419,43 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     a.k = (int)(k_keys ? k_keys : k_pairs);
     a.m = (int)L.m;
     a.sel_only = nullptr;
-    if (k_keys) {
-        keys_geometry(L, G, &a.chunk, &a.n_chunks);
-        // g > 1 (1 CTA/SM per key cluster): select in one launch, gather in a
-        // second bitmap-mode launch with its own (finer) chunking
-        if (bitmap && decode_keys_split(L, G)) {
-            a.sel_only = const_cast<uint32_t*>(bitmap);
-            launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);
-            launch_decode_attend(ctx, L, queries, G, bitmap, nullptr, nullptr, out, st, 0, 0);
-            return;
-        }
-    }
+    if (k_keys) keys_geometry(L, G, &a.chunk, &a.n_chunks);
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
+}
+
+void plan_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_pairs, size_t k_keys,
+                        bool tuple_cls, pqkv_decode_plan_t* out) {
+    AtArgs a{};
+    decode_args(ctx, L, G, k_pairs, k_keys, !k_pairs && !tuple_cls, tuple_cls, a);
+    size_t smem = 0;
+    const int cl = plan_attend_launch(a, (int)G, &smem);
+    out->chunk_tokens = a.chunk;
+    out->ctas_per_head = a.n_chunks;
+    out->cluster = cl;
+    out->staged = (a.src == SRC_PAIRS || a.src == SRC_TUPLE) ? a.stage : 0;
+    out->window = a.win;
+    out->ring_depth = (G > 1 && a.src != SRC_KEYS) ? (a.ring4 ? 4 : 2) : 0;
+    out->smem_bytes = smem;
+}
+
+void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
+                          const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
+                          cudaStream_t st, size_t k_pairs, size_t k_keys) {
+    bind_device(ctx);
+    AtArgs a{};
+    decode_args(ctx, L, G, k_pairs, k_keys, bitmap != nullptr, cls != nullptr, a);
+    a.queries = queries;
+    a.bitmap = bitmap;
+    a.cls = cls;
+    a.cut = cut;
+    // g > 1 (1 CTA/SM per key cluster): select in one launch, gather in a
+    // second bitmap-mode launch with its own (finer) chunking
+    if (k_keys && bitmap && decode_keys_split(L, G)) {
+        a.sel_only = const_cast<uint32_t*>(bitmap);
+        launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);
+        launch_decode_attend(ctx, L, queries, G, bitmap, nullptr, nullptr, out, st, 0, 0);
+        return;
+    }
     a.out = out;
     launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);
 }

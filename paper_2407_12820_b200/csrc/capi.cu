@@ -231,6 +231,25 @@ static void check_layer(const pqkv_layer* L, size_t g, size_t k) {
     if (L->total > 0x7fffffff) fail(PQKV_EINVAL, "decode: context too long");
 }
 
+// The path pqkv_decode takes for a layer (pqkv_decode_plan reports it).
+static int decode_mode(const pqkv_layer& L, size_t g, size_t k, bool with_ids) {
+    const size_t s_mid = L.total - L.n_init - L.n_local;
+    const bool tup = tuple_ok(L.m, L.b, L.tuple_hist, L.tuple_chunk_hist, s_mid);
+    const bool fast = decode_fast_path(L, g);
+    if (!fast) return PQKV_MODE_GENERIC;
+    if (with_ids || k == 0) return PQKV_MODE_BITMAP;
+    // one launch: every attention CTA selects its head's pairs, then
+    // classifies its own codes and gathers
+    if (tup && decode_pairs_fused(L, g)) return PQKV_MODE_PAIRS_FUSED;
+    // per-head cluster computes ADC keys and radix-selects through DSMEM,
+    // then gathers (same launch, or a second finer bitmap-mode launch)
+    if (!(tup && L.b <= 6) && decode_keys_fused(L, g))
+        return decode_keys_split(L, g) ? PQKV_MODE_KEYS_SPLIT : PQKV_MODE_KEYS_FUSED;
+    // pair-level select launch -> attention classifies its own codes
+    if (tup) return PQKV_MODE_PAIRS_SPLIT;
+    return PQKV_MODE_BITMAP;
+}
+
 int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size_t g, size_t k,
                 float* d_out, int64_t* d_ids, void* stream) {
     return guard([&] {
@@ -241,7 +260,6 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         const size_t P = L->n_heads, s_mid = L->total - L->n_init - L->n_local;
         const size_t words = ceil_div(s_mid, 32), C = size_t{1} << L->b;
         const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist, s_mid);
-        const bool fast = decode_fast_path(*L, g);
         SelectSource src;
         src.queries = d_queries;
         src.g = g;
@@ -252,37 +270,37 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         src.codes = L->codes;
         src.codes_head_stride = L->codes_head_stride;
         src.tuple_chunk_stride = L->tuple_chunks;
-        if (tup && fast && !d_ids && k > 0 && decode_pairs_fused(*L, g)) {
-            // one launch: every attention CTA selects its head's pairs, then
-            // classifies its own codes and gathers
-            launch_decode_attend(ctx, *L, d_queries, g, nullptr, nullptr, nullptr, d_out, st, k);
-            return;
-        }
-        if (fast && !d_ids && k > 0 && !(tup && L->b <= 6) && decode_keys_fused(*L, g)) {
-            // per-head cluster computes ADC keys and radix-selects through
-            // DSMEM, then gathers (g = 1: same launch; g > 1: the selection
-            // bitmap feeds a second, finer-grained attention launch)
-            uint32_t* bm = decode_keys_split(*L, g) ? static_cast<uint32_t*>(decode_workspace(ctx, P * words * 4))
-                                                    : nullptr;
-            launch_decode_attend(ctx, *L, d_queries, g, bm, nullptr, nullptr, d_out, st, 0, k);
-            return;
-        }
-        if (tup && fast && !d_ids && k > 0) {
-            // pair-level select -> attention classifies its own codes
-            char* ws = static_cast<char*>(decode_workspace(ctx, round_up(P * C * C, 256) + P * 2 * sizeof(int)));
-            uint8_t* cls = reinterpret_cast<uint8_t*>(ws);
-            int* cut = reinterpret_cast<int*>(ws + round_up(P * C * C, 256));
-            launch_tuple_select(ctx, src, L->tuple_hist, L->tuple_chunk_hist, P, s_mid, k, cls, cut, nullptr,
-                                nullptr, st);
-            launch_decode_attend(ctx, *L, d_queries, g, nullptr, cls, cut, d_out, st);
-            return;
+        const int mode = decode_mode(*L, g, k, d_ids != nullptr);
+        switch (mode) {
+            case PQKV_MODE_PAIRS_FUSED:
+                launch_decode_attend(ctx, *L, d_queries, g, nullptr, nullptr, nullptr, d_out, st, k);
+                return;
+            case PQKV_MODE_KEYS_FUSED:
+            case PQKV_MODE_KEYS_SPLIT: {
+                uint32_t* bm = mode == PQKV_MODE_KEYS_SPLIT
+                                   ? static_cast<uint32_t*>(decode_workspace(ctx, P * words * 4))
+                                   : nullptr;
+                launch_decode_attend(ctx, *L, d_queries, g, bm, nullptr, nullptr, d_out, st, 0, k);
+                return;
+            }
+            case PQKV_MODE_PAIRS_SPLIT: {
+                char* ws = static_cast<char*>(decode_workspace(ctx, round_up(P * C * C, 256) + P * 2 * sizeof(int)));
+                uint8_t* cls = reinterpret_cast<uint8_t*>(ws);
+                int* cut = reinterpret_cast<int*>(ws + round_up(P * C * C, 256));
+                launch_tuple_select(ctx, src, L->tuple_hist, L->tuple_chunk_hist, P, s_mid, k, cls, cut, nullptr,
+                                    nullptr, st);
+                launch_decode_attend(ctx, *L, d_queries, g, nullptr, cls, cut, d_out, st);
+                return;
+            }
+            default:
+                break;
         }
         uint32_t* bm = static_cast<uint32_t*>(decode_workspace(ctx, P * words * 4));
         if (tup)
             launch_select_tuple(ctx, src, L->tuple_hist, L->tuple_chunk_hist, P, s_mid, k, bm, d_ids, st, nullptr);
         else
             launch_select(ctx, src, P, s_mid, k, bm, d_ids, st, nullptr);
-        if (fast) {
+        if (mode == PQKV_MODE_BITMAP) {
             launch_decode_attend(ctx, *L, d_queries, g, bm, nullptr, nullptr, d_out, st);
             return;
         }
@@ -293,6 +311,26 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         launch_bitmap_rows(ctx, bm, P, words, L->n_init, L->n_local, L->total, T, rows, st);
         launch_exact(ctx, d_queries, P, g, L->d_h, L->keys, L->values, L->kv_head_stride, rows, T, d_out, st);
         PQKV_CUDA(cudaFreeAsync(rows, st));
+    });
+}
+
+int pqkv_decode_plan(pqkv_ctx* ctx, const pqkv_layer* L, size_t g, size_t k, int with_ids,
+                     pqkv_decode_plan_t* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!out) fail(PQKV_EINVAL, "decode_plan: out is NULL");
+        check_layer(L, g, k);
+        *out = pqkv_decode_plan_t{};
+        out->mode = decode_mode(*L, g, k, with_ids != 0);
+        out->launches = pqkv_decode_launches(L, g, with_ids);
+        switch (out->mode) {
+            case PQKV_MODE_PAIRS_FUSED: plan_decode_attend(ctx, *L, g, k, 0, false, out); break;
+            case PQKV_MODE_KEYS_FUSED: plan_decode_attend(ctx, *L, g, 0, k, false, out); break;
+            case PQKV_MODE_PAIRS_SPLIT: plan_decode_attend(ctx, *L, g, 0, 0, true, out); break;
+            case PQKV_MODE_KEYS_SPLIT:
+            case PQKV_MODE_BITMAP: plan_decode_attend(ctx, *L, g, 0, 0, false, out); break;
+            default: break;
+        }
     });
 }
 
@@ -312,6 +350,12 @@ int pqkv_decode_step(pqkv_ctx* ctx, pqkv_layer* L, size_t codes_cap, const float
         if (L->m == 2 && L->tuple_hist && L->tuple_chunk_hist &&
             L->tuple_chunks < ceil_div(s_mid + 1, PQKV_TUPLE_CHUNK))
             fail(PQKV_EINVAL, "decode_step: tuple_chunks must cover the grown middle segment");
+        // everything pqkv_decode will check on the grown layer is checked
+        // here, before evict_append mutates the cache, the codes and the pair
+        // tables: a rejected step leaves the device state untouched
+        pqkv_layer grown = *L;
+        grown.total += 1;
+        check_layer(&grown, g, k);
         if (L->n_heads == 0) return;
         launch_evict_append(ctx, *L, d_new_keys, d_new_values, as_stream(stream));
     });
@@ -360,13 +404,7 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
         check_layer(L, g, k);
         cudaStream_t st = as_stream(stream);
         const size_t qbytes = L->n_heads * g * L->d_h * sizeof(float);
-        static thread_local float* dq = nullptr;
-        static thread_local size_t dq_bytes = 0;
-        if (2 * qbytes > dq_bytes) {
-            if (dq) { cudaStreamSynchronize(st); cudaFree(dq); }
-            dq_bytes = 2 * qbytes;
-            PQKV_CUDA(cudaMalloc(&dq, dq_bytes));
-        }
+        float* dq = static_cast<float*>(host_io_staging(ctx, 2 * qbytes));
         float* d_q = dq;
         float* d_o = dq + L->n_heads * g * L->d_h;
         // page-locked, device-mapped output buffer (cudaHostAlloc / pinned
@@ -390,16 +428,16 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
 }
 
 int pqkv_decode_launches(const pqkv_layer* L, size_t g, int with_ids) {
-    if (!L) return 0;
-    bool fast = L->d_h == 128 && (g == 1 || g == 2 || g == 4) && L->kv_head_stride % 4 == 0;
+    if (!L || L->total < L->n_init + L->n_local) return 0;
     const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist, L->total - L->n_init - L->n_local);
-    if (tup && fast && !with_ids && L->b <= 6) return 1;       // pair select fused into the attention
-    if (fast && !with_ids && decode_keys_fused(*L, g)) return decode_keys_split(*L, g) ? 2 : 1;  // key select [+] attention
-    if (tup && fast && !with_ids) return 2;                     // pair select + attention
-    int n = tup ? 2 /*pair select + bitmap*/ : 1 /*cluster select*/;
-    n += with_ids ? 1 : 0 /*sort*/;
-    n += fast ? 1 /*attend with fused combine*/ : 3 /*rows + scores + softmax*/;
-    return n;
+    switch (decode_mode(*L, g, 1, with_ids != 0)) {
+        case PQKV_MODE_PAIRS_FUSED:
+        case PQKV_MODE_KEYS_FUSED: return 1;
+        case PQKV_MODE_KEYS_SPLIT:
+        case PQKV_MODE_PAIRS_SPLIT: return 2;
+        case PQKV_MODE_BITMAP: return (tup ? 2 : 1) + (with_ids ? 1 : 0) + 1;
+        default: return (tup ? 2 : 1) + (with_ids ? 1 : 0) + 3;
+    }
 }
 
 }  // extern "C"

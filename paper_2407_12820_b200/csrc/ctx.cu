@@ -1,6 +1,7 @@
 // ctx.cu -- context, scratch arena, status plumbing and the geometry entry
 // points of the C ABI (include/pqkv_c.h).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -64,6 +65,34 @@ void* decode_workspace(pqkv_ctx* ctx, size_t bytes) {
     return ctx->ws;
 }
 
+void* host_io_staging(pqkv_ctx* ctx, size_t bytes) {
+    if (bytes > ctx->io_bytes) {
+        if (ctx->io) {
+            PQKV_CUDA(cudaDeviceSynchronize());
+            PQKV_CUDA(cudaFree(ctx->io));
+            ctx->io = nullptr;
+            ctx->io_bytes = 0;
+        }
+        size_t want = round_up(bytes, size_t(1) << 12);
+        PQKV_CUDA(cudaMalloc(&ctx->io, want));
+        ctx->io_bytes = want;
+    }
+    return ctx->io;
+}
+
+int current_sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    std::atomic<int>& slot = cache[dev & 63];
+    int v = slot.load(std::memory_order_relaxed);
+    if (v <= 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        slot.store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
 unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st) {
     if (n > ctx->n_arrivals) {
         if (ctx->d_arrivals) {
@@ -113,6 +142,7 @@ int pqkv_ctx_destroy(pqkv_ctx* ctx) {
         if (ctx->d_stats) cudaFree(ctx->d_stats);
         if (ctx->d_arrivals) cudaFree(ctx->d_arrivals);
         if (ctx->ws) cudaFree(ctx->ws);
+        if (ctx->io) cudaFree(ctx->io);
         if (ctx->d_prof) cudaFree(ctx->d_prof);
         delete ctx;
     });

@@ -31,6 +31,9 @@ struct pqkv_ctx {
     // Decode workspace (selection bitmap / pair classes between kernels).
     void* ws = nullptr;
     size_t ws_bytes = 0;
+    // Device staging of pqkv_decode_host (queries in, outputs out).
+    void* io = nullptr;
+    size_t io_bytes = 0;
     // Device counters written by the build kernels (rechecked, total).
     unsigned long long* d_stats = nullptr;
     uint64_t last_rechecked = 0, last_total = 0;
@@ -84,6 +87,11 @@ int guard(F&& f) {
     }
 }
 void* pinned_staging(pqkv_ctx* ctx, size_t bytes);
+// Device staging owned by the context (never aliases the arena or the decode
+// workspace); grown on demand after synchronizing the context's device.
+void* host_io_staging(pqkv_ctx* ctx, size_t bytes);
+// Multiprocessor count of the current device (cached per device id).
+int current_sm_count();
 unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st);
 
 // ---- launchers implemented in the kernel translation units -----------------
@@ -170,6 +178,10 @@ bool decode_keys_split(const pqkv_layer& L, size_t g);
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t g,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
                           cudaStream_t stream, size_t k_pairs = 0, size_t k_keys = 0);
+// Geometry of the attention launch launch_decode_attend would make (chunk,
+// CTAs per head, cluster, staging, window, ring depth, shared memory).
+void plan_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, size_t g, size_t k_pairs, size_t k_keys,
+                        bool tuple_cls, pqkv_decode_plan_t* out);
 // Pair-level select only (writes cls [rows][C*C], cut [rows][2]).
 void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
                          const uint16_t* chist, size_t rows, size_t n, size_t k, uint8_t* cls, int* cut,

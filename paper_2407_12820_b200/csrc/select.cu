@@ -581,8 +581,23 @@ bool launch_select(pqkv_ctx* ctx, const SelectSource& src, size_t rows, size_t n
     }
     if (n > 0x7fffffff) fail(PQKV_EINVAL, "select: too many tokens");
     const bool adc = src.codes != nullptr;
-    if (adc && src.m * src.C * 8 > 64 * 1024)
-        fail(PQKV_EINVAL, "select: fused ADC search needs m * 2^b <= 8192 (use pqkv_pq_score + pqkv_topk)");
+    if (adc && src.m * src.C * 8 > 64 * 1024) {
+        // ADC table beyond shared memory (b >= 13 at m = 1..2, PqConfig allows
+        // b <= 16): materialize the scores (gather_scores_kernel reads the
+        // table from global memory), then select over them -- same keys, same
+        // tie rule, two launches more.
+        float* scores = nullptr;
+        PQKV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scores), rows * n * sizeof(float), st));
+        launch_score(ctx, src.queries, rows, src.g, src.d_h, src.m, src.C, src.centroids, src.codes,
+                     src.codes_head_stride, n, scores, n, st);
+        SelectSource ss;
+        ss.scores = scores;
+        ss.scores_stride = n;
+        bool ok = launch_select(ctx, ss, rows, n, k, bitmap, ids, st, launches);
+        PQKV_CUDA(cudaFreeAsync(scores, st));
+        if (launches) *launches += 2;
+        return ok;
+    }
     const size_t slice = round_up(ceil_div(n, SEL_CL), 32);
     const size_t fixed = (4 * NB + 8 + 32 + 8) * 4 + (adc ? src.m * src.C * 8 : 0);
     int keys_smem = fixed + slice * 4 <= 200 * 1024;

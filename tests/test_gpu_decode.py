@@ -6,6 +6,7 @@ bit-exact; attention within 1e-3 relative on the fp32 fast path and within
 1e-6 (doctest-style mixed abs/rel, attention tests in the reference) on the
 fp64 path."""
 import numpy as np
+from _util import rel_err
 import pytest
 
 import oracle
@@ -168,8 +169,7 @@ def test_fused_search_ragged_and_large(ctx, orc):
             assert np.array_equal(ids[h].astype(np.uint64), want)
 
 
-def _rel(got, want):
-    return np.abs(got - want).max() / max(1.0, np.abs(want).max())
+_rel = rel_err
 
 
 @pytest.mark.parametrize("d_h,t,g", [(8, 50, 1), (128, 1000, 1), (128, 5000, 4), (6, 30, 3), (64, 300, 2)])

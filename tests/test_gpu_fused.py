@@ -6,6 +6,7 @@ pqkv_ctx_set_selection_dump) must equal the oracle's approx_topk set exactly
 (topk.cpp tie rule), and the output must match selective_attention within
 1e-3 relative (north star)."""
 import numpy as np
+from _util import rel_err
 import pytest
 
 import oracle
@@ -13,8 +14,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def _rel(got, want):
-    return np.abs(got - want).max() / max(1.0, np.abs(want).max())
+_rel = rel_err
 
 
 def _run(ctx, orc, cen, codes, keys, vals, qs, b, n_init, n_local, k, tables):

@@ -5,6 +5,7 @@ per-head loop (experiments.cpp:197-260), checked step by step against the
 oracle running the same sequence on the host.  Codes and selected ids
 bit-exact, attention within 1e-3 relative (north star)."""
 import numpy as np
+from _util import rel_err
 import pytest
 
 import oracle
@@ -12,8 +13,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def _rel(got, want):
-    return np.abs(got - want).max() / max(1.0, np.abs(want).max())
+_rel = rel_err
 
 
 @pytest.mark.parametrize("g,kind,tables,m,b", [(1, oracle.GAUSSIAN, True, 2, 6), (4, oracle.POWERLAW, True, 2, 6),
