@@ -9,7 +9,8 @@ CSRC := paper_2407_12820_b200/csrc
 OBJDIR ?= build/obj
 LIB ?= paper_2407_12820_b200/lib/libpqkv.so
 CU := ctx capi kmeans select attend step blocks workload
-OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(OBJDIR)/api.o
+CXXSRC := api kv_store_host pqt_io shape
+OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CXXSRC)))
 HDRS := include/pqkv_c.h $(CSRC)/common.cuh $(CSRC)/internal.cuh $(CSRC)/select_common.cuh
 
 .PHONY: all lib oracle clean
@@ -21,9 +22,10 @@ $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(OBJDIR)/api.o: $(CSRC)/api.cpp include/pqkv/pqkv.hpp include/pqkv_c.h
+CXXHDRS := $(wildcard include/pqkv/*.hpp) include/pqkv_c.h $(CSRC)/runtime_internal.hpp
+$(OBJDIR)/%.o: $(CSRC)/%.cpp $(CXXHDRS)
 	@mkdir -p $(OBJDIR)
-	g++ -std=c++20 -O2 -fPIC -fvisibility=hidden -Iinclude -c $< -o $@
+	g++ -std=c++20 -O2 -Wall -Wextra -fPIC -fvisibility=hidden -Iinclude -I$(CSRC) -c $< -o $@
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)

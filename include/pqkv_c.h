@@ -115,6 +115,11 @@ PQKV_API int pqkv_device_free(pqkv_ctx* ctx, void* ptr);
 /* kind: 0 host->device, 1 device->host, 2 device->device; synchronous. */
 PQKV_API int pqkv_copy(pqkv_ctx* ctx, void* dst, const void* src, size_t bytes, int kind);
 PQKV_API int pqkv_stream_sync(pqkv_ctx* ctx, void* stream);
+/* Row scatter into a token-indexed K/V buffer (host runtimes keep a device
+ * copy of a KV cache this way): row i of d_src_k / d_src_v (n x d_h) goes
+ * to token d_rows[i] of d_dst_k / d_dst_v (row t at + t*d_h). */
+PQKV_API int pqkv_scatter_rows(pqkv_ctx* ctx, const float* d_src_k, const float* d_src_v, const int64_t* d_rows,
+                               size_t n, size_t d_h, float* d_dst_k, float* d_dst_v, void* stream);
 
 /* ---- geometry: PqConfig::create (pq.cpp:13-25) ------------------------- */
 PQKV_API int pqkv_pq_config(size_t m, size_t b, size_t d_h, size_t* d_m, size_t* n_clusters);

@@ -107,6 +107,20 @@ unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st) {
     return ctx->d_arrivals;
 }
 
+namespace {
+
+__global__ void scatter_rows_kernel(const float* src_k, const float* src_v, const int64_t* rows, long long n, int d_h,
+                                    float* dst_k, float* dst_v) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * d_h;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / d_h, j = e % d_h, r = rows[i];
+        dst_k[r * d_h + j] = src_k[e];
+        dst_v[r * d_h + j] = src_v[e];
+    }
+}
+
+}  // namespace
+
 }  // namespace pqkv_dev
 
 using namespace pqkv_dev;
@@ -198,6 +212,21 @@ int pqkv_stream_sync(pqkv_ctx* ctx, void* stream) {
         if (!ctx) fail(PQKV_EINVAL, "pqkv_stream_sync: NULL context");
         bind_device(ctx);
         PQKV_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+    });
+}
+
+int pqkv_scatter_rows(pqkv_ctx* ctx, const float* d_src_k, const float* d_src_v, const int64_t* d_rows, size_t n,
+                      size_t d_h, float* d_dst_k, float* d_dst_v, void* stream) {
+    return guard([&] {
+        if (!ctx) fail(PQKV_EINVAL, "pqkv_scatter_rows: NULL context");
+        bind_device(ctx);
+        if (!n || !d_h) return;
+        if (!d_src_k || !d_src_v || !d_rows || !d_dst_k || !d_dst_v) fail(PQKV_EINVAL, "pqkv_scatter_rows: NULL buffer");
+        const size_t total = n * d_h;
+        const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(total, 256), 4 * (size_t)ctx->sm_count);
+        scatter_rows_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+            d_src_k, d_src_v, d_rows, (long long)n, (int)d_h, d_dst_k, d_dst_v);
+        PQKV_LAUNCHED("scatter_rows_kernel");
     });
 }
 

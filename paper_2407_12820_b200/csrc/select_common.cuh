@@ -75,8 +75,53 @@ __device__ __forceinline__ void lut_entry_multi(double* lut, const float* q, con
     lut[e] = t;
 }
 
+// lut_entry_vec / lut_entry_multi with the query rows already converted to
+// fp64 in shared memory (qd [g][d_h]): one F2F per product instead of two,
+// and the query loads leave the chain.  Same products, same order.
+template <int DM>
+__device__ __forceinline__ void lut_entry_qd(double* lut, const double* qd, const float* cen, int g, int d_h, int e,
+                                             int j) {
+    const float4* cc4 = reinterpret_cast<const float4*>(cen + (long long)e * DM);
+    float4 cv[DM / 4];
+#pragma unroll
+    for (int u = 0; u < DM / 4; ++u) cv[u] = __ldg(cc4 + u);
+    double t = 0.0;
+    for (int r0 = 0; r0 < g; r0 += 4) {
+        const int rn = min(4, g - r0);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < DM / 4; ++u) {
+            const double c0 = (double)cv[u].x, c1 = (double)cv[u].y, c2 = (double)cv[u].z, c3 = (double)cv[u].w;
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                if (rr < rn) {
+                    const double* qq = qd + (r0 + rr) * d_h + j * DM + 4 * u;
+                    acc[rr] = __fma_rn(qq[0], c0, acc[rr]);
+                    acc[rr] = __fma_rn(qq[1], c1, acc[rr]);
+                    acc[rr] = __fma_rn(qq[2], c2, acc[rr]);
+                    acc[rr] = __fma_rn(qq[3], c3, acc[rr]);
+                }
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+            if (rr < rn) t = __dadd_rn(t, acc[rr]);
+    }
+    lut[e] = t;
+}
+
 __device__ inline void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
-                          int C) {
+                          int C, double* qd_scratch = nullptr) {
+    if (qd_scratch && (d_h / m == 64 || d_h / m == 32) &&
+        ((reinterpret_cast<uintptr_t>(cen) & 15) == 0) && (d_h % 4) == 0) {
+        for (int i = threadIdx.x; i < g * d_h; i += blockDim.x) qd_scratch[i] = (double)__ldg(q + i);
+        __syncthreads();
+        for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
+            if (d_h / m == 64) lut_entry_qd<64>(lut, qd_scratch, cen, g, d_h, e, e / C);
+            else lut_entry_qd<32>(lut, qd_scratch, cen, g, d_h, e, e / C);
+        }
+        return;
+    }
     const int d_m = d_h / m;
     const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(cen)) & 15) == 0 &&
                          (d_h % 4) == 0;
@@ -209,7 +254,8 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
         const int t = tid + u * NT;
         w[u] = t < C2 ? __ldg(thist + t) : 0u;
     }
-    build_lut(lut, q, cen, g, d_h, 2, C);
+    // the query rows in fp64 go to hist[] (zeroed only after the compaction)
+    build_lut(lut, q, cen, g, d_h, 2, C, g * d_h * 8 <= NB * 4 ? reinterpret_cast<double*>(hist) : nullptr);
     for (int c = tid; c < n_chunks; c += NT) ceq[c] = 0;
     for (int e = tid; e < (C2 + 3) / 4; e += NT) reinterpret_cast<uint32_t*>(cls)[e] = 0u;
     PQKV_T(1);
@@ -289,17 +335,29 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
     for (int u = 0; u < WMAX; ++u)
         if (u < per && (it[u] & wmask)) alive |= 1u << u;
     double lo = (double)key_score(kmin), hi = (double)key_score(kmax);
+    // First pass over a same-sign score range: bins on the order-preserving
+    // key bits (the top 11 bits of key - kmin: about 1/100 of a binade per
+    // bin), which follow a heavy-tailed positive distribution (powerlaw keys:
+    // scores ~ 1/rank) where value bins would put the whole bulk in bin 0.
+    // Mixed-sign ranges (gaussian keys) bin by value: key bits would split
+    // them by sign and exponent only.  Later passes bin by value.
+    const bool key_bins = (lo > 0.0 && hi > 0.0) || (lo < 0.0 && hi < 0.0);
+    const int kshift = max(0, (32 - __clz((kmax - kmin) | 1u)) - 11);
     for (int pass = 0;; ++pass) {
         if (lo == hi) {  // every candidate has the same key
             kstar = score_key((float)lo);
             break;
         }
         const double scale = (double)NB / (hi - lo);
+        const bool kb = pass == 0 && key_bins;
+        auto bin_of = [&](uint32_t key) {
+            return kb ? (int)((key - kmin) >> kshift) : min(NB - 1, (int)(((double)key_score(key) - lo) * scale));
+        };
 #pragma unroll
         for (int u = 0; u < WMAX; ++u) {
             if (u >= per) break;
             if ((alive >> u) & 1u) {
-                const int b = min(NB - 1, (int)(((double)key_score(kr[u]) - lo) * scale));
+                const int b = bin_of(kr[u]);
                 atomicAdd(&hist[b], it[u] & wmask);
                 atomicAdd(&cnt[b], 1u);
             }
@@ -315,7 +373,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
             if (u >= per) break;
             if ((alive >> u) & 1u) {
                 const float f = key_score(kr[u]);
-                const int b = min(NB - 1, (int)(((double)f - lo) * scale));
+                const int b = bin_of(kr[u]);
                 if (b != bsel) alive &= ~(1u << u);
                 else { vmin = fminf(vmin, f); vmax = fmaxf(vmax, f); }
             }

@@ -1,7 +1,8 @@
-"""Profiling driver (run under ncu on one GPU): one north-star layer
-(32 heads x 128K, m2b6, k=26214), a few fused decodes plus the split
-select / attend calls.  Usage: python tools/prof_decode.py [reps] [heads] [s]"""
-import math
+"""Profiling driver (one GPU; run plain or under ncu): one layer of a bench
+config built exactly as bench.py does (bench.make_layer), a few fused decodes
+plus the split select / attend calls; with PQKV_PHASES=1 the per-CTA phase
+timeline of the fused kernel.
+Usage: python tools/prof_decode.py [config=northstar] [kind=gaussian] [reps=3]"""
 import os
 import sys
 
@@ -10,31 +11,19 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import bench  # noqa: E402
 import paper_2407_12820_b200 as pq  # noqa: E402
 
-reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-H = int(sys.argv[2]) if len(sys.argv) > 2 else 32
-S = int(sys.argv[3]) if len(sys.argv) > 3 else 131072
-DH, G, M, B, NI, NL = 128, 1, 2, 6, 4, 64
-K = round(S / 5)
-SM = S - NI - NL
-dev = torch.device("cuda", 0)
-g = torch.Generator(device=dev)
-g.manual_seed(1)
-keys = torch.empty((H, S, DH), device=dev)
-for h in range(H):
-    means = torch.randn((8, DH), generator=g, device=dev)
-    keys[h] = means[torch.randint(0, 8, (S,), generator=g, device=dev)] + 0.5 * torch.randn((S, DH), generator=g, device=dev)
-vals = torch.randn((H, S, DH), generator=g, device=dev)
-q = torch.randn((H, G, DH), generator=g, device=dev)
+name = sys.argv[1] if len(sys.argv) > 1 else "northstar"
+kind = sys.argv[2] if len(sys.argv) > 2 else "gaussian"
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+cfgd = bench.CONFIGS[name]
+G, B, K = cfgd["g"], cfgd["b"], bench.cfg_k(cfgd)
+SM = cfgd["s"] - bench.N_INIT - bench.N_LOCAL
 ctx = pq.Context(0)
-mode = os.environ.get("PQKV_BUILD", "filtered")
-if mode == "exact":
-    ctx.set_assign_mode(pq.ASSIGN_EXACT)
-cen, codes = ctx.pq_build(keys[:, NI:NI + SM].contiguous(), M, B, 10, list(range(H)))
-tables = ctx.tuple_tables(codes, B) if os.environ.get("PQKV_TUPLE", "1") == "1" else None
-layer = pq.DecodeLayer(keys=keys, values=vals, centroids=cen, codes=codes, total=S, n_init=NI, n_local=NL, b=B,
-                       tables=tables)
+layer, q, _ = bench.make_layer(ctx, name, kind, seed=1)
+cen, codes, tables = layer.centroids, layer.codes, layer.tables
+print(name, kind, ctx.decode_plan(layer, G, K))
 for i in range(reps):
     out = ctx.decode(layer, q + 0.01 * i, K)
 bm, _ = ctx.pq_search(q, cen, codes, B, K, s=SM, ordered=False, tables=tables)
