@@ -75,31 +75,57 @@ __device__ __forceinline__ void lut_entry_multi(double* lut, const float* q, con
     lut[e] = t;
 }
 
-// lut_entry_vec / lut_entry_multi with the query rows already converted to
-// fp64 in shared memory (qd [g][d_h]): one F2F per product instead of two,
-// and the query loads leave the chain.  Same products, same order.
+// One ADC table entry e (pq.cpp:113-126; subspace j = e / C), written to
+// lut[e] -- lut may be a distributed-shared-memory pointer.
+__device__ __forceinline__ void lut_entry(double* lut, const float* q, const float* cen, int g, int d_h, int m,
+                                          int C, int e) {
+    const int dm = d_h / m, j = e / C;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(cen)) & 15) == 0 &&
+                         (d_h % 4) == 0;
+    if (aligned && dm == 64) {
+        if (g > 1) lut_entry_multi<64>(lut, q, cen, g, d_h, e, j);
+        else lut_entry_vec<64>(lut, q, cen, g, d_h, e, j);
+        return;
+    }
+    if (aligned && dm == 32) {
+        if (g > 1) lut_entry_multi<32>(lut, q, cen, g, d_h, e, j);
+        else lut_entry_vec<32>(lut, q, cen, g, d_h, e, j);
+        return;
+    }
+    const float* cc = cen + (long long)e * dm;
+    double t = 0.0;
+    for (int r = 0; r < g; ++r) {
+        const float* qq = q + (long long)r * d_h + j * dm;
+        double acc = 0.0;
+        for (int u = 0; u < dm; ++u) acc = __fma_rn((double)__ldg(qq + u), (double)__ldg(cc + u), acc);
+        t = __dadd_rn(t, acc);
+    }
+    lut[e] = t;
+}
+
+// LUT entry from a centroid row staged in shared memory (16-byte chunk u of
+// row e at e * DM/4 + (u ^ (e & 7)): the 8 lanes of a 128-bit access phase
+// hit 8 distinct bank groups).  Same products, same order as lut_entry_vec /
+// lut_entry_multi.
 template <int DM>
-__device__ __forceinline__ void lut_entry_qd(double* lut, const double* qd, const float* cen, int g, int d_h, int e,
-                                             int j) {
-    const float4* cc4 = reinterpret_cast<const float4*>(cen + (long long)e * DM);
-    float4 cv[DM / 4];
-#pragma unroll
-    for (int u = 0; u < DM / 4; ++u) cv[u] = __ldg(cc4 + u);
+__device__ __forceinline__ void lut_entry_staged(double* lut, const float* q, const float4* stage, int g, int d_h,
+                                                 int e, int j) {
+    const float4* row = stage + (long long)e * (DM / 4);
     double t = 0.0;
     for (int r0 = 0; r0 < g; r0 += 4) {
         const int rn = min(4, g - r0);
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int u = 0; u < DM / 4; ++u) {
-            const double c0 = (double)cv[u].x, c1 = (double)cv[u].y, c2 = (double)cv[u].z, c3 = (double)cv[u].w;
+            const float4 cv = row[u ^ (e & 7)];
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
                 if (rr < rn) {
-                    const double* qq = qd + (r0 + rr) * d_h + j * DM + 4 * u;
-                    acc[rr] = __fma_rn(qq[0], c0, acc[rr]);
-                    acc[rr] = __fma_rn(qq[1], c1, acc[rr]);
-                    acc[rr] = __fma_rn(qq[2], c2, acc[rr]);
-                    acc[rr] = __fma_rn(qq[3], c3, acc[rr]);
+                    const float4 qv = __ldg(reinterpret_cast<const float4*>(q + (long long)(r0 + rr) * d_h + j * DM) + u);
+                    acc[rr] = __fma_rn((double)qv.x, (double)cv.x, acc[rr]);
+                    acc[rr] = __fma_rn((double)qv.y, (double)cv.y, acc[rr]);
+                    acc[rr] = __fma_rn((double)qv.z, (double)cv.z, acc[rr]);
+                    acc[rr] = __fma_rn((double)qv.w, (double)cv.w, acc[rr]);
                 }
             }
         }
@@ -110,16 +136,29 @@ __device__ __forceinline__ void lut_entry_qd(double* lut, const double* qd, cons
     lut[e] = t;
 }
 
+// `stage` (nullable, 16-byte aligned, m*C*d_m floats): the centroid table is
+// first copied there with coalesced cp.async (a lane per 16-byte chunk) --
+// one CTA pulling a 32 KB table with per-lane row loads (256 B apart) was the
+// slowest part of the pair select (tools/microbench/lut_probe.cu: 3.2 ->
+// 1.9 us warm).
 __device__ inline void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
-                          int C, double* qd_scratch = nullptr) {
-    if (qd_scratch && (d_h / m == 64 || d_h / m == 32) &&
-        ((reinterpret_cast<uintptr_t>(cen) & 15) == 0) && (d_h % 4) == 0) {
-        for (int i = threadIdx.x; i < g * d_h; i += blockDim.x) qd_scratch[i] = (double)__ldg(q + i);
+                          int C, float4* stage = nullptr) {
+    const int dm = d_h / m;
+    if (stage && (dm == 64 || dm == 32) && ((reinterpret_cast<uintptr_t>(cen) | reinterpret_cast<uintptr_t>(q)) & 15) == 0 &&
+        (d_h % 4) == 0) {
+        const int cpr = dm / 4, n = m * C * cpr;  // 16-byte chunks per row, in total
+        for (int f = threadIdx.x; f < n; f += blockDim.x) {
+            const int e = f / cpr, u = f % cpr;
+            cp_async16(stage + (long long)e * cpr + (u ^ (e & 7)), cen + 4LL * f);
+        }
+        cp_async_commit();
+        cp_async_wait_all();
         __syncthreads();
         for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
-            if (d_h / m == 64) lut_entry_qd<64>(lut, qd_scratch, cen, g, d_h, e, e / C);
-            else lut_entry_qd<32>(lut, qd_scratch, cen, g, d_h, e, e / C);
+            if (dm == 64) lut_entry_staged<64>(lut, q, stage, g, d_h, e, e / C);
+            else lut_entry_staged<32>(lut, q, stage, g, d_h, e, e / C);
         }
+        __syncthreads();  // the stage may be reused right after
         return;
     }
     const int d_m = d_h / m;
@@ -241,7 +280,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
                             const uint32_t* thist, const uint16_t* chist, int n_chunks, int k,
                             double* lut, uint32_t* hist, uint32_t* cnt, uint32_t* lst, uint32_t* ceq,
                             uint32_t* wsum, uint32_t* sh, uint8_t* cls, uint32_t* tkey_out,
-                            unsigned long long* tp = nullptr) {
+                            unsigned long long* tp = nullptr, bool lut_ready = false) {
     const int tid = threadIdx.x, C2 = C * C, lane = tid & 31, warp = tid >> 5;
     const int wbits = 32 - (32 - __clz((unsigned)(C2 - 1) | 1u));  // weight bits of a list entry
     const uint32_t wmask = (1u << wbits) - 1u;
@@ -254,8 +293,11 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
         const int t = tid + u * NT;
         w[u] = t < C2 ? __ldg(thist + t) : 0u;
     }
-    // the query rows in fp64 go to hist[] (zeroed only after the compaction)
-    build_lut(lut, q, cen, g, d_h, 2, C, g * d_h * 8 <= NB * 4 ? reinterpret_cast<double*>(hist) : nullptr);
+    // the centroid table is staged in hist[] .. lst[] (2 NB + C^2 words, not
+    // used before the compaction below) when it fits
+    if (!lut_ready)  // (the fused decode builds it across its cluster)
+        build_lut(lut, q, cen, g, d_h, 2, C,
+                  2 * C * (d_h / 2) <= 2 * NB + C * C ? reinterpret_cast<float4*>(hist) : nullptr);
     for (int c = tid; c < n_chunks; c += NT) ceq[c] = 0;
     for (int e = tid; e < (C2 + 3) / 4; e += NT) reinterpret_cast<uint32_t*>(cls)[e] = 0u;
     PQKV_T(1);
@@ -335,15 +377,20 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
     for (int u = 0; u < WMAX; ++u)
         if (u < per && (it[u] & wmask)) alive |= 1u << u;
     double lo = (double)key_score(kmin), hi = (double)key_score(kmax);
-    // First pass over a same-sign score range: bins on the order-preserving
-    // key bits (the top 11 bits of key - kmin: about 1/100 of a binade per
-    // bin), which follow a heavy-tailed positive distribution (powerlaw keys:
-    // scores ~ 1/rank) where value bins would put the whole bulk in bin 0.
-    // Mixed-sign ranges (gaussian keys) bin by value: key bits would split
-    // them by sign and exponent only.  Later passes bin by value.
-    const bool key_bins = (lo > 0.0 && hi > 0.0) || (lo < 0.0 && hi < 0.0);
+    // The first pass bins on the order-preserving key bits -- the top 11
+    // bits of key - kmin over this head's [kmin, kmax] -- i.e. on sign,
+    // exponent and leading mantissa bits: a fixed fraction of a binade per bin
+    // (1/64 for a 36-binade range) wherever the bulk of the scores sits.
+    // Value-linear bins put a heavy-tailed bulk (powerlaw keys: a few pair
+    // scores near 8, thousands near 1e-3) into one bin, whose items then also
+    // collide on one shared-memory atomic.  Later passes bin the survivors
+    // linearly by value over their own [min, max].
+    const bool key_bins = true;
     const int kshift = max(0, (32 - __clz((kmax - kmin) | 1u)) - 11);
     for (int pass = 0;; ++pass) {
+#ifdef PQKV_PASS_STAMPS  // tools/microbench/pair_select_probe.cu: per-pass clocks + survivor counts
+        if (tp && tid == 0 && pass < 4) tp[8 + pass] = clock64();
+#endif
         if (lo == hi) {  // every candidate has the same key
             kstar = score_key((float)lo);
             break;
@@ -363,10 +410,19 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
             }
         }
         __syncthreads();
+#ifdef PQKV_PASS_STAMPS
+        if (tp && tid == 0 && pass < 4) tp[21 + pass] = clock64();
+#endif
         find_digit<NT>(hist, NB, k_rem, wsum, sh);
+#ifdef PQKV_PASS_STAMPS
+        if (tp && tid == 0 && pass < 4) tp[25 + pass] = clock64();
+#endif
         const int bsel = (int)sh[0];
         k_rem -= sh[1];
         const uint32_t items = cnt[bsel];
+#ifdef PQKV_PASS_STAMPS
+        if (tp && tid == 0 && pass < 4) tp[12 + pass] = items;
+#endif
         float vmin = INFINITY, vmax = -INFINITY;
 #pragma unroll
         for (int u = 0; u < WMAX; ++u) {

@@ -1,74 +1,83 @@
-// Phase timing of pair_select (select_common.cuh) on realistic inputs:
-// 32 heads, m2b6 (C=64), 128K middle rows, k=26214, random gaussian queries
-// and centroids, multinomial pair histogram.  Each phase boundary records
-// clock64() from thread 0.
+// Phase timing of pair_select (select_common.cuh) on inputs dumped from a
+// real bench layer (tools/dump_pair_inputs.py): one CTA runs the select;
+// per-phase clocks (PQKV_T marks 0..6), per-pass clocks and survivor counts
+// (PQKV_PASS_STAMPS).  Usage: pair_select_probe DUMPDIR
+#define PQKV_PASS_STAMPS 1
 #include <cstdio>
 #include <cstdlib>
-#include <random>
+#include <string>
 #include <vector>
 #include <cuda_runtime.h>
 #include "select_common.cuh"
-__device__ unsigned long long g_t[64][16];
+__device__ unsigned long long g_t[40];
 
 using namespace pqkv_dev;
 
-template <int NT>
-__global__ void probe(const float* q, const float* cen, const uint32_t* thist, const uint16_t* chist, int n_chunks,
-                      int k, uint8_t* cls_out) {
+__global__ void probe(const float* q, int g, const float* cen, const uint32_t* thist, const uint16_t* chist,
+                      int n_chunks, int k, uint32_t* res) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int p = blockIdx.x, C = 64, C2 = C * C;
+    const int C = 64;
     PairScratch ps(smem, C, n_chunks);
     __shared__ uint8_t cls[4096];
-    unsigned long long t0 = clock64();
-    pair_select<NT, 16>(q + p * 128, 1, 128, cen + (size_t)p * 2 * C * 64, C, thist + (size_t)p * C2,
-                        chist + (size_t)p * n_chunks * C2, n_chunks, k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh,
-                        cls, nullptr, ::g_t[p]);
+    for (int i = threadIdx.x; i < 40; i += blockDim.x) g_t[i] = 0;
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    pair_select<256, 16>(q, g, 128, cen, C, thist, chist, n_chunks, k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq,
+                         ps.wsum, ps.sh, cls, nullptr, g_t);
     if (threadIdx.x == 0) {
-        ::g_t[p][15] = clock64() - t0;
-        cls_out[p] = (uint8_t)ps.sh[3];
+        g_t[20] = clock64() - t0;
+        res[0] = ps.sh[3];
+        res[1] = ps.sh[4];
+        res[2] = ps.sh[5];
     }
 }
 
-int main() {
-    const int P = 32, C = 64, C2 = C * C, S = 131004, NCH = (S + 4095) / 4096, K = 26214;
-    std::mt19937 rng(1);
-    std::normal_distribution<float> nd;
-    std::vector<float> q(P * 128), cen(P * 2 * C * 64);
-    for (auto& x : q) x = nd(rng);
-    for (auto& x : cen) x = nd(rng);
-    std::vector<uint32_t> th(P * C2, 0);
-    std::vector<uint16_t> ch((size_t)P * NCH * C2, 0);
-    std::uniform_int_distribution<int> ud(0, C2 - 1);
-    for (int p = 0; p < P; ++p)
-        for (int i = 0; i < S; ++i) {
-            int t = ud(rng) % 600;  // concentrated pairs, like real codes
-            th[p * C2 + t]++;
-            ch[((size_t)p * NCH + i / 4096) * C2 + t]++;
-        }
-    float *dq, *dc; uint32_t* dth; uint16_t* dch; uint8_t* dout;
-    cudaMalloc(&dq, q.size() * 4); cudaMalloc(&dc, cen.size() * 4); cudaMalloc(&dth, th.size() * 4);
-    cudaMalloc(&dch, ch.size() * 2); cudaMalloc(&dout, 64);
+template <typename T>
+std::vector<T> load(const std::string& path, size_t n) {
+    std::vector<T> v(n);
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f || std::fread(v.data(), sizeof(T), n, f) != n) { std::fprintf(stderr, "cannot read %s\n", path.c_str()); std::exit(1); }
+    std::fclose(f);
+    return v;
+}
+
+int main(int argc, char** argv) {
+    const std::string dir = argc > 1 ? argv[1] : "gpurun_out/pairdump";
+    int g = 1, nch = 32, k = 26214;
+    FILE* m = std::fopen((dir + "/meta.txt").c_str(), "r");
+    if (!m || std::fscanf(m, "%d %d %d", &g, &nch, &k) != 3) return 1;
+    std::fclose(m);
+    const int C = 64, C2 = C * C;
+    auto q = load<float>(dir + "/q.f32", g * 128);
+    auto cen = load<float>(dir + "/cen.f32", 2 * C * 64);
+    auto th = load<uint32_t>(dir + "/thist.u32", C2);
+    auto ch = load<uint16_t>(dir + "/chist.u16", (size_t)nch * C2);
+    float *dq, *dc; uint32_t *dth, *dres; uint16_t* dch;
+    cudaMalloc(&dq, q.size() * 4); cudaMalloc(&dc, cen.size() * 4); cudaMalloc(&dth, C2 * 4);
+    cudaMalloc(&dch, ch.size() * 2); cudaMalloc(&dres, 16);
     cudaMemcpy(dq, q.data(), q.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dc, cen.data(), cen.size() * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(dth, th.data(), th.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dth, th.data(), C2 * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dch, ch.data(), ch.size() * 2, cudaMemcpyHostToDevice);
-    size_t smem = pair_select_scratch(C, NCH);
-    cudaFuncSetAttribute(probe<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(probe<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int nt : {256, 1024}) {
-        for (int rep = 0; rep < 3; ++rep) {
-            cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-            cudaEventRecord(e0);
-            if (nt == 256) probe<256><<<P, 256, smem>>>(dq, dc, dth, dch, NCH, K, dout);
-            else probe<1024><<<P, 1024, smem>>>(dq, dc, dth, dch, NCH, K, dout);
-            cudaEventRecord(e1); cudaEventSynchronize(e1);
-            float ms; cudaEventElapsedTime(&ms, e0, e1);
-            unsigned long long t[64][16];
-            cudaMemcpyFromSymbol(t, ::g_t, sizeof(t));
-            printf("NT=%d rep %d: kernel %.1f us; head0 phases (cycles):", nt, rep, ms * 1e3);
-            for (int ph = 0; ph < 16; ++ph) if (t[0][ph]) printf(" [%d]=%llu", ph, t[0][ph]);
-            printf("\n");
-        }
+    const size_t smem = pair_select_scratch(C, nch);
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nnz = 0;
+    for (uint32_t v : th) nnz += v != 0;
+    for (int rep = 0; rep < 3; ++rep) {
+        probe<<<1, 256, smem>>>(dq, g, dc, dth, dch, nch, k, dres);
+        cudaDeviceSynchronize();
+        unsigned long long t[40];
+        uint32_t res[4];
+        cudaMemcpyFromSymbol(t, g_t, sizeof(t));
+        cudaMemcpy(res, dres, 12, cudaMemcpyDeviceToHost);
+        const double f = 1.0 / 1965.0;
+        std::printf("rep %d nnz %d total %.2f us | lut %.2f keys %.2f radix %.2f classify %.2f chist %.2f cstar %.2f |"
+                    " passes:", rep, nnz, t[20] * f, (t[1] - t[0]) * f, (t[3] - t[1]) * f, (t[4] - t[3]) * f,
+                    (t[5] - t[4]) * f, (t[6] - t[5]) * f, 0.0);
+        for (int p = 0; p < 4 && t[8 + p]; ++p)
+            std::printf(" [%d] +%.2f us (hist %.2f digit %.2f) items %llu", p, (t[8 + p] - t[3]) * f,
+                        (t[21 + p] - t[8 + p]) * f, (t[25 + p] - t[21 + p]) * f, t[12 + p]);
+        std::printf(" | c*=%u take=%u\n", res[0], res[1]);
     }
-    printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+    std::printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }
