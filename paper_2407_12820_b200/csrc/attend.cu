@@ -608,11 +608,145 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     __syncthreads();
 }
 
+// ---- g > 1 gather: one warp per K/V row ----
+// Each warp streams its rows (rows[warp], rows[warp + 8], ...) through a
+// private ring of `depth` 1 KB slots in shared memory: every lane copies 16 B
+// of the K row and 16 B of the V row with cp.async (one commit group per
+// row, so cp.async.wait_group depth-1 means "the oldest row has landed"; no
+// barrier -- each lane reads back only what it copied).  A lane holds dims
+// 4*lane..4*lane+3 of the G query rows and accumulators (2*4*G floats: half
+// the registers of the half-warp layout, so 4 CTAs fit per SM), and the G
+// partial dots are reduced by a transpose-reduce: after the xor-16 (and for
+// G = 4 xor-8) exchange a lane keeps a partial of one query row only, three
+// (four) more shuffles complete it -- the lanes of group r then own row r's
+// online-softmax state and broadcast its weight.  Measured on cfg3's shape
+// (tools/microbench/gqa_probe.cu): 4.95 TB/s vs 4.2-4.35 TB/s for the
+// half-warp-per-row ring.
+template <int G>
+__device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int c, int* rows, int nrows, int sel_total,
+                                                 const uint32_t* words, uint32_t* wtot, unsigned char* smem_raw,
+                                                 float (*wm)[G], float (*wl)[G]) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float4* kb = reinterpret_cast<const float4*>(a.keys + (long long)p * a.kv_head_stride);
+    const float4* vb = reinterpret_cast<const float4*>(a.values + (long long)p * a.kv_head_stride);
+    const uint64_t pol = l2_evict_first_policy();
+    const int depth = a.ring4 ? 4 : 2;
+    float4* ring = reinterpret_cast<float4*>(smem_raw + a.ring_off) + (size_t)warp * depth * 64;
+    float4 q[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(a.queries + ((long long)p * G + r) * DH) + lane);
+        q[r] = make_float4(v.x * a.scale_log2, v.y * a.scale_log2, v.z * a.scale_log2, v.w * a.scale_log2);
+    }
+    const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
+    float m_own = -INFINITY, l_own = 0.f;  // state of query row `own` (lane group)
+    float4 acc[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int win_base = 0;; win_base += a.win) {
+        const int mine = nrows > warp ? (nrows - warp + AT_WARPS - 1) / AT_WARPS : 0;
+        auto issue = [&](int it, int slot) {
+            if (it < mine) {
+                const long long row = rows[warp + AT_WARPS * it];
+                cp_async16_hint(ring + slot * 64 + lane, kb + row * (DH / 4) + lane, pol);
+                cp_async16_hint(ring + slot * 64 + 32 + lane, vb + row * (DH / 4) + lane, pol);
+            }
+            cp_async_commit();
+        };
+        for (int sl = 0; sl < depth; ++sl) issue(sl, sl);
+        for (int it = 0; it < mine; ++it) {
+            const int sl = it & (depth - 1);
+            if (depth == 4) cp_async_wait_group<3>();
+            else cp_async_wait_group<1>();
+            const float4 k = ring[sl * 64 + lane], v = ring[sl * 64 + 32 + lane];
+            issue(it + depth, sl);
+            float d[G];
+#pragma unroll
+            for (int r = 0; r < G; ++r) d[r] = fmaf(q[r].x, k.x, fmaf(q[r].y, k.y, fmaf(q[r].z, k.z, q[r].w * k.w)));
+            float x;
+            if constexpr (G == 4) {
+                float a0 = b4 ? d[2] : d[0], a1 = b4 ? d[3] : d[1];
+                const float s0 = b4 ? d[0] : d[2], s1 = b4 ? d[1] : d[3];
+                a0 += __shfl_xor_sync(FULL, s0, 16);
+                a1 += __shfl_xor_sync(FULL, s1, 16);
+                x = b3 ? a1 : a0;
+                x += __shfl_xor_sync(FULL, b3 ? a0 : a1, 8);
+            } else {  // G == 2: own row = bit 4
+                x = b4 ? d[1] : d[0];
+                x += __shfl_xor_sync(FULL, b4 ? d[0] : d[1], 16);
+                x += __shfl_xor_sync(FULL, x, 8);
+            }
+            x += __shfl_xor_sync(FULL, x, 4);
+            x += __shfl_xor_sync(FULL, x, 2);
+            x += __shfl_xor_sync(FULL, x, 1);
+            float alpha = 1.f;
+            if (x > m_own) {  // lazy rescale: only when the running max grows
+                alpha = safe_scale(m_own, x);
+                l_own *= alpha;
+                m_own = x;
+            }
+            const float pw = exp2f(x - m_own);
+            l_own += pw;
+            const bool grew = __any_sync(FULL, alpha != 1.f);
+            constexpr int GRP = 32 / G;  // lanes per query row group
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+                const float pr = __shfl_sync(FULL, pw, GRP * r);
+                if (grew) {
+                    const float ar = __shfl_sync(FULL, alpha, GRP * r);
+                    acc[r].x *= ar;
+                    acc[r].y *= ar;
+                    acc[r].z *= ar;
+                    acc[r].w *= ar;
+                }
+                acc[r].x = fmaf(pr, v.x, acc[r].x);
+                acc[r].y = fmaf(pr, v.y, acc[r].y);
+                acc[r].z = fmaf(pr, v.z, acc[r].z);
+                acc[r].w = fmaf(pr, v.w, acc[r].w);
+            }
+        }
+        cp_async_wait_all();
+        if (win_base + a.win >= sel_total) break;
+        // next window of this CTA's selected middle rows (+ the local rows after the last)
+        __syncthreads();
+        {
+            const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
+            const int nw = (max(0, r1 - r0) + 31) / 32;
+            const int nb = win_base + a.win;
+            nrows = expand_words_range(words, nw, a.n_init + r0, rows, 0, (uint32_t)nb, (uint32_t)(nb + a.win), wtot);
+            if (c == a.n_chunks - 1 && nb + a.win >= sel_total) {
+                for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
+                nrows += a.n_local;
+            }
+            __syncthreads();
+        }
+    }
+    if (a.prof) {
+        __syncthreads();
+        const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+        if (tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 3] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 6] = globaltimer_ns(); }
+    }
+    __syncthreads();  // every warp is past the gather loop: rows[] is free
+    // this warp's partial (m, l, acc per query row) -> the per-warp merge area
+    float* wacc = reinterpret_cast<float*>(smem_raw);  // [AT_WARPS][G][DH]
+    constexpr int GRP = 32 / G;
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        const float mr = __shfl_sync(FULL, m_own, GRP * r), lr = __shfl_sync(FULL, l_own, GRP * r);
+        reinterpret_cast<float4*>(wacc + (warp * G + r) * DH)[lane] = acc[r];
+        if (lane == 0) {
+            wm[warp][r] = mr;
+            wl[warp][r] = lr;
+        }
+    }
+    __syncthreads();
+}
+
 // MODE: 0 = the list modes (rows / bitmap / tuple classes, a.src at run
 // time), SRC_PAIRS or SRC_KEYS -- the fused single-launch modes get their own
 // instantiation so their prologues do not perturb the others' code.
 template <int G, int MODE>
-__global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtArgs a) {
+__global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 4) attend_kernel(AtArgs a) {
     const int src = MODE == 0 ? a.src : MODE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint32_t wtot[AT_WARPS];
@@ -796,6 +930,7 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     nrows = nrows_s;
     if (a.prof && tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 2] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 5] = globaltimer_ns(); }
 
+    if constexpr (G == 1) {
     // ---- 2. queries in the lane layout: dims {64j + 4hl + e} ----
     float q[G][4 * VPL];
 #pragma unroll
@@ -967,7 +1102,11 @@ __global__ void __launch_bounds__(AT_THREADS, G == 1 ? 4 : 2) attend_kernel(AtAr
     }
     __syncthreads();
 
+    } else {
+        gather_rows_warp<G>(a, p, c, rows, nrows, sel_total, words, wtot, smem_raw, wm, wl);
+    }
     // ---- 5. merge warps, write this CTA's partial ----
+    const float* wacc = reinterpret_cast<const float*>(smem_raw);  // [AT_WARPS][G][DH]
     for (int e = tid; e < G * DH; e += AT_THREADS) {
         int r = e / DH, d = e % DH;
         float M = -INFINITY;
@@ -1164,7 +1303,7 @@ void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_
 // gather_probe.cu); middle chunks are multiples of PQKV_TUPLE_CHUNK so the
 // code-pair classification never splits a tuple chunk.
 static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
-    const size_t occ = G == 1 ? 4 : 2;
+    const size_t occ = 4;
     const size_t target = (size_t)ctx->sm_count * occ;
     const size_t per_head = std::max<size_t>(1, target / std::max<size_t>(P, 1));
     const size_t tcs = std::max<size_t>(1, ceil_div(s_mid, PQKV_TUPLE_CHUNK));
@@ -1190,30 +1329,37 @@ static size_t attend_smem(AtArgs& a, int G) {
     {
         const size_t full_rows = ((size_t)a.chunk + a.n_init + a.n_local) * 4;
         const size_t tail_est = (size_t)a.chunk / 32 * 8 + ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
-        const size_t ring2 = (G > 1 && a.src != SRC_KEYS) ? (size_t)AT_WARPS * 2 * 2 * 2 * DH * 4 : 0;
-        const size_t budget = (G == 1 ? 55 : 110) * 1024;
+        const size_t ring2 = (G > 1 && a.src != SRC_KEYS) ? (size_t)AT_WARPS * 2 * 2 * DH * 4 : 0;
+        const size_t budget = 55 * 1024;
         const bool full = a.src == SRC_ROWS || a.chunk <= 8192 || full_rows + tail_est + ring2 <= budget;
         a.win = full ? a.chunk : 4096;
         a.stage = full;
     }
     size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.win + a.n_init + a.n_local;
-    size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
-    size_t region = std::max(rows_cap * 4, merge);
-    if (a.src == SRC_PAIRS) region = std::max(region, pair_select_scratch(a.C, a.n_tchunks));
-    if (a.src == SRC_KEYS) region = std::max(region, (size_t)a.chunk * 4 + (size_t)a.m * a.C * 8);
-    region = round_up(region, 16);
-    a.region = (int)region;
-    size_t tail = (size_t)a.chunk / 32 * 4 + (a.src == SRC_KEYS ? (size_t)NB * 12 : (size_t)a.chunk / 32 * 4) +
-                  ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
-    a.ring_off = (int)round_up(region + tail, 16);
-    // g > 1: 16 half-warps x 4 rows x (K + V) of cp.async ring (not for the
-    // key path, whose g > 1 launch only selects)
-    // depth 4 unless that costs the second CTA per SM (227 KB / 2 less the
-    // 1 KB per-CTA reservation): then depth 2
+    const size_t rows_bytes = round_up(rows_cap * 4, 16);
+    const size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
+    // g > 1: the per-warp cp.async row ring (8 warps x depth rows x K + V)
+    // sits right after rows[]; the pair select's scratch (selector CTA, before
+    // the gather) and the per-warp merge (after it) alias it.  Not for the
+    // key path, whose g > 1 launch only selects.
     const bool ring = G > 1 && a.src != SRC_KEYS;
-    const size_t ring4 = (size_t)AT_WARPS * 2 * 4 * 2 * DH * 4;
-    a.ring4 = !ring || (size_t)a.ring_off + ring4 <= 110 * 1024;
-    return (size_t)a.ring_off + (ring ? (a.ring4 ? ring4 : ring4 / 2) : 0);
+    const size_t ring4 = (size_t)AT_WARPS * 4 * 2 * DH * 4;
+    auto region_for = [&](size_t ring_bytes) {
+        size_t r = std::max(rows_bytes + ring_bytes, merge);
+        if (a.src == SRC_PAIRS) r = std::max(r, pair_select_scratch(a.C, a.n_tchunks));
+        if (a.src == SRC_KEYS) r = std::max(r, (size_t)a.chunk * 4 + (size_t)a.m * a.C * 8);
+        return round_up(r, 16);
+    };
+    const size_t tail = (size_t)a.chunk / 32 * 4 + (a.src == SRC_KEYS ? (size_t)NB * 12 : (size_t)a.chunk / 32 * 4) +
+                        ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
+    // depth 4 unless only depth 2 keeps 4 CTAs per SM (227 KB / 4 less the
+    // 1 KB per-CTA reservation)
+    const size_t per4 = 55 * 1024;
+    a.ring4 = !ring || region_for(ring4) + tail <= per4 || region_for(ring4 / 2) + tail > per4;
+    const size_t region = region_for(ring ? (a.ring4 ? ring4 : ring4 / 2) : 0);
+    a.region = (int)region;
+    a.ring_off = (int)rows_bytes;
+    return region + round_up(tail, 16);
 }
 
 template <int G, int MODE>
@@ -1337,7 +1483,7 @@ void launch_attend_rows(pqkv_ctx* ctx, const float* queries, size_t P, size_t G,
     a.src = SRC_ROWS;
     a.rows = rows;
     a.t = (int)t;
-    const size_t target = (size_t)ctx->sm_count * (G == 1 ? 4 : 2);
+    const size_t target = (size_t)ctx->sm_count * 4;
     const size_t per_head = std::max<size_t>(1, target / P);
     a.chunk = (int)std::min<size_t>(8192, round_up(std::max<size_t>(32, ceil_div(t, per_head)), 32));
     a.n_chunks = (int)ceil_div(t, (size_t)a.chunk);

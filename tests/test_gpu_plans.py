@@ -29,7 +29,7 @@ EXPECT = {
                       window=8192),
     "cfg1": dict(mode="pairs_fused", launches=1),
     "cfg2": dict(mode="pairs_fused", launches=1, chunk_tokens=2048, ctas_per_head=16, cluster=8, staged=1),
-    "cfg3_layer": dict(mode="pairs_fused", launches=1, chunk_tokens=4096, ctas_per_head=32, cluster=8, staged=1),
+    "cfg3_layer": dict(mode="pairs_fused", launches=1, chunk_tokens=2048, ctas_per_head=64, cluster=8, staged=1),
     "cfg5_per_gpu": dict(mode="keys_split", launches=2),
 }
 
