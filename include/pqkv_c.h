@@ -307,6 +307,26 @@ PQKV_API int pqkv_gen_workload(pqkv_ctx* ctx, int kind, size_t s, size_t d_h, si
  * gpu_launches accounting). */
 PQKV_API int pqkv_decode_launches(const pqkv_layer* layer, size_t g, int with_ids);
 
+/* ---- multi-GPU: head / request sharded decode over NCCL ----
+ * Units shard across GPUs with no exchange inside the path; the one
+ * collective is the all-gather of the per-unit attention outputs, batched
+ * over the layers of a call.  NCCL is loaded at run time (libnccl.so.2, the
+ * process's own when already loaded).  Protocol = ncclCommInitRank: rank 0
+ * calls pqkv_comm_unique_id, the host broadcasts the 128 bytes, every rank
+ * calls pqkv_comm_init. */
+typedef struct pqkv_comm pqkv_comm;
+PQKV_API int pqkv_comm_unique_id(uint8_t out[128]);
+PQKV_API int pqkv_comm_init(pqkv_ctx* ctx, const uint8_t id[128], int n_ranks, int rank, pqkv_comm** out);
+PQKV_API int pqkv_comm_destroy(pqkv_comm* comm);
+/* This rank decodes its units of every layer (layers[l]: this rank's shard,
+ * at most units_per_rank units; fewer pad with zero rows) with queries
+ * d_queries[l] [units][g][d_h], then one all-gather over the communicator
+ * (its own stream, ordered after the decodes; `stream` waits for it) fills
+ * d_out_all [n_ranks][n_layers][units_per_rank][g][d_h]. */
+PQKV_API int pqkv_decode_sharded(pqkv_ctx* ctx, pqkv_comm* comm, const pqkv_layer* layers, size_t n_layers,
+                                 size_t units_per_rank, const float* const* d_queries, size_t g, size_t k,
+                                 float* d_out_all, void* stream);
+
 /* The launch plan pqkv_decode picks for this layer, g, k (on ctx's device):
  * which fused mode runs, how the middle tokens are split over attention CTAs
  * and how those CTAs are grouped.  Used by tests to pin a parity case to the

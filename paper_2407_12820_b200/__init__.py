@@ -88,6 +88,10 @@ _SIGS = {
     "pqkv_decode_host": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp]),
     "pqkv_decode_launches": (_i, [C.POINTER(pqkv_layer), _sz, _i]),
     "pqkv_decode_plan": (_i, [_vp, C.POINTER(pqkv_layer), _sz, _sz, _i, C.POINTER(pqkv_decode_plan_t)]),
+    "pqkv_comm_unique_id": (_i, [C.c_char_p]),
+    "pqkv_comm_init": (_i, [_vp, C.c_char_p, _i, _i, C.POINTER(_vp)]),
+    "pqkv_comm_destroy": (_i, [_vp]),
+    "pqkv_decode_sharded": (_i, [_vp, _vp, C.POINTER(pqkv_layer), _sz, _sz, C.POINTER(_vp), _sz, _sz, _vp, _vp]),
 }
 
 _lib = None
@@ -347,6 +351,30 @@ class Context:
         d["mode"] = PLAN_MODES.get(d["mode"], d["mode"])
         return d
 
+    def comm_init(self, unique_id: bytes, n_ranks: int, rank: int) -> "Comm":
+        """NCCL communicator for pqkv_decode_sharded (ncclCommInitRank protocol:
+        rank 0's comm_unique_id() broadcast to every rank)."""
+        h = _vp()
+        _check(lib().pqkv_comm_init(self.h, C.c_char_p(bytes(unique_id)), n_ranks, rank, C.byref(h)))
+        return Comm(h, n_ranks, rank)
+
+    def decode_sharded(self, comm: "Comm", layers, queries, k: int, units_per_rank: int, out=None):
+        """This rank's shard of every layer decoded + one all-gather of all
+        ranks' outputs -> [n_ranks][n_layers][units_per_rank][g][d_h]."""
+        import torch
+
+        n = len(layers)
+        g, d_h = queries[0].shape[1], queries[0].shape[2]
+        if out is None:
+            out = torch.empty((comm.n_ranks, n, units_per_rank, g, d_h), dtype=torch.float32,
+                              device=queries[0].device)
+        arr = (pqkv_layer * n)(*[l.struct() for l in layers])
+        qp = (_vp * n)(*[q.data_ptr() for q in queries])
+        for q in queries:
+            _ptr(q)
+        _check(lib().pqkv_decode_sharded(self.h, comm.h, arr, n, units_per_rank, qp, g, k, _ptr(out), _stream()))
+        return out
+
     def decode_step(self, layer: "DecodeLayer", new_keys, new_values, queries, k: int, want_ids: bool = False):
         """One e2e step (evict_local_append + decode, pqkv_decode_step): new_keys /
         new_values [P][d_h] become token layer.total; layer.total grows by one."""
@@ -416,6 +444,31 @@ class Context:
         P, g, d_h = h_queries.shape
         _check(lib().pqkv_decode_host(self.h, layer.ref(), C.c_void_p(h_queries.data_ptr()), g, k,
                                       C.c_void_p(h_out.data_ptr()), _stream()))
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through libpqkv (run on rank 0, then broadcast)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().pqkv_comm_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """A pqkv_comm (NCCL communicator + its collective stream)."""
+
+    def __init__(self, h, n_ranks: int, rank: int):
+        self.h, self.n_ranks, self.rank = h, n_ranks, rank
+
+    def close(self):
+        if self.h:
+            lib().pqkv_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 @dataclass

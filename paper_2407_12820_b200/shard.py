@@ -2,10 +2,13 @@
 
 (request, layer, kv_head) units are independent in both hot paths, so the
 path shards without any data exchange: each rank owns a contiguous range of
-units.  The only collective is the optional all-gather of per-head attention
-outputs when one layer's heads are split across ranks (BASELINE cfg4), which
-the next layer's projection would need.  torch.distributed is plumbing here
-(NCCL on GPUs, gloo in the CPU tests); no kernel depends on it.
+units.  The only collective is the all-gather of per-head attention outputs
+when one layer's heads are split across ranks (BASELINE cfg4), which the next
+layer's projection needs: in the product it runs inside the C ABI
+(pqkv_decode_sharded: the rank's decodes of a batch of layers, then one NCCL
+all-gather on a collective stream); torch.distributed only exchanges the NCCL
+unique id (nccl_comm) and, in the CPU tests, stands in for the gather over
+gloo (gather_heads).
 """
 from __future__ import annotations
 
@@ -53,3 +56,29 @@ def gather_heads(local_out, n_heads: int):
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad)
     return torch.cat([p[:s] for p, s in zip(parts, sizes)], 0)
+
+
+def nccl_comm(ctx):
+    """The libpqkv NCCL communicator of this torch.distributed job: rank 0's
+    unique id is broadcast over the process group (any backend)."""
+    import torch.distributed as dist
+
+    import paper_2407_12820_b200 as pq
+
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank() if world > 1 else 0
+    box = [pq.comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(box, src=0)
+    return ctx.comm_init(box[0], world, rank)
+
+
+def unshard(gathered, n_heads: int):
+    """[n_ranks][n_layers][units_per_rank][g][d_h] from pqkv_decode_sharded ->
+    [n_layers][n_heads][g][d_h] in head order (drops the padding rows of
+    ranks that own fewer heads)."""
+    import torch
+
+    world = gathered.shape[0]
+    sizes = [len(partition(n_heads, world, r)) for r in range(world)]
+    return torch.cat([gathered[r, :, :sizes[r]] for r in range(world)], dim=1)
