@@ -8,7 +8,7 @@ NVFLAGS := $(EXTRA) -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC,-fvisibili
 CSRC := paper_2407_12820_b200/csrc
 OBJDIR ?= build/obj
 LIB ?= paper_2407_12820_b200/lib/libpqkv.so
-CU := ctx capi kmeans select attend step blocks workload collective
+CU := ctx capi kmeans select attend step blocks workload collective metrics
 CXXSRC := api kv_store_host pqt_io shape
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CXXSRC)))
 HDRS := include/pqkv_c.h $(CSRC)/common.cuh $(CSRC)/internal.cuh $(CSRC)/select_common.cuh

@@ -496,6 +496,24 @@ def main():
             del made, ls, qx
             torch.cuda.empty_cache()
 
+    # ---- run_recall on the device (experiments.cpp:74-139) ----
+    recall_info = None
+    if not args.no_extra:
+        from paper_2407_12820_b200 import recall as rc
+
+        rs, rh = 32768, 8
+        wl = {sd: ctx.gen_workload(rs, DH, h_kv=rh, g=1, kind="powerlaw", seed=7000 + sd) for sd in (1, 2)}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rrows = rc.run_recall(ctx, wl, [2], [6], [round(rs / 20), round(rs / 10), round(rs / 5)], max_iter=15)
+        torch.cuda.synchronize()
+        recall_info = {"what": f"run_recall on the GPU: {rh} heads x {rs} tokens powerlaw, m2b6, T=15, "
+                               "k = s/20, s/10, s/5, 2 seeds (fp64 attention path, reference arithmetic)",
+                       "seconds": time.perf_counter() - t0,
+                       "rows": [[r.k, r.seed, round(r.recall, 4), round(r.random_recall, 4), round(r.output_error, 4)]
+                                for r in rrows]}
+        del wl
+
     # ---- numbers ----
     # The step is ONE launch of attend_kernel (pair select + classification +
     # gather + softmax + combine fused), so the dominant
@@ -539,6 +557,7 @@ def main():
                 "d2h_bytes_per_step": H * G * DH * 4, "api": "pqkv_decode_host (C ABI, pinned host buffers)"},
         "gpu_launches": launches_per_step * args.steps * 2,
         "configs": extra,
+        "recall_gpu": recall_info,
         "head_sharded": {"config": "cfg4: each layer's 32 heads split over the ranks; pqkv_decode_sharded = the "
                                    "rank's decodes + one NCCL all-gather of the per-head outputs (C ABI, collective "
                                    "stream), 8 rotating layers",

@@ -221,6 +221,34 @@ PQKV_API int pqkv_exact_scores(pqkv_ctx* ctx, const float* d_queries, size_t n_h
                                size_t d_h, const float* d_keys, size_t kv_head_stride,
                                const int64_t* d_rows, size_t t, float* d_scores, void* stream);
 
+/* ---- experiment metrics on the device (experiments.cpp:26-139) ---- */
+
+/* exact_topk of the summed group query (sum_query_rows + exact_scores +
+ * top_k_desc, experiments.cpp:26-31, attention.cpp:11-33) for every unit p:
+ * the k best of key rows [0, n) of d_keys + p*kv_head_stride for the f32 sum
+ * of d_queries [p][0..g) -> d_ids [p][k], (score desc, id asc). */
+PQKV_API int pqkv_exact_topk(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
+                             const float* d_keys, size_t kv_head_stride, size_t n, size_t k, int64_t* d_ids,
+                             void* stream);
+/* Softmax attention of d_queries [p][g][d_h] over key/value rows [0, t) of
+ * every unit (gqa_group_attention over all stored tokens). */
+PQKV_API int pqkv_attend_dense(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h,
+                               const float* d_keys, const float* d_values, size_t kv_head_stride, size_t t,
+                               int precision, float* d_out, void* stream);
+/* relative_error (experiments.cpp:41-50) per row of n floats -> d_out [rows] f64. */
+PQKV_API int pqkv_relative_error(pqkv_ctx* ctx, const float* d_got, const float* d_want, size_t n_rows, size_t n,
+                                 double* d_out, void* stream);
+/* overlap_fraction (experiments.cpp:61-70) per row: |got ∩ want| / |want|,
+ * ids in [0, n_ids) -> d_out [rows] f64. */
+PQKV_API int pqkv_overlap_fraction(pqkv_ctx* ctx, const int64_t* d_got, size_t k_got, const int64_t* d_want,
+                                   size_t k_want, size_t n_rows, size_t n_ids, double* d_out, void* stream);
+/* The seeder draws of run_recall (experiments.cpp:90-113; Rng, rng.hpp): for
+ * each of h_kv heads one fork_seed (-> fork_seeds[h]) then, for every k of
+ * ks[0..n_k), k distinct ids of [0, s) by partial Fisher-Yates
+ * (-> random_ids[h][sum of earlier ks .. + k)). */
+PQKV_API int pqkv_recall_seeds(uint64_t seed, size_t h_kv, const size_t* ks, size_t n_k, size_t s,
+                               uint64_t* fork_seeds, int64_t* random_ids);
+
 /* One decode layer's KV cache + PQ index, device resident.  Token ids of a
  * head are its row indices: init [0,n_init), middle [n_init, total-n_local)
  * (middle row r = token n_init+r = code row r), local [total-n_local, total),

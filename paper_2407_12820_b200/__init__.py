@@ -88,6 +88,11 @@ _SIGS = {
     "pqkv_decode_host": (_i, [_vp, C.POINTER(pqkv_layer), _vp, _sz, _sz, _vp, _vp]),
     "pqkv_decode_launches": (_i, [C.POINTER(pqkv_layer), _sz, _i]),
     "pqkv_decode_plan": (_i, [_vp, C.POINTER(pqkv_layer), _sz, _sz, _i, C.POINTER(pqkv_decode_plan_t)]),
+    "pqkv_exact_topk": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _sz, _sz, _sz, _vp, _vp]),
+    "pqkv_attend_dense": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, _vp, _sz, _sz, _i, _vp, _vp]),
+    "pqkv_relative_error": (_i, [_vp, _vp, _vp, _sz, _sz, _vp, _vp]),
+    "pqkv_overlap_fraction": (_i, [_vp, _vp, _sz, _vp, _sz, _sz, _sz, _vp, _vp]),
+    "pqkv_recall_seeds": (_i, [_u64, _sz, C.POINTER(_sz), _sz, _sz, _vp, _vp]),
     "pqkv_comm_unique_id": (_i, [C.c_char_p]),
     "pqkv_comm_init": (_i, [_vp, C.c_char_p, _i, _i, C.POINTER(_vp)]),
     "pqkv_comm_destroy": (_i, [_vp]),
@@ -351,6 +356,52 @@ class Context:
         d["mode"] = PLAN_MODES.get(d["mode"], d["mode"])
         return d
 
+    # ---- experiment metrics (experiments.cpp:26-139) -------------------------
+    def exact_topk(self, queries, keys, k: int, n: int | None = None):
+        """Top-k of the f32 row sum of queries [P][g][d_h] against key rows
+        [0, n) of keys [P][S][d_h] (exact_scores, topk tie rule) -> [P][k] i64."""
+        import torch
+
+        P, g, d_h = queries.shape
+        n = keys.shape[1] if n is None else n
+        ids = torch.empty((P, max(k, 1)), dtype=torch.int64, device=queries.device)
+        _check(lib().pqkv_exact_topk(self.h, _ptr(queries), P, g, d_h, _ptr(keys), keys[0].numel(), n, k, _ptr(ids),
+                                     _stream()))
+        return ids[:, :k]
+
+    def attend_dense(self, queries, keys, values, t: int | None = None, precision: int = PREC_F64):
+        """Attention of queries [P][g][d_h] over rows [0, t) -> [P][g][d_h]."""
+        import torch
+
+        P, g, d_h = queries.shape
+        t = keys.shape[1] if t is None else t
+        out = torch.empty((P, g, d_h), dtype=torch.float32, device=queries.device)
+        _check(lib().pqkv_attend_dense(self.h, _ptr(queries), P, g, d_h, _ptr(keys), _ptr(values), keys[0].numel(), t,
+                                       precision, _ptr(out), _stream()))
+        return out
+
+    def relative_error(self, got, want):
+        """Per-row relative_error of [rows][...] f32 tensors -> [rows] f64."""
+        import torch
+
+        rows = got.shape[0]
+        n = got[0].numel()
+        out = torch.empty((rows,), dtype=torch.float64, device=got.device)
+        _check(lib().pqkv_relative_error(self.h, _ptr(got.contiguous()), _ptr(want.contiguous()), rows, n, _ptr(out),
+                                         _stream()))
+        return out
+
+    def overlap_fraction(self, got_ids, want_ids, n_ids: int):
+        """Per-row |got ∩ want| / |want| of id lists [rows][k] -> [rows] f64."""
+        import torch
+
+        rows = want_ids.shape[0]
+        out = torch.empty((rows,), dtype=torch.float64, device=want_ids.device)
+        _check(lib().pqkv_overlap_fraction(self.h, _ptr(got_ids.contiguous()), got_ids.shape[1],
+                                           _ptr(want_ids.contiguous()), want_ids.shape[1], rows, n_ids, _ptr(out),
+                                           _stream()))
+        return out
+
     def comm_init(self, unique_id: bytes, n_ranks: int, rank: int) -> "Comm":
         """NCCL communicator for pqkv_decode_sharded (ncclCommInitRank protocol:
         rank 0's comm_unique_id() broadcast to every rank)."""
@@ -444,6 +495,19 @@ class Context:
         P, g, d_h = h_queries.shape
         _check(lib().pqkv_decode_host(self.h, layer.ref(), C.c_void_p(h_queries.data_ptr()), g, k,
                                       C.c_void_p(h_out.data_ptr()), _stream()))
+
+
+def recall_seeds(seed: int, h_kv: int, ks, s: int):
+    """run_recall's seeder draws (experiments.cpp:90-113): (fork seeds [h_kv]
+    u64, random ids [h_kv][sum ks] i64 -- per k, k distinct ids of [0, s))."""
+    import numpy as np
+
+    ks = [int(k) for k in ks]
+    fs = np.zeros(h_kv, np.uint64)
+    ri = np.zeros((h_kv, max(1, sum(ks))), np.int64)
+    karr = (_sz * len(ks))(*ks)
+    _check(lib().pqkv_recall_seeds(int(seed) & (2**64 - 1), h_kv, karr, len(ks), s, fs.ctypes.data, ri.ctypes.data))
+    return fs, ri
 
 
 def comm_unique_id() -> bytes:

@@ -702,3 +702,35 @@ TensorF32 gqa_group_attention(const TensorF32& queries, const TensorF32& keys, c
 }
 
 }  // namespace pqkv
+
+// run_recall's seeder stream (experiments.cpp:90-113): host arithmetic on
+// the reference's Rng, exported for device-side recall drivers.
+extern "C" PQKV_CXX_API int pqkv_recall_seeds(uint64_t seed, size_t h_kv, const size_t* ks, size_t n_k, size_t s,
+                                              uint64_t* fork_seeds, int64_t* random_ids) {
+    try {
+        if ((n_k && !ks) || (h_kv && !fork_seeds)) throw std::invalid_argument("recall_seeds: NULL buffer");
+        std::size_t total = 0;
+        for (std::size_t i = 0; i < n_k; ++i) {
+            if (ks[i] < 1 || ks[i] > s) throw std::invalid_argument("recall: k must be in [1, s]");
+            total += ks[i];
+        }
+        if (h_kv && total && !random_ids) throw std::invalid_argument("recall_seeds: NULL buffer");
+        pqkv::Rng rng(seed);
+        std::vector<std::size_t> pool(s);
+        for (std::size_t h = 0; h < h_kv; ++h) {
+            fork_seeds[h] = rng.fork_seed();
+            std::size_t off = h * total;
+            for (std::size_t ki = 0; ki < n_k; ++ki) {
+                std::iota(pool.begin(), pool.end(), std::size_t{0});
+                for (std::size_t i = 0; i < ks[ki]; ++i) std::swap(pool[i], pool[i + rng.index(s - i)]);
+                for (std::size_t i = 0; i < ks[ki]; ++i) random_ids[off + i] = static_cast<int64_t>(pool[i]);
+                off += ks[ki];
+            }
+        }
+        return PQKV_OK;
+    } catch (const std::invalid_argument&) {
+        return PQKV_EINVAL;
+    } catch (...) {
+        return PQKV_ERUNTIME;
+    }
+}

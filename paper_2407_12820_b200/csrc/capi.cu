@@ -217,6 +217,63 @@ int pqkv_exact_scores(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, siz
     });
 }
 
+int pqkv_exact_topk(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h, const float* d_keys,
+                    size_t kv_head_stride, size_t n, size_t k, int64_t* d_ids, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (d_h < 1) fail(PQKV_EINVAL, "attention: query dim must match key dim");
+        if (g < 1) fail(PQKV_EINVAL, "attention: queries must be a non-empty 2-d grid");
+        if (k > n) fail(PQKV_EINVAL, "top_k: k too large for the candidate set");
+        if (!n_heads || !k) return;
+        if (!d_queries || !d_keys || !d_ids) fail(PQKV_EINVAL, "exact_topk: NULL buffer");
+        cudaStream_t st = as_stream(stream);
+        float* scores = nullptr;
+        PQKV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scores), n_heads * n * sizeof(float), st));
+        launch_summed_scores(ctx, d_queries, n_heads, g, d_h, d_keys, kv_head_stride, n, scores, st);
+        SelectSource src;
+        src.scores = scores;
+        src.scores_stride = n;
+        launch_select(ctx, src, n_heads, n, k, nullptr, d_ids, st, nullptr);
+        PQKV_CUDA(cudaFreeAsync(scores, st));
+    });
+}
+
+int pqkv_attend_dense(pqkv_ctx* ctx, const float* d_queries, size_t n_heads, size_t g, size_t d_h, const float* d_keys,
+                      const float* d_values, size_t kv_head_stride, size_t t, int precision, float* d_out,
+                      void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (t < 1) fail(PQKV_EINVAL, "attention: need at least one token");
+        if (!n_heads) return;
+        cudaStream_t st = as_stream(stream);
+        int64_t* rows = nullptr;
+        PQKV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), n_heads * t * sizeof(int64_t), st));
+        launch_iota_rows(ctx, rows, n_heads, t, st);
+        const int rc = pqkv_attend_rows(ctx, d_queries, n_heads, g, d_h, d_keys, d_values, kv_head_stride, rows, t,
+                                        precision, d_out, stream);
+        PQKV_CUDA(cudaFreeAsync(rows, st));
+        if (rc != PQKV_OK) fail(rc, pqkv_last_error());
+    });
+}
+
+int pqkv_relative_error(pqkv_ctx* ctx, const float* d_got, const float* d_want, size_t n_rows, size_t n,
+                        double* d_out, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (n_rows && (!d_got || !d_want || !d_out)) fail(PQKV_EINVAL, "relative_error: NULL buffer");
+        launch_relative_error(ctx, d_got, d_want, n_rows, n, d_out, as_stream(stream));
+    });
+}
+
+int pqkv_overlap_fraction(pqkv_ctx* ctx, const int64_t* d_got, size_t k_got, const int64_t* d_want, size_t k_want,
+                          size_t n_rows, size_t n_ids, double* d_out, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (n_rows && !d_out) fail(PQKV_EINVAL, "overlap_fraction: NULL buffer");
+        launch_overlap(ctx, d_got, k_got, d_want, k_want, n_rows, n_ids, d_out, as_stream(stream));
+    });
+}
+
 static void check_layer(const pqkv_layer* L, size_t g, size_t k) {
     if (!L) fail(PQKV_EINVAL, "decode: layer is NULL");
     check_pq(L->m, L->b, L->d_h);

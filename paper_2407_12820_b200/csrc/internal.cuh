@@ -198,4 +198,13 @@ void launch_bitmap_rows(pqkv_ctx* ctx, const uint32_t* bitmap, size_t P, size_t 
                         size_t n_init, size_t n_local, size_t total, size_t T, int64_t* rows,
                         cudaStream_t st);
 
+// metrics.cu (experiment metrics on the device)
+void launch_summed_scores(pqkv_ctx* ctx, const float* queries, size_t P, size_t g, size_t d_h, const float* keys,
+                          size_t kv_head_stride, size_t n, float* scores, cudaStream_t st);
+void launch_relative_error(pqkv_ctx* ctx, const float* got, const float* want, size_t rows, size_t n, double* out,
+                           cudaStream_t st);
+void launch_overlap(pqkv_ctx* ctx, const int64_t* got, size_t k_got, const int64_t* want, size_t k_want, size_t rows,
+                    size_t n_ids, double* out, cudaStream_t st);
+void launch_iota_rows(pqkv_ctx* ctx, int64_t* rows, size_t P, size_t t, cudaStream_t st);
+
 }  // namespace pqkv_dev
