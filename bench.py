@@ -386,6 +386,9 @@ def main():
     us_per_layer = ms * 1e3 / (args.steps * world)
     layers, base_qs, queries = heads[worst]
     plan = ctx.decode_plan(layers[0], G, K_SEL)
+    launches_per_step = layers[0].launches(G)
+
+    peak, peak_kind = peaks()
 
     # ---- dominant kernel (attention gather + combine) timed alone ----
     stream = torch.cuda.current_stream()
@@ -474,7 +477,6 @@ def main():
     del subs, qsub
 
     # ---- the other BASELINE configs, device-timed (rotating layers) ----
-    peak, peak_kind = peaks()
     extra = {}
     if not args.no_extra:
         for name in ("cfg1", "cfg2", "cfg3_layer", "cfg5_per_gpu"):
@@ -495,6 +497,51 @@ def main():
                            "layers_rotated": len(ls)}
             del made, ls, qx
             torch.cuda.empty_cache()
+
+    # ---- configs[2] whole model: Llama-3-8B shape, 32 layers x 8 kv heads x g4
+    # x 128K, prefill PQ build + decode of every layer per token on one B200
+    # (32 GB of fp32 K/V).  The headline layers except gaussian layer 0 (the
+    # CPU-baseline sample) are released first.
+    model_info = None
+    if not args.no_extra:
+        for kind in ("gaussian", "powerlaw"):
+            ls, qs_, _ = heads[kind]
+            keep = 1 if kind == "gaussian" else 0
+            heads[kind] = (ls[:keep], qs_[:keep], [])
+        layers = bms = hq = None
+        torch.cuda.empty_cache()
+        c3 = CONFIGS["cfg3_layer"]
+        n_model = 32
+        mlayers, mq, build_total = [], [], 0.0
+        for li in range(n_model):
+            ly, bq, secs = make_layer(ctx, "cfg3_layer", "gaussian", seed=9000 + li)
+            mlayers.append(ly)
+            mq.append(bq)
+            build_total += secs
+        k3 = cfg_k(c3)
+        n_tok = max(4, min(args.steps // 8, 32))
+        tq = [[mq[li] + sigma * torch.randn(mq[0].shape, generator=gq, device=dev) for li in range(n_model)]
+              for _ in range(2)]
+        for li in range(n_model):  # warm every layer
+            ctx.decode(mlayers[li], tq[0][li], k3)
+        torch.cuda.synchronize()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for t in range(n_tok):
+            for li in range(n_model):
+                ctx.decode(mlayers[li], tq[t & 1][li], k3)
+        m1.record(stream)
+        torch.cuda.synchronize()
+        ms_tok = m0.elapsed_time(m1) / n_tok
+        us_l = ms_tok * 1e3 / n_model
+        model_info = {"what": "configs[2]: 32 layers x 8 kv heads x g4 x 128K (Llama-3-8B shape), m2b6, top 1/5 "
+                              "+ 4 + 64; every token decodes all 32 layers (one launch each)",
+                      "prefill_build_s": build_total, "build_context_tokens_per_s": c3["s"] / build_total,
+                      "decode_ms_per_token": ms_tok, "us_per_layer": us_l,
+                      "frac": cfg_bytes(c3) / (us_l * 1e-6) / 1e9 / peak, "tokens": n_tok,
+                      "kv_gb": n_model * c3["units"] * c3["s"] * DH * 4 * 2 / 1e9}
+        del mlayers, mq, tq
+        torch.cuda.empty_cache()
 
     # ---- run_recall on the device (experiments.cpp:74-139) ----
     recall_info = None
@@ -530,7 +577,6 @@ def main():
         except Exception:
             traffic = None
     build_layer_s = float(np.median(build_s))
-    launches_per_step = layers[0].launches(G)
     line = {
         "metric": METRIC, "value": us_per_layer, "unit": "us/layer", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -558,6 +604,7 @@ def main():
         "gpu_launches": launches_per_step * args.steps * 2,
         "configs": extra,
         "recall_gpu": recall_info,
+        "model_cfg3": model_info,
         "head_sharded": {"config": "cfg4: each layer's 32 heads split over the ranks; pqkv_decode_sharded = the "
                                    "rank's decodes + one NCCL all-gather of the per-head outputs (C ABI, collective "
                                    "stream), 8 rotating layers",
