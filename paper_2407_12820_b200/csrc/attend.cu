@@ -608,6 +608,192 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     __syncthreads();
 }
 
+// ---- g = 1 gather: one half-warp per K/V row ----
+// 16 lanes x 2 float4 cover a 512 B row; each half-warp double-buffers its
+// next row in registers (128-bit loads, L2 evict-first), fp32 online softmax
+// in the log2 domain with lazy rescale; half-warps then merge into the
+// per-warp area (wacc / wm / wl).  Rows: rows[0..nrows) of this CTA, and for
+// windowed chunks the later windows of its selection words.
+__device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int c, int* rows, int nrows,
+                                                     int sel_total, const uint32_t* words, uint32_t* wtot,
+                                                     unsigned char* smem_raw, float (*wm)[1], float (*wl)[1]) {
+    constexpr int G = 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int half = lane >> 4, hl = lane & 15;
+    const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+    // ---- 2. queries in the lane layout: dims {64j + 4hl + e} ----
+    float q[G][4 * VPL];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        const float4* qp = reinterpret_cast<const float4*>(a.queries + ((long long)p * G + r) * DH);
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            float4 v = __ldg(qp + j * LPR + hl);
+            q[r][4 * j + 0] = v.x * a.scale_log2;
+            q[r][4 * j + 1] = v.y * a.scale_log2;
+            q[r][4 * j + 2] = v.z * a.scale_log2;
+            q[r][4 * j + 3] = v.w * a.scale_log2;
+        }
+    }
+    float m[G], l[G], acc[G][4 * VPL];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        m[r] = -INFINITY;
+        l[r] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4 * VPL; ++e) acc[r][e] = 0.f;
+    }
+
+    // ---- 3. gather (double-buffered 128-bit loads) + online softmax ----
+    const float4* kb = reinterpret_cast<const float4*>(a.keys + (long long)p * a.kv_head_stride);
+    const float4* vb = reinterpret_cast<const float4*>(a.values + (long long)p * a.kv_head_stride);
+    const int slot = warp * 2 + half;          // 0..15
+    constexpr int STEP = AT_WARPS * 2;         // rows per CTA step
+    const uint64_t pol = l2_evict_first_policy();
+    float4 kc[VPL], vc[VPL], kn[VPL], vn[VPL];
+    // g > 1: a RING-deep cp.async pipeline per half-warp in shared memory
+    // (each lane copies and later reads back only its own 16-byte chunks, so
+    // no barrier is needed); g = 1: two rows in registers
+    const int RING = a.ring4 ? 4 : 2;
+    float4* ring = G > 1 ? reinterpret_cast<float4*>(smem_raw + a.ring_off) + (size_t)slot * RING * 64 : nullptr;
+    auto issue = [&](int rr, int u) {
+        if (rr < nrows) {
+            const long long row = rows[rr];
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                cp_async16_hint(ring + u * 64 + j * LPR + hl, kb + row * (DH / 4) + j * LPR + hl, pol);
+                cp_async16_hint(ring + u * 64 + 32 + j * LPR + hl, vb + row * (DH / 4) + j * LPR + hl, pol);
+            }
+        }
+        cp_async_commit();
+    };
+    for (int win_base = 0;; win_base += a.win) {
+    int ri = slot;
+    if constexpr (G > 1) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (u < RING) issue(slot + u * STEP, u);
+    } else if (ri < nrows) {
+        const long long row = rows[ri];
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            kc[j] = ldg_stream(kb + row * (DH / 4) + j * LPR + hl, pol);
+            vc[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
+        }
+    }
+    for (int it = 0; ri < nrows; ri += STEP, ++it) {  // half-warp uniform trip count
+        if constexpr (G > 1) {
+            if (a.ring4) cp_async_wait_group<3>();  // this half-warp's oldest row has landed
+            else cp_async_wait_group<1>();
+            const int u = it & (RING - 1);
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                kc[j] = ring[u * 64 + j * LPR + hl];
+                vc[j] = ring[u * 64 + 32 + j * LPR + hl];
+            }
+            issue(ri + RING * STEP, u);
+        } else {
+            const int rn = ri + STEP;
+            if (rn < nrows) {  // prefetch the next row of this half-warp
+                const long long row = rows[rn];
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) {
+                    kn[j] = ldg_stream(kb + row * (DH / 4) + j * LPR + hl, pol);
+                    vn[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            float d = 0.f;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                d = fmaf(q[r][4 * j + 0], kc[j].x, d);
+                d = fmaf(q[r][4 * j + 1], kc[j].y, d);
+                d = fmaf(q[r][4 * j + 2], kc[j].z, d);
+                d = fmaf(q[r][4 * j + 3], kc[j].w, d);
+            }
+            d += __shfl_xor_sync(0xffffu << (half * 16), d, 1, 16);
+            d += __shfl_xor_sync(0xffffu << (half * 16), d, 2, 16);
+            d += __shfl_xor_sync(0xffffu << (half * 16), d, 4, 16);
+            d += __shfl_xor_sync(0xffffu << (half * 16), d, 8, 16);
+            if (d > m[r]) {  // lazy rescale: only when the running max grows
+                const float alpha = safe_scale(m[r], d);
+                l[r] *= alpha;
+#pragma unroll
+                for (int e = 0; e < 4 * VPL; ++e) acc[r][e] *= alpha;
+                m[r] = d;
+            }
+            const float pw = exp2f(d - m[r]);
+            l[r] += pw;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                acc[r][4 * j + 0] = fmaf(pw, vc[j].x, acc[r][4 * j + 0]);
+                acc[r][4 * j + 1] = fmaf(pw, vc[j].y, acc[r][4 * j + 1]);
+                acc[r][4 * j + 2] = fmaf(pw, vc[j].z, acc[r][4 * j + 2]);
+                acc[r][4 * j + 3] = fmaf(pw, vc[j].w, acc[r][4 * j + 3]);
+            }
+        }
+        if constexpr (G == 1) {
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                kc[j] = kn[j];
+                vc[j] = vn[j];
+            }
+        }
+    }
+    if constexpr (G > 1) cp_async_wait_all();
+    if (win_base + a.win >= sel_total) break;
+    // next window of this CTA's selected middle rows (+ the local rows after the last)
+    __syncthreads();
+    {
+        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
+        const int nw = (max(0, r1 - r0) + 31) / 32;
+        const int nb = win_base + a.win;
+        nrows = expand_words_range(words, nw, a.n_init + r0, rows, 0, (uint32_t)nb, (uint32_t)(nb + a.win), wtot);
+        if (c == a.n_chunks - 1 && nb + a.win >= sel_total) {
+            for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
+            nrows += a.n_local;
+        }
+        __syncthreads();
+    }
+    }
+
+    if (a.prof) {
+        __syncthreads();
+        if (tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 3] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 6] = globaltimer_ns(); }
+    }
+    // ---- 4. merge the two half-warps (lanes hl and hl+16 hold the same dims) ----
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        float mo = __shfl_xor_sync(FULL, m[r], 16);
+        float lo = __shfl_xor_sync(FULL, l[r], 16);
+        float mn = fmaxf(m[r], mo);
+        float sa = safe_scale(m[r], mn), sb = safe_scale(mo, mn);
+        l[r] = l[r] * sa + lo * sb;
+#pragma unroll
+        for (int e = 0; e < 4 * VPL; ++e) {
+            float ao = __shfl_xor_sync(FULL, acc[r][e], 16);
+            acc[r][e] = acc[r][e] * sa + ao * sb;
+        }
+        m[r] = mn;
+    }
+    __syncthreads();  // every warp is past the gather loop: rows[] is free
+    float* wacc = reinterpret_cast<float*>(smem_raw);  // [AT_WARPS][G][DH]
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        if (half == 0) {
+#pragma unroll
+            for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) wacc[(warp * G + r) * DH + 64 * j + 4 * hl + e] = acc[r][4 * j + e];
+            if (hl == 0) { wm[warp][r] = m[r]; wl[warp][r] = l[r]; }
+        }
+    }
+    __syncthreads();
+
+}
+
 // ---- g > 1 gather: one warp per K/V row ----
 // Each warp streams its rows (rows[warp], rows[warp + 8], ...) through a
 // private ring of `depth` 1 KB slots in shared memory: every lane copies 16 B
@@ -742,6 +928,75 @@ __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int c, 
     __syncthreads();
 }
 
+// Per-warp partials (wacc / wm / wl in shared memory) -> this CTA's partial
+// part[p][c] = (M, L, O[d]) per query row.
+template <int G>
+__device__ __forceinline__ void write_partial(const AtArgs& a, int p, int c, unsigned char* smem_raw, float (*wm)[G],
+                                              float (*wl)[G]) {
+    const float* wacc = reinterpret_cast<const float*>(smem_raw);  // [AT_WARPS][G][DH]
+    for (int e = threadIdx.x; e < G * DH; e += AT_THREADS) {
+        const int r = e / DH, d = e % DH;
+        float M = -INFINITY;
+        for (int w = 0; w < AT_WARPS; ++w) M = fmaxf(M, wm[w][r]);
+        float L = 0.f, O = 0.f;
+        if (M != -INFINITY) {
+            for (int w = 0; w < AT_WARPS; ++w) {
+                const float sc = safe_scale(wm[w][r], M);
+                L += wl[w][r] * sc;
+                O += wacc[(w * G + r) * DH + d] * sc;
+            }
+        }
+        float* o = a.part + (((long long)p * a.n_chunks + c) * G + r) * (DH + 2);
+        o[2 + d] = O;
+        if (d == 0) { o[0] = M; o[1] = L; }
+    }
+}
+
+// The last CTA of head p merges the head's n_chunks partials into out[p]
+// (and re-arms the head's arrival counter).
+template <int G>
+__device__ __forceinline__ void merge_head(const AtArgs& a, int p, unsigned char* smem_raw) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float* sc = reinterpret_cast<float*>(smem_raw) + AT_WARPS * G * DH;  // [G][n_chunks] + [G]
+    const int nc = a.n_chunks;
+    const float* pb = a.part + (long long)p * nc * G * (DH + 2);
+    for (int r = warp; r < G; r += AT_WARPS) {
+        float M = -INFINITY;
+        for (int cc = lane; cc < nc; cc += 32) M = fmaxf(M, __ldcg(pb + ((long long)cc * G + r) * (DH + 2)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(FULL, M, o));
+        float L = 0.f;
+        for (int cc = lane; cc < nc; cc += 32) {
+            const float* pc = pb + ((long long)cc * G + r) * (DH + 2);
+            float f = safe_scale(__ldcg(pc), M);
+            sc[r * nc + cc] = f;
+            L += __ldcg(pc + 1) * f;
+        }
+        L = warp_sum(L);
+        if (lane == 0) sc[G * nc + r] = L;
+    }
+    __syncthreads();
+    // the partial rows are L2-resident but the merge sits on the kernel's
+    // critical tail: 16 loads in flight per thread (same cc order)
+    for (int e = tid; e < G * DH; e += AT_THREADS) {
+        const int r = e / DH, d = e % DH;
+        const float* pr = pb + (long long)r * (DH + 2) + 2 + d;
+        const long long cstr = (long long)G * (DH + 2);
+        float O = 0.f;
+        int cc = 0;
+        for (; cc + 16 <= nc; cc += 16) {
+            float v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = __ldcg(pr + (cc + u) * cstr);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) O = fmaf(v[u], sc[r * nc + cc + u], O);
+        }
+        for (; cc < nc; ++cc) O = fmaf(__ldcg(pr + cc * cstr), sc[r * nc + cc], O);
+        a.out[((long long)p * G + r) * DH + d] = O / sc[G * nc + r];
+    }
+    if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
+}
+
 // MODE: 0 = the list modes (rows / bitmap / tuple classes, a.src at run
 // time), SRC_PAIRS or SRC_KEYS -- the fused single-launch modes get their own
 // instantiation so their prologues do not perturb the others' code.
@@ -755,7 +1010,6 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
 
     const int p = blockIdx.y, c = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int half = lane >> 4, hl = lane & 15;
     const int nwords = a.chunk / 32;
     int* rows = reinterpret_cast<int*>(smem_raw);
     uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + a.region);
@@ -930,199 +1184,10 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
     nrows = nrows_s;
     if (a.prof && tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 2] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 5] = globaltimer_ns(); }
 
-    if constexpr (G == 1) {
-    // ---- 2. queries in the lane layout: dims {64j + 4hl + e} ----
-    float q[G][4 * VPL];
-#pragma unroll
-    for (int r = 0; r < G; ++r) {
-        const float4* qp = reinterpret_cast<const float4*>(a.queries + ((long long)p * G + r) * DH);
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-            float4 v = __ldg(qp + j * LPR + hl);
-            q[r][4 * j + 0] = v.x * a.scale_log2;
-            q[r][4 * j + 1] = v.y * a.scale_log2;
-            q[r][4 * j + 2] = v.z * a.scale_log2;
-            q[r][4 * j + 3] = v.w * a.scale_log2;
-        }
-    }
-    float m[G], l[G], acc[G][4 * VPL];
-#pragma unroll
-    for (int r = 0; r < G; ++r) {
-        m[r] = -INFINITY;
-        l[r] = 0.f;
-#pragma unroll
-        for (int e = 0; e < 4 * VPL; ++e) acc[r][e] = 0.f;
-    }
-
-    // ---- 3. gather (double-buffered 128-bit loads) + online softmax ----
-    const float4* kb = reinterpret_cast<const float4*>(a.keys + (long long)p * a.kv_head_stride);
-    const float4* vb = reinterpret_cast<const float4*>(a.values + (long long)p * a.kv_head_stride);
-    const int slot = warp * 2 + half;          // 0..15
-    constexpr int STEP = AT_WARPS * 2;         // rows per CTA step
-    const uint64_t pol = l2_evict_first_policy();
-    float4 kc[VPL], vc[VPL], kn[VPL], vn[VPL];
-    // g > 1: a RING-deep cp.async pipeline per half-warp in shared memory
-    // (each lane copies and later reads back only its own 16-byte chunks, so
-    // no barrier is needed); g = 1: two rows in registers
-    const int RING = a.ring4 ? 4 : 2;
-    float4* ring = G > 1 ? reinterpret_cast<float4*>(smem_raw + a.ring_off) + (size_t)slot * RING * 64 : nullptr;
-    auto issue = [&](int rr, int u) {
-        if (rr < nrows) {
-            const long long row = rows[rr];
-#pragma unroll
-            for (int j = 0; j < VPL; ++j) {
-                cp_async16_hint(ring + u * 64 + j * LPR + hl, kb + row * (DH / 4) + j * LPR + hl, pol);
-                cp_async16_hint(ring + u * 64 + 32 + j * LPR + hl, vb + row * (DH / 4) + j * LPR + hl, pol);
-            }
-        }
-        cp_async_commit();
-    };
-    for (int win_base = 0;; win_base += a.win) {
-    int ri = slot;
-    if constexpr (G > 1) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (u < RING) issue(slot + u * STEP, u);
-    } else if (ri < nrows) {
-        const long long row = rows[ri];
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-            kc[j] = ldg_stream(kb + row * (DH / 4) + j * LPR + hl, pol);
-            vc[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
-        }
-    }
-    for (int it = 0; ri < nrows; ri += STEP, ++it) {  // half-warp uniform trip count
-        if constexpr (G > 1) {
-            if (a.ring4) cp_async_wait_group<3>();  // this half-warp's oldest row has landed
-            else cp_async_wait_group<1>();
-            const int u = it & (RING - 1);
-#pragma unroll
-            for (int j = 0; j < VPL; ++j) {
-                kc[j] = ring[u * 64 + j * LPR + hl];
-                vc[j] = ring[u * 64 + 32 + j * LPR + hl];
-            }
-            issue(ri + RING * STEP, u);
-        } else {
-            const int rn = ri + STEP;
-            if (rn < nrows) {  // prefetch the next row of this half-warp
-                const long long row = rows[rn];
-#pragma unroll
-                for (int j = 0; j < VPL; ++j) {
-                    kn[j] = ldg_stream(kb + row * (DH / 4) + j * LPR + hl, pol);
-                    vn[j] = ldg_stream(vb + row * (DH / 4) + j * LPR + hl, pol);
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < G; ++r) {
-            float d = 0.f;
-#pragma unroll
-            for (int j = 0; j < VPL; ++j) {
-                d = fmaf(q[r][4 * j + 0], kc[j].x, d);
-                d = fmaf(q[r][4 * j + 1], kc[j].y, d);
-                d = fmaf(q[r][4 * j + 2], kc[j].z, d);
-                d = fmaf(q[r][4 * j + 3], kc[j].w, d);
-            }
-            d += __shfl_xor_sync(0xffffu << (half * 16), d, 1, 16);
-            d += __shfl_xor_sync(0xffffu << (half * 16), d, 2, 16);
-            d += __shfl_xor_sync(0xffffu << (half * 16), d, 4, 16);
-            d += __shfl_xor_sync(0xffffu << (half * 16), d, 8, 16);
-            if (d > m[r]) {  // lazy rescale: only when the running max grows
-                const float alpha = safe_scale(m[r], d);
-                l[r] *= alpha;
-#pragma unroll
-                for (int e = 0; e < 4 * VPL; ++e) acc[r][e] *= alpha;
-                m[r] = d;
-            }
-            const float pw = exp2f(d - m[r]);
-            l[r] += pw;
-#pragma unroll
-            for (int j = 0; j < VPL; ++j) {
-                acc[r][4 * j + 0] = fmaf(pw, vc[j].x, acc[r][4 * j + 0]);
-                acc[r][4 * j + 1] = fmaf(pw, vc[j].y, acc[r][4 * j + 1]);
-                acc[r][4 * j + 2] = fmaf(pw, vc[j].z, acc[r][4 * j + 2]);
-                acc[r][4 * j + 3] = fmaf(pw, vc[j].w, acc[r][4 * j + 3]);
-            }
-        }
-        if constexpr (G == 1) {
-#pragma unroll
-            for (int j = 0; j < VPL; ++j) {
-                kc[j] = kn[j];
-                vc[j] = vn[j];
-            }
-        }
-    }
-    if constexpr (G > 1) cp_async_wait_all();
-    if (win_base + a.win >= sel_total) break;
-    // next window of this CTA's selected middle rows (+ the local rows after the last)
-    __syncthreads();
-    {
-        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
-        const int nw = (max(0, r1 - r0) + 31) / 32;
-        const int nb = win_base + a.win;
-        nrows = expand_words_range(words, nw, a.n_init + r0, rows, 0, (uint32_t)nb, (uint32_t)(nb + a.win), wtot);
-        if (c == a.n_chunks - 1 && nb + a.win >= sel_total) {
-            for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
-            nrows += a.n_local;
-        }
-        __syncthreads();
-    }
-    }
-
-    if (a.prof) {
-        __syncthreads();
-        if (tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 3] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 6] = globaltimer_ns(); }
-    }
-    // ---- 4. merge the two half-warps (lanes hl and hl+16 hold the same dims) ----
-#pragma unroll
-    for (int r = 0; r < G; ++r) {
-        float mo = __shfl_xor_sync(FULL, m[r], 16);
-        float lo = __shfl_xor_sync(FULL, l[r], 16);
-        float mn = fmaxf(m[r], mo);
-        float sa = safe_scale(m[r], mn), sb = safe_scale(mo, mn);
-        l[r] = l[r] * sa + lo * sb;
-#pragma unroll
-        for (int e = 0; e < 4 * VPL; ++e) {
-            float ao = __shfl_xor_sync(FULL, acc[r][e], 16);
-            acc[r][e] = acc[r][e] * sa + ao * sb;
-        }
-        m[r] = mn;
-    }
-    __syncthreads();  // every warp is past the gather loop: rows[] is free
-    float* wacc = reinterpret_cast<float*>(smem_raw);  // [AT_WARPS][G][DH]
-#pragma unroll
-    for (int r = 0; r < G; ++r) {
-        if (half == 0) {
-#pragma unroll
-            for (int j = 0; j < VPL; ++j)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) wacc[(warp * G + r) * DH + 64 * j + 4 * hl + e] = acc[r][4 * j + e];
-            if (hl == 0) { wm[warp][r] = m[r]; wl[warp][r] = l[r]; }
-        }
-    }
-    __syncthreads();
-
-    } else {
-        gather_rows_warp<G>(a, p, c, rows, nrows, sel_total, words, wtot, smem_raw, wm, wl);
-    }
+    if constexpr (G == 1) gather_rows_halfwarp(a, p, c, rows, nrows, sel_total, words, wtot, smem_raw, wm, wl);
+    else gather_rows_warp<G>(a, p, c, rows, nrows, sel_total, words, wtot, smem_raw, wm, wl);
     // ---- 5. merge warps, write this CTA's partial ----
-    const float* wacc = reinterpret_cast<const float*>(smem_raw);  // [AT_WARPS][G][DH]
-    for (int e = tid; e < G * DH; e += AT_THREADS) {
-        int r = e / DH, d = e % DH;
-        float M = -INFINITY;
-        for (int w = 0; w < AT_WARPS; ++w) M = fmaxf(M, wm[w][r]);
-        float L = 0.f, O = 0.f;
-        if (M != -INFINITY) {
-            for (int w = 0; w < AT_WARPS; ++w) {
-                float sc = safe_scale(wm[w][r], M);
-                L += wl[w][r] * sc;
-                O += wacc[(w * G + r) * DH + d] * sc;
-            }
-        }
-        float* o = a.part + (((long long)p * a.n_chunks + c) * G + r) * (DH + 2);
-        o[2 + d] = O;
-        if (d == 0) { o[0] = M; o[1] = L; }
-    }
+    write_partial<G>(a, p, c, smem_raw, wm, wl);
 
     // ---- 6. the last CTA of this head merges all partials (no extra launch) ----
     __shared__ unsigned ticket;
@@ -1136,44 +1201,7 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
     if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
     if (ticket != (unsigned)a.n_chunks - 1) return;
     __threadfence();
-    float* sc = reinterpret_cast<float*>(smem_raw) + AT_WARPS * G * DH;  // [G][n_chunks] + [G]
-    const int nc = a.n_chunks;
-    const float* pb = a.part + (long long)p * nc * G * (DH + 2);
-    for (int r = warp; r < G; r += AT_WARPS) {
-        float M = -INFINITY;
-        for (int cc = lane; cc < nc; cc += 32) M = fmaxf(M, __ldcg(pb + ((long long)cc * G + r) * (DH + 2)));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(FULL, M, o));
-        float L = 0.f;
-        for (int cc = lane; cc < nc; cc += 32) {
-            const float* pc = pb + ((long long)cc * G + r) * (DH + 2);
-            float f = safe_scale(__ldcg(pc), M);
-            sc[r * nc + cc] = f;
-            L += __ldcg(pc + 1) * f;
-        }
-        L = warp_sum(L);
-        if (lane == 0) sc[G * nc + r] = L;
-    }
-    __syncthreads();
-    // the partial rows are L2-resident but the merge sits on the kernel's
-    // critical tail: 16 loads in flight per thread (same cc order)
-    for (int e = tid; e < G * DH; e += AT_THREADS) {
-        const int r = e / DH, d = e % DH;
-        const float* pr = pb + (long long)r * (DH + 2) + 2 + d;
-        const long long cstr = (long long)G * (DH + 2);
-        float O = 0.f;
-        int cc = 0;
-        for (; cc + 16 <= nc; cc += 16) {
-            float v[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) v[u] = __ldcg(pr + (cc + u) * cstr);
-#pragma unroll
-            for (int u = 0; u < 16; ++u) O = fmaf(v[u], sc[r * nc + cc + u], O);
-        }
-        for (; cc < nc; ++cc) O = fmaf(__ldcg(pr + cc * cstr), sc[r * nc + cc], O);
-        a.out[((long long)p * G + r) * DH + d] = O / sc[G * nc + r];
-    }
-    if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
+    merge_head<G>(a, p, smem_raw);
     if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
 }
 

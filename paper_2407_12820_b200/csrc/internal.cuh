@@ -23,6 +23,7 @@ struct pqkv_ctx {
     // between launches by the kernel itself).
     unsigned* d_arrivals = nullptr;
     size_t n_arrivals = 0;
+
     // Profiling mode: attention-kernel phase timestamps of the last launch.
     int profiling = 0;
     uint32_t* sel_dump = nullptr;  // test hook: fused decodes write their selection words here
@@ -93,6 +94,7 @@ void* host_io_staging(pqkv_ctx* ctx, size_t bytes);
 // Multiprocessor count of the current device (cached per device id).
 int current_sm_count();
 unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st);
+
 
 // ---- launchers implemented in the kernel translation units -----------------
 
