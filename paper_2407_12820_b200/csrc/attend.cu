@@ -1473,7 +1473,10 @@ static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cuda
     a.arrivals = arrival_counters(ctx, P, st);
     a.prof = nullptr;
     a.sel_dump = ctx->sel_dump;
-    if (ctx->profiling) {
+    // PQKV_PROF_SELECT=1: profile only the key path's select launch (the
+    // bitmap gather that follows would otherwise overwrite its stamps)
+    static const bool prof_select_only = std::getenv("PQKV_PROF_SELECT") != nullptr;
+    if (ctx->profiling && (!prof_select_only || a.sel_only)) {
         if (ctx->d_prof) cudaFree(ctx->d_prof);
         ctx->n_prof = (size_t)a.n_chunks * P;
         PQKV_CUDA(cudaMalloc(&ctx->d_prof, ctx->n_prof * PQKV_PROF_SLOTS * sizeof(unsigned long long)));
