@@ -474,7 +474,54 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
             k_rem -= sh[6];
             break;
         }
-        // more than 32 pairs left: next pass over their [min, max]
+        if (items <= 128) {
+            // up to 128 survivors: rank them directly (a survivor's rank =
+            // survivors with a larger (key, weight) word, ties by list slot),
+            // scatter into rank order and scan the weights -- replaces another
+            // histogram pass plus the warp sort (powerlaw keys: ~100
+            // survivors after the first pass; select 6.7 -> 5.6 us in
+            // tools/microbench/pair_select_probe.cu; the quadratic ranking
+            // loses above ~200 survivors)
+            unsigned long long* small = reinterpret_cast<unsigned long long*>(hist);   // [items]
+            unsigned long long* srt = reinterpret_cast<unsigned long long*>(cnt);      // [items] rank order
+            if (tid == 0) sh[2] = 0;
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < WMAX; ++u) {
+                if (u >= per) break;
+                if ((alive >> u) & 1u) small[atomicAdd(&sh[2], 1u)] = (unsigned long long)kr[u] << 32 | (it[u] & wmask);
+            }
+            __syncthreads();
+            const int n = (int)sh[2];
+            for (int i = tid; i < n; i += NT) {
+                const unsigned long long v = small[i];
+                int rank = 0;
+                for (int j = 0; j < n; ++j) {
+                    const unsigned long long o = small[j];
+                    rank += (o > v) || (o == v && j < i);
+                }
+                srt[rank] = v;
+            }
+            __syncthreads();
+            // thread t owns ranks 2t, 2t+1
+            const int r0 = 2 * tid;
+            const uint32_t w0 = r0 < n ? (uint32_t)srt[r0] : 0u, w1 = r0 + 1 < n ? (uint32_t)srt[r0 + 1] : 0u;
+            const uint32_t before = block_excl_scan<NT>(w0 + w1, wsum, nullptr);
+            if (r0 < n && before < k_rem && k_rem <= before + w0) sh[5] = (uint32_t)(srt[r0] >> 32);
+            if (r0 + 1 < n && before + w0 < k_rem && k_rem <= before + w0 + w1) sh[5] = (uint32_t)(srt[r0 + 1] >> 32);
+            __syncthreads();
+            const uint32_t ks = sh[5];
+            // weight above K*: the cumulative weight before the first rank with key K*
+            if (r0 < n && (uint32_t)(srt[r0] >> 32) == ks && (r0 == 0 || (uint32_t)(srt[r0 - 1] >> 32) != ks))
+                sh[6] = before;
+            if (r0 + 1 < n && (uint32_t)(srt[r0 + 1] >> 32) == ks && (uint32_t)(srt[r0] >> 32) != ks)
+                sh[6] = before + w0;
+            __syncthreads();
+            kstar = ks;
+            k_rem -= sh[6];
+            break;
+        }
+        // more than 128 pairs left: next pass over their [min, max]
         vmin = warp_min(vmin);
         vmax = warp_max(vmax);
         if (lane == 0) { reinterpret_cast<float*>(wsum)[warp] = vmin; reinterpret_cast<float*>(wsum)[32 + warp] = vmax; }
