@@ -194,117 +194,102 @@ __device__ int expand_words_range(const uint32_t* words, int nwords, int token_b
 __device__ __forceinline__ int code_swz(int f) { return (f & ~255) | ((f & 7) << 5) | ((f >> 3) & 31); }
 
 // Tuple classification of middle tokens [r0, r1) into selection words
-// (pq.cpp:128-140 pair score, topk.cpp tie rule via the pair-select cut):
-// a token is selected when its pair class is "above", or "equal" and it is
-// among the first `take` equal tokens of tuple chunk c* (all equal tokens of
-// earlier chunks, none of later ones).  Each lane builds one 32-token word
-// of "above" bits (words[]) and of "equal" bits (eqw[]) from 8 128-bit code
-// loads -- from shared memory (`staged`: this CTA's range copied with the
-// code_swz layout) or from global memory (cd_g, absolute rows) -- then the
-// equal bits are resolved per chunk.  Warp segments never straddle a
-// PQKV_TUPLE_CHUNK chunk (chunk % (8*512) and PQKV_TUPLE_CHUNK % segment hold
-// by construction).
-__device__ void classify_words(const AtArgs& a, int r0, int r1, const uint32_t* cd_g, const uint32_t* staged,
+// (pq.cpp:128-140 pair score, topk.cpp tie rule via the pair-select cut).
+// r0 is a multiple of 32 (r1 too, unless it is s_mid), so a 32-token word
+// never straddles a PQKV_TUPLE_CHUNK chunk.  Code pairs come from shared
+// memory (`staged`: this CTA's range with the code_swz layout) or from
+// global memory (cd_g, absolute rows).  Each warp owns a contiguous run of
+// words; each lane builds whole words from 8 128-bit loads.
+//  * FINAL: cls in {0 below / absent, 1 above, 2 equal}.  A token is
+//    selected when its pair class is "above", or "equal" and it is among the
+//    first `take` equal tokens of tuple chunk c* in id order (all equal
+//    tokens of earlier chunks, none of later ones).  words[] = selection.
+//  * PRELIM (early release): cls in {0 below, 1 above, 3 pending}.
+//    words[] = above, eqw[] = pending.
+template <bool PRELIM>
+__device__ void classify_range(const AtArgs& a, int r0, int r1, const uint32_t* cd_g, const uint32_t* staged,
                                uint32_t* words, uint32_t* eqw, const uint8_t* cls, uint32_t* wtot, int cstar,
                                uint32_t take) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int seg = a.chunk / AT_WARPS;  // tokens per warp (multiple of 512)
-    const int s0 = r0 + warp * seg, s1 = min(r1, s0 + seg);
-    const int tc = s0 / PQKV_TUPLE_CHUNK;
+    const int nw = (max(0, r1 - r0) + 31) >> 5;
+    const int per = (nw + AT_WARPS - 1) / AT_WARPS;
+    const int w0 = min(nw, warp * per), w1 = min(nw, w0 + per);
     const uint32_t C = (uint32_t)a.C;
+    const uint32_t eqc = PRELIM ? 3u : 2u;
     const bool gvec = (reinterpret_cast<uintptr_t>(cd_g + r0) & 15) == 0;
-    // ---- step 1: above / equal words, one word per lane ----
-    {
-        const int w0 = (s0 - r0) >> 5, w1 = (max(s0, s1) - r0 + 31) >> 5;
-        for (int wb = w0; wb < w1; wb += 32) {
-            const int wi = wb + lane;
-            if (wi >= w1) continue;
-            const int nvalid = min(32, r1 - (r0 + 32 * wi));
-            uint32_t gt = 0, eq = 0;
+    // ---- step 1: above / equal (pending) words, one word per lane ----
+    for (int wb = w0; wb < w1; wb += 32) {
+        const int wi = wb + lane;
+        if (wi >= w1) continue;
+        const int nvalid = min(32, r1 - (r0 + 32 * wi));
+        uint32_t gt = 0, eq = 0;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                uint4 v;
-                if (staged) {
-                    v = reinterpret_cast<const uint4*>(staged)[code_swz(wi * 8 + u)];
-                } else if (gvec && nvalid == 32) {
-                    v = *reinterpret_cast<const uint4*>(cd_g + r0 + 32 * wi + 4 * u);
-                } else {
-                    const uint32_t* c = cd_g + r0 + 32 * wi + 4 * u;
-                    v.x = 4 * u + 0 < nvalid ? c[0] : 0u;
-                    v.y = 4 * u + 1 < nvalid ? c[1] : 0u;
-                    v.z = 4 * u + 2 < nvalid ? c[2] : 0u;
-                    v.w = 4 * u + 3 < nvalid ? c[3] : 0u;
-                }
-                const uint32_t pv[4] = {v.x, v.y, v.z, v.w};
+        for (int u = 0; u < 8; ++u) {
+            uint4 v;
+            if (staged) {
+                v = reinterpret_cast<const uint4*>(staged)[code_swz(wi * 8 + u)];
+            } else if (gvec && nvalid == 32) {
+                v = *reinterpret_cast<const uint4*>(cd_g + r0 + 32 * wi + 4 * u);
+            } else {
+                const uint32_t* c = cd_g + r0 + 32 * wi + 4 * u;
+                v.x = 4 * u + 0 < nvalid ? c[0] : 0u;
+                v.y = 4 * u + 1 < nvalid ? c[1] : 0u;
+                v.z = 4 * u + 2 < nvalid ? c[2] : 0u;
+                v.w = 4 * u + 3 < nvalid ? c[3] : 0u;
+            }
+            const uint32_t pv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int t = 4 * u + e;
-                    if (t < nvalid) {
-                        const uint32_t cl = cls[(pv[e] & 0xffffu) * C + (pv[e] >> 16)];
-                        gt |= (uint32_t)(cl == 1) << t;
-                        eq |= (uint32_t)(cl == 2) << t;
-                    }
+            for (int e = 0; e < 4; ++e) {
+                const int t = 4 * u + e;
+                if (t < nvalid) {
+                    const uint32_t cl = cls[(pv[e] & 0xffffu) * C + (pv[e] >> 16)];
+                    gt |= (uint32_t)(cl == 1) << t;
+                    eq |= (uint32_t)(cl == eqc) << t;
                 }
             }
-            words[wi] = gt;
-            eqw[wi] = eq;
+        }
+        words[wi] = gt;
+        eqw[wi] = eq;
+    }
+    __syncthreads();
+    if constexpr (PRELIM) return;
+    // ---- step 2: equal tokens: all of chunks before c*, the first `take` of
+    // c* in id order, none after ----
+    const int a0 = cstar * PQKV_TUPLE_CHUNK, a1 = a0 + PQKV_TUPLE_CHUNK;
+    for (int w = tid; w < nw; w += AT_THREADS)
+        if ((r0 + 32 * w) / PQKV_TUPLE_CHUNK < cstar) words[w] |= eqw[w];
+    const int b0 = max(r0, a0), b1 = min(r1, a1);
+    if (b0 < b1) {  // this range holds part of chunk c* (block-uniform)
+        // equal tokens of c* before this range (other CTAs' tokens)
+        uint32_t pre = 0;
+        for (int i = a0 + tid; i < r0; i += AT_THREADS) {
+            const uint32_t pr = cd_g[i];
+            pre += cls[(pr & 0xffffu) * C + (pr >> 16)] == 2;
+        }
+        pre = warp_sum(pre);
+        if (lane == 0) wtot[warp] = pre;
+        __syncthreads();
+        pre = 0;
+#pragma unroll
+        for (int w = 0; w < AT_WARPS; ++w) pre += wtot[w];
+        __syncthreads();
+        // ordered prefix over the words of c* in this range: <= 128 words,
+        // thread t owns word wb0 + t
+        const int wb0 = (b0 - r0) >> 5, wb1 = (b1 - r0 + 31) >> 5;
+        const int w = wb0 + tid;
+        const uint32_t e = w < wb1 ? eqw[w] : 0u;
+        const uint32_t before = pre + block_excl_scan<AT_THREADS>((uint32_t)__popc(e), wtot, nullptr);
+        if (w < wb1 && e) {
+            uint32_t keep = 0;
+            const uint32_t c = __popc(e);
+            if (before + c <= take) keep = e;
+            else if (before < take) {
+                uint32_t mm = e;
+                for (uint32_t k = take - before; k; --k) { keep |= mm & (0u - mm); mm &= mm - 1; }
+            }
+            words[w] |= keep;
         }
     }
-    __syncwarp();
-    const int w0 = (s0 - r0) >> 5, w1 = (max(s0, s1) - r0 + 31) >> 5;
-    // ---- step 2: resolve the equal tokens ----
-    const bool boundary = tc == cstar && s0 < s1;
-    if (__syncthreads_or(boundary)) {
-        // equal tokens of c* before this warp (warps of the chunk in id order)
-        uint32_t neq = 0;
-        if (boundary)
-            for (int w = w0 + lane; w < w1; w += 32) neq += __popc(eqw[w]);
-        neq = warp_sum(neq);
-        if (lane == 0) wtot[warp] = boundary ? neq : 0;
-        __syncthreads();
-        uint32_t run = 0;
-        for (int v = 0; v < warp; ++v)
-            if ((r0 + v * seg) / PQKV_TUPLE_CHUNK == tc) run += wtot[v];
-        // a CTA that starts inside chunk c* (chunks below PQKV_TUPLE_CHUNK for
-        // few heads) also counts the equal tokens of c* before its range
-        const int a0 = cstar * PQKV_TUPLE_CHUNK;
-        if (r0 > a0 && r0 < a0 + PQKV_TUPLE_CHUNK) {
-            uint32_t pre = 0;
-            for (int i = a0 + tid; i < r0; i += AT_THREADS) {
-                const uint32_t pr = cd_g[i];
-                pre += cls[(pr & 0xffffu) * C + (pr >> 16)] == 2;
-            }
-            pre = warp_sum(pre);
-            __syncthreads();  // wtot reads above are done
-            if (lane == 0) wtot[warp] = pre;
-            __syncthreads();
-            for (int v = 0; v < AT_WARPS; ++v) run += wtot[v];
-        }
-        __syncthreads();
-        if (boundary)
-            for (int wb = w0; wb < w1; wb += 32) {
-                const int w = wb + lane;
-                const uint32_t e = w < w1 ? eqw[w] : 0u;
-                const uint32_t c = __popc(e);
-                uint32_t x = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(FULL, x, o);
-                    if (lane >= o) x += y;
-                }
-                const uint32_t before = run + x - c;
-                uint32_t keep = 0;
-                if (before + c <= take) keep = e;
-                else if (before < take) {
-                    uint32_t m = e;
-                    for (uint32_t n = take - before; n; --n) { keep |= m & (0u - m); m &= m - 1; }
-                }
-                if (w < w1) words[w] |= keep;
-                run += __shfl_sync(FULL, x, 31);
-            }
-    }
-    if (tc < cstar)
-        for (int w = w0 + lane; w < w1; w += 32) words[w] |= eqw[w];
     __syncthreads();
 }
 
@@ -1139,7 +1124,7 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
             cp_async_wait_all();
             __syncthreads();
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 19] = clock64();
-            classify_words(a, r0, r1, cd_g, staged, words, eqw, cls, wtot, cstar, take);
+            classify_range<false>(a, r0, r1, cd_g, staged, words, eqw, cls, wtot, cstar, take);
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 20] = clock64();
             if (c == 0)  // after the staged codes are consumed (they share rows[])
                 for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
@@ -1152,7 +1137,7 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
                 for (int e = tid; e < C2; e += AT_THREADS) cls[e] = a.cls[(long long)p * C2 + e];
             }
             __syncthreads();
-            classify_words(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), nullptr,
+            classify_range<false>(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), nullptr,
                            words, eqw, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
         }
         __syncthreads();
