@@ -593,14 +593,42 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     __syncthreads();
 }
 
+// Row-list refill of the gather loops: called when the current rows are
+// consumed; returns the next rows' count, or < 0 when the CTA is done.
+// WindowRefill: windowed chunks (selected rows expanded `win` at a time from
+// the CTA's selection words; the local rows follow the last window).
+struct WindowRefill {
+    const AtArgs& a;
+    int c;
+    const uint32_t* words;
+    uint32_t* wtot;
+    int sel_total;
+    int win_base;
+    __device__ int operator()(int* rows) {
+        if (win_base + a.win >= sel_total) return -1;
+        __syncthreads();
+        win_base += a.win;
+        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
+        const int nw = (max(0, r1 - r0) + 31) / 32;
+        int nrows = expand_words_range(words, nw, a.n_init + r0, rows, 0, (uint32_t)win_base,
+                                       (uint32_t)(win_base + a.win), wtot);
+        if (c == a.n_chunks - 1 && win_base + a.win >= sel_total) {
+            for (int e = threadIdx.x; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
+            nrows += a.n_local;
+        }
+        __syncthreads();
+        return nrows;
+    }
+};
+
 // ---- g = 1 gather: one half-warp per K/V row ----
 // 16 lanes x 2 float4 cover a 512 B row; each half-warp double-buffers its
 // next row in registers (128-bit loads, L2 evict-first), fp32 online softmax
 // in the log2 domain with lazy rescale; half-warps then merge into the
 // per-warp area (wacc / wm / wl).  Rows: rows[0..nrows) of this CTA, and for
 // windowed chunks the later windows of its selection words.
-__device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int c, int* rows, int nrows,
-                                                     int sel_total, const uint32_t* words, uint32_t* wtot,
+template <class Refill>
+__device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int* rows, int nrows, Refill& refill,
                                                      unsigned char* smem_raw, float (*wm)[1], float (*wl)[1]) {
     constexpr int G = 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -652,7 +680,7 @@ __device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int
         }
         cp_async_commit();
     };
-    for (int win_base = 0;; win_base += a.win) {
+    for (;;) {
     int ri = slot;
     if constexpr (G > 1) {
 #pragma unroll
@@ -728,19 +756,10 @@ __device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int
         }
     }
     if constexpr (G > 1) cp_async_wait_all();
-    if (win_base + a.win >= sel_total) break;
-    // next window of this CTA's selected middle rows (+ the local rows after the last)
-    __syncthreads();
     {
-        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
-        const int nw = (max(0, r1 - r0) + 31) / 32;
-        const int nb = win_base + a.win;
-        nrows = expand_words_range(words, nw, a.n_init + r0, rows, 0, (uint32_t)nb, (uint32_t)(nb + a.win), wtot);
-        if (c == a.n_chunks - 1 && nb + a.win >= sel_total) {
-            for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
-            nrows += a.n_local;
-        }
-        __syncthreads();
+        const int nn = refill(rows);  // the next window's rows, or < 0: done
+        if (nn < 0) break;
+        nrows = nn;
     }
     }
 
@@ -793,10 +812,9 @@ __device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int
 // online-softmax state and broadcast its weight.  Measured on cfg3's shape
 // (tools/microbench/gqa_probe.cu): 4.95 TB/s vs 4.2-4.35 TB/s for the
 // half-warp-per-row ring.
-template <int G>
-__device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int c, int* rows, int nrows, int sel_total,
-                                                 const uint32_t* words, uint32_t* wtot, unsigned char* smem_raw,
-                                                 float (*wm)[G], float (*wl)[G]) {
+template <int G, class Refill>
+__device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int* rows, int nrows, Refill& refill,
+                                                 unsigned char* smem_raw, float (*wm)[G], float (*wl)[G]) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float4* kb = reinterpret_cast<const float4*>(a.keys + (long long)p * a.kv_head_stride);
     const float4* vb = reinterpret_cast<const float4*>(a.values + (long long)p * a.kv_head_stride);
@@ -814,7 +832,7 @@ __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int c, 
     float4 acc[G];
 #pragma unroll
     for (int r = 0; r < G; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int win_base = 0;; win_base += a.win) {
+    for (;;) {
         const int mine = nrows > warp ? (nrows - warp + AT_WARPS - 1) / AT_WARPS : 0;
         auto issue = [&](int it, int slot) {
             if (it < mine) {
@@ -877,20 +895,9 @@ __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int c, 
             }
         }
         cp_async_wait_all();
-        if (win_base + a.win >= sel_total) break;
-        // next window of this CTA's selected middle rows (+ the local rows after the last)
-        __syncthreads();
-        {
-            const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
-            const int nw = (max(0, r1 - r0) + 31) / 32;
-            const int nb = win_base + a.win;
-            nrows = expand_words_range(words, nw, a.n_init + r0, rows, 0, (uint32_t)nb, (uint32_t)(nb + a.win), wtot);
-            if (c == a.n_chunks - 1 && nb + a.win >= sel_total) {
-                for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
-                nrows += a.n_local;
-            }
-            __syncthreads();
-        }
+        const int nn = refill(rows);  // the next window's rows, or < 0: done
+        if (nn < 0) break;
+        nrows = nn;
     }
     if (a.prof) {
         __syncthreads();
@@ -1169,8 +1176,9 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
     nrows = nrows_s;
     if (a.prof && tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 2] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 5] = globaltimer_ns(); }
 
-    if constexpr (G == 1) gather_rows_halfwarp(a, p, c, rows, nrows, sel_total, words, wtot, smem_raw, wm, wl);
-    else gather_rows_warp<G>(a, p, c, rows, nrows, sel_total, words, wtot, smem_raw, wm, wl);
+    WindowRefill refill{a, c, words, wtot, sel_total, 0};
+    if constexpr (G == 1) gather_rows_halfwarp(a, p, rows, nrows, refill, smem_raw, wm, wl);
+    else gather_rows_warp<G>(a, p, rows, nrows, refill, smem_raw, wm, wl);
     // ---- 5. merge warps, write this CTA's partial ----
     write_partial<G>(a, p, c, smem_raw, wm, wl);
 
