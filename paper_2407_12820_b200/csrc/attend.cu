@@ -1368,6 +1368,8 @@ static size_t attend_smem(AtArgs& a, int G) {
     auto region_for = [&](size_t ring_bytes) {
         size_t r = std::max(rows_bytes + ring_bytes, merge);
         if (a.src == SRC_PAIRS) r = std::max(r, pair_select_scratch(a.C, a.n_tchunks));
+        // staged code pairs: the code_swz layout fills whole 1024-token blocks
+        if ((a.src == SRC_PAIRS || a.src == SRC_TUPLE) && a.stage) r = std::max(r, round_up((size_t)a.chunk, 1024) * 4);
         if (a.src == SRC_KEYS) r = std::max(r, (size_t)a.chunk * 4 + (size_t)a.m * a.C * 8);
         return round_up(r, 16);
     };
