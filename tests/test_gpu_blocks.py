@@ -21,7 +21,10 @@ def _want(ids, n_tokens, bs, k_cache):
 
 
 @pytest.mark.parametrize("n_tokens,bs,n,k_cache", [(131072, 128, 26214, 32), (5000, 7, 900, 5), (300, 1000, 50, 3),
-                                                   (70000, 64, 1, 4), (4096, 16, 0, 2)])
+                                                   (70000, 64, 1, 4), (4096, 16, 0, 2),
+                                                   # bitmap + sort keys beyond shared memory: the global-memory
+                                                   # path (block size 1 over 100K tokens; 16 over 600K)
+                                                   (100000, 1, 30000, 40), (600000, 16, 50000, 64)])
 def test_block_rank_matches_by_block_map(ctx, n_tokens, bs, n, k_cache):
     import torch
 
