@@ -303,6 +303,197 @@ __global__ void __launch_bounds__(256, MINB) gqa_w2(const float* __restrict__ K,
     }
 }
 
+
+// ---- W2P: W2 with packed fp32 (FFMA2 / FMUL2) dots and accumulators ----
+template <int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) gqa_w2p(const float* __restrict__ K, const float* __restrict__ V,
+                                                    const int* __restrict__ rows, int per_cta, const float* __restrict__ Q,
+                                                    float scale_log2, float* part) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int p = blockIdx.y, c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    float4* ring = reinterpret_cast<float4*>(sm) + (size_t)warp * D * 64;
+    const int r0 = c * per_cta, n = max(0, min(per_cta, SEL - r0));
+    const int* rl = rows + (size_t)p * SEL + r0;
+    const float4* kb = reinterpret_cast<const float4*>(K + (size_t)p * S * DH);
+    const float4* vb = reinterpret_cast<const float4*>(V + (size_t)p * S * DH);
+    const uint64_t pol = evict_first();
+    const int mine = n > warp ? (n - warp + 7) / 8 : 0;
+    auto issue = [&](int it, int s) {
+        if (it < mine) {
+            const long long row = rl[warp + 8 * it];
+            cp16(ring + s * 64 + lane, kb + row * 32 + lane, pol);
+            cp16(ring + s * 64 + 32 + lane, vb + row * 32 + lane, pol);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int s = 0; s < D; ++s) issue(s, s);
+    float4 q[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        float4 v = reinterpret_cast<const float4*>(Q + ((size_t)p * G + r) * DH)[lane];
+        q[r] = make_float4(v.x * scale_log2, v.y * scale_log2, v.z * scale_log2, v.w * scale_log2);
+    }
+    const bool b4 = lane & 16, b3 = lane & 8;
+    float m_own = -INFINITY, l_own = 0.f;
+    float4 acc[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int it = 0; it < mine; ++it) {
+        const int s = it % D;
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+        const float4 k = ring[s * 64 + lane], v = ring[s * 64 + 32 + lane];
+        issue(it + D, s);
+        float d[G];
+        const float2 kxy = make_float2(k.x, k.y), kzw = make_float2(k.z, k.w);
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const float2 t = __ffma2_rn(make_float2(q[r].z, q[r].w), kzw, __fmul2_rn(make_float2(q[r].x, q[r].y), kxy));
+            d[r] = t.x + t.y;
+        }
+        float a0 = b4 ? d[2] : d[0], a1 = b4 ? d[3] : d[1];
+        const float s0 = b4 ? d[0] : d[2], s1 = b4 ? d[1] : d[3];
+        a0 += __shfl_xor_sync(FULL, s0, 16);
+        a1 += __shfl_xor_sync(FULL, s1, 16);
+        float x = b3 ? a1 : a0;
+        x += __shfl_xor_sync(FULL, b3 ? a0 : a1, 8);
+        x += __shfl_xor_sync(FULL, x, 4);
+        x += __shfl_xor_sync(FULL, x, 2);
+        x += __shfl_xor_sync(FULL, x, 1);
+        float alpha = 1.f;
+        if (x > m_own) {
+            alpha = safe_scale(m_own, x);
+            l_own *= alpha;
+            m_own = x;
+        }
+        const float pw = exp2f(x - m_own);
+        l_own += pw;
+        const bool grew = __any_sync(FULL, alpha != 1.f);
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const float pr = __shfl_sync(FULL, pw, 8 * r);
+            float2 axy = make_float2(acc[r].x, acc[r].y), azw = make_float2(acc[r].z, acc[r].w);
+            if (grew) {
+                const float ar = __shfl_sync(FULL, alpha, 8 * r);
+                axy = __fmul2_rn(axy, make_float2(ar, ar));
+                azw = __fmul2_rn(azw, make_float2(ar, ar));
+            }
+            axy = __ffma2_rn(make_float2(pr, pr), make_float2(v.x, v.y), axy);
+            azw = __ffma2_rn(make_float2(pr, pr), make_float2(v.z, v.w), azw);
+            acc[r] = make_float4(axy.x, axy.y, azw.x, azw.y);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    float* o = part + ((((size_t)p * gridDim.x + c) * 8 + warp) * G) * (DH + 2);
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        const float mr = __shfl_sync(FULL, m_own, 8 * r), lr = __shfl_sync(FULL, l_own, 8 * r);
+        float* orow = o + r * (DH + 2);
+        if (lane == 0) { orow[0] = mr; orow[1] = lr; }
+        orow[2 + 4 * lane + 0] = acc[r].x;
+        orow[2 + 4 * lane + 1] = acc[r].y;
+        orow[2 + 4 * lane + 2] = acc[r].z;
+        orow[2 + 4 * lane + 3] = acc[r].w;
+    }
+}
+
+
+// ---- W3: W2 with two rows per warp iteration (independent reduction chains interleaved) ----
+template <int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) gqa_w3(const float* __restrict__ K, const float* __restrict__ V,
+                                                    const int* __restrict__ rows, int per_cta, const float* __restrict__ Q,
+                                                    float scale_log2, float* part) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int p = blockIdx.y, c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    float4* ring = reinterpret_cast<float4*>(sm) + (size_t)warp * D * 64;
+    const int r0 = c * per_cta, n = max(0, min(per_cta, SEL - r0));
+    const int* rl = rows + (size_t)p * SEL + r0;
+    const float4* kb = reinterpret_cast<const float4*>(K + (size_t)p * S * DH);
+    const float4* vb = reinterpret_cast<const float4*>(V + (size_t)p * S * DH);
+    const uint64_t pol = evict_first();
+    const int mine = n > warp ? (n - warp + 7) / 8 : 0;
+    auto issue = [&](int it, int s) {
+        if (it < mine) {
+            const long long row = rl[warp + 8 * it];
+            cp16(ring + s * 64 + lane, kb + row * 32 + lane, pol);
+            cp16(ring + s * 64 + 32 + lane, vb + row * 32 + lane, pol);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int s = 0; s < D; ++s) issue(s, s);
+    float4 q[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        float4 v = reinterpret_cast<const float4*>(Q + ((size_t)p * G + r) * DH)[lane];
+        q[r] = make_float4(v.x * scale_log2, v.y * scale_log2, v.z * scale_log2, v.w * scale_log2);
+    }
+    const bool b4 = lane & 16, b3 = lane & 8;
+    float m_own = -INFINITY, l_own = 0.f;
+    float4 acc[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int it = 0; it < mine; it += 2) {
+        const bool two = it + 1 < mine;
+        const int s0 = it % D, s1 = (it + 1) % D;
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
+        const float4 k0 = ring[s0 * 64 + lane], v0 = ring[s0 * 64 + 32 + lane];
+        const float4 k1 = two ? ring[s1 * 64 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 v1 = two ? ring[s1 * 64 + 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        issue(it + D, s0);
+        issue(it + 1 + D, s1);
+        float x[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float4 k = h ? k1 : k0;
+            float d[G];
+#pragma unroll
+            for (int r = 0; r < G; ++r) d[r] = fmaf(q[r].x, k.x, fmaf(q[r].y, k.y, fmaf(q[r].z, k.z, q[r].w * k.w)));
+            float a0 = b4 ? d[2] : d[0], a1 = b4 ? d[3] : d[1];
+            const float s0_ = b4 ? d[0] : d[2], s1_ = b4 ? d[1] : d[3];
+            a0 += __shfl_xor_sync(FULL, s0_, 16);
+            a1 += __shfl_xor_sync(FULL, s1_, 16);
+            float xx = b3 ? a1 : a0;
+            xx += __shfl_xor_sync(FULL, b3 ? a0 : a1, 8);
+            xx += __shfl_xor_sync(FULL, xx, 4);
+            xx += __shfl_xor_sync(FULL, xx, 2);
+            xx += __shfl_xor_sync(FULL, xx, 1);
+            x[h] = xx;
+        }
+        if (!two) x[1] = -INFINITY;
+        const float mx = fmaxf(x[0], x[1]);
+        float alpha = 1.f;
+        if (mx > m_own) { alpha = safe_scale(m_own, mx); l_own *= alpha; m_own = mx; }
+        const float pw0 = exp2f(x[0] - m_own), pw1 = two ? exp2f(x[1] - m_own) : 0.f;
+        l_own += pw0 + pw1;
+        const bool grew = __any_sync(FULL, alpha != 1.f);
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const float p0 = __shfl_sync(FULL, pw0, 8 * r), p1 = __shfl_sync(FULL, pw1, 8 * r);
+            if (grew) {
+                const float ar = __shfl_sync(FULL, alpha, 8 * r);
+                acc[r].x *= ar; acc[r].y *= ar; acc[r].z *= ar; acc[r].w *= ar;
+            }
+            acc[r].x = fmaf(p0, v0.x, fmaf(p1, v1.x, acc[r].x));
+            acc[r].y = fmaf(p0, v0.y, fmaf(p1, v1.y, acc[r].y));
+            acc[r].z = fmaf(p0, v0.z, fmaf(p1, v1.z, acc[r].z));
+            acc[r].w = fmaf(p0, v0.w, fmaf(p1, v1.w, acc[r].w));
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    float* o = part + ((((size_t)p * gridDim.x + c) * 8 + warp) * G) * (DH + 2);
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        const float mr = __shfl_sync(FULL, m_own, 8 * r), lr = __shfl_sync(FULL, l_own, 8 * r);
+        float* orow = o + r * (DH + 2);
+        if (lane == 0) { orow[0] = mr; orow[1] = lr; }
+        orow[2 + 4 * lane + 0] = acc[r].x;
+        orow[2 + 4 * lane + 1] = acc[r].y;
+        orow[2 + 4 * lane + 2] = acc[r].z;
+        orow[2 + 4 * lane + 3] = acc[r].w;
+    }
+}
+
 // merge partials [P][n_parts][G][DH+2] -> out [P][G][DH]
 __global__ void merge(const float* part, int n_parts, float* out) {
     const int p = blockIdx.x / G, r = blockIdx.x % G, d = threadIdx.x;
@@ -385,7 +576,7 @@ int main() {
         for (size_t i = 0; i < ho.size(); ++i) { num = std::max(num, fabs(ho[i] - ref[i])); den = std::max(den, fabs(ref[i])); }
         printf("%-46s %8.1f us  %7.0f GB/s  rel err %.2e\n", name, ms * 1e3, bytes / (ms * 1e-3) / 1e9, num / den);
     };
-    for (int per : {205, 410, 820}) {
+    for (int per : {205, 410}) {
         const int nc = (SEL + per - 1) / per;
         dim3 grid(nc, P);
         char nm[128];
@@ -398,12 +589,9 @@ int main() {
             snprintf(nm, sizeof nm, "%s D=%d rows/CTA=%d", tag, D, per);
             run(nm, nc * 8, [&] { kern<<<grid, 256, smem>>>(K, V, drows, per, Q, sl, part); });
         };
-        runw(gqa_w2<2, 8>, 2, "W2 cp.async minB8");
-        runw(gqa_w2<3, 6>, 3, "W2 cp.async minB6");
-        runw(gqa_w2<3, 5>, 3, "W2 cp.async minB5");
         runw(gqa_w2<4, 4>, 4, "W2 cp.async minB4");
-        runw(gqa_w2<4, 5>, 4, "W2 cp.async minB5");
-        runw(gqa_w2<5, 4>, 5, "W2 cp.async minB4");
+        runw(gqa_w2p<4, 4>, 4, "W2P packed minB4");
+        runw(gqa_w2p<4, 5>, 4, "W2P packed minB5");
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
