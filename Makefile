@@ -16,7 +16,12 @@ HDRS := include/pqkv_c.h $(CSRC)/common.cuh $(CSRC)/internal.cuh $(CSRC)/select_
 .PHONY: all lib oracle clean
 all: lib oracle
 
-lib: $(LIB)
+CXX_E2E := paper_2407_12820_b200/lib/pqkv_cxx_e2e
+lib: $(LIB) $(CXX_E2E)
+
+# the run_e2e decode loop on the C++ drop-in API (bench.py's e2e_cxx line)
+$(CXX_E2E): tools/cxx_e2e.cpp $(LIB) $(CXXHDRS)
+	g++ -std=c++20 -O2 -Iinclude -o $@ $< -L$(dir $(LIB)) -lpqkv -Wl,-rpath,'$$ORIGIN'
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)

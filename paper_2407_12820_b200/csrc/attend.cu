@@ -1214,53 +1214,96 @@ __global__ void exact_scores_kernel(const float* queries, int G, int d_h, const 
     scores[(long long)pr * t + i] = (float)__dmul_rn(acc, scale);
 }
 
-// softmax_attention (attention.cpp:35-60) given the f32 scores.
-__global__ void softmax_exact_kernel(const float* scores, int G, int d_h, const float* values,
-                                     long long kv_head_stride, const int64_t* rows, int t,
-                                     double* w, float* out) {
-    const int pr = blockIdx.x, p = pr / G;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// softmax_attention (attention.cpp:35-60) given the f32 scores, in two
+// kernels: softmax_weights_kernel (max_element, exp of max-subtracted scores,
+// the serial fp64 total in row order, w / total) and weighted_sum_kernel
+// (acc[j] += w_i * v_ij in row order per output dim).  Same operations and
+// order as the reference; the serial chains read their operands from shared
+// memory / registers filled ahead of them, so they run at add latency.
+constexpr int SW_THREADS = 1024, SW_CHUNK = 4096;
+
+__global__ void __launch_bounds__(SW_THREADS) softmax_weights_kernel(const float* scores, int t, double* w) {
+    const int pr = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float* sc = scores + (long long)pr * t;
     double* wr = w + (long long)pr * t;
     __shared__ float smax[32];
+    __shared__ double buf[SW_CHUNK];
     __shared__ double stotal;
-    // max_element: first maximal f32 score
     float mx = -INFINITY;
-    for (int i = tid; i < t; i += blockDim.x) mx = fmaxf(mx, sc[i]);
+    for (int i = tid; i < t; i += SW_THREADS) mx = fmaxf(mx, sc[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
     if (lane == 0) smax[warp] = mx;
     __syncthreads();
     if (tid == 0) {
         float v = smax[0];
-        for (int e = 1; e < (int)(blockDim.x >> 5); ++e) v = fmaxf(v, smax[e]);
+        for (int e = 1; e < SW_THREADS / 32; ++e) v = fmaxf(v, smax[e]);
         smax[0] = v;
     }
     __syncthreads();
     const double max_score = (double)smax[0];
-    for (int i = tid; i < t; i += blockDim.x) wr[i] = exp(__dsub_rn((double)sc[i], max_score));
-    __syncthreads();
-    if (warp == 0) {  // serial total in row order
-        double total = 0.0;
-        for (int i0 = 0; i0 < t; i0 += 32) {
-            double v = (i0 + lane < t) ? wr[i0 + lane] : 0.0;
-            int cnt = min(32, t - i0);
-            for (int e = 0; e < cnt; ++e) total = __dadd_rn(total, __shfl_sync(FULL, v, e));
+    double total = 0.0;  // thread 0's serial running total
+    for (int c0 = 0; c0 < t; c0 += SW_CHUNK) {
+        const int cnt = min(SW_CHUNK, t - c0);
+        for (int i = tid; i < cnt; i += SW_THREADS) {
+            const double e = exp(__dsub_rn((double)sc[c0 + i], max_score));
+            buf[i] = e;
+            wr[c0 + i] = e;
         }
-        if (lane == 0) stotal = total;
+        __syncthreads();
+        if (tid == 0) {
+            int i = 0;
+            for (; i + 8 <= cnt; i += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = buf[i + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) total = __dadd_rn(total, v[u]);
+            }
+            for (; i < cnt; ++i) total = __dadd_rn(total, buf[i]);
+        }
+        __syncthreads();
     }
+    if (tid == 0) stotal = total;
     __syncthreads();
-    const double total = stotal;
-    for (int i = tid; i < t; i += blockDim.x) wr[i] = __ddiv_rn(wr[i], total);
-    __syncthreads();
+    const double tot = stotal;
+    for (int i = tid; i < t; i += SW_THREADS) wr[i] = __ddiv_rn(wr[i], tot);
+}
+
+// one CTA per (head, query row) x 32-dim group; thread = output dim
+constexpr int WS_DIMS = 32, WS_TILE = 2048;
+
+__global__ void __launch_bounds__(WS_DIMS) weighted_sum_kernel(int G, int d_h, const float* values,
+                                                               long long kv_head_stride, const int64_t* rows, int t,
+                                                               const double* w, float* out) {
+    const int pr = blockIdx.x, p = pr / G, j = blockIdx.y * WS_DIMS + threadIdx.x;
     const float* vb = values + p * kv_head_stride;
     const int64_t* rr = rows + (long long)p * t;
-    for (int j = tid; j < d_h; j += blockDim.x) {
-        double accv = 0.0;
-        for (int i = 0; i < t; ++i)
-            accv = __dadd_rn(accv, __dmul_rn(wr[i], (double)__ldg(vb + rr[i] * d_h + j)));
-        out[(long long)pr * d_h + j] = (float)accv;
+    const double* wr = w + (long long)pr * t;
+    __shared__ int ids[WS_TILE];
+    __shared__ double ws[WS_TILE];
+    double acc = 0.0;
+    const bool live = j < d_h;
+    for (int c0 = 0; c0 < t; c0 += WS_TILE) {
+        const int cnt = min(WS_TILE, t - c0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += WS_DIMS) {
+            ids[i] = (int)rr[c0 + i];
+            ws[i] = wr[c0 + i];
+        }
+        __syncthreads();
+        if (!live) continue;
+        int i = 0;
+        for (; i + 32 <= cnt; i += 32) {
+            float v[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = __ldg(vb + (long long)ids[i + u] * d_h + j);
+#pragma unroll
+            for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, __dmul_rn(ws[i + u], (double)v[u]));
+        }
+        for (; i < cnt; ++i) acc = __dadd_rn(acc, __dmul_rn(ws[i], (double)__ldg(vb + (long long)ids[i] * d_h + j)));
     }
+    if (live) out[(long long)pr * d_h + j] = (float)acc;
 }
 
 // bitmap -> ascending row list (init ++ selected ++ local), one CTA per head
@@ -1312,11 +1355,12 @@ void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_
     exact_scores_kernel<<<g1, 128, 0, st>>>(queries, (int)G, (int)d_h, keys, (long long)kv_head_stride,
                                            rows, (int)t, scale, scores);
     PQKV_LAUNCHED("exact_scores_kernel");
-    int threads = (int)std::min<size_t>(1024, std::max<size_t>(128, round_up(d_h, 32)));
-    softmax_exact_kernel<<<(unsigned)(P * G), threads, 0, st>>>(scores, (int)G, (int)d_h, values,
-                                                               (long long)kv_head_stride, rows,
-                                                               (int)t, w, out);
-    PQKV_LAUNCHED("softmax_exact_kernel");
+    softmax_weights_kernel<<<(unsigned)(P * G), SW_THREADS, 0, st>>>(scores, (int)t, w);
+    PQKV_LAUNCHED("softmax_weights_kernel");
+    dim3 g2((unsigned)(P * G), (unsigned)ceil_div(d_h, WS_DIMS));
+    weighted_sum_kernel<<<g2, WS_DIMS, 0, st>>>((int)G, (int)d_h, values, (long long)kv_head_stride, rows, (int)t, w,
+                                               out);
+    PQKV_LAUNCHED("weighted_sum_kernel");
 }
 
 // Chunk geometry: all CTAs resident in one wave where possible (the gather
