@@ -623,6 +623,21 @@ def main():
     }
     clk.stop()
     line["clocks"] = clk.summary()
+    if rank == 0 and not args.no_extra:
+        # the reference's run_e2e decode loop on the C++ drop-in API
+        # (include/pqkv/*.hpp: evict_local_append, pq_score_gqa, approx_topk,
+        # fetch_topk, selective_attention per head, value semantics, fp64
+        # attention), timed per layer-step by tools/cxx_e2e.cpp
+        import subprocess
+
+        exe = os.path.join(ROOT, "paper_2407_12820_b200", "lib", "pqkv_cxx_e2e")
+        try:
+            r = subprocess.run([exe, "8", "32768", "1", "5", "3"], capture_output=True, text=True, timeout=300)
+            line["e2e_cxx"] = json.loads(r.stdout.strip().splitlines()[-1])
+            line["e2e_cxx"]["what"] = ("run_e2e's per-head decode calls through the C++ drop-in API (host value "
+                                       "types, device mirrors), 8 heads x 32K, m2b6, k = s/5, us per layer-step")
+        except Exception as e:  # reported, not fatal
+            line["e2e_cxx"] = {"error": repr(e)[:200]}
     if rank == 0 and not args.no_cpu_baseline:
         gl, gqs, _ = heads["gaussian"]
         words = torch.zeros((H, (S_MID + 31) // 32), dtype=torch.int32, device=dev)
