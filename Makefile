@@ -9,8 +9,9 @@ CSRC := paper_2407_12820_b200/csrc
 OBJDIR ?= build/obj
 LIB ?= paper_2407_12820_b200/lib/libpqkv.so
 CU := ctx capi kmeans select attend step blocks workload collective metrics
-CXXSRC := api kv_store_host pqt_io shape
+CXXSRC := api kv_store_host pqt_io shape host_pool
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CXXSRC)))
+CXXHDRS := $(wildcard include/pqkv/*.hpp) include/pqkv_c.h $(CSRC)/runtime_internal.hpp
 HDRS := include/pqkv_c.h $(CSRC)/common.cuh $(CSRC)/internal.cuh $(CSRC)/select_common.cuh
 
 .PHONY: all lib oracle clean
@@ -27,14 +28,13 @@ $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-CXXHDRS := $(wildcard include/pqkv/*.hpp) include/pqkv_c.h $(CSRC)/runtime_internal.hpp
 $(OBJDIR)/%.o: $(CSRC)/%.cpp $(CXXHDRS)
 	@mkdir -p $(OBJDIR)
 	g++ -std=c++20 -O2 -Wall -Wextra -fPIC -fvisibility=hidden -Iinclude -I$(CSRC) -c $< -o $@
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -ldl -Xlinker --exclude-libs,ALL
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -ldl -lpthread -Xlinker --exclude-libs,ALL
 
 oracle:
 	$(MAKE) -C oracle

@@ -675,6 +675,19 @@ def main():
                                        "types, device mirrors), 8 heads x 32K, m2b6, k = s/5, us per layer-step")
         except Exception as e:  # reported, not fatal
             line["e2e_cxx"] = {"error": repr(e)[:200]}
+        # the same decode loop built entirely from the reference's sources
+        # (oracle/Makefile cxx_e2e_ref), timed on the host cores: the CPU arm
+        ref_exe = os.path.join(ROOT, "oracle", "_ref", "dropin", "cxx_e2e_ref")
+        if not args.no_cpu_baseline and "error" not in line["e2e_cxx"] and os.path.exists(ref_exe):
+            try:
+                r = subprocess.run([ref_exe, "4", "32768", "1", "5", "2"], capture_output=True, text=True,
+                                   timeout=600)
+                ref = json.loads(r.stdout.strip().splitlines()[-1])
+                line["e2e_cxx"]["cpu_baseline"] = {
+                    "kind": "reference", "cores": 1, "sample": "4 heads x 32K, 2 decode steps (per-head-step "
+                    "comparable)", "us_per_head_step": ref["us_per_head_step"], "per_call_us": ref["per_call_us"]}
+            except Exception as e:
+                line["e2e_cxx"]["cpu_baseline"] = {"error": repr(e)[:200]}
     if rank == 0 and not args.no_cpu_baseline:
         gl, gqs, _ = heads["gaussian"]
         words = torch.zeros((H, (S_MID + 31) // 32), dtype=torch.int32, device=dev)

@@ -13,6 +13,8 @@
 //     new rows and each call's query/result across PCIe.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <list>
@@ -192,6 +194,36 @@ void CallScratch::copy_h2d(void* d, const void* h, std::size_t bytes) {
     if (bytes) check(pqkv_copy(t_rt.slots[slot_].ctx, d, h, bytes, 0));
 }
 
+namespace {
+struct PhaseTotals {
+    double us[kPhases] = {};
+    long calls[kPhases] = {};
+    ~PhaseTotals() {
+        if (!api_profile()) return;
+        static const char* names[kPhases] = {"sa_prep", "sa_mirror", "sa_compute", "ft_rank",
+                                             "ft_account", "ft_entries", "ft_admit"};
+        std::fprintf(stderr, "{\"api_profile_us\": {");
+        for (int i = 0; i < kPhases; ++i)
+            std::fprintf(stderr, "%s\"%s\": [%.1f, %ld]", i ? ", " : "", names[i], us[i], calls[i]);
+        std::fprintf(stderr, "}}\n");
+    }
+};
+PhaseTotals g_phases;
+}  // namespace
+
+bool api_profile() {
+    static const bool on = [] {
+        const char* e = std::getenv("PQKV_API_PROFILE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+
+void phase_add(Phase p, double us) {
+    g_phases.us[p] += us;
+    ++g_phases.calls[p];
+}
+
 void copy_to_host(void* host, const void* dev, std::size_t bytes) {
     if (bytes) check(pqkv_copy(t_rt.slot().ctx, host, dev, bytes, 1));
 }
@@ -235,7 +267,8 @@ IndexView mirror(const PqIndex& index) {
     if (rows > mr.rows) {
         const std::size_t row_bytes = m * sizeof(std::uint16_t);
         if (mr.d_codes.bytes < rows * row_bytes)
-            grow_buf(s.ctx, mr.d_codes, std::max(rows * row_bytes, 2 * mr.d_codes.bytes), mr.rows * row_bytes);
+            grow_buf(s.ctx, mr.d_codes, std::max((rows + rows / 4 + 4096) * row_bytes, 2 * mr.d_codes.bytes),
+                     mr.rows * row_bytes);
         check(pqkv_copy(s.ctx, static_cast<char*>(mr.d_codes.p) + mr.rows * row_bytes,
                         index.codes.data() + mr.rows * m, (rows - mr.rows) * row_bytes, 0));
         mr.rows = rows;
@@ -304,7 +337,9 @@ StateView mirror(const HeadState& st, std::size_t d_h, std::span<const std::int6
     }
     const std::size_t need = st.total_tokens;
     if (mr.cap_tokens < need) {
-        const std::size_t cap = std::max(need, mr.cap_tokens + mr.cap_tokens / 2);
+        // headroom: decode appends one token per step; a regrow is a
+        // cudaMalloc + D2D copy + cudaFree of the whole mirror
+        const std::size_t cap = std::max(need + need / 4 + 1024, mr.cap_tokens + mr.cap_tokens / 2);
         grow_buf(s.ctx, mr.d_k, cap * d_h * sizeof(float), mr.cap_tokens * d_h * sizeof(float));
         grow_buf(s.ctx, mr.d_v, cap * d_h * sizeof(float), mr.cap_tokens * d_h * sizeof(float));
         mr.cap_tokens = cap;
@@ -352,14 +387,21 @@ BlockRanking rank_blocks(std::span<const std::size_t> ids, std::size_t n_tokens,
     CallScratch sc;
     std::vector<std::int64_t> h_ids(ids.begin(), ids.end());
     const std::int64_t* d_ids = sc.upload(h_ids.data(), h_ids.size());
-    auto* d_bits = sc.alloc<std::uint32_t>(words);
-    auto* d_counts = sc.alloc<std::uint32_t>(n_blocks);
-    auto* d_ranked = sc.alloc<std::int64_t>(k_rank);
+    // the three results packed in one scratch span: one device->host copy
+    const std::size_t o_counts = (words * 4 + 255) & ~std::size_t{255};
+    const std::size_t o_ranked = o_counts + ((n_blocks * 4 + 255) & ~std::size_t{255});
+    const std::size_t span = o_ranked + k_rank * 8;
+    char* d_out = sc.alloc<char>(span);
+    auto* d_bits = reinterpret_cast<std::uint32_t*>(d_out);
+    auto* d_counts = reinterpret_cast<std::uint32_t*>(d_out + o_counts);
+    auto* d_ranked = reinterpret_cast<std::int64_t*>(d_out + o_ranked);
     check(pqkv_block_rank(t_rt.slot().ctx, d_ids, 1, h_ids.size(), h_ids.size(), n_tokens, block_size, k_rank,
                           d_bits, d_counts, d_ranked, nullptr, nullptr));
-    copy_to_host(br.bits.data(), d_bits, words * 4);
-    copy_to_host(br.counts.data(), d_counts, n_blocks * 4);
-    copy_to_host(br.ranked.data(), d_ranked, k_rank * 8);
+    std::vector<char> h_out(span);
+    copy_to_host(h_out.data(), d_out, span);
+    std::memcpy(br.bits.data(), h_out.data(), words * 4);
+    std::memcpy(br.counts.data(), h_out.data() + o_counts, n_blocks * 4);
+    std::memcpy(br.ranked.data(), h_out.data() + o_ranked, k_rank * 8);
     return br;
 }
 
@@ -649,10 +691,30 @@ std::vector<float> softmax_attention(std::span<const float> query, const TensorF
 
 std::vector<float> selective_attention(std::span<const float> query, const HeadState& state,
                                        std::span<const std::size_t> selected_middle_ids) {
-    std::vector<std::size_t> ids(selected_middle_ids.begin(), selected_middle_ids.end());
-    std::sort(ids.begin(), ids.end());
-    if (std::adjacent_find(ids.begin(), ids.end()) != ids.end())
-        throw std::invalid_argument("attention: duplicate middle token id");
+    detail::PhaseTimer pt;
+    // ascending, duplicate-free ids: a bitmap over the token ids (all ids are
+    // < total_tokens in any valid call; otherwise sort)
+    std::vector<std::size_t> ids;
+    ids.reserve(selected_middle_ids.size());
+    const std::size_t n_tok = state.total_tokens;
+    if (std::all_of(selected_middle_ids.begin(), selected_middle_ids.end(),
+                    [&](std::size_t id) { return id < n_tok; })) {
+        std::vector<std::uint64_t> seen((n_tok + 63) / 64, 0);
+        for (std::size_t id : selected_middle_ids) {
+            std::uint64_t& w = seen[id >> 6];
+            const std::uint64_t bit = std::uint64_t{1} << (id & 63);
+            if (w & bit) throw std::invalid_argument("attention: duplicate middle token id");
+            w |= bit;
+        }
+        for (std::size_t wi = 0; wi < seen.size(); ++wi)
+            for (std::uint64_t w = seen[wi]; w; w &= w - 1)
+                ids.push_back(wi * 64 + static_cast<std::size_t>(__builtin_ctzll(w)));
+    } else {
+        ids.assign(selected_middle_ids.begin(), selected_middle_ids.end());
+        std::sort(ids.begin(), ids.end());
+        if (std::adjacent_find(ids.begin(), ids.end()) != ids.end())
+            throw std::invalid_argument("attention: duplicate middle token id");
+    }
     const std::size_t d_h = query.size();
     const std::size_t t = state.init_entries.size() + ids.size() + state.local.size();
     if (t == 0 || d_h == 0) throw std::invalid_argument("tensor: zero-sized dimension");
@@ -678,7 +740,9 @@ std::vector<float> selective_attention(std::span<const float> query, const HeadS
     if (std::any_of(state.init_entries.begin(), state.init_entries.end(), bad_dim) ||
         std::any_of(state.local.begin(), state.local.end(), [&](const auto& lt) { return bad_dim(lt.second); }))
         throw std::invalid_argument("attention: entry dim mismatch");
+    pt.lap(detail::kSaPrep);
     const detail::StateView sv = detail::mirror(state, d_h, rows);
+    pt.lap(detail::kSaMirror);
     CallScratch sc;
     const float* dq = sc.upload(query.data(), d_h);
     const std::int64_t* dr = sc.upload(rows.data(), t);
@@ -687,6 +751,7 @@ std::vector<float> selective_attention(std::span<const float> query, const HeadS
                            nullptr));
     std::vector<float> out(d_h);
     copy_to_host(out.data(), dout, d_h * 4);
+    pt.lap(detail::kSaCompute);
     return out;
 }
 

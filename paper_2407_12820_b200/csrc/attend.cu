@@ -1219,10 +1219,10 @@ __global__ void exact_scores_kernel(const float* queries, int G, int d_h, const 
     scores[(long long)pr * t + i] = (float)__dmul_rn(acc, scale);
 }
 
-// softmax_attention (attention.cpp:35-60) given the f32 scores, in two
-// kernels: softmax_weights_kernel (max_element, exp of max-subtracted scores,
-// the serial fp64 total in row order, w / total) and weighted_sum_kernel
-// (acc[j] += w_i * v_ij in row order per output dim).  Same operations and
+// softmax_attention (attention.cpp:35-60) given the f32 scores:
+// softmax_weights_kernel (max_element, exp of max-subtracted scores, the
+// serial fp64 total in row order, w / total), then weighted_products_kernel +
+// sum_chain_kernel (acc[j] += w_i * v_ij in row order per output dim).  Same operations and
 // order as the reference; the serial chains read their operands from shared
 // memory / registers filled ahead of them, so they run at add latency.
 constexpr int SW_THREADS = 1024, SW_CHUNK = 4096;
@@ -1275,40 +1275,81 @@ __global__ void __launch_bounds__(SW_THREADS) softmax_weights_kernel(const float
     for (int i = tid; i < t; i += SW_THREADS) wr[i] = __ddiv_rn(wr[i], tot);
 }
 
-// one CTA per (head, query row) x 32-dim group; thread = output dim
-constexpr int WS_DIMS = 32, WS_TILE = 2048;
+// The output sum is one serial fp64 chain per (query row, dim): acc +=
+// w_i * v_ij in row order.  The products are independent, so
+// weighted_products_kernel forms them with the whole GPU (the row gather)
+// into a [dim group][rows][32] fp64 block, and sum_chain_kernel runs the
+// chains: one warp per 32 dims, lane = dim, the group's contiguous rows
+// streamed through a shared-memory ring by bulk copies (one lane issues one
+// cp.async.bulk per 32-row stage, completion on an mbarrier) SC_STAGES
+// stages ahead of the adds, so each add waits only on the previous one.
+constexpr int SC_DIMS = 32, SC_STAGE = 32, SC_STAGES = 16;  // 16 x 32 rows x 256 B = 128 KB ring
+constexpr size_t SC_SMEM = (size_t)SC_STAGES * SC_STAGE * SC_DIMS * sizeof(double) + SC_STAGES * 8;
 
-__global__ void __launch_bounds__(WS_DIMS) weighted_sum_kernel(int G, int d_h, const float* values,
-                                                               long long kv_head_stride, const int64_t* rows, int t,
-                                                               const double* w, float* out) {
-    const int pr = blockIdx.x, p = pr / G, j = blockIdx.y * WS_DIMS + threadIdx.x;
+__global__ void weighted_products_kernel(int G, int d_h, int ldp, const float* values, long long kv_head_stride,
+                                         const int64_t* rows, int t, const double* w, int pr0, double* prod) {
+    const int pr = pr0 + blockIdx.y, p = pr / G;
+    const long long n = (long long)t * ldp;
     const float* vb = values + p * kv_head_stride;
     const int64_t* rr = rows + (long long)p * t;
     const double* wr = w + (long long)pr * t;
-    __shared__ int ids[WS_TILE];
-    __shared__ double ws[WS_TILE];
-    double acc = 0.0;
-    const bool live = j < d_h;
-    for (int c0 = 0; c0 < t; c0 += WS_TILE) {
-        const int cnt = min(WS_TILE, t - c0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += WS_DIMS) {
-            ids[i] = (int)rr[c0 + i];
-            ws[i] = wr[c0 + i];
-        }
-        __syncthreads();
-        if (!live) continue;
-        int i = 0;
-        for (; i + 32 <= cnt; i += 32) {
-            float v[32];
-#pragma unroll
-            for (int u = 0; u < 32; ++u) v[u] = __ldg(vb + (long long)ids[i + u] * d_h + j);
-#pragma unroll
-            for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, __dmul_rn(ws[i + u], (double)v[u]));
-        }
-        for (; i < cnt; ++i) acc = __dadd_rn(acc, __dmul_rn(ws[i], (double)__ldg(vb + (long long)ids[i] * d_h + j)));
+    double* out = prod + (long long)blockIdx.y * n;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / ldp), j = (int)(e - (long long)i * ldp);
+        const double v = j < d_h ? __dmul_rn(wr[i], (double)__ldg(vb + rr[i] * d_h + j)) : 0.0;
+        out[((long long)(j / SC_DIMS) * t + i) * SC_DIMS + (j % SC_DIMS)] = v;
     }
-    if (live) out[(long long)pr * d_h + j] = (float)acc;
+}
+
+__global__ void __launch_bounds__(SC_DIMS) sum_chain_kernel(int d_h, int ldp, int t, const double* prod, int pr0,
+                                                            float* out) {
+    extern __shared__ __align__(128) double ring[];  // [SC_STAGES][SC_STAGE][SC_DIMS], then the mbarriers
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)SC_STAGES * SC_STAGE * SC_DIMS);
+    const int lane = threadIdx.x, j0 = blockIdx.x * SC_DIMS;
+    const double* src = prod + ((long long)blockIdx.y * ldp / SC_DIMS + blockIdx.x) * (long long)t * SC_DIMS;
+    const int n_stages = (t + SC_STAGE - 1) / SC_STAGE;
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring), full_s = (unsigned)__cvta_generic_to_shared(full);
+    if (lane == 0) {
+        for (int b = 0; b < SC_STAGES; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_s + b * 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int s) {  // lane 0: stage s into slot s % SC_STAGES
+        if (s >= n_stages) return;
+        const int slot = s % SC_STAGES;
+        const unsigned bytes = (unsigned)(min(SC_STAGE, t - s * SC_STAGE) * SC_DIMS * sizeof(double));
+        const unsigned bar = full_s + slot * 8, dst = ring_s + slot * (SC_STAGE * SC_DIMS * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(src + (long long)s * SC_STAGE * SC_DIMS), "r"(bytes), "r"(bar) : "memory");
+    };
+    if (lane == 0)
+        for (int s = 0; s < SC_STAGES; ++s) issue(s);
+    double acc = 0.0;
+#pragma unroll 1
+    for (int s = 0; s < n_stages; ++s) {
+        const int slot = s % SC_STAGES;
+        const unsigned parity = (unsigned)(s / SC_STAGES) & 1u;
+        unsigned done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(full_s + slot * 8), "r"(parity) : "memory");
+        const double* cur = ring + (size_t)slot * SC_STAGE * SC_DIMS + lane;
+        const int cnt = min(SC_STAGE, t - s * SC_STAGE);
+        if (cnt == SC_STAGE) {
+            double v[SC_STAGE];
+#pragma unroll
+            for (int u = 0; u < SC_STAGE; ++u) v[u] = cur[u * SC_DIMS];
+#pragma unroll
+            for (int u = 0; u < SC_STAGE; ++u) acc = __dadd_rn(acc, v[u]);
+        } else {
+            for (int u = 0; u < cnt; ++u) acc = __dadd_rn(acc, cur[u * SC_DIMS]);
+        }
+        __syncwarp();  // every lane is done with slot s % SC_STAGES ...
+        if (lane == 0) issue(s + SC_STAGES);  // ... before it is refilled
+    }
+    if (j0 + lane < d_h) out[(long long)(pr0 + blockIdx.y) * d_h + j0 + lane] = (float)acc;
 }
 
 // bitmap -> ascending row list (init ++ selected ++ local), one CTA per head
@@ -1350,11 +1391,15 @@ __global__ void bitmap_rows_kernel(const uint32_t* bitmap, int words, int n_init
 void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_t d_h,
                   const float* keys, const float* values, size_t kv_head_stride,
                   const int64_t* rows, size_t t, float* out, cudaStream_t st) {
+    // the product block of up to `batch` (head, query row) pairs at a time
+    const size_t ldp = round_up(d_h, (size_t)SC_DIMS), per_pr = t * ldp;
+    const size_t batch = std::max<size_t>(1, std::min(P * G, (size_t(256) << 20) / (per_pr * sizeof(double))));
     Scratch sc(ctx);
-    size_t h_s = sc.plan<float>(P * G * t), h_w = sc.plan<double>(P * G * t);
+    size_t h_s = sc.plan<float>(P * G * t), h_w = sc.plan<double>(P * G * t), h_p = sc.plan<double>(batch * per_pr);
     sc.commit();
     float* scores = sc.get<float>(h_s);
     double* w = sc.get<double>(h_w);
+    double* prod = sc.get<double>(h_p);
     double scale = 1.0 / std::sqrt(static_cast<double>(d_h));
     dim3 g1((unsigned)ceil_div(t, 128), (unsigned)(P * G));
     exact_scores_kernel<<<g1, 128, 0, st>>>(queries, (int)G, (int)d_h, keys, (long long)kv_head_stride,
@@ -1362,10 +1407,18 @@ void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_
     PQKV_LAUNCHED("exact_scores_kernel");
     softmax_weights_kernel<<<(unsigned)(P * G), SW_THREADS, 0, st>>>(scores, (int)t, w);
     PQKV_LAUNCHED("softmax_weights_kernel");
-    dim3 g2((unsigned)(P * G), (unsigned)ceil_div(d_h, WS_DIMS));
-    weighted_sum_kernel<<<g2, WS_DIMS, 0, st>>>((int)G, (int)d_h, values, (long long)kv_head_stride, rows, (int)t, w,
-                                               out);
-    PQKV_LAUNCHED("weighted_sum_kernel");
+    for (size_t pr0 = 0; pr0 < P * G; pr0 += batch) {
+        const size_t nb = std::min(batch, P * G - pr0);
+        const unsigned gx = (unsigned)std::min<size_t>(ceil_div(per_pr, 256), 4 * (size_t)ctx->sm_count);
+        weighted_products_kernel<<<dim3(gx, (unsigned)nb), 256, 0, st>>>((int)G, (int)d_h, (int)ldp, values,
+                                                                         (long long)kv_head_stride, rows, (int)t, w,
+                                                                         (int)pr0, prod);
+        PQKV_LAUNCHED("weighted_products_kernel");
+        PQKV_CUDA(cudaFuncSetAttribute(sum_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SC_SMEM));
+        sum_chain_kernel<<<dim3((unsigned)(ldp / SC_DIMS), (unsigned)nb), SC_DIMS, SC_SMEM, st>>>(
+            (int)d_h, (int)ldp, (int)t, prod, (int)pr0, out);
+        PQKV_LAUNCHED("sum_chain_kernel");
+    }
 }
 
 // Chunk geometry: all CTAs resident in one wave where possible (the gather

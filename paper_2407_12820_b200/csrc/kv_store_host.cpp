@@ -108,6 +108,7 @@ void KvStore::make_room(HeadState& st, std::size_t incoming_tokens) {
         auto victim = std::min_element(st.cache.begin(), st.cache.end(),
                                        [&](const auto& a, const auto& b) { return rank(a) < rank(b); });
         st.occupancy_tokens -= victim->second.snapshot.size();
+        retired_.push_back(std::move(victim->second.snapshot));
         st.cache.erase(victim);
     }
 }
@@ -115,20 +116,23 @@ void KvStore::make_room(HeadState& st, std::size_t incoming_tokens) {
 // (Re)admits one ranked block: a fresh snapshot of its middle tokens; a block
 // already cached keeps its counters (so a stale snapshot heals); a block
 // larger than the whole cache is dropped.
-void KvStore::admit_block(HeadState& st, std::size_t block_id) {
+void KvStore::admit_block(HeadState& st, std::size_t block_id, std::map<std::size_t, KvEntry>&& snapshot) {
     HeadState::CachedBlock blk;
-    for (std::size_t id = block_id * block_size_, end = id + block_size_; id < end; ++id)
-        if (auto m = st.middle.find(id); m != st.middle.end()) blk.snapshot.emplace(id, m->second);
+    blk.snapshot = std::move(snapshot);
     bool refreshed = false;
     if (auto old = st.cache.find(block_id); old != st.cache.end()) {
         blk.freq = old->second.freq;
         blk.last_used = old->second.last_used;
         st.occupancy_tokens -= old->second.snapshot.size();
+        retired_.push_back(std::move(old->second.snapshot));
         st.cache.erase(old);
         refreshed = true;
     }
     const std::size_t tokens = blk.snapshot.size();
-    if (tokens > cache_capacity_) return;
+    if (tokens > cache_capacity_) {
+        retired_.push_back(std::move(blk.snapshot));
+        return;
+    }
     make_room(st, tokens);
     if (!refreshed) {
         blk.freq = 1;
@@ -140,6 +144,7 @@ void KvStore::admit_block(HeadState& st, std::size_t block_id) {
 
 FetchReport KvStore::fetch_topk(std::size_t layer, std::size_t kv_head, std::span<const std::size_t> token_ids,
                                 std::size_t k_cache) {
+    detail::PhaseTimer pt;
     HeadState& st = states_[slot(layer, kv_head)];
     for (std::size_t id : token_ids)
         if (!st.middle.contains(id))
@@ -149,6 +154,7 @@ FetchReport KvStore::fetch_topk(std::size_t layer, std::size_t kv_head, std::spa
     // (1) request analysis on the GPU
     const std::size_t bs = block_size_, n_tokens = st.total_tokens;
     const detail::BlockRanking br = detail::rank_blocks(token_ids, n_tokens, bs, k_cache);
+    pt.lap(detail::kFtRank);
 
     // (2) one lookup per touched block, ascending block id
     FetchReport rep;
@@ -176,16 +182,37 @@ FetchReport KvStore::fetch_topk(std::size_t layer, std::size_t kv_head, std::spa
     st.misses += rep.misses;
     st.requests += touched;
 
+    pt.lap(detail::kFtAccount);
     // entries come from the middle segment (cache snapshots are copies of it)
-    rep.entries.reserve(token_ids.size());
-    std::transform(token_ids.begin(), token_ids.end(), std::back_inserter(rep.entries),
-                   [&](std::size_t id) { return st.middle.at(id); });
+    // (thousands of KvEntry copies: spread over the host worker pool)
+    rep.entries.resize(token_ids.size());
+    detail::parallel_for(token_ids.size(), 256, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) rep.entries[i] = st.middle.find(token_ids[i])->second;  // ids checked above
+    });
 
+    pt.lap(detail::kFtEntries);
     // (3) admission of this request's top-k_cache blocks
-    for (std::int64_t b : br.ranked) {
-        if (b < 0) break;
-        admit_block(st, static_cast<std::size_t>(b));
-    }
+    // snapshots first (copies of the middle tokens, built in parallel), then
+    // the sequential cache-state updates in rank order
+    std::size_t n_ranked = 0;
+    while (n_ranked < br.ranked.size() && br.ranked[n_ranked] >= 0) ++n_ranked;
+    std::vector<std::map<std::size_t, KvEntry>> snaps(n_ranked);
+    detail::parallel_for(n_ranked, 1, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t r = lo; r < hi; ++r) {
+            const std::size_t b0 = static_cast<std::size_t>(br.ranked[r]) * bs;
+            for (std::size_t id = b0; id < b0 + bs; ++id)
+                if (auto m = st.middle.find(id); m != st.middle.end()) snaps[r].emplace_hint(snaps[r].end(), id, m->second);
+        }
+    });
+    for (std::size_t r = 0; r < n_ranked; ++r)
+        admit_block(st, static_cast<std::size_t>(br.ranked[r]), std::move(snaps[r]));
+    // snapshots replaced or evicted above: thousands of KvEntry frees, spread
+    // over the host worker pool
+    detail::parallel_for(retired_.size(), 1, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) retired_[i].clear();
+    });
+    retired_.clear();
+    pt.lap(detail::kFtAdmit);
     return rep;
 }
 

@@ -3,8 +3,10 @@
 // mirrors of long-lived reference objects (PqIndex, HeadState).
 #pragma once
 
+#include <chrono>
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <span>
 #include <vector>
 
@@ -13,6 +15,32 @@
 #include "pqkv_c.h"
 
 namespace pqkv::detail {
+
+// fn(begin, end) over [0, n) in chunks of >= grain on the host worker pool
+// (host_pool.cpp); the calling thread takes chunks too.
+void parallel_for(std::size_t n, std::size_t grain, const std::function<void(std::size_t, std::size_t)>& fn);
+
+// Host-side phase timing of the drop-in calls (PQKV_API_PROFILE=1: per-phase
+// totals in microseconds printed to stderr at exit).  Diagnostics only.
+enum Phase { kSaPrep, kSaMirror, kSaCompute, kFtRank, kFtAccount, kFtEntries, kFtAdmit, kPhases };
+bool api_profile();
+void phase_add(Phase p, double us);
+class PhaseTimer {
+public:
+    PhaseTimer() : on_(api_profile()) {
+        if (on_) t_ = std::chrono::steady_clock::now();
+    }
+    void lap(Phase p) {
+        if (!on_) return;
+        const auto now = std::chrono::steady_clock::now();
+        phase_add(p, std::chrono::duration<double, std::micro>(now - t_).count());
+        t_ = now;
+    }
+
+private:
+    bool on_;
+    std::chrono::steady_clock::time_point t_;
+};
 
 [[noreturn]] void rethrow(int rc, const char* what);
 inline void check(int rc) {

@@ -11,7 +11,12 @@
 #include <random>
 #include <vector>
 
-#include "pqkv/pqkv.hpp"
+#include "pqkv/attention.hpp"
+#include "pqkv/kv_store.hpp"
+#include "pqkv/model.hpp"
+#include "pqkv/pq.hpp"
+#include "pqkv/tensor.hpp"
+#include "pqkv/topk.hpp"
 
 using namespace pqkv;
 
