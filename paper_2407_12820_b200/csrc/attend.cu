@@ -75,7 +75,9 @@ struct AtArgs {
     int t;
     float scale_log2;    // log2(e) / sqrt(d_h)
     float* part;         // [P][n_chunks][G][DH + 2]
-    unsigned* arrivals;  // [P] zero on entry; reset by the combining CTA
+    float* part2;        // two-level merge: [P][n_groups][G][DH + 2] group partials, else null
+    int n_groups;        // two-level merge: ceil(n_chunks / MERGE_GROUP)
+    unsigned* arrivals;  // [P] (+ [P][n_groups] two-level) zero on entry; reset by the combining CTAs
     float* out;          // [P][G][DH]
     uint32_t* sel_dump;        // [P][words] selection words of the fused modes (test hook) or null
     int ring_off;              // g > 1: byte offset of the cp.async row ring in dynamic smem
@@ -949,49 +951,102 @@ __device__ __forceinline__ void write_partial(const AtArgs& a, int p, int c, uns
     }
 }
 
-// The last CTA of head p merges the head's n_chunks partials into out[p]
-// (and re-arms the head's arrival counter).
+// Merges n partial results (pb: [n][G][DH + 2] = running max, sum of
+// weights, unnormalised output) into dst_out [G][DH] (normalised) or, when
+// dst_part is set, into one partial [G][DH + 2].  m and l of every partial
+// are read in one pass; the output sums read 2 x 16 partial values in flight
+// per thread (the merge sits on the kernel's critical tail, so its cost is
+// the number of dependent L2 round trips).
+constexpr int MERGE_GROUP = 8;
+
 template <int G>
-__device__ __forceinline__ void merge_head(const AtArgs& a, int p, unsigned char* smem_raw) {
+__device__ __forceinline__ void merge_parts(const float* pb, int n, float* dst_part, float* dst_out,
+                                            unsigned char* smem_raw) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    float* sc = reinterpret_cast<float*>(smem_raw) + AT_WARPS * G * DH;  // [G][n_chunks] + [G]
-    const int nc = a.n_chunks;
-    const float* pb = a.part + (long long)p * nc * G * (DH + 2);
+    float* sm = reinterpret_cast<float*>(smem_raw) + AT_WARPS * G * DH;  // [G][n]: m, then the scale
+    float* sl = sm + G * n;                                                // [G][n]: l
+    float* sml = sl + G * n;                                               // [G][2]: M, L
+    const long long cstr = (long long)G * (DH + 2);
+    // this thread's first 16 partial values of its (up to) two outputs are
+    // loaded before m and l, so both round trips overlap
+    constexpr int PF = 16;
+    const int e0 = tid, e1 = tid + AT_THREADS;
+    const bool has0 = e0 < G * DH, has1 = e1 < G * DH;
+    const int r0 = has0 ? e0 / DH : 0, d0 = has0 ? e0 % DH : 0, r1 = has1 ? e1 / DH : 0, d1 = has1 ? e1 % DH : 0;
+    const float* p0 = pb + (long long)r0 * (DH + 2) + 2 + d0;
+    const float* p1 = pb + (long long)r1 * (DH + 2) + 2 + d1;
+    float v0[PF], v1[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+        v0[u] = has0 && u < n ? __ldcg(p0 + u * cstr) : 0.f;
+        v1[u] = has1 && u < n ? __ldcg(p1 + u * cstr) : 0.f;
+    }
+    for (int i = tid; i < n * G; i += AT_THREADS) {  // i = cc * G + r
+        const float* pc = pb + (long long)i * (DH + 2);
+        const int cc = i / G, r = i - cc * G;
+        sm[r * n + cc] = __ldcg(pc);
+        sl[r * n + cc] = __ldcg(pc + 1);
+    }
+    __syncthreads();
     for (int r = warp; r < G; r += AT_WARPS) {
         float M = -INFINITY;
-        for (int cc = lane; cc < nc; cc += 32) M = fmaxf(M, __ldcg(pb + ((long long)cc * G + r) * (DH + 2)));
+        for (int cc = lane; cc < n; cc += 32) M = fmaxf(M, sm[r * n + cc]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(FULL, M, o));
         float L = 0.f;
-        for (int cc = lane; cc < nc; cc += 32) {
-            const float* pc = pb + ((long long)cc * G + r) * (DH + 2);
-            float f = safe_scale(__ldcg(pc), M);
-            sc[r * nc + cc] = f;
-            L += __ldcg(pc + 1) * f;
+        for (int cc = lane; cc < n; cc += 32) {
+            const float f = safe_scale(sm[r * n + cc], M);
+            sm[r * n + cc] = f;
+            L += sl[r * n + cc] * f;
         }
         L = warp_sum(L);
-        if (lane == 0) sc[G * nc + r] = L;
+        if (lane == 0) { sml[2 * r] = M; sml[2 * r + 1] = L; }
     }
     __syncthreads();
-    // the partial rows are L2-resident but the merge sits on the kernel's
-    // critical tail: 16 loads in flight per thread (same cc order)
-    for (int e = tid; e < G * DH; e += AT_THREADS) {
-        const int r = e / DH, d = e % DH;
-        const float* pr = pb + (long long)r * (DH + 2) + 2 + d;
-        const long long cstr = (long long)G * (DH + 2);
-        float O = 0.f;
-        int cc = 0;
-        for (; cc + 16 <= nc; cc += 16) {
-            float v[16];
+    // outputs e0, e1 (G * DH <= 2 * AT_THREADS for G <= 4), then any others
+    {
+        const float* f0 = sm + r0 * n;
+        const float* f1 = sm + r1 * n;
+        float O0 = 0.f, O1 = 0.f;
 #pragma unroll
-            for (int u = 0; u < 16; ++u) v[u] = __ldcg(pr + (cc + u) * cstr);
+        for (int u = 0; u < PF; ++u)
+            if (u < n) {
+                O0 = fmaf(v0[u], f0[u], O0);
+                O1 = fmaf(v1[u], f1[u], O1);
+            }
+        for (int cc = PF; cc < n; cc += PF) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) O = fmaf(v[u], sc[r * nc + cc + u], O);
+            for (int u = 0; u < PF; ++u) {
+                v0[u] = has0 && cc + u < n ? __ldcg(p0 + (cc + u) * cstr) : 0.f;
+                v1[u] = has1 && cc + u < n ? __ldcg(p1 + (cc + u) * cstr) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < PF; ++u)
+                if (cc + u < n) {
+                    O0 = fmaf(v0[u], f0[cc + u], O0);
+                    O1 = fmaf(v1[u], f1[cc + u], O1);
+                }
         }
-        for (; cc < nc; ++cc) O = fmaf(__ldcg(pr + cc * cstr), sc[r * nc + cc], O);
-        a.out[((long long)p * G + r) * DH + d] = O / sc[G * nc + r];
+        if (dst_out) {
+            if (has0) dst_out[e0] = O0 / sml[2 * r0 + 1];
+            if (has1) dst_out[e1] = O1 / sml[2 * r1 + 1];
+        } else {
+            if (has0) dst_part[r0 * (DH + 2) + 2 + d0] = O0;
+            if (has1) dst_part[r1 * (DH + 2) + 2 + d1] = O1;
+        }
     }
-    if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
+    for (int e = tid + 2 * AT_THREADS; e < G * DH; e += AT_THREADS) {  // G > 4
+        const int r = e / DH, d = e % DH;
+        const float* pe = pb + (long long)r * (DH + 2) + 2 + d;
+        float O = 0.f;
+        for (int cc = 0; cc < n; ++cc) O = fmaf(__ldcg(pe + cc * cstr), sm[r * n + cc], O);
+        if (dst_out) dst_out[e] = O / sml[2 * r + 1];
+        else dst_part[r * (DH + 2) + 2 + d] = O;
+    }
+    if (dst_part && tid < G) {
+        dst_part[tid * (DH + 2)] = sml[2 * tid];
+        dst_part[tid * (DH + 2) + 1] = sml[2 * tid + 1];
+    }
 }
 
 // MODE: 0 = the list modes (rows / bitmap / tuple classes, a.src at run
@@ -1187,19 +1242,41 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
     // ---- 5. merge warps, write this CTA's partial ----
     write_partial<G>(a, p, c, smem_raw, wm, wl);
 
-    // ---- 6. the last CTA of this head merges all partials (no extra launch) ----
+    // ---- 6. the last CTA of this head merges all partials (no extra launch);
+    // many chunks: the last CTA of each group of MERGE_GROUP merges the
+    // group's partials, the last group's merger merges the group partials ----
     __shared__ unsigned ticket;
     __threadfence();
     __syncthreads();
-    if (tid == 0) ticket = atomicAdd(&a.arrivals[p], 1u);
+    unsigned* grp_ctr = a.part2 ? a.arrivals + gridDim.y + (long long)p * a.n_groups + c / MERGE_GROUP : nullptr;
+    if (tid == 0) ticket = atomicAdd(a.part2 ? grp_ctr : &a.arrivals[p], 1u);
     // pair mode: pairs with the cluster arrive after the DSMEM reads (no CTA
     // of the cluster exits while another may still read its shared memory)
     if ((MODE == SRC_PAIRS) || (MODE == SRC_KEYS)) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     __syncthreads();
     if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
-    if (ticket != (unsigned)a.n_chunks - 1) return;
-    __threadfence();
-    merge_head<G>(a, p, smem_raw);
+    const float* pb = a.part + (long long)p * a.n_chunks * G * (DH + 2);
+    if (a.part2) {
+        const int g0 = c / MERGE_GROUP * MERGE_GROUP, gn = min(MERGE_GROUP, a.n_chunks - g0);
+        if (ticket != (unsigned)gn - 1) return;
+        __threadfence();
+        float* gp = a.part2 + ((long long)p * a.n_groups + c / MERGE_GROUP) * G * (DH + 2);
+        merge_parts<G>(pb + (long long)g0 * G * (DH + 2), gn, gp, nullptr, smem_raw);
+        if (tid == 0) *grp_ctr = 0;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) ticket = atomicAdd(&a.arrivals[p], 1u);
+        __syncthreads();
+        if (ticket != (unsigned)a.n_groups - 1) return;
+        __threadfence();
+        merge_parts<G>(a.part2 + (long long)p * a.n_groups * G * (DH + 2), a.n_groups, nullptr,
+                       a.out + (long long)p * G * DH, smem_raw);
+    } else {
+        if (ticket != (unsigned)a.n_chunks - 1) return;
+        __threadfence();
+        merge_parts<G>(pb, a.n_chunks, nullptr, a.out + (long long)p * G * DH, smem_raw);
+    }
+    if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
     if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
 }
 
@@ -1460,7 +1537,7 @@ static size_t attend_smem(AtArgs& a, int G) {
     }
     size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.win + a.n_init + a.n_local;
     const size_t rows_bytes = round_up(rows_cap * 4, 16);
-    const size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)G * a.n_chunks + G) * 4;
+    const size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)2 * G * a.n_chunks + 2 * G) * 4;
     // g > 1: the per-warp cp.async row ring (8 warps x depth rows x K + V)
     // sits right after rows[]; the pair select's scratch (selector CTA, before
     // the gather) and the per-warp merge (after it) alias it.  Not for the
@@ -1563,11 +1640,16 @@ static int plan_attend_launch(AtArgs& a, int G, size_t* smem) {
 static void launch_attend_kernel(pqkv_ctx* ctx, AtArgs& a, size_t P, int G, cudaStream_t st) {
     size_t smem = 0;
     const int cl = plan_attend_launch(a, G, &smem);
+    // two-level merge from 32 chunks per head (a one-level merge of n
+    // partials costs n / 16 dependent L2 round trips on the kernel's tail)
+    a.n_groups = a.n_chunks >= 32 ? (a.n_chunks + MERGE_GROUP - 1) / MERGE_GROUP : 0;
     Scratch sc(ctx);
     size_t h_part = sc.plan<float>(P * a.n_chunks * G * (DH + 2));
+    size_t h_part2 = sc.plan<float>(std::max<size_t>(1, P * a.n_groups * G * (DH + 2)));
     sc.commit();
     a.part = sc.get<float>(h_part);
-    a.arrivals = arrival_counters(ctx, P, st);
+    a.part2 = a.n_groups ? sc.get<float>(h_part2) : nullptr;
+    a.arrivals = arrival_counters(ctx, P * (1 + a.n_groups), st);
     a.prof = nullptr;
     a.sel_dump = ctx->sel_dump;
     // PQKV_PROF_SELECT=1: profile only the key path's select launch (the
