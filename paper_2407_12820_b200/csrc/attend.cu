@@ -1503,6 +1503,11 @@ void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_
 // gather_probe.cu); middle chunks are multiples of PQKV_TUPLE_CHUNK so the
 // code-pair classification never splits a tuple chunk.
 static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
+    static const int forced = [] {  // experiments only: PQKV_CHUNK_TOKENS=1024|2048|4096k
+        const char* e = std::getenv("PQKV_CHUNK_TOKENS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return forced;
     const size_t occ = 4;
     const size_t target = (size_t)ctx->sm_count * occ;
     const size_t per_head = std::max<size_t>(1, target / std::max<size_t>(P, 1));
@@ -1628,8 +1633,13 @@ static int plan_attend_launch(AtArgs& a, int G, size_t* smem) {
     // pair-select mode: 8-CTA clusters share one pair select (pad the chunk
     // count to a multiple of the cluster; padded CTAs own empty ranges)
     int cl = 1;
+    static const int forced_cl = [] {  // experiments only: PQKV_CLUSTER=4|8
+        const char* e = std::getenv("PQKV_CLUSTER");
+        return e ? std::atoi(e) : 0;
+    }();
     if (a.src == SRC_PAIRS && a.n_chunks >= 4) {
         cl = a.n_chunks >= 8 ? 8 : 4;  // 4 chunks per head (many heads): no empty padded CTAs
+        if (forced_cl == 4 || forced_cl == 8) cl = forced_cl;
         a.n_chunks = (int)round_up((size_t)a.n_chunks, (size_t)cl);
     }
     if (a.src == SRC_KEYS) cl = a.n_chunks;  // one cluster per head (<= 16 CTAs)

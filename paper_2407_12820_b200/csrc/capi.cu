@@ -2,6 +2,7 @@
 // the reference's rejection rules, then the launchers in kmeans.cu,
 // select.cu and attend.cu.  Nothing here computes on the host.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -295,9 +296,10 @@ static int decode_mode(const pqkv_layer& L, size_t g, size_t k, bool with_ids) {
     const bool fast = decode_fast_path(L, g);
     if (!fast) return PQKV_MODE_GENERIC;
     if (with_ids || k == 0) return PQKV_MODE_BITMAP;
+    static const bool force_split = std::getenv("PQKV_PAIRS_SPLIT") != nullptr;  // experiments only
     // one launch: every attention CTA selects its head's pairs, then
     // classifies its own codes and gathers
-    if (tup && decode_pairs_fused(L, g)) return PQKV_MODE_PAIRS_FUSED;
+    if (tup && decode_pairs_fused(L, g) && !force_split) return PQKV_MODE_PAIRS_FUSED;
     // per-head cluster computes ADC keys and radix-selects through DSMEM,
     // then gathers (same launch, or a second finer bitmap-mode launch)
     if (!(tup && L.b <= 6) && decode_keys_fused(L, g))

@@ -49,3 +49,18 @@ per = ctas_per_sm[sm.ravel()]
 for n in sorted(set(per.tolist())):
     m = per == n
     print(f"CTAs on SMs with {n} CTAs: {m.sum()}, median span {np.median(sp[m]):.1f} us, median rows {np.median(r[m]):.0f}")
+# per-SM view: total rows and the latest gather end of the SM's CTAs, and the
+# same by SM-id block of 16 (to spot GPC-level structure)
+end = (raw[:, 6] - raw[:, 4].min()).reshape(c["units"], nch) / 1e3
+sm_rows = np.bincount(sm.ravel(), weights=rows.ravel())
+sm_end = np.zeros(sm_rows.shape[0])
+np.maximum.at(sm_end, sm.ravel(), end.ravel())
+used = sm_rows > 0
+print("per-SM rows p0/p50/p100:", np.percentile(sm_rows[used], [0, 50, 100]).astype(int),
+      " per-SM last gather end us p0/p50/p100:", np.round(np.percentile(sm_end[used], [0, 50, 100]), 1))
+for b0 in range(0, sm_rows.shape[0], 16):
+    sl = slice(b0, b0 + 16)
+    u = used[sl]
+    if u.any():
+        print(f"  SMs {b0:3d}-{b0 + 15:3d}: CTAs {int(ctas_per_sm[sl].sum()):3d} rows/SM {sm_rows[sl][u].mean():6.0f} "
+              f"end us mean {sm_end[sl][u].mean():5.1f} max {sm_end[sl][u].max():5.1f}")

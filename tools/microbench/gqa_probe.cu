@@ -495,6 +495,121 @@ __global__ void __launch_bounds__(256, MINB) gqa_w3(const float* __restrict__ K,
 }
 
 // merge partials [P][n_parts][G][DH+2] -> out [P][G][DH]
+
+// ---- W2D: W2 with NW warps per CTA claiming rows dynamically (smem counter,
+// CB rows per claim) -- fewer, larger CTAs whose warps all finish together ----
+template <int D, int NW, int CB>
+__global__ void __launch_bounds__(NW * 32, 32 / NW) gqa_w2d(const float* __restrict__ K, const float* __restrict__ V,
+                                                      const int* __restrict__ rows, int per_cta, const float* __restrict__ Q,
+                                                      float scale_log2, float* part) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ int ctr;
+    const int p = blockIdx.y, c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    float4* ring = reinterpret_cast<float4*>(sm) + (size_t)warp * D * 64;
+    const int r0 = c * per_cta, n = max(0, min(per_cta, SEL - r0));
+    const int* rl = rows + (size_t)p * SEL + r0;
+    const float4* kb = reinterpret_cast<const float4*>(K + (size_t)p * S * DH);
+    const float4* vb = reinterpret_cast<const float4*>(V + (size_t)p * S * DH);
+    const uint64_t pol = evict_first();
+    if (tid == 0) ctr = NW * CB;  // the first batch of each warp is static
+    __syncthreads();
+    int q_base = warp * CB, q_pos = 0;  // current batch [q_base, q_base + CB)
+    int n_valid = 0;
+    bool dry = false;
+    auto next_row = [&]() -> int {
+        if (q_pos == CB) {
+            int b = 0;
+            if (lane == 0) b = atomicAdd(&ctr, CB);
+            q_base = __shfl_sync(FULL, b, 0);
+            q_pos = 0;
+        }
+        const int i = q_base + q_pos++;
+        return i < n ? rl[i] : -1;
+    };
+    auto issue = [&](int s) {
+        if (!dry) {
+            const int row = next_row();
+            if (row >= 0) {
+                cp16(ring + s * 64 + lane, kb + (long long)row * 32 + lane, pol);
+                cp16(ring + s * 64 + 32 + lane, vb + (long long)row * 32 + lane, pol);
+                ++n_valid;
+            } else {
+                dry = true;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int s = 0; s < D; ++s) issue(s);
+    float4 q[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        float4 v = reinterpret_cast<const float4*>(Q + ((size_t)p * G + r) * DH)[lane];
+        q[r] = make_float4(v.x * scale_log2, v.y * scale_log2, v.z * scale_log2, v.w * scale_log2);
+    }
+    const bool b4 = lane & 16, b3 = lane & 8;
+    float m_own = -INFINITY, l_own = 0.f;
+    float4 acc[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int it = 0; it < n_valid; ++it) {
+        const int s = it % D;
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+        const float4 k = ring[s * 64 + lane], v = ring[s * 64 + 32 + lane];
+        issue(s);
+        float d[G];
+        const float2 kxy = make_float2(k.x, k.y), kzw = make_float2(k.z, k.w);
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const float2 t = __ffma2_rn(make_float2(q[r].z, q[r].w), kzw, __fmul2_rn(make_float2(q[r].x, q[r].y), kxy));
+            d[r] = t.x + t.y;
+        }
+        float a0 = b4 ? d[2] : d[0], a1 = b4 ? d[3] : d[1];
+        const float s0 = b4 ? d[0] : d[2], s1 = b4 ? d[1] : d[3];
+        a0 += __shfl_xor_sync(FULL, s0, 16);
+        a1 += __shfl_xor_sync(FULL, s1, 16);
+        float x = b3 ? a1 : a0;
+        x += __shfl_xor_sync(FULL, b3 ? a0 : a1, 8);
+        x += __shfl_xor_sync(FULL, x, 4);
+        x += __shfl_xor_sync(FULL, x, 2);
+        x += __shfl_xor_sync(FULL, x, 1);
+        float alpha = 1.f;
+        if (x > m_own) {
+            alpha = safe_scale(m_own, x);
+            l_own *= alpha;
+            m_own = x;
+        }
+        const float pw = exp2f(x - m_own);
+        l_own += pw;
+        const bool grew = __any_sync(FULL, alpha != 1.f);
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const float pr = __shfl_sync(FULL, pw, 8 * r);
+            float2 axy = make_float2(acc[r].x, acc[r].y), azw = make_float2(acc[r].z, acc[r].w);
+            if (grew) {
+                const float ar = __shfl_sync(FULL, alpha, 8 * r);
+                axy = __fmul2_rn(axy, make_float2(ar, ar));
+                azw = __fmul2_rn(azw, make_float2(ar, ar));
+            }
+            axy = __ffma2_rn(make_float2(pr, pr), make_float2(v.x, v.y), axy);
+            azw = __ffma2_rn(make_float2(pr, pr), make_float2(v.z, v.w), azw);
+            acc[r] = make_float4(axy.x, axy.y, azw.x, azw.y);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    float* o = part + ((((size_t)p * gridDim.x + c) * NW + warp) * G) * (DH + 2);
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        const float mr = __shfl_sync(FULL, m_own, 8 * r), lr = __shfl_sync(FULL, l_own, 8 * r);
+        float* orow = o + r * (DH + 2);
+        if (lane == 0) { orow[0] = mr; orow[1] = lr; }
+        orow[2 + 4 * lane + 0] = acc[r].x;
+        orow[2 + 4 * lane + 1] = acc[r].y;
+        orow[2 + 4 * lane + 2] = acc[r].z;
+        orow[2 + 4 * lane + 3] = acc[r].w;
+    }
+}
+
 __global__ void merge(const float* part, int n_parts, float* out) {
     const int p = blockIdx.x / G, r = blockIdx.x % G, d = threadIdx.x;
     float M = -INFINITY;
@@ -592,6 +707,25 @@ int main() {
         runw(gqa_w2<4, 4>, 4, "W2 cp.async minB4");
         runw(gqa_w2p<4, 4>, 4, "W2P packed minB4");
         runw(gqa_w2p<4, 5>, 4, "W2P packed minB5");
+    }
+    {
+        char nm[128];
+        auto rund = [&](auto kern, int nw, int per_head, const char* tag, int d = 4) {
+            const int per = (SEL + per_head - 1) / per_head;
+            const int smem = nw * d * 1024;
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            snprintf(nm, sizeof nm, "%s CTAs/head=%d rows/CTA=%d", tag, per_head, per);
+            dim3 grid(per_head, P);
+            run(nm, per_head * nw, [&] { kern<<<grid, nw * 32, smem>>>(K, V, drows, per, Q, sl, part); });
+        };
+        rund(gqa_w2d<4, 32, 2>, 32, 18, "W2D 32 warps CB2");
+        rund(gqa_w2d<4, 32, 4>, 32, 18, "W2D 32 warps CB4");
+        rund(gqa_w2d<4, 16, 2>, 16, 37, "W2D 16 warps CB2");
+        rund(gqa_w2d<4, 8, 2>, 8, 74, "W2D 8 warps CB2");
+        rund(gqa_w2d<4, 8, 2>, 8, 64, "W2D 8 warps CB2");
+        rund(gqa_w2d<6, 32, 4>, 32, 18, "W2D D6 32 warps CB4", 6);
+        rund(gqa_w2d<4, 32, 4>, 32, 16, "W2D 32 warps CB4", 4);
+        rund(gqa_w2d<4, 32, 8>, 32, 18, "W2D 32 warps CB8", 4);
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
