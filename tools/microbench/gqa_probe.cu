@@ -704,6 +704,9 @@ int main() {
             snprintf(nm, sizeof nm, "%s D=%d rows/CTA=%d", tag, D, per);
             run(nm, nc * 8, [&] { kern<<<grid, 256, smem>>>(K, V, drows, per, Q, sl, part); });
         };
+        runw(gqa_w<4, 4>, 4, "W bulk-copy ring minB4");
+        runw(gqa_w<8, 3>, 8, "W bulk-copy ring minB3");
+        runw(gqa_w<6, 4>, 6, "W bulk-copy ring minB4");
         runw(gqa_w2<4, 4>, 4, "W2 cp.async minB4");
         runw(gqa_w2p<4, 4>, 4, "W2P packed minB4");
         runw(gqa_w2p<4, 5>, 4, "W2P packed minB5");
