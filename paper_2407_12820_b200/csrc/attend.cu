@@ -84,6 +84,8 @@ struct AtArgs {
     int ring4;                 // g > 1: ring depth 4 (else 2: large chunks keep 2 CTAs/SM)
     int win;                   // selected middle rows expanded per gather window (list modes: chunk)
     int stage;                 // pair mode: stage the CTA's codes in shared memory
+    int nt;                    // threads per CTA (AT_THREADS, or 1024 for the wide g > 1 plans)
+    int claim;                 // wide plans: warps claim rows dynamically (experiment: PQKV_CLAIM=1)
     uint32_t* sel_only;        // SRC_KEYS: write the selection bitmap [P][words] here and stop (split launch)
     unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
@@ -102,10 +104,11 @@ struct AtSmem {
 // Expands selection words (bit b of word w = middle token base + 32w + b) into
 // ascending token ids at rows[off...]; every warp owns a contiguous range of
 // words.  Returns the number of rows written (block-uniform).
+template <int NT = AT_THREADS>
 __device__ int expand_words(const uint32_t* words, int nwords, int token_base, int* rows, int off,
                             uint32_t* wtot) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per = (nwords + AT_WARPS - 1) / AT_WARPS;
+    const int per = (nwords + (NT / 32) - 1) / (NT / 32);
     const int w0 = warp * per, w1 = min(nwords, w0 + per);
     uint32_t cnt = 0;
     for (int w = w0 + lane; w < w1; w += 32) cnt += __popc(words[w]);
@@ -114,7 +117,7 @@ __device__ int expand_words(const uint32_t* words, int nwords, int token_base, i
     __syncthreads();
     uint32_t before = 0, total = 0;
 #pragma unroll
-    for (int w = 0; w < AT_WARPS; ++w) {
+    for (int w = 0; w < (NT / 32); ++w) {
         uint32_t v = wtot[w];
         before += w < warp ? v : 0;
         total += v;
@@ -145,10 +148,11 @@ __device__ int expand_words(const uint32_t* words, int nwords, int token_base, i
 // expand_words restricted to the selected bits of rank [lo, hi) (rank = the
 // bit's position among all set bits of words[0..nwords) in id order); the
 // row of rank j goes to rows[off + j - lo].  Returns the number written.
+template <int NT = AT_THREADS>
 __device__ int expand_words_range(const uint32_t* words, int nwords, int token_base, int* rows, int off, uint32_t lo,
                                   uint32_t hi, uint32_t* wtot) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per = (nwords + AT_WARPS - 1) / AT_WARPS;
+    const int per = (nwords + (NT / 32) - 1) / (NT / 32);
     const int w0 = warp * per, w1 = min(nwords, w0 + per);
     uint32_t cnt = 0;
     for (int w = w0 + lane; w < w1; w += 32) cnt += __popc(words[w]);
@@ -157,7 +161,7 @@ __device__ int expand_words_range(const uint32_t* words, int nwords, int token_b
     __syncthreads();
     uint32_t before = 0, total = 0;
 #pragma unroll
-    for (int w = 0; w < AT_WARPS; ++w) {
+    for (int w = 0; w < (NT / 32); ++w) {
         uint32_t v = wtot[w];
         before += w < warp ? v : 0;
         total += v;
@@ -208,13 +212,13 @@ __device__ __forceinline__ int code_swz(int f) { return (f & ~255) | ((f & 7) <<
 //    tokens of earlier chunks, none of later ones).  words[] = selection.
 //  * PRELIM (early release): cls in {0 below, 1 above, 3 pending}.
 //    words[] = above, eqw[] = pending.
-template <bool PRELIM>
+template <bool PRELIM, int NT = AT_THREADS>
 __device__ void classify_range(const AtArgs& a, int r0, int r1, const uint32_t* cd_g, const uint32_t* staged,
                                uint32_t* words, uint32_t* eqw, const uint8_t* cls, uint32_t* wtot, int cstar,
                                uint32_t take) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nw = (max(0, r1 - r0) + 31) >> 5;
-    const int per = (nw + AT_WARPS - 1) / AT_WARPS;
+    const int per = (nw + (NT / 32) - 1) / (NT / 32);
     const int w0 = min(nw, warp * per), w1 = min(nw, w0 + per);
     const uint32_t C = (uint32_t)a.C;
     const uint32_t eqc = PRELIM ? 3u : 2u;
@@ -258,13 +262,13 @@ __device__ void classify_range(const AtArgs& a, int r0, int r1, const uint32_t* 
     // ---- step 2: equal tokens: all of chunks before c*, the first `take` of
     // c* in id order, none after ----
     const int a0 = cstar * PQKV_TUPLE_CHUNK, a1 = a0 + PQKV_TUPLE_CHUNK;
-    for (int w = tid; w < nw; w += AT_THREADS)
+    for (int w = tid; w < nw; w += NT)
         if ((r0 + 32 * w) / PQKV_TUPLE_CHUNK < cstar) words[w] |= eqw[w];
     const int b0 = max(r0, a0), b1 = min(r1, a1);
     if (b0 < b1) {  // this range holds part of chunk c* (block-uniform)
         // equal tokens of c* before this range (other CTAs' tokens)
         uint32_t pre = 0;
-        for (int i = a0 + tid; i < r0; i += AT_THREADS) {
+        for (int i = a0 + tid; i < r0; i += NT) {
             const uint32_t pr = cd_g[i];
             pre += cls[(pr & 0xffffu) * C + (pr >> 16)] == 2;
         }
@@ -273,14 +277,14 @@ __device__ void classify_range(const AtArgs& a, int r0, int r1, const uint32_t* 
         __syncthreads();
         pre = 0;
 #pragma unroll
-        for (int w = 0; w < AT_WARPS; ++w) pre += wtot[w];
+        for (int w = 0; w < (NT / 32); ++w) pre += wtot[w];
         __syncthreads();
         // ordered prefix over the words of c* in this range: <= 128 words,
         // thread t owns word wb0 + t
         const int wb0 = (b0 - r0) >> 5, wb1 = (b1 - r0 + 31) >> 5;
         const int w = wb0 + tid;
         const uint32_t e = w < wb1 ? eqw[w] : 0u;
-        const uint32_t before = pre + block_excl_scan<AT_THREADS>((uint32_t)__popc(e), wtot, nullptr);
+        const uint32_t before = pre + block_excl_scan<NT>((uint32_t)__popc(e), wtot, nullptr);
         if (w < wb1 && e) {
             uint32_t keep = 0;
             const uint32_t c = __popc(e);
@@ -599,6 +603,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
 // consumed; returns the next rows' count, or < 0 when the CTA is done.
 // WindowRefill: windowed chunks (selected rows expanded `win` at a time from
 // the CTA's selection words; the local rows follow the last window).
+template <int NT = AT_THREADS>
 struct WindowRefill {
     const AtArgs& a;
     int c;
@@ -612,10 +617,10 @@ struct WindowRefill {
         win_base += a.win;
         const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
         const int nw = (max(0, r1 - r0) + 31) / 32;
-        int nrows = expand_words_range(words, nw, a.n_init + r0, rows, 0, (uint32_t)win_base,
+        int nrows = expand_words_range<NT>(words, nw, a.n_init + r0, rows, 0, (uint32_t)win_base,
                                        (uint32_t)(win_base + a.win), wtot);
         if (c == a.n_chunks - 1 && win_base + a.win >= sel_total) {
-            for (int e = threadIdx.x; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
+            for (int e = threadIdx.x; e < a.n_local; e += NT) rows[nrows + e] = a.total - a.n_local + e;
             nrows += a.n_local;
         }
         __syncthreads();
@@ -814,9 +819,10 @@ __device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int
 // online-softmax state and broadcast its weight.  Measured on cfg3's shape
 // (tools/microbench/gqa_probe.cu): 4.95 TB/s vs 4.2-4.35 TB/s for the
 // half-warp-per-row ring.
-template <int G, class Refill>
+template <int G, int NT, class Refill>
 __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int* rows, int nrows, Refill& refill,
-                                                 unsigned char* smem_raw, float (*wm)[G], float (*wl)[G]) {
+                                                 unsigned char* smem_raw, float (*wm)[G], float (*wl)[G],
+                                                 unsigned* claim = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float4* kb = reinterpret_cast<const float4*>(a.keys + (long long)p * a.kv_head_stride);
     const float4* vb = reinterpret_cast<const float4*>(a.values + (long long)p * a.kv_head_stride);
@@ -835,17 +841,41 @@ __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int* ro
 #pragma unroll
     for (int r = 0; r < G; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (;;) {
-        const int mine = nrows > warp ? (nrows - warp + AT_WARPS - 1) / AT_WARPS : 0;
+        int mine = nrows > warp ? (nrows - warp + (NT / 32) - 1) / (NT / 32) : 0;
+        // claim != null (wide CTAs): the warps take CLAIM rows at a time from
+        // a shared counter, so all 32 finish within a row of each other; a
+        // warp's first batch is rows [warp * CLAIM, warp * CLAIM + CLAIM)
+        constexpr int CLAIM = 4;
+        int q_base = warp * CLAIM, q_pos = 0, n_got = 0;
+        bool dry = false;
         auto issue = [&](int it, int slot) {
-            if (it < mine) {
-                const long long row = rows[warp + AT_WARPS * it];
+            if (claim) {
+                if (!dry) {
+                    if (q_pos == CLAIM) {
+                        int b = 0;
+                        if (lane == 0) b = (int)atomicAdd(claim, (unsigned)CLAIM);
+                        q_base = __shfl_sync(FULL, b, 0);
+                        q_pos = 0;
+                    }
+                    const int i = q_base + q_pos++;
+                    if (i < nrows) {
+                        const long long row = rows[i];
+                        cp_async16_hint(ring + slot * 64 + lane, kb + row * (DH / 4) + lane, pol);
+                        cp_async16_hint(ring + slot * 64 + 32 + lane, vb + row * (DH / 4) + lane, pol);
+                        ++n_got;
+                    } else {
+                        dry = true;
+                    }
+                }
+            } else if (it < mine) {
+                const long long row = rows[warp + (NT / 32) * it];
                 cp_async16_hint(ring + slot * 64 + lane, kb + row * (DH / 4) + lane, pol);
                 cp_async16_hint(ring + slot * 64 + 32 + lane, vb + row * (DH / 4) + lane, pol);
             }
             cp_async_commit();
         };
         for (int sl = 0; sl < depth; ++sl) issue(sl, sl);
-        for (int it = 0; it < mine; ++it) {
+        for (int it = 0; claim ? it < n_got : it < mine; ++it) {
             const int sl = it & (depth - 1);
             if (depth == 4) cp_async_wait_group<3>();
             else cp_async_wait_group<1>();
@@ -902,6 +932,7 @@ __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int* ro
             }
         }
         cp_async_wait_all();
+        if (claim) break;  // wide plans keep whole lists (no windows)
         const int nn = refill(rows);  // the next window's rows, or < 0: done
         if (nn < 0) break;
         nrows = nn;
@@ -913,7 +944,7 @@ __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int* ro
     }
     __syncthreads();  // every warp is past the gather loop: rows[] is free
     // this warp's partial (m, l, acc per query row) -> the per-warp merge area
-    float* wacc = reinterpret_cast<float*>(smem_raw);  // [AT_WARPS][G][DH]
+    float* wacc = reinterpret_cast<float*>(smem_raw);  // [(NT / 32)][G][DH]
     constexpr int GRP = 32 / G;
 #pragma unroll
     for (int r = 0; r < G; ++r) {
@@ -929,17 +960,17 @@ __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int* ro
 
 // Per-warp partials (wacc / wm / wl in shared memory) -> this CTA's partial
 // part[p][c] = (M, L, O[d]) per query row.
-template <int G>
+template <int G, int NT = AT_THREADS>
 __device__ __forceinline__ void write_partial(const AtArgs& a, int p, int c, unsigned char* smem_raw, float (*wm)[G],
                                               float (*wl)[G]) {
-    const float* wacc = reinterpret_cast<const float*>(smem_raw);  // [AT_WARPS][G][DH]
-    for (int e = threadIdx.x; e < G * DH; e += AT_THREADS) {
+    const float* wacc = reinterpret_cast<const float*>(smem_raw);  // [(NT / 32)][G][DH]
+    for (int e = threadIdx.x; e < G * DH; e += NT) {
         const int r = e / DH, d = e % DH;
         float M = -INFINITY;
-        for (int w = 0; w < AT_WARPS; ++w) M = fmaxf(M, wm[w][r]);
+        for (int w = 0; w < (NT / 32); ++w) M = fmaxf(M, wm[w][r]);
         float L = 0.f, O = 0.f;
         if (M != -INFINITY) {
-            for (int w = 0; w < AT_WARPS; ++w) {
+            for (int w = 0; w < (NT / 32); ++w) {
                 const float sc = safe_scale(wm[w][r], M);
                 L += wl[w][r] * sc;
                 O += wacc[(w * G + r) * DH + d] * sc;
@@ -959,36 +990,37 @@ __device__ __forceinline__ void write_partial(const AtArgs& a, int p, int c, uns
 // the number of dependent L2 round trips).
 constexpr int MERGE_GROUP = 8;
 
-template <int G>
+template <int G, int NT = AT_THREADS>
 __device__ __forceinline__ void merge_parts(const float* pb, int n, float* dst_part, float* dst_out,
                                             unsigned char* smem_raw) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    float* sm = reinterpret_cast<float*>(smem_raw) + AT_WARPS * G * DH;  // [G][n]: m, then the scale
+    float* sm = reinterpret_cast<float*>(smem_raw) + (NT / 32) * G * DH;  // [G][n]: m, then the scale
     float* sl = sm + G * n;                                                // [G][n]: l
     float* sml = sl + G * n;                                               // [G][2]: M, L
     const long long cstr = (long long)G * (DH + 2);
-    // this thread's first 16 partial values of its (up to) two outputs are
-    // loaded before m and l, so both round trips overlap
-    constexpr int PF = 16;
-    const int e0 = tid, e1 = tid + AT_THREADS;
-    const bool has0 = e0 < G * DH, has1 = e1 < G * DH;
+    // this thread's outputs (one, or two when G * DH > NT): their first PF
+    // partial values are loaded before m and l, so both round trips overlap
+    constexpr bool TWO = G * DH > NT;
+    constexpr int PF = TWO ? 16 : 32;
+    const int e0 = tid, e1 = tid + NT;
+    const bool has0 = e0 < G * DH, has1 = TWO && e1 < G * DH;
     const int r0 = has0 ? e0 / DH : 0, d0 = has0 ? e0 % DH : 0, r1 = has1 ? e1 / DH : 0, d1 = has1 ? e1 % DH : 0;
     const float* p0 = pb + (long long)r0 * (DH + 2) + 2 + d0;
     const float* p1 = pb + (long long)r1 * (DH + 2) + 2 + d1;
-    float v0[PF], v1[PF];
+    float v0[PF], v1[TWO ? PF : 1];
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
         v0[u] = has0 && u < n ? __ldcg(p0 + u * cstr) : 0.f;
-        v1[u] = has1 && u < n ? __ldcg(p1 + u * cstr) : 0.f;
+        if constexpr (TWO) v1[u] = has1 && u < n ? __ldcg(p1 + u * cstr) : 0.f;
     }
-    for (int i = tid; i < n * G; i += AT_THREADS) {  // i = cc * G + r
+    for (int i = tid; i < n * G; i += NT) {  // i = cc * G + r
         const float* pc = pb + (long long)i * (DH + 2);
         const int cc = i / G, r = i - cc * G;
         sm[r * n + cc] = __ldcg(pc);
         sl[r * n + cc] = __ldcg(pc + 1);
     }
     __syncthreads();
-    for (int r = warp; r < G; r += AT_WARPS) {
+    for (int r = warp; r < G; r += (NT / 32)) {
         float M = -INFINITY;
         for (int cc = lane; cc < n; cc += 32) M = fmaxf(M, sm[r * n + cc]);
 #pragma unroll
@@ -1003,7 +1035,6 @@ __device__ __forceinline__ void merge_parts(const float* pb, int n, float* dst_p
         if (lane == 0) { sml[2 * r] = M; sml[2 * r + 1] = L; }
     }
     __syncthreads();
-    // outputs e0, e1 (G * DH <= 2 * AT_THREADS for G <= 4), then any others
     {
         const float* f0 = sm + r0 * n;
         const float* f1 = sm + r1 * n;
@@ -1012,19 +1043,19 @@ __device__ __forceinline__ void merge_parts(const float* pb, int n, float* dst_p
         for (int u = 0; u < PF; ++u)
             if (u < n) {
                 O0 = fmaf(v0[u], f0[u], O0);
-                O1 = fmaf(v1[u], f1[u], O1);
+                if constexpr (TWO) O1 = fmaf(v1[u], f1[u], O1);
             }
         for (int cc = PF; cc < n; cc += PF) {
 #pragma unroll
             for (int u = 0; u < PF; ++u) {
                 v0[u] = has0 && cc + u < n ? __ldcg(p0 + (cc + u) * cstr) : 0.f;
-                v1[u] = has1 && cc + u < n ? __ldcg(p1 + (cc + u) * cstr) : 0.f;
+                if constexpr (TWO) v1[u] = has1 && cc + u < n ? __ldcg(p1 + (cc + u) * cstr) : 0.f;
             }
 #pragma unroll
             for (int u = 0; u < PF; ++u)
                 if (cc + u < n) {
                     O0 = fmaf(v0[u], f0[cc + u], O0);
-                    O1 = fmaf(v1[u], f1[cc + u], O1);
+                    if constexpr (TWO) O1 = fmaf(v1[u], f1[cc + u], O1);
                 }
         }
         if (dst_out) {
@@ -1035,7 +1066,7 @@ __device__ __forceinline__ void merge_parts(const float* pb, int n, float* dst_p
             if (has1) dst_part[r1 * (DH + 2) + 2 + d1] = O1;
         }
     }
-    for (int e = tid + 2 * AT_THREADS; e < G * DH; e += AT_THREADS) {  // G > 4
+    for (int e = tid + 2 * NT; e < G * DH; e += NT) {  // G * DH > 2 NT (not instantiated today)
         const int r = e / DH, d = e % DH;
         const float* pe = pb + (long long)r * (DH + 2) + 2 + d;
         float O = 0.f;
@@ -1052,13 +1083,13 @@ __device__ __forceinline__ void merge_parts(const float* pb, int n, float* dst_p
 // MODE: 0 = the list modes (rows / bitmap / tuple classes, a.src at run
 // time), SRC_PAIRS or SRC_KEYS -- the fused single-launch modes get their own
 // instantiation so their prologues do not perturb the others' code.
-template <int G, int MODE>
-__global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 4) attend_kernel(AtArgs a) {
+template <int G, int MODE, int NT = AT_THREADS>
+__global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS && G > 1) ? 2 : 4)) attend_kernel(AtArgs a) {
     const int src = MODE == 0 ? a.src : MODE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ uint32_t wtot[AT_WARPS];
+    __shared__ uint32_t wtot[(NT / 32)];
     __shared__ int nrows_s;
-    __shared__ float wm[AT_WARPS][G], wl[AT_WARPS][G];
+    __shared__ float wm[(NT / 32)][G], wl[(NT / 32)][G];
 
     const int p = blockIdx.y, c = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1089,12 +1120,12 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
         const int C2 = a.C * a.C;
         const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
         const char* cd = reinterpret_cast<const char*>(a.codes + p * a.codes_head_stride + 2 * (long long)r0);
-        for (int o = tid * 128; o < 4 * (r1 - r0); o += AT_THREADS * 128) prefetch_l2(cd + o);
+        for (int o = tid * 128; o < 4 * (r1 - r0); o += NT * 128) prefetch_l2(cd + o);
         if ((c & 7) == 0) {  // one CTA per cluster: the head's select tables
             const char* ce = reinterpret_cast<const char*>(a.centroids + (long long)p * 2 * a.C * (DH / 2));
-            for (int o = tid * 128; o < 4 * a.C * DH; o += AT_THREADS * 128) prefetch_l2(ce + o);
+            for (int o = tid * 128; o < 4 * a.C * DH; o += NT * 128) prefetch_l2(ce + o);
             const char* th = reinterpret_cast<const char*>(a.thist + (long long)p * C2);
-            for (int o = tid * 128; o < 4 * C2; o += AT_THREADS * 128) prefetch_l2(th + o);
+            for (int o = tid * 128; o < 4 * C2; o += NT * 128) prefetch_l2(th + o);
         }
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1104,23 +1135,23 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
     int sel_total = 0;  // windowed list: selected middle rows of this CTA (0: one window)
     if (src == SRC_ROWS) {
         const int b0 = c * a.chunk, cnt = max(0, min(a.chunk, a.t - b0));
-        for (int e = tid; e < cnt; e += AT_THREADS) rows[e] = (int)a.rows[(long long)p * a.t + b0 + e];
+        for (int e = tid; e < cnt; e += NT) rows[e] = (int)a.rows[(long long)p * a.t + b0 + e];
         nrows = cnt;
     } else {
         if (c == 0 && (MODE != SRC_PAIRS) && (MODE != SRC_KEYS))  // written after the select (shared region)
-            for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
+            for (int e = tid; e < a.n_init; e += NT) rows[e] = e;
         nrows = c == 0 ? a.n_init : 0;
         const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
         const int nw = (max(0, r1 - r0) + 31) / 32;
         if (src == SRC_BITMAP) {
-            for (int w = tid; w < nw; w += AT_THREADS) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
+            for (int w = tid; w < nw; w += NT) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
         } else if ((MODE == SRC_KEYS)) {
             __shared__ uint32_t pub_s[4], sh_s[4];
             keys_select_words<G>(a, p, r0, r1, smem_raw, words, eqw /* [2][NB/2] in keys mode */, pub_s, wtot, sh_s,
                                  a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr);
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 1] = clock64();
             if (a.sel_only) {  // select-only launch: the bitmap-mode attention follows
-                for (int w = tid; w < nw; w += AT_THREADS) {
+                for (int w = tid; w < nw; w += NT) {
                     a.sel_only[(long long)p * a.words + r0 / 32 + w] = words[w];
                     if (a.sel_dump) a.sel_dump[(long long)p * a.words + r0 / 32 + w] = words[w];
                 }
@@ -1128,7 +1159,7 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
                 return;
             }
             if (c == 0)
-                for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
+                for (int e = tid; e < a.n_init; e += NT) rows[e] = e;
         } else if ((MODE == SRC_PAIRS)) {
             // per-head pair-level top-k: computed by one CTA of each thread-block
             // cluster and shared with the others through DSMEM.  The selecting
@@ -1145,28 +1176,32 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
             // works; the selector reads them from L2 (prefetched)
             const uint32_t* cd_g = reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride);
             const uint32_t* staged = nullptr;
+            auto stage_codes = [&](uint32_t* dst) {
+                const int n = max(0, r1 - r0);
+                const uint32_t* src = cd_g + r0;
+                int head = 0;
+                if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                    head = n & ~3;
+                    for (int f = tid; f < head / 4; f += NT) cp_async16(dst + 4 * code_swz(f), src + 4 * f);
+                }
+                for (int e = head + tid; e < n; e += NT) cp_async4(dst + 4 * code_swz(e >> 2) + (e & 3), src + e);
+                cp_async_commit();
+            };
             {
                 const int n = max(0, r1 - r0);
                 const uint32_t* src = cd_g + r0;
                 if (crank == sel || !a.stage) {
-                    for (int o = tid * 32; o < n; o += AT_THREADS * 32) prefetch_l2(src + o);
+                    for (int o = tid * 32; o < n; o += NT * 32) prefetch_l2(src + o);
                 } else {
-                    uint32_t* dst = reinterpret_cast<uint32_t*>(smem_raw);
-                    int head = 0;
-                    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-                        head = n & ~3;
-                        for (int f = tid; f < head / 4; f += AT_THREADS) cp_async16(dst + 4 * code_swz(f), src + 4 * f);
-                    }
-                    for (int e = head + tid; e < n; e += AT_THREADS) cp_async4(dst + 4 * code_swz(e >> 2) + (e & 3), src + e);
-                    cp_async_commit();
-                    staged = dst;
+                    stage_codes(reinterpret_cast<uint32_t*>(smem_raw));
+                    staged = reinterpret_cast<const uint32_t*>(smem_raw);
                 }
             }
             __shared__ uint32_t cut_s[2];
             const int C = a.C, C2 = C * C;
             if (crank == sel) {
                 PairScratch ps(smem_raw, C, a.n_tchunks);  // aliases rows[]: free until expansion
-                pair_select<AT_THREADS, 16>(a.queries + (long long)p * G * DH, G, DH,
+                pair_select<NT, (4096 + NT - 1) / NT>(a.queries + (long long)p * G * DH, G, DH,
                                             a.centroids + (long long)p * 2 * C * (DH / 2), C,
                                             a.thist + (long long)p * C2, a.chist + (long long)p * a.tchunk_stride * C2,
                                             a.n_tchunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
@@ -1178,7 +1213,7 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 15] = clock64();
             if (crank != sel) {
                 const uint32_t* rc = cluster.map_shared_rank(reinterpret_cast<const uint32_t*>(cls), sel);
-                for (int e = tid; e < (C2 + 3) / 4; e += AT_THREADS) reinterpret_cast<uint32_t*>(cls)[e] = rc[e];
+                for (int e = tid; e < (C2 + 3) / 4; e += NT) reinterpret_cast<uint32_t*>(cls)[e] = rc[e];
                 if (tid < 2) cut_s[tid] = cluster.map_shared_rank(cut_s, sel)[tid];
             }
             // the selector's cls[]/cut_s are never written again; its exit is
@@ -1191,43 +1226,43 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
             cp_async_wait_all();
             __syncthreads();
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 19] = clock64();
-            classify_range<false>(a, r0, r1, cd_g, staged, words, eqw, cls, wtot, cstar, take);
+            classify_range<false, NT>(a, r0, r1, cd_g, staged, words, eqw, cls, wtot, cstar, take);
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 20] = clock64();
             if (c == 0)  // after the staged codes are consumed (they share rows[])
-                for (int e = tid; e < a.n_init; e += AT_THREADS) rows[e] = e;
+                for (int e = tid; e < a.n_init; e += NT) rows[e] = e;
         } else {
             const int C2 = a.C * a.C;
             if ((C2 & 3) == 0) {
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(a.cls + (long long)p * C2);
-                for (int e = tid; e < C2 / 4; e += AT_THREADS) reinterpret_cast<uint32_t*>(cls)[e] = src[e];
+                for (int e = tid; e < C2 / 4; e += NT) reinterpret_cast<uint32_t*>(cls)[e] = src[e];
             } else {
-                for (int e = tid; e < C2; e += AT_THREADS) cls[e] = a.cls[(long long)p * C2 + e];
+                for (int e = tid; e < C2; e += NT) cls[e] = a.cls[(long long)p * C2 + e];
             }
             __syncthreads();
-            classify_range<false>(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), nullptr,
+            classify_range<false, NT>(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), nullptr,
                            words, eqw, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
         }
         __syncthreads();
         if (a.sel_dump && ((MODE == SRC_PAIRS) || (MODE == SRC_KEYS)))
-            for (int w = tid; w < nw; w += AT_THREADS) a.sel_dump[(long long)p * a.words + r0 / 32 + w] = words[w];
+            for (int w = tid; w < nw; w += NT) a.sel_dump[(long long)p * a.words + r0 / 32 + w] = words[w];
         if (a.win >= a.chunk) {
-            nrows += expand_words(words, nw, a.n_init + r0, rows, nrows, wtot);
+            nrows += expand_words<NT>(words, nw, a.n_init + r0, rows, nrows, wtot);
             sel_total = 0;
         } else {  // windowed: the first a.win selected middle rows now, the rest after each gather window
             uint32_t t = 0;
-            for (int w = tid; w < nw; w += AT_THREADS) t += __popc(words[w]);
+            for (int w = tid; w < nw; w += NT) t += __popc(words[w]);
             t = warp_sum(t);
             if (lane == 0) wtot[warp] = t;
             __syncthreads();
             t = 0;
 #pragma unroll
-            for (int w = 0; w < AT_WARPS; ++w) t += wtot[w];
+            for (int w = 0; w < (NT / 32); ++w) t += wtot[w];
             __syncthreads();
             sel_total = (int)t;
-            nrows += expand_words_range(words, nw, a.n_init + r0, rows, nrows, 0u, (uint32_t)a.win, wtot);
+            nrows += expand_words_range<NT>(words, nw, a.n_init + r0, rows, nrows, 0u, (uint32_t)a.win, wtot);
         }
         if (c == a.n_chunks - 1 && sel_total <= a.win) {
-            for (int e = tid; e < a.n_local; e += AT_THREADS) rows[nrows + e] = a.total - a.n_local + e;
+            for (int e = tid; e < a.n_local; e += NT) rows[nrows + e] = a.total - a.n_local + e;
             nrows += a.n_local;
         }
     }
@@ -1236,11 +1271,19 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
     nrows = nrows_s;
     if (a.prof && tid == 0) { a.prof[cta * PQKV_PROF_SLOTS + 2] = clock64(); a.prof[cta * PQKV_PROF_SLOTS + 5] = globaltimer_ns(); }
 
-    WindowRefill refill{a, c, words, wtot, sel_total, 0};
-    if constexpr (G == 1) gather_rows_halfwarp(a, p, rows, nrows, refill, smem_raw, wm, wl);
-    else gather_rows_warp<G>(a, p, rows, nrows, refill, smem_raw, wm, wl);
+    WindowRefill<NT> refill{a, c, words, wtot, sel_total, 0};
+    if constexpr (G == 1) {
+        gather_rows_halfwarp(a, p, rows, nrows, refill, smem_raw, wm, wl);
+    } else if (NT > AT_THREADS && a.claim) {
+        __shared__ unsigned claim_ctr;
+        if (tid == 0) claim_ctr = (unsigned)(NT / 32) * 4u;  // the warps' first batches are static
+        __syncthreads();
+        gather_rows_warp<G, NT>(a, p, rows, nrows, refill, smem_raw, wm, wl, &claim_ctr);
+    } else {
+        gather_rows_warp<G, NT>(a, p, rows, nrows, refill, smem_raw, wm, wl);
+    }
     // ---- 5. merge warps, write this CTA's partial ----
-    write_partial<G>(a, p, c, smem_raw, wm, wl);
+    write_partial<G, NT>(a, p, c, smem_raw, wm, wl);
 
     // ---- 6. the last CTA of this head merges all partials (no extra launch);
     // many chunks: the last CTA of each group of MERGE_GROUP merges the
@@ -1261,7 +1304,7 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
         if (ticket != (unsigned)gn - 1) return;
         __threadfence();
         float* gp = a.part2 + ((long long)p * a.n_groups + c / MERGE_GROUP) * G * (DH + 2);
-        merge_parts<G>(pb + (long long)g0 * G * (DH + 2), gn, gp, nullptr, smem_raw);
+        merge_parts<G, NT>(pb + (long long)g0 * G * (DH + 2), gn, gp, nullptr, smem_raw);
         if (tid == 0) *grp_ctr = 0;
         __threadfence();
         __syncthreads();
@@ -1269,12 +1312,12 @@ __global__ void __launch_bounds__(AT_THREADS, (MODE == SRC_KEYS && G > 1) ? 2 : 
         __syncthreads();
         if (ticket != (unsigned)a.n_groups - 1) return;
         __threadfence();
-        merge_parts<G>(a.part2 + (long long)p * a.n_groups * G * (DH + 2), a.n_groups, nullptr,
+        merge_parts<G, NT>(a.part2 + (long long)p * a.n_groups * G * (DH + 2), a.n_groups, nullptr,
                        a.out + (long long)p * G * DH, smem_raw);
     } else {
         if (ticket != (unsigned)a.n_chunks - 1) return;
         __threadfence();
-        merge_parts<G>(pb, a.n_chunks, nullptr, a.out + (long long)p * G * DH, smem_raw);
+        merge_parts<G, NT>(pb, a.n_chunks, nullptr, a.out + (long long)p * G * DH, smem_raw);
     }
     if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
     if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
@@ -1524,6 +1567,8 @@ static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
 // Shared memory: region (rows[] / merge partials / pair-select scratch)
 // followed by words[] and the pair classes.
 static size_t attend_smem(AtArgs& a, int G) {
+    const size_t nw = (size_t)(a.nt > 0 ? a.nt : AT_THREADS) / 32;  // warps per CTA
+    const bool wide = a.nt > AT_THREADS;
     // Chunks whose full row list + staged codes would cost CTAs per SM (many
     // heads: one wave of CTAs needs few, large chunks) expand and gather their
     // rows in windows of 4096 and, in pair mode, classify codes straight from
@@ -1534,21 +1579,24 @@ static size_t attend_smem(AtArgs& a, int G) {
     {
         const size_t full_rows = ((size_t)a.chunk + a.n_init + a.n_local) * 4;
         const size_t tail_est = (size_t)a.chunk / 32 * 8 + ((a.src == SRC_TUPLE || a.src == SRC_PAIRS) ? (size_t)a.C * a.C : 0);
-        const size_t ring2 = (G > 1 && a.src != SRC_KEYS) ? (size_t)AT_WARPS * 2 * 2 * DH * 4 : 0;
+        const size_t ring2 = (G > 1 && a.src != SRC_KEYS) ? nw * 2 * 2 * DH * 4 : 0;
         const size_t budget = 55 * 1024;
-        const bool full = a.src == SRC_ROWS || a.chunk <= 8192 || full_rows + tail_est + ring2 <= budget;
+        const bool full = wide || a.src == SRC_ROWS || a.chunk <= 8192 || full_rows + tail_est + ring2 <= budget;
         a.win = full ? a.chunk : 4096;
-        a.stage = full;
+        // wide pair CTAs are their own selectors and classify from L2 (staging
+        // their codes behind the select's scratch: select +1.5 us, classify
+        // -0.6 us)
+        a.stage = full && !(wide && a.src == SRC_PAIRS);
     }
     size_t rows_cap = a.src == SRC_ROWS ? (size_t)a.chunk : (size_t)a.win + a.n_init + a.n_local;
     const size_t rows_bytes = round_up(rows_cap * 4, 16);
-    const size_t merge = (size_t)AT_WARPS * G * DH * 4 + ((size_t)2 * G * a.n_chunks + 2 * G) * 4;
+    const size_t merge = nw * G * DH * 4 + ((size_t)2 * G * a.n_chunks + 2 * G) * 4;
     // g > 1: the per-warp cp.async row ring (8 warps x depth rows x K + V)
     // sits right after rows[]; the pair select's scratch (selector CTA, before
     // the gather) and the per-warp merge (after it) alias it.  Not for the
     // key path, whose g > 1 launch only selects.
     const bool ring = G > 1 && a.src != SRC_KEYS;
-    const size_t ring4 = (size_t)AT_WARPS * 4 * 2 * DH * 4;
+    const size_t ring4 = nw * 4 * 2 * DH * 4;
     auto region_for = [&](size_t ring_bytes) {
         size_t r = std::max(rows_bytes + ring_bytes, merge);
         if (a.src == SRC_PAIRS) r = std::max(r, pair_select_scratch(a.C, a.n_tchunks));
@@ -1562,16 +1610,16 @@ static size_t attend_smem(AtArgs& a, int G) {
     // depth 4 unless only depth 2 keeps 4 CTAs per SM (227 KB / 4 less the
     // 1 KB per-CTA reservation)
     const size_t per4 = 55 * 1024;
-    a.ring4 = !ring || region_for(ring4) + tail <= per4 || region_for(ring4 / 2) + tail > per4;
+    a.ring4 = wide || !ring || region_for(ring4) + tail <= per4 || region_for(ring4 / 2) + tail > per4;
     const size_t region = region_for(ring ? (a.ring4 ? ring4 : ring4 / 2) : 0);
     a.region = (int)region;
     a.ring_off = (int)rows_bytes;
     return region + round_up(tail, 16);
 }
 
-template <int G, int MODE>
+template <int G, int MODE, int NT = AT_THREADS>
 static void launch_attend_gm(const AtArgs& a, dim3 grid, size_t smem, int cl, cudaStream_t st) {
-    auto kern = attend_kernel<G, MODE>;
+    auto kern = attend_kernel<G, MODE, NT>;
     // attributes only grow: set once per (instantiation, device, thread) and
     // new size instead of on every decode
     static thread_local int smem_set[64], np_set[64];
@@ -1593,7 +1641,7 @@ static void launch_attend_gm(const AtArgs& a, dim3 grid, size_t smem, int cl, cu
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(AT_THREADS);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
@@ -1622,6 +1670,13 @@ static void launch_attend_gm(const AtArgs& a, dim3 grid, size_t smem, int cl, cu
 
 template <int G>
 static void launch_attend_g(const AtArgs& a, dim3 grid, size_t smem, int cl, cudaStream_t st) {
+    if constexpr (G > 1) {
+        if (a.nt > AT_THREADS) {  // wide g > 1 plans (1024 threads, no key path)
+            if (a.src == SRC_PAIRS) launch_attend_gm<G, SRC_PAIRS, 1024>(a, grid, smem, cl, st);
+            else launch_attend_gm<G, 0, 1024>(a, grid, smem, cl, st);
+            return;
+        }
+    }
     if (a.src == SRC_PAIRS) launch_attend_gm<G, SRC_PAIRS>(a, grid, smem, cl, st);
     else if (a.src == SRC_KEYS) launch_attend_gm<G, SRC_KEYS>(a, grid, smem, cl, st);
     else launch_attend_gm<G, 0>(a, grid, smem, cl, st);
@@ -1637,7 +1692,7 @@ static int plan_attend_launch(AtArgs& a, int G, size_t* smem) {
         const char* e = std::getenv("PQKV_CLUSTER");
         return e ? std::atoi(e) : 0;
     }();
-    if (a.src == SRC_PAIRS && a.n_chunks >= 4) {
+    if (a.src == SRC_PAIRS && a.n_chunks >= 4 && a.nt <= AT_THREADS) {  // wide CTAs select on their own
         cl = a.n_chunks >= 8 ? 8 : 4;  // 4 chunks per head (many heads): no empty padded CTAs
         if (forced_cl == 4 || forced_cl == 8) cl = forced_cl;
         a.n_chunks = (int)round_up((size_t)a.n_chunks, (size_t)cl);
@@ -1757,6 +1812,21 @@ bool decode_keys_split(const pqkv_layer& L, size_t G) {
     return ctas < 2 * (size_t)sms || ctas > per_sm * (size_t)sms;
 }
 
+// Wide plans (1024-thread CTAs) for the g > 1 gathers: on unless
+// PQKV_WIDE=0; needs the whole row list of a chunk in shared memory next to
+// the 128 KB row ring.
+static bool wide_plan(pqkv_ctx* ctx, const pqkv_layer& L, size_t G) {
+    static const bool on = [] {
+        const char* e = std::getenv("PQKV_WIDE");
+        return !(e && *e == '0');
+    }();
+    if (!on || G < 2 || L.n_heads == 0) return false;
+    const size_t s_mid = L.total - L.n_init - L.n_local;
+    const size_t per_head = std::max<size_t>(1, (size_t)ctx->sm_count / L.n_heads);
+    const size_t chunk = round_up(ceil_div(s_mid, per_head), (size_t)32);
+    return (chunk + L.n_init + L.n_local) * 4 + chunk / 8 + 128 * 1024 + 8192 <= 200 * 1024;
+}
+
 // AtArgs of a decode attention launch (everything but queries, out and the
 // selection inputs).
 static void decode_args(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_pairs, size_t k_keys, bool bitmap,
@@ -1785,7 +1855,20 @@ static void decode_args(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_p
     a.k = (int)(k_keys ? k_keys : k_pairs);
     a.m = (int)L.m;
     a.sel_only = nullptr;
-    if (k_keys) keys_geometry(L, G, &a.chunk, &a.n_chunks);
+    a.nt = AT_THREADS;
+    if (k_keys) {
+        keys_geometry(L, G, &a.chunk, &a.n_chunks);
+    } else if (wide_plan(ctx, L, G)) {
+        // g > 1: one 1024-thread CTA per SM whose 32 warps claim rows
+        // dynamically (every SM gets the same share of rows and no warp idles
+        // at the end); pair mode selects in every CTA (no clusters)
+        const size_t per_head = std::max<size_t>(1, (size_t)ctx->sm_count / L.n_heads);
+        a.nt = 1024;
+        static const bool claim = std::getenv("PQKV_CLAIM") != nullptr;
+        a.claim = claim;
+        a.chunk = (int)round_up(ceil_div(s_mid, per_head), (size_t)32);
+        a.n_chunks = (int)std::max<size_t>(1, ceil_div(s_mid, (size_t)a.chunk));
+    }
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)L.d_h));
 }
 

@@ -280,7 +280,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
                             const uint32_t* thist, const uint16_t* chist, int n_chunks, int k,
                             double* lut, uint32_t* hist, uint32_t* cnt, uint32_t* lst, uint32_t* ceq,
                             uint32_t* wsum, uint32_t* sh, uint8_t* cls, uint32_t* tkey_out,
-                            unsigned long long* tp = nullptr, bool lut_ready = false) {
+                            unsigned long long* tp = nullptr) {
     const int tid = threadIdx.x, C2 = C * C, lane = tid & 31, warp = tid >> 5;
     const int wbits = 32 - (32 - __clz((unsigned)(C2 - 1) | 1u));  // weight bits of a list entry
     const uint32_t wmask = (1u << wbits) - 1u;
@@ -295,9 +295,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
     }
     // the centroid table is staged in hist[] .. lst[] (2 NB + C^2 words, not
     // used before the compaction below) when it fits
-    if (!lut_ready)  // (the fused decode builds it across its cluster)
-        build_lut(lut, q, cen, g, d_h, 2, C,
-                  2 * C * (d_h / 2) <= 2 * NB + C * C ? reinterpret_cast<float4*>(hist) : nullptr);
+    build_lut(lut, q, cen, g, d_h, 2, C, 2 * C * (d_h / 2) <= 2 * NB + C * C ? reinterpret_cast<float4*>(hist) : nullptr);
     for (int c = tid; c < n_chunks; c += NT) ceq[c] = 0;
     for (int e = tid; e < (C2 + 3) / 4; e += NT) reinterpret_cast<uint32_t*>(cls)[e] = 0u;
     PQKV_T(1);
