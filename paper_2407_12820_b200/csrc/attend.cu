@@ -361,7 +361,7 @@ __device__ __forceinline__ uint32_t dsmem_ld(const void* local_ptr, unsigned ran
     return v;
 }
 
-template <int G>
+template <int G, int NT = AT_THREADS>
 __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsigned char* region, uint32_t* words,
                                   uint32_t* hbuf /*[2][NB] + own[NB]*/, uint32_t* pub /*[4]*/, uint32_t* wtot,
                                   uint32_t* sh, unsigned long long* tp) {
@@ -372,7 +372,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
     uint32_t* keys = reinterpret_cast<uint32_t*>(region);            // [chunk]
     double* lut = reinterpret_cast<double*>(keys + a.chunk);          // [m][C]
-    for (int e = tid; e < 2 * NB; e += AT_THREADS) hbuf[e] = 0u;      // both buffers
+    for (int e = tid; e < 2 * NB; e += NT) hbuf[e] = 0u;      // both buffers
     // ADC table split over the cluster: rank r computes its share of the
     // m*C entries, then copies the others' through DSMEM
     {
@@ -382,7 +382,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
                         m, C, e0, e1);
         __syncthreads();
         cluster_barrier();
-        for (int e = tid; e < ME; e += AT_THREADS)
+        for (int e = tid; e < ME; e += NT)
             if (e < e0 || e >= e1) lut[e] = dsmem_ld64(lut + e, (unsigned)(e / share));
     }
     __syncthreads();
@@ -391,18 +391,18 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     const uint16_t* cd = a.codes + p * a.codes_head_stride + (long long)r0 * m;
     uint32_t kmin = 0xffffffffu, kmax = 0u;
     const bool v4 = m == 4 && (reinterpret_cast<uintptr_t>(cd) & 7) == 0;
-    for (int i0 = 0; i0 < n; i0 += 8 * AT_THREADS) {
+    for (int i0 = 0; i0 < n; i0 += 8 * NT) {
         uint2 cv[8];
         if (v4) {  // eight code rows in flight per thread
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const int i = i0 + u * AT_THREADS + tid;
+                const int i = i0 + u * NT + tid;
                 cv[u] = i < n ? *reinterpret_cast<const uint2*>(cd + 4LL * i) : make_uint2(0u, 0u);
             }
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * AT_THREADS + tid;
+            const int i = i0 + u * NT + tid;
             if (i >= n) break;
             double acc = 0.0;
             if (v4) {
@@ -428,7 +428,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     __syncthreads();
     if (tid == 0) {
         uint32_t lo = 0xffffffffu;
-        for (int w = 0; w < AT_WARPS; ++w) lo = min(lo, wtot[w]);
+        for (int w = 0; w < (NT / 32); ++w) lo = min(lo, wtot[w]);
         pub[1] = lo;
     }
     __syncthreads();
@@ -436,7 +436,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     __syncthreads();
     if (tid == 0) {
         uint32_t hi = 0u;
-        for (int w = 0; w < AT_WARPS; ++w) hi = max(hi, wtot[w]);
+        for (int w = 0; w < (NT / 32); ++w) hi = max(hi, wtot[w]);
         pub[2] = hi;
     }
     __syncthreads();
@@ -464,10 +464,10 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
         const int nb = 1 << width;
         uint32_t* h = hbuf + (pass & 1) * NB;
         if (pass >= 2) {  // this buffer was last read before the previous pass's barriers
-            for (int e = tid; e < NB; e += AT_THREADS) h[e] = 0u;
+            for (int e = tid; e < NB; e += NT) h[e] = 0u;
             __syncthreads();
         }
-        for (int i0 = 0; i0 < n; i0 += AT_THREADS) {
+        for (int i0 = 0; i0 < n; i0 += NT) {
             const int i = i0 + tid;
             uint32_t bin = 0xffffffffu;
             if (i < n) {
@@ -484,7 +484,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
         {
             const int o0 = (int)crank * share, o1 = min(nb, o0 + share);
             uint32_t tot = 0;
-            for (int bn = o0 + tid; bn < o1; bn += AT_THREADS) {
+            for (int bn = o0 + tid; bn < o1; bn += NT) {
                 uint32_t v = 0;
                 for (unsigned r = 0; r < ncl; ++r) v += dsmem_ld(h + bn, r);
                 own[bn - o0] = v;
@@ -495,7 +495,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
             __syncthreads();
             if (tid == 0) {
                 uint32_t t = 0;
-                for (int w = 0; w < AT_WARPS; ++w) t += wtot[w];
+                for (int w = 0; w < (NT / 32); ++w) t += wtot[w];
                 pub[3] = t;
             }
             __syncthreads();
@@ -521,8 +521,8 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
         const uint32_t above_share = sh[3];
         // digit inside share rs: thread t owns share bins [hi - per, hi), top down
         const int o0 = (int)rs * share, cnt_bins = min(nb, o0 + share) - o0;
-        const int nbe = max(cnt_bins, AT_THREADS);
-        const int per = (nbe + AT_THREADS - 1) / AT_THREADS;  // 1..8
+        const int nbe = max(cnt_bins, NT);
+        const int per = (nbe + NT - 1) / NT;  // 1..8
         const int hi = nbe - per * tid;
         uint32_t cnt[8];
         uint32_t local = 0;
@@ -533,7 +533,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
             local += cnt[e];
         }
         const uint32_t kk = k_rem - above_share;
-        const uint32_t above = block_excl_scan<AT_THREADS>(local, wtot, nullptr);
+        const uint32_t above = block_excl_scan<NT>(local, wtot, nullptr);
         if (above < kk && kk <= above + local) {
             uint32_t acc = above;
 #pragma unroll
@@ -569,7 +569,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     const uint32_t take = k_rem > eq_before ? min(cta_eq, k_rem - eq_before) : 0u;
     // ---- selection words in id order ----
-    const int seg = a.chunk / AT_WARPS;
+    const int seg = a.chunk / (NT / 32);
     const int s0 = warp * seg, s1 = min(n, s0 + seg);
     // this CTA's ties are all taken or none is (the usual case): no per-warp
     // tie prefix needed
