@@ -347,7 +347,7 @@ __device__ void build_lut_range(double* lut, const float* q, const float* cen, i
         for (int r = 0; r < g; ++r) {
             const float* qq = q + (long long)r * d_h + j * d_m;
             double acc = 0.0;
-            for (int u = 0; u < d_m; ++u) acc = __fma_rn((double)__ldg(qq + u), (double)__ldg(cc + u), acc);
+            for (int u = 0; u < d_m; ++u) acc = __fma_rn((double)qq[u], (double)__ldg(cc + u), acc);
             t = __dadd_rn(t, acc);
         }
         lut[e] = t;
@@ -362,7 +362,8 @@ __device__ __forceinline__ uint32_t dsmem_ld(const void* local_ptr, unsigned ran
 }
 
 template <int G, int NT = AT_THREADS>
-__device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsigned char* region, uint32_t* words,
+__device__ void keys_select_words(const AtArgs& a, const float* q, int p, int r0, int r1, unsigned char* region,
+                                  uint32_t* words,
                                   uint32_t* hbuf /*[2][NB] + own[NB]*/, uint32_t* pub /*[4]*/, uint32_t* wtot,
                                   uint32_t* sh, unsigned long long* tp) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -378,7 +379,7 @@ __device__ void keys_select_words(const AtArgs& a, int p, int r0, int r1, unsign
     {
         const int ME = m * C, share = (ME + (int)ncl - 1) / (int)ncl;
         const int e0 = min(ME, (int)crank * share), e1 = min(ME, e0 + share);
-        build_lut_range(lut, a.queries + (long long)p * G * DH, a.centroids + (long long)p * m * C * (DH / m), G, DH,
+        build_lut_range(lut, q, a.centroids + (long long)p * m * C * (DH / m), G, DH,
                         m, C, e0, e1);
         __syncthreads();
         cluster_barrier();
@@ -635,7 +636,8 @@ struct WindowRefill {
 // per-warp area (wacc / wm / wl).  Rows: rows[0..nrows) of this CTA, and for
 // windowed chunks the later windows of its selection words.
 template <class Refill>
-__device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int* rows, int nrows, Refill& refill,
+__device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, const float* qsrc, int p, int* rows, int nrows,
+                                                     Refill& refill,
                                                      unsigned char* smem_raw, float (*wm)[1], float (*wl)[1]) {
     constexpr int G = 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -645,10 +647,10 @@ __device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int
     float q[G][4 * VPL];
 #pragma unroll
     for (int r = 0; r < G; ++r) {
-        const float4* qp = reinterpret_cast<const float4*>(a.queries + ((long long)p * G + r) * DH);
+        const float4* qp = reinterpret_cast<const float4*>(qsrc + r * DH);
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
-            float4 v = __ldg(qp + j * LPR + hl);
+            float4 v = qp[j * LPR + hl];
             q[r][4 * j + 0] = v.x * a.scale_log2;
             q[r][4 * j + 1] = v.y * a.scale_log2;
             q[r][4 * j + 2] = v.z * a.scale_log2;
@@ -820,7 +822,8 @@ __device__ __forceinline__ void gather_rows_halfwarp(const AtArgs& a, int p, int
 // (tools/microbench/gqa_probe.cu): 4.95 TB/s vs 4.2-4.35 TB/s for the
 // half-warp-per-row ring.
 template <int G, int NT, class Refill>
-__device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int* rows, int nrows, Refill& refill,
+__device__ __forceinline__ void gather_rows_warp(const AtArgs& a, const float* qsrc, int p, int* rows, int nrows,
+                                                 Refill& refill,
                                                  unsigned char* smem_raw, float (*wm)[G], float (*wl)[G],
                                                  unsigned* claim = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -832,7 +835,7 @@ __device__ __forceinline__ void gather_rows_warp(const AtArgs& a, int p, int* ro
     float4 q[G];
 #pragma unroll
     for (int r = 0; r < G; ++r) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(a.queries + ((long long)p * G + r) * DH) + lane);
+        const float4 v = reinterpret_cast<const float4*>(qsrc + r * DH)[lane];
         q[r] = make_float4(v.x * a.scale_log2, v.y * a.scale_log2, v.z * a.scale_log2, v.w * a.scale_log2);
     }
     const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
@@ -1130,6 +1133,18 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
+    // g > 1: this head's G query rows, read once into shared memory (they
+    // may sit in page-locked host memory: pqkv_decode_host passes mapped
+    // queries straight through).  g = 1 reads them from global memory (the
+    // shared copy cost the north star's gather ~9 us: bimodal CTA spans).
+    __shared__ __align__(16) float q_sh[G > 1 ? G * DH : 4];
+    const float* q_s = a.queries + (long long)p * G * DH;
+    if constexpr (G > 1) {
+        for (int i = tid; i < G * DH / 4; i += NT)
+            reinterpret_cast<float4*>(q_sh)[i] = reinterpret_cast<const float4*>(q_s)[i];
+        __syncthreads();
+        q_s = q_sh;
+    }
     // ---- 1. this CTA's row list (ascending token ids) ----
     int nrows = 0;
     int sel_total = 0;  // windowed list: selected middle rows of this CTA (0: one window)
@@ -1147,7 +1162,7 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
             for (int w = tid; w < nw; w += NT) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
         } else if ((MODE == SRC_KEYS)) {
             __shared__ uint32_t pub_s[4], sh_s[4];
-            keys_select_words<G>(a, p, r0, r1, smem_raw, words, eqw /* [2][NB/2] in keys mode */, pub_s, wtot, sh_s,
+            keys_select_words<G>(a, q_s, p, r0, r1, smem_raw, words, eqw /* [2][NB/2] in keys mode */, pub_s, wtot, sh_s,
                                  a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr);
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 1] = clock64();
             if (a.sel_only) {  // select-only launch: the bitmap-mode attention follows
@@ -1201,7 +1216,7 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
             const int C = a.C, C2 = C * C;
             if (crank == sel) {
                 PairScratch ps(smem_raw, C, a.n_tchunks);  // aliases rows[]: free until expansion
-                pair_select<NT, (4096 + NT - 1) / NT>(a.queries + (long long)p * G * DH, G, DH,
+                pair_select<NT, (4096 + NT - 1) / NT>(q_s, G, DH,
                                             a.centroids + (long long)p * 2 * C * (DH / 2), C,
                                             a.thist + (long long)p * C2, a.chist + (long long)p * a.tchunk_stride * C2,
                                             a.n_tchunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
@@ -1273,14 +1288,14 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
 
     WindowRefill<NT> refill{a, c, words, wtot, sel_total, 0};
     if constexpr (G == 1) {
-        gather_rows_halfwarp(a, p, rows, nrows, refill, smem_raw, wm, wl);
+        gather_rows_halfwarp(a, q_s, p, rows, nrows, refill, smem_raw, wm, wl);
     } else if (NT > AT_THREADS && a.claim) {
         __shared__ unsigned claim_ctr;
         if (tid == 0) claim_ctr = (unsigned)(NT / 32) * 4u;  // the warps' first batches are static
         __syncthreads();
-        gather_rows_warp<G, NT>(a, p, rows, nrows, refill, smem_raw, wm, wl, &claim_ctr);
+        gather_rows_warp<G, NT>(a, q_s, p, rows, nrows, refill, smem_raw, wm, wl, &claim_ctr);
     } else {
-        gather_rows_warp<G, NT>(a, p, rows, nrows, refill, smem_raw, wm, wl);
+        gather_rows_warp<G, NT>(a, q_s, p, rows, nrows, refill, smem_raw, wm, wl);
     }
     // ---- 5. merge warps, write this CTA's partial ----
     write_partial<G, NT>(a, p, c, smem_raw, wm, wl);

@@ -470,16 +470,25 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
         // tensors under UVA): the combining CTAs write the outputs straight
         // into host memory, so no D2H copy sits between the kernel and the
         // synchronize
-        float* mapped = nullptr;
-        {
+        auto device_view = [](const void* h) -> void* {
             cudaPointerAttributes pa{};
-            if (cudaPointerGetAttributes(&pa, h_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-                pa.devicePointer != nullptr)
-                mapped = static_cast<float*>(pa.devicePointer);
+            void* d = nullptr;
+            if (cudaPointerGetAttributes(&pa, h) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+                d = pa.devicePointer;
             cudaGetLastError();
-        }
-        PQKV_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, st));
-        int rc = pqkv_decode(ctx, L, d_q, g, k, mapped ? mapped : d_o, nullptr, stream);
+            return d;
+        };
+        float* mapped = static_cast<float*>(device_view(h_out));
+        // with g > 1 the attention-kernel modes read each head's queries
+        // once into shared memory, so page-locked, device-mapped queries go
+        // straight in (no copy launch ahead of the kernel); g = 1 and the
+        // other modes' select kernels read them repeatedly: device copy
+        const int mode = decode_mode(*L, g, k, false);
+        const bool direct = g > 1 && (mode == PQKV_MODE_PAIRS_FUSED || mode == PQKV_MODE_KEYS_FUSED ||
+                                      mode == PQKV_MODE_KEYS_SPLIT);
+        const float* mapped_q = direct ? static_cast<const float*>(device_view(h_queries)) : nullptr;
+        if (!mapped_q) PQKV_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, st));
+        int rc = pqkv_decode(ctx, L, mapped_q ? mapped_q : d_q, g, k, mapped ? mapped : d_o, nullptr, stream);
         if (rc != PQKV_OK) fail(rc, pqkv_last_error());
         if (!mapped) PQKV_CUDA(cudaMemcpyAsync(h_out, d_o, qbytes, cudaMemcpyDeviceToHost, st));
         PQKV_CUDA(cudaStreamSynchronize(st));

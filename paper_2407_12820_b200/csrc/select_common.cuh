@@ -29,7 +29,7 @@ __device__ __forceinline__ void lut_entry_vec(double* lut, const float* q, const
         const float4* q4 = reinterpret_cast<const float4*>(q + (long long)r * d_h + j * DM);
         float4 qv[DM / 4];
 #pragma unroll
-        for (int u = 0; u < DM / 4; ++u) qv[u] = __ldg(q4 + u);
+        for (int u = 0; u < DM / 4; ++u) qv[u] = q4[u];  // q may be in shared memory
         double acc = 0.0;
 #pragma unroll
         for (int u = 0; u < DM / 4; ++u) {
@@ -60,7 +60,7 @@ __device__ __forceinline__ void lut_entry_multi(double* lut, const float* q, con
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
                 if (rr < rn) {
-                    const float4 qv = __ldg(reinterpret_cast<const float4*>(q + (long long)(r0 + rr) * d_h + j * DM) + u);
+                    const float4 qv = reinterpret_cast<const float4*>(q + (long long)(r0 + rr) * d_h + j * DM)[u];
                     acc[rr] = __fma_rn((double)qv.x, (double)cv.x, acc[rr]);
                     acc[rr] = __fma_rn((double)qv.y, (double)cv.y, acc[rr]);
                     acc[rr] = __fma_rn((double)qv.z, (double)cv.z, acc[rr]);
@@ -97,7 +97,7 @@ __device__ __forceinline__ void lut_entry(double* lut, const float* q, const flo
     for (int r = 0; r < g; ++r) {
         const float* qq = q + (long long)r * d_h + j * dm;
         double acc = 0.0;
-        for (int u = 0; u < dm; ++u) acc = __fma_rn((double)__ldg(qq + u), (double)__ldg(cc + u), acc);
+        for (int u = 0; u < dm; ++u) acc = __fma_rn((double)qq[u], (double)__ldg(cc + u), acc);
         t = __dadd_rn(t, acc);
     }
     lut[e] = t;
@@ -121,7 +121,7 @@ __device__ __forceinline__ void lut_entry_staged(double* lut, const float* q, co
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
                 if (rr < rn) {
-                    const float4 qv = __ldg(reinterpret_cast<const float4*>(q + (long long)(r0 + rr) * d_h + j * DM) + u);
+                    const float4 qv = reinterpret_cast<const float4*>(q + (long long)(r0 + rr) * d_h + j * DM)[u];
                     acc[rr] = __fma_rn((double)qv.x, (double)cv.x, acc[rr]);
                     acc[rr] = __fma_rn((double)qv.y, (double)cv.y, acc[rr]);
                     acc[rr] = __fma_rn((double)qv.z, (double)cv.z, acc[rr]);
@@ -194,7 +194,7 @@ __device__ inline void build_lut(double* lut, const float* q, const float* cen, 
                     const float* qq = q + (long long)(r0 + r) * d_h + j * d_m + t0;
                     float qv[16];
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) qv[u] = (t0 + u < d_m) ? __ldg(qq + u) : 0.0f;
+                    for (int u = 0; u < 16; ++u) qv[u] = (t0 + u < d_m) ? qq[u] : 0.0f;
 #pragma unroll
                     for (int u = 0; u < 16; ++u)
                         if (t0 + u < d_m) acc[r] = __fma_rn((double)qv[u], (double)cv[u], acc[r]);
