@@ -112,10 +112,25 @@ __device__ __forceinline__ void lut_entry_staged(double* lut, const float* q, co
                                                  int e, int j) {
     const float4* row = stage + (long long)e * (DM / 4);
     double t = 0.0;
+    if (g == 1) {  // one chain; a partial unroll keeps the query loads from
+                   // crowding the registers (the fused decode runs at 64)
+        const float4* q4 = reinterpret_cast<const float4*>(q + j * DM);
+        double acc = 0.0;
+#pragma unroll 4
+        for (int u = 0; u < DM / 4; ++u) {
+            const float4 cv = row[u ^ (e & 7)], qv = q4[u];
+            acc = __fma_rn((double)qv.x, (double)cv.x, acc);
+            acc = __fma_rn((double)qv.y, (double)cv.y, acc);
+            acc = __fma_rn((double)qv.z, (double)cv.z, acc);
+            acc = __fma_rn((double)qv.w, (double)cv.w, acc);
+        }
+        lut[e] = __dadd_rn(t, acc);
+        return;
+    }
     for (int r0 = 0; r0 < g; r0 += 4) {
         const int rn = min(4, g - r0);
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+#pragma unroll 4
         for (int u = 0; u < DM / 4; ++u) {
             const float4 cv = row[u ^ (e & 7)];
 #pragma unroll

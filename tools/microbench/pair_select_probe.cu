@@ -13,7 +13,7 @@ __device__ unsigned long long g_t[40];
 
 using namespace pqkv_dev;
 
-__global__ void probe(const float* q, int g, const float* cen, const uint32_t* thist, const uint16_t* chist,
+__global__ void __launch_bounds__(256, PROBE_MINB) probe(const float* q, int g, const float* cen, const uint32_t* thist, const uint16_t* chist,
                       int n_chunks, int k, uint32_t* res) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = 64;
