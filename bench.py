@@ -35,6 +35,18 @@ S_MID = S - N_INIT - N_LOCAL
 N_LAYERS = 8
 METRIC = "decode PQ-retrieve+attend us/layer @128K ctx"
 WORKLOAD = "northstar-1layer-32h-128d-128Kctx-m2b6-top1/5+4init+64local-bs1"
+KINDS = ("gaussian", "powerlaw")  # the reference's two key distributions (workload.cpp)
+
+
+def workload_config(world):
+    """The workload both arms run (ours and --impl reference print the same
+    dict): geometry, the two key distributions and which one `value` is."""
+    return {"workload": WORKLOAD, "global_batch": 1, "seq_len": S, "heads": H, "head_dim": DH, "g": G,
+            "m": M, "b": B, "k": K_SEL, "n_init": N_INIT, "n_local": N_LOCAL,
+            "key_distributions": list(KINDS), "value_is": "the slower of the two distributions",
+            "parallelism": f"dp{world} (independent layers per GPU)",
+            "l2": "inputs larger than L2: 8 rotating layers x 4.3 GB K/V per distribution (+26 MB codes and "
+                  "pair tables each: 206 MB > L2), 0.86 GB gathered per step"}
 
 # BASELINE.json configs as decode units (one unit = one (request, layer,
 # kv_head) K/V set shared by g query heads).  "northstar" is the headline;
@@ -191,8 +203,7 @@ def run_reference(args, rank, world):
         return
     line = {"impl": "reference", "metric": METRIC, "unit": "us/layer", "higher_is_better": False,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "scaling": "weak",
-            "dtype": "f32 storage, f64 arithmetic", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": 1, "seq_len": S}}
+            "dtype": "f32 storage, f64 arithmetic", "data": "synthetic", "config": workload_config(args.gpus)}
     if not oracle.has_ref():
         line["unavailable"] = "oracle/_ref/libpqkv_ref.so was not built (needs /root/reference at build time)"
         print(json.dumps(line), flush=True)
@@ -201,31 +212,35 @@ def run_reference(args, rank, world):
     cores = os.cpu_count() or 1
     P = min(H, max(1, cores))  # one head per host thread
     rng = np.random.default_rng(17)
-    keys = np.empty((P, S, DH), np.float32)
-    vals = rng.standard_normal((P, S, DH), dtype=np.float32)
-    for p in range(P):
-        means = rng.standard_normal((8, DH)).astype(np.float32)
-        keys[p] = means[rng.integers(0, 8, S)] + 0.5 * rng.standard_normal((S, DH), dtype=np.float32)
-    queries = rng.standard_normal((P, G, DH)).astype(np.float32)
-    # the reference builds its own index (pq_construct on all host cores, untimed setup)
-    mids = np.ascontiguousarray(keys[:, N_INIT:N_INIT + S_MID])
-    _, cen, codes = ref.bench_build(mids, M, B, T_ITERS, np.arange(P, dtype=np.uint64) + 11, 0)
-    del mids
     n_total = args.warmup + args.steps
     sigma = 0.25 / math.sqrt(DH)
-    queries = (queries[None] + sigma * rng.standard_normal((n_total, P, G, DH))).astype(np.float32)
-    # HeadStates are built once (kv_store offload_prefill); every step is one
-    # decode of the P sampled heads (pq_score_gqa + approx_topk +
-    # selective_attention), one head per host thread
-    secs, _ = ref.bench_decode_steps(keys, vals, queries, cen, codes, N_INIT, N_LOCAL, K_SEL, 0)
-    timed = secs[args.warmup:]
-    per_layer_us = float(np.mean(timed)) * 1e6 * (H / P)
+    per_kind = {}
+    for kind in KINDS:
+        # the reference's own generator (workload.cpp: gaussian mixture /
+        # powerlaw keys) and its own index (pq_construct on all host cores),
+        # both untimed setup
+        keys, vals, queries = ref.gen_workload(S, DH, h_kv=P, g=G, kind=oracle.KINDS[kind], n_components=8,
+                                               spread=0.5, seed=17 + KINDS.index(kind))
+        mids = np.ascontiguousarray(keys[:, N_INIT:N_INIT + S_MID])
+        _, cen, codes = ref.bench_build(mids, M, B, T_ITERS, np.arange(P, dtype=np.uint64) + 11, 0)
+        del mids
+        qs = (queries[None] + sigma * rng.standard_normal((n_total, P, G, DH))).astype(np.float32)
+        # HeadStates are built once (kv_store offload_prefill); every step is
+        # one decode of the P sampled heads (pq_score_gqa + approx_topk +
+        # selective_attention), one head per host thread
+        secs, _ = ref.bench_decode_steps(keys, vals, qs, cen, codes, N_INIT, N_LOCAL, K_SEL, 0)
+        per_kind[kind] = float(np.mean(secs[args.warmup:])) * 1e6 * (H / P)
+        del keys, vals, qs, cen, codes
+    worst = max(per_kind, key=per_kind.get)
+    per_layer_us = per_kind[worst]
     line.update({"value": per_layer_us, "ms_per_step": per_layer_us / 1e3,
+                 "distributions": {"us_per_layer": per_kind, "slower": worst},
                  "cpu_baseline": {"value": per_layer_us, "unit": "us/layer", "cores": min(cores, P),
                                   "kind": "reference",
                                   "sample": f"{P} of {H} heads per step (x{H / P:g} to a layer), "
-                                            "pq_score_gqa+approx_topk+selective_attention, index built by "
-                                            "the reference's pq_construct"},
+                                            "pq_score_gqa+approx_topk+selective_attention, keys from the "
+                                            "reference's generator, index built by the reference's pq_construct; "
+                                            "the slower of the two distributions"},
                  "e2e": {"value": per_layer_us, "unit": "us/layer", "h2d_bytes_per_step": 0,
                          "d2h_bytes_per_step": 0}})
     print(json.dumps(line), flush=True)
@@ -618,15 +633,11 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 (K/V, attention), f64 (ADC table), u16 codes", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": 1, "seq_len": S, "heads": H, "head_dim": DH,
-                   "m": M, "b": B, "k": K_SEL, "n_init": N_INIT, "n_local": N_LOCAL,
-                   "layers_rotated": N_LAYERS, "parallelism": f"dp{world} (independent layers per GPU)",
-                   "key_distributions": {kd: timed[kd] * 1e3 / (args.steps * world) for kd in timed},
-                   "value_is": f"the slower distribution ({worst}); each timed over its own {args.steps} steps",
-                   "warmup_note": f"max(W, 2 x {N_LAYERS} rotating layers) untimed steps before each timed region",
-                   "plan": plan,
-                   "l2": "inputs larger than L2: 8 rotating layers x 4.3 GB K/V per distribution (+26 MB codes "
-                         "and pair tables each: 206 MB > L2), 0.86 GB gathered per step"},
+        "config": workload_config(world),
+        "distributions": {"us_per_layer": {kd: timed[kd] * 1e3 / (args.steps * world) for kd in timed},
+                          "slower": worst, "steps_each": args.steps, "layers_rotated": N_LAYERS,
+                          "warmup": f"max(W, 2 x {N_LAYERS} rotating layers) untimed steps before each timed region"},
+        "plan": plan,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "attend_kernel<1,3> pair mode (the whole fused decode step, 1 launch/layer)",

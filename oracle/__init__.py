@@ -23,6 +23,7 @@ REF_SO = os.path.join(HERE, "_ref", "libpqkv_ref.so")
 
 EINVAL, ERANGE, ESTATE = 1, 2, 3
 GAUSSIAN, POWERLAW = 0, 1
+KINDS = {"gaussian": GAUSSIAN, "powerlaw": POWERLAW}
 
 
 class OracleError(Exception):

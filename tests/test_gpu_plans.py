@@ -23,7 +23,7 @@ import bench  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 # The plan each config runs on one B200 (148 SMs); bench.py reports the same
-# dict under config.plan / configs.<name>.plan.
+# dict under plan / configs.<name>.plan.
 EXPECT = {
     "northstar": dict(mode="pairs_fused", launches=1, chunk_tokens=8192, ctas_per_head=16, cluster=8, staged=1,
                       window=8192),

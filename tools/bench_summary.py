@@ -5,7 +5,7 @@ import sys
 
 d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
 print("headline %.1f us (frac %.3f) dists %s" % (d["value"], d["roofline"]["frac"],
-                                                 {k: round(v, 1) for k, v in d["config"]["key_distributions"].items()}))
+                                                 {k: round(v, 1) for k, v in d["distributions"]["us_per_layer"].items()}))
 for k, v in (d.get("configs") or {}).items():
     print("  %-14s %6.1f us  frac %.3f" % (k, v.get("us_per_layer", float("nan")), v.get("frac", float("nan"))))
 for k in ("attend_only", "e2e", "head_sharded", "model_cfg3", "build", "e2e_cxx", "clocks"):
