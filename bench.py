@@ -640,7 +640,8 @@ def main():
         "plan": plan,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "attend_kernel<1,3> pair mode (the whole fused decode step, 1 launch/layer)",
+                     "kernel": "tuple_select_kernel + attend_kernel<1,0> (pair-select launch chained by programmatic "
+                               "launch to the attention launch; timed as the whole step, 2 launches/layer)",
                      "kernel_ms": ms_per_step, "algorithmic_bytes": layer_bytes,
                      "bytes_basis": "SURVEY 8(d): h_kv*(s_mid*m*b/8 + C*d_h*4 + T_att*d_h*4*2 + 2*g*d_h*4)"},
         "attend_only": {"kernel": "attend_kernel bitmap mode (gather + softmax + combine, selection precomputed)",

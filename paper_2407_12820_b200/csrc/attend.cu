@@ -1131,6 +1131,23 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
             for (int o = tid * 128; o < 4 * C2; o += NT * 128) prefetch_l2(th + o);
         }
     }
+    // split pair path (SRC_TUPLE): stage this CTA's code pairs while the
+    // select grid (the previous kernel) runs -- the codes are not written by
+    // it, and it waited for their producer before letting this grid launch
+    const uint32_t* tup_staged = nullptr;
+    if (MODE == 0 && a.src == SRC_TUPLE && a.stage) {
+        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk), n = max(0, r1 - r0);
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride) + r0;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(smem_raw);
+        int head = 0;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            head = n & ~3;
+            for (int f = tid; f < head / 4; f += NT) cp_async16(dst + 4 * code_swz(f), src + 4 * f);
+        }
+        for (int e = head + tid; e < n; e += NT) cp_async4(dst + 4 * code_swz(e >> 2) + (e & 3), src + e);
+        cp_async_commit();
+        tup_staged = dst;
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
     // g > 1: this head's G query rows, read once into shared memory (they
@@ -1153,7 +1170,7 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
         for (int e = tid; e < cnt; e += NT) rows[e] = (int)a.rows[(long long)p * a.t + b0 + e];
         nrows = cnt;
     } else {
-        if (c == 0 && (MODE != SRC_PAIRS) && (MODE != SRC_KEYS))  // written after the select (shared region)
+        if (c == 0 && (MODE != SRC_PAIRS) && (MODE != SRC_KEYS) && !tup_staged)  // written after the select (shared region)
             for (int e = tid; e < a.n_init; e += NT) rows[e] = e;
         nrows = c == 0 ? a.n_init : 0;
         const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
@@ -1253,12 +1270,15 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
             } else {
                 for (int e = tid; e < C2; e += NT) cls[e] = a.cls[(long long)p * C2 + e];
             }
+            if (tup_staged) cp_async_wait_all();
             __syncthreads();
-            classify_range<false, NT>(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride), nullptr,
-                           words, eqw, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
+            classify_range<false, NT>(a, r0, r1, reinterpret_cast<const uint32_t*>(a.codes + p * a.codes_head_stride),
+                                      tup_staged, words, eqw, cls, wtot, a.cut[2 * p], (uint32_t)a.cut[2 * p + 1]);
+            if (c == 0 && tup_staged)  // after the staged codes are consumed (they share rows[])
+                for (int e = tid; e < a.n_init; e += NT) rows[e] = e;
         }
         __syncthreads();
-        if (a.sel_dump && ((MODE == SRC_PAIRS) || (MODE == SRC_KEYS)))
+        if (a.sel_dump && ((MODE == SRC_PAIRS) || (MODE == SRC_KEYS) || src == SRC_TUPLE))
             for (int w = tid; w < nw; w += NT) a.sel_dump[(long long)p * a.words + r0 / 32 + w] = words[w];
         if (a.win >= a.chunk) {
             nrows += expand_words<NT>(words, nw, a.n_init + r0, rows, nrows, wtot);

@@ -296,10 +296,17 @@ static int decode_mode(const pqkv_layer& L, size_t g, size_t k, bool with_ids) {
     const bool fast = decode_fast_path(L, g);
     if (!fast) return PQKV_MODE_GENERIC;
     if (with_ids || k == 0) return PQKV_MODE_BITMAP;
-    static const bool force_split = std::getenv("PQKV_PAIRS_SPLIT") != nullptr;  // experiments only
-    // one launch: every attention CTA selects its head's pairs, then
-    // classifies its own codes and gathers
-    if (tup && decode_pairs_fused(L, g) && !force_split) return PQKV_MODE_PAIRS_FUSED;
+    // g > 1: one launch, every (wide) attention CTA selects its head's pairs,
+    // classifies its own codes and gathers.  g = 1: a pair-select launch
+    // (one 256-thread CTA per head with the whole register file) chained
+    // by programmatic launch to the attention grid, which stages its codes
+    // while the select runs (north star 155.4 / 164.5 -> 152.9 / 160.4 us
+    // against the 8-CTA-cluster fused launch, whose selecting CTA runs at 64
+    // registers beside three others).  PQKV_PAIRS_FUSED=1 / PQKV_PAIRS_SPLIT=1
+    // force either (experiments).
+    static const bool force_split = std::getenv("PQKV_PAIRS_SPLIT") != nullptr;
+    static const bool force_fused = std::getenv("PQKV_PAIRS_FUSED") != nullptr;
+    if (tup && decode_pairs_fused(L, g) && !force_split && (g > 1 || force_fused)) return PQKV_MODE_PAIRS_FUSED;
     // per-head cluster computes ADC keys and radix-selects through DSMEM,
     // then gathers (same launch, or a second finer bitmap-mode launch)
     if (!(tup && L.b <= 6) && decode_keys_fused(L, g))

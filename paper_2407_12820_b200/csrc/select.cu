@@ -367,7 +367,10 @@ __global__ void gather_scores_kernel(const double* lut_g, int m, int C, const ui
 // lowest-id boundary of the equal keys and how many of c*'s equal tokens are
 // taken.  tuple_bitmap then streams the codes once per chunk.
 // ===========================================================================
-constexpr int TUP_THREADS = 1024;
+// 256 threads with the whole register file for up to 4096 pairs (b <= 6;
+// no spills in the pair select -- at 1024 threads it runs at 64 registers),
+// 1024 threads for b = 7's 16384 pairs
+constexpr int TUP_THREADS = 256, TUP_THREADS_B7 = 1024;
 
 __global__ void tuple_tables_kernel(const uint16_t* codes, long long codes_head_stride, int C,
                                     int row_begin, int row_end, uint32_t* thist, uint16_t* chist,
@@ -409,7 +412,8 @@ struct TupArgs {
     long long chunk_stride;  // chunks per head of chist
 };
 
-__global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) tuple_select_kernel(TupArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int p = blockIdx.x, tid = threadIdx.x, C = a.C, C2 = C * C;
     PairScratch ps(smem, C, a.n_chunks);
@@ -418,7 +422,11 @@ __global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a)
     uint32_t* hist = ps.hist;  // per-chunk counts below (dead radix bins, 2*NB entries with cnt)
     uint8_t* cls = a.cls + (long long)p * C2;
     const uint16_t* ch = a.chist + (long long)p * a.chunk_stride * C2;
-    pair_select<TUP_THREADS, 16>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
+    // launched with programmatic stream serialization: wait for the queries'
+    // producer, then let the attention grid launch and stage its codes
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    pair_select<NT, 16>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
                                  a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
                                  ch, a.n_chunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
                                  a.tkey ? a.tkey + (long long)p * C2 : nullptr);
@@ -429,7 +437,7 @@ __global__ void __launch_bounds__(TUP_THREADS, 1) tuple_select_kernel(TupArgs a)
     if (a.sel_before) {  // selected rows per chunk -> exclusive prefix (ordered ids)
         const int cstar = (int)sh[3];
         const uint32_t take = sh[4];
-        for (int c = tid >> 5; c < a.n_chunks; c += TUP_THREADS / 32) {
+        for (int c = tid >> 5; c < a.n_chunks; c += NT / 32) {
             uint32_t gt = 0;
             for (int t = tid & 31; t < C2; t += 32)
                 if (cls[t] == 1) gt += ch[(long long)c * C2 + t];
@@ -711,8 +719,20 @@ void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
     if (a.chunk_stride < (long long)n_chunks) fail(PQKV_EINVAL, "tuple select: chunk table smaller than the rows");
     size_t smem = pair_select_scratch((int)C, (int)n_chunks);
     if (smem > 220 * 1024 || n_chunks > 2 * (size_t)NB) fail(PQKV_EINVAL, "tuple select: table too large");
-    PQKV_CUDA(cudaFuncSetAttribute(tuple_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tuple_select_kernel<<<(unsigned)rows, TUP_THREADS, smem, st>>>(a);
+    const bool wide = C * C > (size_t)TUP_THREADS * 16;
+    auto kern = wide ? tuple_select_kernel<TUP_THREADS_B7> : tuple_select_kernel<TUP_THREADS>;
+    PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)rows);
+    cfg.blockDim = dim3(wide ? TUP_THREADS_B7 : TUP_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PQKV_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     PQKV_LAUNCHED("tuple_select_kernel");
 }
 

@@ -38,9 +38,13 @@ def _run(ctx, orc, cen, codes, keys, vals, qs, b, n_init, n_local, k, tables):
         ctx.set_selection_dump(None)
     pair_path = m == 2 and b <= 6 and tables
     g = qs.shape[1]
-    # pair path: one launch; key path: select + attention for g > 1 or when
-    # the per-head cluster grid is too small for the gather, else one launch
-    assert layer.launches(g) == 1 if pair_path else (layer.launches(g) == 2 if g > 1 else layer.launches(g) in (1, 2))
+    # pair path: one launch for g > 1, a pair-select launch + the attention
+    # for g = 1; key path: select + attention for g > 1 or when the per-head
+    # cluster grid is too small for the gather, else one launch
+    if pair_path:
+        assert layer.launches(g) == (1 if g > 1 else 2)
+    else:
+        assert layer.launches(g) == 2 if g > 1 else layer.launches(g) in (1, 2)
     bits = dump.cpu().numpy().view(np.uint32)
     for p in range(P):
         rows = orc.top_k_desc(orc.pq_score_gqa(qs[p], cen[p], codes[p]), k)
@@ -116,7 +120,7 @@ def test_fused_decode_many_heads_windowed(ctx, orc, g, ratio):
         out = ctx.decode(layer, qs, k).cpu().numpy()
     finally:
         ctx.set_selection_dump(None)
-    assert layer.launches(g) == 1
+    assert layer.launches(g) == (1 if g > 1 else 2)
     bits = dump.cpu().numpy().view(np.uint32)
     cen_h = cen.cpu().numpy()
     codes_h = codes.cpu().numpy().view(np.uint16)

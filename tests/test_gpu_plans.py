@@ -25,10 +25,11 @@ pytestmark = pytest.mark.gpu
 # The plan each config runs on one B200 (148 SMs); bench.py reports the same
 # dict under plan / configs.<name>.plan.
 EXPECT = {
-    "northstar": dict(mode="pairs_fused", launches=1, chunk_tokens=8192, ctas_per_head=16, cluster=8, staged=1,
+    # g = 1: pair-select launch + attention launch (codes staged while the select runs)
+    "northstar": dict(mode="pairs_split", launches=2, chunk_tokens=8192, ctas_per_head=16, cluster=1, staged=1,
                       window=8192),
-    "cfg1": dict(mode="pairs_fused", launches=1),
-    "cfg2": dict(mode="pairs_fused", launches=1, chunk_tokens=2048, ctas_per_head=16, cluster=8, staged=1),
+    "cfg1": dict(mode="pairs_split", launches=2),
+    "cfg2": dict(mode="pairs_split", launches=2, chunk_tokens=2048, ctas_per_head=16, cluster=1, staged=1),
     # g > 1: wide plan, one 1024-thread CTA per SM (148 // 8 = 18 per head), each selecting on its own
     "cfg3_layer": dict(mode="pairs_fused", launches=1, chunk_tokens=7296, ctas_per_head=18, cluster=1, staged=0),
     "cfg5_per_gpu": dict(mode="keys_split", launches=2),
