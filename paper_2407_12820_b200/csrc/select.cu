@@ -367,10 +367,10 @@ __global__ void gather_scores_kernel(const double* lut_g, int m, int C, const ui
 // lowest-id boundary of the equal keys and how many of c*'s equal tokens are
 // taken.  tuple_bitmap then streams the codes once per chunk.
 // ===========================================================================
-// 256 threads with the whole register file for up to 4096 pairs (b <= 6;
-// no spills in the pair select -- at 1024 threads it runs at 64 registers),
-// 1024 threads for b = 7's 16384 pairs
-constexpr int TUP_THREADS = 256, TUP_THREADS_B7 = 1024;
+// 512 threads (128 registers, 8 pairs per thread) for up to 4096 pairs
+// (b <= 6): powerlaw select 11.3 -> 9.6 us against 256 threads
+// (tools/microbench/pair_select_probe.cu); 1024 threads for b = 7's 16384
+constexpr int TUP_THREADS = 512, TUP_THREADS_B7 = 1024;
 
 __global__ void tuple_tables_kernel(const uint16_t* codes, long long codes_head_stride, int C,
                                     int row_begin, int row_end, uint32_t* thist, uint16_t* chist,
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(NT, 1) tuple_select_kernel(TupArgs a) {
     // producer, then let the attention grid launch and stage its codes
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
-    pair_select<NT, 16>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
+    pair_select<NT, NT >= 1024 ? 16 : 4096 / NT>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
                                  a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
                                  ch, a.n_chunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
                                  a.tkey ? a.tkey + (long long)p * C2 : nullptr);
@@ -719,7 +719,7 @@ void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
     if (a.chunk_stride < (long long)n_chunks) fail(PQKV_EINVAL, "tuple select: chunk table smaller than the rows");
     size_t smem = pair_select_scratch((int)C, (int)n_chunks);
     if (smem > 220 * 1024 || n_chunks > 2 * (size_t)NB) fail(PQKV_EINVAL, "tuple select: table too large");
-    const bool wide = C * C > (size_t)TUP_THREADS * 16;
+    const bool wide = C * C > (size_t)4096;
     auto kern = wide ? tuple_select_kernel<TUP_THREADS_B7> : tuple_select_kernel<TUP_THREADS>;
     PQKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg{};

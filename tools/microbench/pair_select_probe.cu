@@ -3,6 +3,12 @@
 // per-phase clocks (PQKV_T marks 0..6), per-pass clocks and survivor counts
 // (PQKV_PASS_STAMPS).  Usage: pair_select_probe DUMPDIR
 #define PQKV_PASS_STAMPS 1
+#ifndef PROBE_NT
+#define PROBE_NT 256
+#endif
+#ifndef PROBE_MINB
+#define PROBE_MINB 1
+#endif
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -13,7 +19,7 @@ __device__ unsigned long long g_t[40];
 
 using namespace pqkv_dev;
 
-__global__ void __launch_bounds__(256, PROBE_MINB) probe(const float* q, int g, const float* cen, const uint32_t* thist, const uint16_t* chist,
+__global__ void __launch_bounds__(PROBE_NT, PROBE_MINB) probe(const float* q, int g, const float* cen, const uint32_t* thist, const uint16_t* chist,
                       int n_chunks, int k, uint32_t* res) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = 64;
@@ -22,7 +28,7 @@ __global__ void __launch_bounds__(256, PROBE_MINB) probe(const float* q, int g, 
     for (int i = threadIdx.x; i < 40; i += blockDim.x) g_t[i] = 0;
     __syncthreads();
     const unsigned long long t0 = clock64();
-    pair_select<256, 16>(q, g, 128, cen, C, thist, chist, n_chunks, k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq,
+    pair_select<PROBE_NT, 4096 / PROBE_NT>(q, g, 128, cen, C, thist, chist, n_chunks, k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq,
                          ps.wsum, ps.sh, cls, nullptr, g_t);
     if (threadIdx.x == 0) {
         g_t[20] = clock64() - t0;
@@ -64,7 +70,7 @@ int main(int argc, char** argv) {
     int nnz = 0;
     for (uint32_t v : th) nnz += v != 0;
     for (int rep = 0; rep < 3; ++rep) {
-        probe<<<1, 256, smem>>>(dq, g, dc, dth, dch, nch, k, dres);
+        probe<<<1, PROBE_NT, smem>>>(dq, g, dc, dth, dch, nch, k, dres);
         cudaDeviceSynchronize();
         unsigned long long t[40];
         uint32_t res[4];
