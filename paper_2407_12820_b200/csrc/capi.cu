@@ -1,7 +1,9 @@
 // capi.cu -- C-ABI entry points (include/pqkv_c.h): argument validation with
 // the reference's rejection rules, then the launchers in kmeans.cu,
 // select.cu and attend.cu.  Nothing here computes on the host.
+#include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <cstdlib>
 #include <vector>
 
@@ -463,12 +465,11 @@ int pqkv_decode_attend(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_querie
     });
 }
 
-int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries, size_t g, size_t k,
-                     float* h_out, void* stream) {
+// The stream work of pqkv_decode_host: queries in, the decode launches, the
+// outputs out (no synchronize).
+static int decode_host_ops(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries, size_t g, size_t k,
+                           float* h_out, cudaStream_t st) {
     return guard([&] {
-        need_ctx(ctx);
-        check_layer(L, g, k);
-        cudaStream_t st = as_stream(stream);
         const size_t qbytes = L->n_heads * g * L->d_h * sizeof(float);
         float* dq = static_cast<float*>(host_io_staging(ctx, 2 * qbytes));
         float* d_q = dq;
@@ -495,9 +496,110 @@ int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries,
                                       mode == PQKV_MODE_KEYS_SPLIT);
         const float* mapped_q = direct ? static_cast<const float*>(device_view(h_queries)) : nullptr;
         if (!mapped_q) PQKV_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, st));
-        int rc = pqkv_decode(ctx, L, mapped_q ? mapped_q : d_q, g, k, mapped ? mapped : d_o, nullptr, stream);
+        int rc = pqkv_decode(ctx, L, mapped_q ? mapped_q : d_q, g, k, mapped ? mapped : d_o, nullptr, st);
         if (rc != PQKV_OK) fail(rc, pqkv_last_error());
         if (!mapped) PQKV_CUDA(cudaMemcpyAsync(h_out, d_o, qbytes, cudaMemcpyDeviceToHost, st));
+    });
+}
+
+// Everything a captured pqkv_decode_host baked into its graph: the layer
+// struct, the host buffers, g, k, the stream and the context's scratch and
+// workspace allocations (a regrow between calls changes the key).
+static std::vector<unsigned char> host_graph_key(const pqkv_ctx* ctx, const pqkv_layer* L, const float* hq, size_t g,
+                                                 size_t k, const float* ho, cudaStream_t st) {
+    std::vector<unsigned char> key(sizeof(pqkv_layer));
+    std::memcpy(key.data(), L, sizeof(pqkv_layer));
+    auto put = [&](const void* v, size_t n) {
+        const auto* b = static_cast<const unsigned char*>(v);
+        key.insert(key.end(), b, b + n);
+    };
+    put(&hq, sizeof hq);
+    put(&ho, sizeof ho);
+    put(&g, sizeof g);
+    put(&k, sizeof k);
+    put(&st, sizeof st);
+    put(&ctx->arena, sizeof ctx->arena);
+    put(&ctx->arena_bytes, sizeof ctx->arena_bytes);
+    put(&ctx->ws, sizeof ctx->ws);
+    put(&ctx->ws_bytes, sizeof ctx->ws_bytes);
+    put(&ctx->io, sizeof ctx->io);
+    put(&ctx->d_arrivals, sizeof ctx->d_arrivals);
+    return key;
+}
+
+int pqkv_decode_host(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_queries, size_t g, size_t k,
+                     float* h_out, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_layer(L, g, k);
+        cudaStream_t st = as_stream(stream);
+        // repeated calls replay a CUDA graph of the copy-in + decode launches
+        // (one launch call instead of the copy and two kernel launches, and
+        // no per-launch host work): captured on a context stream the second
+        // time a key is seen, launched on the caller's stream
+        static const bool graphs_on = std::getenv("PQKV_NO_GRAPHS") == nullptr;
+        const bool graphable = graphs_on && !ctx->profiling && !ctx->sel_dump;
+        std::vector<unsigned char> key;
+        if (graphable) {
+            key = host_graph_key(ctx, L, h_queries, g, k, h_out, st);
+            for (auto& hg : ctx->host_graphs)
+                if (hg.key == key) {
+                    hg.last_use = ++ctx->host_graph_clock;
+                    if (!hg.exec) break;  // this key did not capture: plain launches
+                    PQKV_CUDA(cudaGraphLaunch(hg.exec, st));
+                    PQKV_CUDA(cudaStreamSynchronize(st));
+                    return;
+                }
+        }
+        bool capture = false;
+        const bool failed_before = graphable && std::any_of(ctx->host_graphs.begin(), ctx->host_graphs.end(),
+                                                            [&](const auto& hg) { return hg.key == key; });
+        if (graphable && !failed_before) {
+            auto& seen = ctx->host_graph_seen;
+            auto it = std::find(seen.begin(), seen.end(), key);
+            if (it != seen.end()) {
+                capture = true;
+                seen.erase(it);
+            } else {
+                seen.push_back(key);
+                if (seen.size() > 64) seen.erase(seen.begin());
+            }
+        }
+        if (capture) {
+            if (!ctx->capture_stream) PQKV_CUDA(cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking));
+            cudaGraph_t graph = nullptr;
+            cudaGraphExec_t exec = nullptr;
+            bool ok = cudaStreamBeginCapture(ctx->capture_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                const int rc = decode_host_ops(ctx, L, h_queries, g, k, h_out, ctx->capture_stream);
+                ok = cudaStreamEndCapture(ctx->capture_stream, &graph) == cudaSuccess && rc == PQKV_OK && graph;
+            }
+            if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            if (ok && host_graph_key(ctx, L, h_queries, g, k, h_out, st) == key) {
+                if (ctx->host_graphs.size() >= 32) {  // drop the least recently used
+                    auto lru = std::min_element(ctx->host_graphs.begin(), ctx->host_graphs.end(),
+                                                [](const auto& a, const auto& b) { return a.last_use < b.last_use; });
+                    if (lru->exec) cudaGraphExecDestroy(lru->exec);
+                    ctx->host_graphs.erase(lru);
+                }
+                ctx->host_graphs.push_back({key, exec, ++ctx->host_graph_clock});
+                PQKV_CUDA(cudaGraphLaunch(exec, st));
+                PQKV_CUDA(cudaStreamSynchronize(st));
+                return;
+            }
+            if (exec) cudaGraphExecDestroy(exec);
+            if (ctx->host_graphs.size() >= 32) {
+                auto lru = std::min_element(ctx->host_graphs.begin(), ctx->host_graphs.end(),
+                                            [](const auto& a, const auto& b) { return a.last_use < b.last_use; });
+                if (lru->exec) cudaGraphExecDestroy(lru->exec);
+                ctx->host_graphs.erase(lru);
+            }
+            ctx->host_graphs.push_back({key, nullptr, ++ctx->host_graph_clock});  // remembered as not capturable
+        }
+        const int rc = decode_host_ops(ctx, L, h_queries, g, k, h_out, st);
+        if (rc != PQKV_OK) fail(rc, pqkv_last_error());
         PQKV_CUDA(cudaStreamSynchronize(st));
     });
 }

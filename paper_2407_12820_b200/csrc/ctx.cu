@@ -158,6 +158,9 @@ int pqkv_ctx_destroy(pqkv_ctx* ctx) {
         if (ctx->ws) cudaFree(ctx->ws);
         if (ctx->io) cudaFree(ctx->io);
         if (ctx->d_prof) cudaFree(ctx->d_prof);
+        for (auto& hg : ctx->host_graphs)
+            if (hg.exec) cudaGraphExecDestroy(hg.exec);
+        if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
         delete ctx;
     });
 }

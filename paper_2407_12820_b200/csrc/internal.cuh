@@ -39,6 +39,17 @@ struct pqkv_ctx {
     unsigned long long* d_stats = nullptr;
     uint64_t last_rechecked = 0, last_total = 0;
     unsigned long long last_phase_cycles[8] = {};  // problem 0 of the last build
+    // pqkv_decode_host: CUDA graphs of repeated calls (copy in + decode
+    // launches), keyed by everything the captured launches bake in
+    struct HostGraph {
+        std::vector<unsigned char> key;
+        cudaGraphExec_t exec = nullptr;
+        unsigned long long last_use = 0;
+    };
+    std::vector<HostGraph> host_graphs;
+    std::vector<std::vector<unsigned char>> host_graph_seen;  // keys seen once (captured on the second call)
+    cudaStream_t capture_stream = nullptr;
+    unsigned long long host_graph_clock = 0;
 };
 
 namespace pqkv_dev {
