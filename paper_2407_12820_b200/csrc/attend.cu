@@ -361,18 +361,130 @@ __device__ __forceinline__ uint32_t dsmem_ld(const void* local_ptr, unsigned ran
     return v;
 }
 
+// One cluster-wide select step over a histogram pass, entered after the
+// barrier that completes every CTA's histogram h[nb] (bins ascending in key
+// order): CTA r sums its 1/ncl share of the bins over the cluster (DSMEM)
+// into own[] -> barrier -> every CTA locates the share holding the k_rem-th
+// largest participant and reads that share's merged bins.  Result: sh[0] =
+// the bin, sh[1] = participants in higher bins, sh[4] = the bin's count.
+template <int NT>
+__device__ void cluster_locate(const uint32_t* h, uint32_t* own, int nb, uint32_t k_rem, unsigned crank,
+                               unsigned ncl, uint32_t* pub, uint32_t* wtot, uint32_t* sh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int share = (nb + (int)ncl - 1) / (int)ncl;  // bins per CTA
+    {
+        const int o0 = (int)crank * share, o1 = min(nb, o0 + share);
+        uint32_t tot = 0;
+        for (int bn = o0 + tid; bn < o1; bn += NT) {
+            uint32_t v = 0;
+            for (unsigned r = 0; r < ncl; ++r) v += dsmem_ld(h + bn, r);
+            own[bn - o0] = v;
+            tot += v;
+        }
+        tot = warp_sum(tot);
+        if (lane == 0) wtot[warp] = tot;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < (NT / 32); ++w) t += wtot[w];
+            pub[3] = t;
+        }
+        __syncthreads();
+    }
+    cluster_barrier();  // every share is merged
+    if (tid < 32) {  // the share holding the k_rem-th largest key (shares in descending bin order)
+        const unsigned r = ncl - 1 - (unsigned)lane;
+        const uint32_t t = lane < (int)ncl ? dsmem_ld(pub + 3, r) : 0u;
+        uint32_t x = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        const unsigned hit = __ballot_sync(FULL, lane < (int)ncl && x >= k_rem && x - t < k_rem);
+        const int l = __ffs(hit) - 1;
+        if (lane == l) { sh[2] = r; sh[3] = x - t; }
+    }
+    __syncthreads();
+    const unsigned rs = sh[2];
+    const uint32_t above_share = sh[3];
+    // digit inside share rs: thread t owns share bins [hi - per, hi), top down
+    const int o0 = (int)rs * share, cnt_bins = min(nb, o0 + share) - o0;
+    const int nbe = max(cnt_bins, NT);
+    const int per = (nbe + NT - 1) / NT;  // 1..8
+    const int hi = nbe - per * tid;
+    uint32_t cnt[8];
+    uint32_t local = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int bn = hi - per + e;
+        cnt[e] = (e < per && bn >= 0 && bn < cnt_bins) ? dsmem_ld(own + bn, rs) : 0u;
+        local += cnt[e];
+    }
+    const uint32_t kk = k_rem - above_share;
+    const uint32_t above = block_excl_scan<NT>(local, wtot, nullptr);
+    if (above < kk && kk <= above + local) {
+        uint32_t acc = above;
+#pragma unroll
+        for (int e = 7; e >= 0; --e) {  // bins from the top
+            if (e >= per) continue;
+            if (kk <= acc + cnt[e]) {
+                sh[0] = (uint32_t)(o0 + hi - per + e);
+                sh[1] = above_share + acc;
+                sh[4] = cnt[e];
+                break;
+            }
+            acc += cnt[e];
+        }
+    }
+    __syncthreads();
+}
+
+// Value-linear bin of score v over [lo, lo + NB / sc): monotone
+// non-decreasing in v (every step rounds monotonically and the ends clamp),
+// so bins are ordered like keys whatever the rounding.
+__device__ __forceinline__ int vbin(float v, float lo, float sc) {
+    const int b = __float2int_rz(__fmul_rn(__fsub_rn(v, lo), sc));
+    return min(NB - 1, max(0, b));
+}
+
+// Last u32 key in [k0, k1] for which pred holds, pred holding on a prefix
+// of the range and at k0 (k0 - 1 if it holds nowhere): a warp-wide 33-ary
+// search, ~7 rounds for a full 32-bit range.
+template <class Pred>
+__device__ uint32_t warp_last_true(uint32_t k0, uint32_t k1, Pred pred) {
+    const int lane = threadIdx.x & 31;
+    // the first key where pred fails lies in [lo, hi] (hi = k1 + 1: nowhere)
+    unsigned long long lo = k0, hi = (unsigned long long)k1 + 1;
+    while (hi > lo) {
+        const unsigned long long span = hi - lo;
+        const unsigned long long pt = lo + span * (unsigned long long)(lane + 1) / 33;  // < hi
+        const unsigned t = __ballot_sync(FULL, pred((uint32_t)pt));
+        const int c = __popc(t);  // lanes 0..c-1 hold (probes ascend with the lane)
+        const unsigned long long p_last = __shfl_sync(FULL, pt, max(c - 1, 0));
+        const unsigned long long p_next = __shfl_sync(FULL, pt, min(c, 31));
+        if (c > 0) lo = p_last + 1;
+        if (c < 32) hi = p_next;
+    }
+    return (uint32_t)(lo - 1);
+}
+
+constexpr uint32_t KEYS_CAND_CAP = 512;  // final-bin keys resolved by counting (else the radix passes)
+
 template <int G, int NT = AT_THREADS>
 __device__ void keys_select_words(const AtArgs& a, const float* q, int p, int r0, int r1, unsigned char* region,
                                   uint32_t* words,
                                   uint32_t* hbuf /*[2][NB] + own[NB]*/, uint32_t* pub /*[4]*/, uint32_t* wtot,
-                                  uint32_t* sh, unsigned long long* tp) {
+                                  uint32_t* sh /*[8]*/, unsigned long long* tp) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = max(0, r1 - r0), C = a.C, m = a.m;
     uint32_t crank, ncl;
     asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
     asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
-    uint32_t* keys = reinterpret_cast<uint32_t*>(region);            // [chunk]
-    double* lut = reinterpret_cast<double*>(keys + a.chunk);          // [m][C]
+    // scores as floats with -0 folded onto +0: float compares are the
+    // reference's (topk.cpp:17-22)
+    float* sc_s = reinterpret_cast<float*>(region);                  // [chunk]
+    double* lut = reinterpret_cast<double*>(sc_s + a.chunk);          // [m][C]
     for (int e = tid; e < 2 * NB; e += NT) hbuf[e] = 0u;      // both buffers
     // ADC table split over the cluster: rank r computes its share of the
     // m*C entries, then copies the others' through DSMEM
@@ -387,44 +499,280 @@ __device__ void keys_select_words(const AtArgs& a, const float* q, int p, int r0
             if (e < e0 || e >= e1) lut[e] = dsmem_ld64(lut + e, (unsigned)(e / share));
     }
     __syncthreads();
-    PQKV_T(0);
-    // ---- keys (pq.cpp:128-140 in j order, one f32 rounding) + local range ----
-    const uint16_t* cd = a.codes + p * a.codes_head_stride + (long long)r0 * m;
-    uint32_t kmin = 0xffffffffu, kmax = 0u;
-    const bool v4 = m == 4 && (reinterpret_cast<uintptr_t>(cd) & 7) == 0;
-    for (int i0 = 0; i0 < n; i0 += 8 * NT) {
-        uint2 cv[8];
-        if (v4) {  // eight code rows in flight per thread
+    // a-priori score range: fp64 addition and the f32 rounding are monotone,
+    // so f32(((min T0 + min T1) + ...)) <= every score <= the same over the
+    // maxima.  Every CTA holds the same table: the same range cluster-wide.
+    __shared__ double tmin_s[DH], tmax_s[DH];  // m <= d_h
+    for (int j = warp; j < m; j += NT / 32) {
+        double lo = INFINITY, hi = -INFINITY;
+        for (int c = lane; c < C; c += 32) {
+            lo = fmin(lo, lut[j * C + c]);
+            hi = fmax(hi, lut[j * C + c]);
+        }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(FULL, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(FULL, hi, o));
+        }
+        if (lane == 0) { tmin_s[j] = lo; tmax_s[j] = hi; }
+    }
+    __syncthreads();
+    float lo0, hi0;
+    {
+        double slo = 0.0, shi = 0.0;
+        for (int j = 0; j < m; ++j) {
+            slo = __dadd_rn(slo, tmin_s[j]);
+            shi = __dadd_rn(shi, tmax_s[j]);
+        }
+        lo0 = (float)slo;
+        hi0 = (float)shi;
+    }
+    // first value pass fused into the score loop (w0 > 0 checked by all CTAs alike)
+    const float w0 = __fsub_rn(hi0, lo0), sc0 = __fdiv_rn((float)NB, w0);
+    const bool fuse0 = w0 > 0.f && sc0 > 0.f && !isinf(w0) && !isinf(sc0);
+    uint32_t* h0 = hbuf;
+    PQKV_T(0);
+    // ---- scores (pq.cpp:128-140 in j order, one f32 rounding) ----
+    // eight code rows in flight per thread and eight independent fp64 chains
+    const uint16_t* cd = a.codes + p * a.codes_head_stride + (long long)r0 * m;
+    const bool v4 = m == 4 && (reinterpret_cast<uintptr_t>(cd) & 7) == 0;
+    constexpr int RIF = 16;  // code rows in flight per thread
+    for (int i0 = 0; i0 < n; i0 += RIF * NT) {
+        if (v4) {
+            uint2 cv[RIF];
+#pragma unroll
+            for (int u = 0; u < RIF; ++u) {
                 const int i = i0 + u * NT + tid;
                 cv[u] = i < n ? *reinterpret_cast<const uint2*>(cd + 4LL * i) : make_uint2(0u, 0u);
             }
-        }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * NT + tid;
-            if (i >= n) break;
-            double acc = 0.0;
-            if (v4) {
+            for (int u = 0; u < RIF; ++u) {
+                const int i = i0 + u * NT + tid;
+                double acc = 0.0;
                 acc = __dadd_rn(acc, lut[0 * C + (cv[u].x & 0xffffu)]);
                 acc = __dadd_rn(acc, lut[1 * C + (cv[u].x >> 16)]);
                 acc = __dadd_rn(acc, lut[2 * C + (cv[u].y & 0xffffu)]);
                 acc = __dadd_rn(acc, lut[3 * C + (cv[u].y >> 16)]);
-            } else {
-                for (int j = 0; j < m; ++j) acc = __dadd_rn(acc, lut[j * C + cd[(long long)i * m + j]]);
+                float f = (float)acc;
+                if (f == 0.0f) f = 0.0f;
+                if (i < n) {
+                    sc_s[i] = f;
+                    if (fuse0) atomicAdd(&h0[vbin(f, lo0, sc0)], 1u);
+                }
             }
-            const uint32_t key = score_key((float)acc);
-            keys[i] = key;
-            kmin = min(kmin, key);
-            kmax = max(kmax, key);
+        } else {
+            for (int u = 0; u < RIF; ++u) {
+                const int i = i0 + u * NT + tid;
+                if (i >= n) break;
+                double acc = 0.0;
+                for (int j = 0; j < m; ++j) acc = __dadd_rn(acc, lut[j * C + cd[(long long)i * m + j]]);
+                float f = (float)acc;
+                if (f == 0.0f) f = 0.0f;
+                sc_s[i] = f;
+                if (fuse0) atomicAdd(&h0[vbin(f, lo0, sc0)], 1u);
+            }
         }
+    }
+    __syncthreads();
+    PQKV_T(1);
+    uint32_t* own = hbuf + 2 * NB;  // [NB] merged counts of this CTA's share
+    uint32_t k_rem = (uint32_t)a.k;
+
+    // ---- value-linear passes: bins linear in the score over the current
+    // interval [ylo, xhi] of scores (the a-priori range, then the chosen
+    // bin's exact range), at most three, until the bin holding the k-th
+    // largest has at most KEYS_CAND_CAP scores cluster-wide.  A radix digit
+    // of the u32 key is exponent-major: scores spanning zero (gaussian keys)
+    // leave ~5-10K of a 128K unit in the first digit's bin; value bins leave
+    // ~100 (gaussian) or, after one refinement, ~20 (powerlaw, whose k-th
+    // score sits in the dense low end of a long tail).  A chosen bin is a
+    // score interval (vbin is monotone): its exact ends are found by two
+    // warp-parallel searches over the float order, so every later scan tests
+    // a score with two compares.  Every CTA derives the same numbers from
+    // the same cluster-wide inputs, so the decisions are uniform.
+    __shared__ float ends_s[2];
+    float ylo = lo0, xhi = hi0;  // scores taking part in the current pass: [ylo, xhi]
+    int nv = 0;
+    bool cand_ok = false;
+    if (fuse0) {
+#pragma unroll 1
+        for (int pass = 0; pass < 3; ++pass) {
+            const float lo = ylo;
+            const float w = __fsub_rn(xhi, lo);
+            const float scl = __fdiv_rn((float)NB, w);
+            if (!(w > 0.f) || !(scl > 0.f) || isinf(w) || isinf(scl)) break;
+            uint32_t* h = hbuf + (pass & 1) * NB;
+            if (pass >= 1) {
+                if (pass >= 2) {  // this buffer was last read before the previous pass's barriers
+                    for (int e = tid; e < NB; e += NT) h[e] = 0u;
+                    __syncthreads();
+                }
+                for (int i = 4 * tid; i < n; i += 4 * NT) {
+                    const float4 x = reinterpret_cast<const float4*>(sc_s)[i >> 2];
+                    const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (i + e < n && xv[e] >= ylo && xv[e] <= xhi) atomicAdd(&h[vbin(xv[e], lo, scl)], 1u);
+                }
+                __syncthreads();
+            }
+            cluster_barrier();  // every CTA's histogram of this pass is complete
+            if (pass == 0) PQKV_T(2);
+            cluster_locate<NT>(h, own, NB, k_rem, crank, ncl, pub, wtot, sh);
+            if (pass == 0) PQKV_T(3);
+            const int b = (int)sh[0];
+            k_rem -= sh[1];
+            const uint32_t nbin = sh[4];
+            // the chosen bin's scores: [ylo', xhi'] inside [ylo, xhi]; warp 0
+            // finds the last score with bin <= b, warp 1 the last with bin < b
+            if (warp < 2) {
+                const int bb = warp == 0 ? b : b - 1;
+                const uint32_t k0 = score_key(ylo), k1 = score_key(xhi);
+                const uint32_t last = warp_last_true(k0, k1, [&](uint32_t key) {
+                    return vbin(key_score(key), lo, scl) <= bb;
+                });
+                if (lane == 0) ends_s[warp] = warp == 0 ? key_score(last) : key_score(last + 1);
+            }
+            __syncthreads();
+            xhi = ends_s[0];
+            ylo = ends_s[1];
+            nv = pass + 1;
+            __syncthreads();
+            if (nbin <= KEYS_CAND_CAP) {
+                cand_ok = true;
+                break;
+            }
+        }
+    }
+    PQKV_T(4);
+    if (tp && tid == 0) { tp[13] = (unsigned long long)nv | ((unsigned long long)cand_ok << 8); tp[15] = sh[4]; }
+    const int seg = a.chunk / (NT / 32);
+    const int s0 = warp * seg, s1 = min(n, s0 + seg);
+    if (cand_ok) {
+        // ---- one scan: provisional words (scores above the final bin) and
+        // this CTA's candidates (scores in it: value + middle-row index), in
+        // the histogram buffer the next pass would have used (nobody reads it)
+        float* cand = reinterpret_cast<float*>(hbuf + (nv & 1) * NB);
+        uint32_t* cidx = hbuf + (nv & 1) * NB + KEYS_CAND_CAP;
+        __shared__ uint32_t coff[17];
+        if (tid == 0) sh[5] = 0;
+        __syncthreads();
+        for (int i0 = s0; i0 < s1; i0 += 128) {  // four words per round, loads first
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + 32 * u + lane;
+                v[u] = i < s1 ? sc_s[i] : -INFINITY;
+            }
+            unsigned wd[4], cb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                wd[u] = __ballot_sync(FULL, v[u] > xhi);
+                cb[u] = __ballot_sync(FULL, v[u] >= ylo && v[u] <= xhi);
+            }
+            if (lane < 4 && i0 + 32 * lane < s1)
+                words[(i0 >> 5) + lane] = lane == 0 ? wd[0] : lane == 1 ? wd[1] : lane == 2 ? wd[2] : wd[3];
+            if (cb[0] | cb[1] | cb[2] | cb[3]) {  // rare: ~100 scores of a 128K unit
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (!cb[u]) continue;
+                    uint32_t base = 0;
+                    if (lane == 0) base = atomicAdd(&sh[5], (uint32_t)__popc(cb[u]));
+                    base = __shfl_sync(FULL, base, 0);
+                    if ((cb[u] >> lane) & 1u) {
+                        const uint32_t at = base + __popc(cb[u] & lanemask_lt());
+                        cand[at] = v[u];
+                        cidx[at] = (uint32_t)(i0 + 32 * u + lane);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        PQKV_T(5);
+        if (tid == 0) pub[0] = sh[5];
+        cluster_barrier();  // every CTA's candidates are listed (and every locate is done)
+        PQKV_T(6);
+        if (tid < 32) {
+            const uint32_t cr = lane < (int)ncl ? dsmem_ld(pub, (unsigned)lane) : 0u;
+            uint32_t x = cr;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane <= (int)ncl) coff[lane] = x - cr;  // lane ncl: the total
+        }
+        __syncthreads();
+        const uint32_t T = coff[ncl];
+        if (tp && tid == 0) tp[14] = T;
+        float* all = reinterpret_cast<float*>(own);  // every CTA's candidate values, in rank (= id) order
+        for (uint32_t e = tid; e < T; e += NT) {
+            unsigned r = 0;
+            while (e >= coff[r + 1]) ++r;
+            const uint32_t o = e - coff[r];
+            all[e] = r == crank ? cand[o] : __uint_as_float(dsmem_ld(cand + o, r));
+        }
+        // no remote reads of this CTA's buffers after this point; the
+        // matching wait is at the end of the kernel (no CTA leaves early)
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        __syncthreads();
+        // K* = the candidate x with #{> x} < k_rem <= #{>= x} (one thread per
+        // candidate, the others read in lockstep: broadcast loads)
+        for (uint32_t i = tid; i < (T + NT - 1) / NT * NT; i += NT) {
+            const float x = i < T ? all[i] : 0.f;
+            uint32_t gt = 0, eq = 0;
+            for (uint32_t j = 0; j < T; ++j) {
+                const float y = all[j];
+                gt += y > x;
+                eq += y == x;
+            }
+            if (i < T && gt < k_rem && k_rem <= gt + eq) { sh[6] = __float_as_uint(x); sh[7] = gt; }
+        }
+        __syncthreads();
+        PQKV_T(7);
+        const float kv = __uint_as_float(sh[6]);
+        const uint32_t budget = k_rem - sh[7];  // ties at K* taken, lowest ranks (ids) first
+        const uint32_t o0 = coff[crank];
+        uint32_t eb = 0;
+        for (uint32_t j = tid; j < o0; j += NT) eb += all[j] == kv;
+        eb = warp_sum(eb);
+        if (lane == 0) wtot[warp] = eb;
+        __syncthreads();
+        uint32_t eq_before = 0;
+#pragma unroll
+        for (int w = 0; w < (NT / 32); ++w) eq_before += wtot[w];
+        const uint32_t take = budget > eq_before ? budget - eq_before : 0u;
+        // this CTA's candidates: above K*, or among the `take` lowest-index ties
+        const uint32_t mine = coff[crank + 1] - o0;
+        for (uint32_t e = tid; e < mine; e += NT) {
+            const float v = cand[e];
+            bool sel = v > kv;
+            if (v == kv) {
+                uint32_t before = 0;
+                for (uint32_t f = 0; f < mine; ++f) before += cand[f] == kv && cidx[f] < cidx[e];
+                sel = before < take;
+            }
+            if (sel) atomicOr(&words[cidx[e] >> 5], 1u << (cidx[e] & 31));
+        }
+        __syncthreads();
+        return;
+    }
+    // ---- fallback: radix digits over rel = key - kmin of the order-preserving
+    // u32 keys (the first spans [kmin, kmax], later ones refine 11 bits at a
+    // time), when the value passes cannot isolate the k-th largest (hundreds
+    // of equal scores at K*, or a degenerate range) ----
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (int i = tid; i < n; i += NT) {
+        const uint32_t key = score_key(sc_s[i]);
+        kmin = min(kmin, key);
+        kmax = max(kmax, key);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
     }
+    __syncthreads();  // every warp is past the value passes' use of wtot / sh
     if (lane == 0) wtot[warp] = kmin;
     __syncthreads();
     if (tid == 0) {
@@ -440,31 +788,25 @@ __device__ void keys_select_words(const AtArgs& a, const float* q, int p, int r0
         for (int w = 0; w < (NT / 32); ++w) hi = max(hi, wtot[w]);
         pub[2] = hi;
     }
+    for (int e = tid; e < 2 * NB; e += NT) hbuf[e] = 0u;  // not read remotely since the last locate
     __syncthreads();
-    PQKV_T(1);
-    cluster_barrier();  // every CTA's keys and range are published
-    PQKV_T(2);
+    cluster_barrier();  // every CTA's key range is published
     kmin = 0xffffffffu;
     kmax = 0u;
     for (unsigned r = 0; r < ncl; ++r) {
         kmin = min(kmin, dsmem_ld(pub + 1, r));
         kmax = max(kmax, dsmem_ld(pub + 2, r));
     }
-    // ---- radix digits over rel = key - kmin: the first spans [kmin, kmax]
-    // (nearby scores share their top bits), later ones refine 11 bits at a time.
-    // Per pass: local histograms -> barrier -> CTA r sums its share of the
-    // bins over the cluster (DSMEM) -> barrier -> every CTA locates the share
-    // holding the k_rem-th largest key and reads that share's merged bins.
+    k_rem = (uint32_t)a.k;
     const uint32_t range = kmax - kmin;
     const int bits = 32 - __clz(range | 1u);
     int shift = max(0, bits - 11), width = bits - shift;
-    uint32_t k_rem = (uint32_t)a.k, prefix = 0;
-    uint32_t* own = hbuf + 2 * NB;  // [NB] merged counts of this CTA's share
-    uint32_t neq_local = 0;         // this CTA's keys equal to K* (bin count of the last pass)
+    uint32_t prefix = 0;
+    uint32_t neq_local = 0;  // this CTA's scores equal to K* (bin count of the last pass)
     for (int pass = 0;; ++pass) {
         const int nb = 1 << width;
         uint32_t* h = hbuf + (pass & 1) * NB;
-        if (pass >= 2) {  // this buffer was last read before the previous pass's barriers
+        if (pass >= 2) {
             for (int e = tid; e < NB; e += NT) h[e] = 0u;
             __syncthreads();
         }
@@ -472,94 +814,24 @@ __device__ void keys_select_words(const AtArgs& a, const float* q, int p, int r0
             const int i = i0 + tid;
             uint32_t bin = 0xffffffffu;
             if (i < n) {
-                const uint32_t rel = keys[i] - kmin;
+                const uint32_t rel = score_key(sc_s[i]) - kmin;
                 if (pass == 0 || (rel >> (shift + width)) == prefix) bin = (rel >> shift) & (uint32_t)(nb - 1);
             }
             hist_inc(h, bin);
         }
         __syncthreads();
-        if (pass == 0) PQKV_T(3);
         cluster_barrier();  // every CTA's histogram of this pass is complete
-        if (pass == 0) PQKV_T(4);
-        const int share = (nb + (int)ncl - 1) / (int)ncl;  // bins per CTA
-        {
-            const int o0 = (int)crank * share, o1 = min(nb, o0 + share);
-            uint32_t tot = 0;
-            for (int bn = o0 + tid; bn < o1; bn += NT) {
-                uint32_t v = 0;
-                for (unsigned r = 0; r < ncl; ++r) v += dsmem_ld(h + bn, r);
-                own[bn - o0] = v;
-                tot += v;
-            }
-            tot = warp_sum(tot);
-            if (lane == 0) wtot[warp] = tot;
-            __syncthreads();
-            if (tid == 0) {
-                uint32_t t = 0;
-                for (int w = 0; w < (NT / 32); ++w) t += wtot[w];
-                pub[3] = t;
-            }
-            __syncthreads();
-        }
-        if (pass == 0) PQKV_T(5);
-        cluster_barrier();  // every share is merged
-        if (pass == 0) PQKV_T(6);
-        if (tid < 32) {  // the share holding the k_rem-th largest key (shares in descending bin order)
-            const unsigned r = ncl - 1 - (unsigned)lane;
-            const uint32_t t = lane < (int)ncl ? dsmem_ld(pub + 3, r) : 0u;
-            uint32_t x = t;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(FULL, x, o);
-                if (lane >= o) x += y;
-            }
-            const unsigned hit = __ballot_sync(FULL, lane < (int)ncl && x >= k_rem && x - t < k_rem);
-            const int l = __ffs(hit) - 1;
-            if (lane == l) { sh[2] = r; sh[3] = x - t; }
-        }
-        __syncthreads();
-        const unsigned rs = sh[2];
-        const uint32_t above_share = sh[3];
-        // digit inside share rs: thread t owns share bins [hi - per, hi), top down
-        const int o0 = (int)rs * share, cnt_bins = min(nb, o0 + share) - o0;
-        const int nbe = max(cnt_bins, NT);
-        const int per = (nbe + NT - 1) / NT;  // 1..8
-        const int hi = nbe - per * tid;
-        uint32_t cnt[8];
-        uint32_t local = 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int bn = hi - per + e;
-            cnt[e] = (e < per && bn >= 0 && bn < cnt_bins) ? dsmem_ld(own + bn, rs) : 0u;
-            local += cnt[e];
-        }
-        const uint32_t kk = k_rem - above_share;
-        const uint32_t above = block_excl_scan<NT>(local, wtot, nullptr);
-        if (above < kk && kk <= above + local) {
-            uint32_t acc = above;
-#pragma unroll
-            for (int e = 7; e >= 0; --e) {  // bins from the top
-                if (e >= per) continue;
-                if (kk <= acc + cnt[e]) {
-                    sh[0] = (uint32_t)(o0 + hi - per + e);
-                    sh[1] = above_share + acc;
-                    break;
-                }
-                acc += cnt[e];
-            }
-        }
-        __syncthreads();
+        cluster_locate<NT>(h, own, nb, k_rem, crank, ncl, pub, wtot, sh);
         k_rem -= sh[1];
         prefix = (prefix << width) | sh[0];
-        if (shift == 0) neq_local = h[sh[0]];  // local keys in the final bin == K*
+        if (shift == 0) neq_local = h[sh[0]];  // local scores in the final bin == K*
         __syncthreads();
         if (shift == 0) break;
         width = min(11, shift);
         shift -= width;
     }
-    PQKV_T(7);
-    const uint32_t kstar = kmin + prefix;  // the k-th largest key; k_rem of its ties are taken
-    // ---- ties: equal keys of lower ranks come first ----
+    const float kv = key_score(kmin + prefix);  // the k-th largest; k_rem of its ties are taken
+    // ---- ties: equal scores of lower ranks come first ----
     const uint32_t cta_eq = neq_local;
     if (tid == 0) pub[0] = cta_eq;
     cluster_barrier();
@@ -569,30 +841,23 @@ __device__ void keys_select_words(const AtArgs& a, const float* q, int p, int r0
     // matching wait is at the end of the kernel (no CTA leaves early)
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     const uint32_t take = k_rem > eq_before ? min(cta_eq, k_rem - eq_before) : 0u;
+    PQKV_T(7);
     // ---- selection words in id order ----
-    const int seg = a.chunk / (NT / 32);
-    const int s0 = warp * seg, s1 = min(n, s0 + seg);
-    // this CTA's ties are all taken or none is (the usual case): no per-warp
-    // tie prefix needed
-    const bool all_or_none = take == 0 || take == cta_eq;
-    uint32_t run = 0;
-    if (!all_or_none) {
-        uint32_t weq = 0;
-        for (int i0 = s0; i0 < s1; i0 += 32) {
-            const int i = i0 + lane;
-            weq += __popc(__ballot_sync(FULL, i < s1 && keys[i] == kstar));
-        }
-        if (lane == 0) wtot[warp] = weq;
-        __syncthreads();
-        for (int v = 0; v < warp; ++v) run += wtot[v];
-    }
-    const uint32_t take_eff = all_or_none ? (take ? 0xffffffffu : 0u) : take;
+    uint32_t weq = 0;
     for (int i0 = s0; i0 < s1; i0 += 32) {
         const int i = i0 + lane;
-        const uint32_t key = i < s1 ? keys[i] : 0u;
-        const bool gt = i < s1 && key > kstar, eq = i < s1 && key == kstar;
+        weq += __popc(__ballot_sync(FULL, i < s1 && sc_s[i] == kv));
+    }
+    if (lane == 0) wtot[warp] = weq;
+    __syncthreads();
+    uint32_t run = 0;
+    for (int v = 0; v < warp; ++v) run += wtot[v];
+    for (int i0 = s0; i0 < s1; i0 += 32) {
+        const int i = i0 + lane;
+        const float v = i < s1 ? sc_s[i] : -INFINITY;
+        const bool gt = i < s1 && v > kv, eq = i < s1 && v == kv;
         const unsigned em = __ballot_sync(FULL, eq);
-        const bool sel = gt || (eq && run + __popc(em & lanemask_lt()) < take_eff);
+        const bool sel = gt || (eq && run + __popc(em & lanemask_lt()) < take);
         const unsigned word = __ballot_sync(FULL, sel);
         if (lane == 0) words[i0 >> 5] = word;
         run += __popc(em);
@@ -1131,6 +1396,24 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
             for (int o = tid * 128; o < 4 * C2; o += NT * 128) prefetch_l2(th + o);
         }
     }
+    if (MODE == SRC_KEYS) {  // this CTA's code rows and its share of the centroids (ADC table)
+        const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
+        const char* cd = reinterpret_cast<const char*>(a.codes + p * a.codes_head_stride + (long long)r0 * a.m);
+        const uint32_t bytes = 2u * a.m * (uint32_t)max(0, r1 - r0);
+        if ((reinterpret_cast<uintptr_t>(cd) & 15) == 0) {  // one bulk (TMA) prefetch of the rows
+            if (tid == 0 && bytes >= 16)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cd), "r"(bytes & ~15u) : "memory");
+        } else {
+            for (int o = tid * 128; o < (int)bytes; o += NT * 128) prefetch_l2(cd + o);
+        }
+        unsigned crk, ncl;
+        asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crk));
+        asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+        const int me = a.m * a.C, share = (me + (int)ncl - 1) / (int)ncl;
+        const int e0 = min(me, (int)crk * share), e1 = min(me, e0 + share);
+        const char* ce = reinterpret_cast<const char*>(a.centroids + (long long)p * a.C * DH) + (long long)e0 * (DH / a.m) * 4;
+        for (int o = tid * 128; o < (e1 - e0) * (DH / a.m) * 4; o += NT * 128) prefetch_l2(ce + o);
+    }
     // split pair path (SRC_TUPLE): stage this CTA's code pairs while the
     // select grid (the previous kernel) runs -- the codes are not written by
     // it, and it waited for their producer before letting this grid launch
@@ -1178,7 +1461,7 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
         if (src == SRC_BITMAP) {
             for (int w = tid; w < nw; w += NT) words[w] = a.bitmap[(long long)p * a.words + r0 / 32 + w];
         } else if ((MODE == SRC_KEYS)) {
-            __shared__ uint32_t pub_s[4], sh_s[4];
+            __shared__ uint32_t pub_s[4], sh_s[8];
             keys_select_words<G>(a, q_s, p, r0, r1, smem_raw, words, eqw /* [2][NB/2] in keys mode */, pub_s, wtot, sh_s,
                                  a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr);
             if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 1] = clock64();

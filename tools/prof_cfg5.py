@@ -90,5 +90,14 @@ print("    select (clock) us", cy(0, 1), "words->rows", cy(1, 2), "gather", cy(2
 print("    SMs used", len(set(raw[:, 16].tolist())))
 names = ["start->lut", "keys", "B0", "hist0", "A0", "merge0", "B0'", "rest passes"]
 print("    select phases us (median):", {nm: cy(a_, b_)[1] for nm, a_, b_ in
-      [("lut", 0, 8), ("keys", 8, 9), ("barrier0", 9, 10), ("hist0", 10, 11), ("barrierA0", 11, 12),
-       ("merge0", 12, 13), ("barrierB0", 13, 14), ("rest", 14, 15), ("ties+words", 15, 1)]})
+      [("lut", 0, 8), ("scores+hist0", 8, 9), ("barrier0", 9, 10), ("locate0", 10, 11), ("refine", 11, 12),
+       ("words scan", 12, 13), ("cand barrier", 13, 14), ("gather+K*", 14, 15), ("patch", 15, 1)]})
+print("    select phases us p10/p50/p90:", {nm: cy(a_, b_) for nm, a_, b_ in
+      [("scores+hist0", 8, 9), ("barrier0", 9, 10), ("words scan", 12, 13), ("cand barrier", 13, 14),
+       ("gather+K*", 14, 15), ("patch", 15, 1)]})
+if os.environ.get("PQKV_PROF_SELECT"):
+    nvs = raw[:, 21] & 0xff
+    print("    value passes", np.bincount(nvs.astype(np.int64)).tolist(), "cand_ok", int(((raw[:, 21] >> 8) & 1).sum()),
+          "of", len(raw), "final-bin count p50/p100", int(np.median(raw[:, 23])), int(raw[:, 23].max()),
+          "T p50/p100", int(np.median(raw[:, 22])), int(raw[:, 22].max()))
+
