@@ -87,6 +87,8 @@ struct AtArgs {
     int nt;                    // threads per CTA (AT_THREADS, or 1024 for the wide g > 1 plans)
     int claim;                 // wide plans: warps claim rows dynamically (experiment: PQKV_CLAIM=1)
     uint32_t* sel_only;        // SRC_KEYS: write the selection bitmap [P][words] here and stop (split launch)
+    unsigned* ready;           // split key path: [P] select CTAs done per unit (select bumps, gather polls), or null
+    unsigned ready_need;       // gather: select CTAs per unit
     unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
 
@@ -1431,7 +1433,23 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
         cp_async_commit();
         tup_staged = dst;
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.ready) {
+        // split key path: the bitmap of this unit is complete once its select
+        // CTAs have counted in (the select grid waited for everything before
+        // it, and its release publishes that too), so the gather does not
+        // wait for the slowest unit's select
+        if (tid == 0) {
+            unsigned v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.ready + p) : "memory");
+                if (v >= a.ready_need) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     asm volatile("griddepcontrol.launch_dependents;");
     // g > 1: this head's G query rows, read once into shared memory (they
     // may sit in page-locked host memory: pqkv_decode_host passes mapped
@@ -1469,6 +1487,12 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
                 for (int w = tid; w < nw; w += NT) {
                     a.sel_only[(long long)p * a.words + r0 / 32 + w] = words[w];
                     if (a.sel_dump) a.sel_dump[(long long)p * a.words + r0 / 32 + w] = words[w];
+                }
+                // this unit's gather CTAs start as soon as its 8 select CTAs are done
+                __syncthreads();
+                if (a.ready && tid == 0) {
+                    __threadfence();
+                    atomicAdd(&a.ready[p], 1u);
                 }
                 asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
                 return;
@@ -1637,7 +1661,10 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
         __threadfence();
         merge_parts<G, NT>(pb, a.n_chunks, nullptr, a.out + (long long)p * G * DH, smem_raw);
     }
-    if (tid == 0) a.arrivals[p] = 0;  // ready for the next launch on this stream
+    if (tid == 0) {
+        a.arrivals[p] = 0;  // ready for the next launch on this stream
+        if (a.ready) a.ready[p] = 0;
+    }
     if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
 }
 
@@ -2219,8 +2246,16 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     // second bitmap-mode launch with its own (finer) chunking
     if (k_keys && bitmap && decode_keys_split(L, G)) {
         a.sel_only = const_cast<uint32_t*>(bitmap);
+        a.ready = ready_counters(ctx, L.n_heads, st);
         launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);
-        launch_decode_attend(ctx, L, queries, G, bitmap, nullptr, nullptr, out, st, 0, 0);
+        AtArgs b{};
+        decode_args(ctx, L, G, 0, 0, true, false, b);
+        b.queries = queries;
+        b.bitmap = bitmap;
+        b.out = out;
+        b.ready = a.ready;
+        b.ready_need = (unsigned)a.n_chunks;
+        launch_attend_kernel(ctx, b, L.n_heads, (int)G, st);
         return;
     }
     a.out = out;

@@ -524,6 +524,7 @@ static std::vector<unsigned char> host_graph_key(const pqkv_ctx* ctx, const pqkv
     put(&ctx->ws_bytes, sizeof ctx->ws_bytes);
     put(&ctx->io, sizeof ctx->io);
     put(&ctx->d_arrivals, sizeof ctx->d_arrivals);
+    put(&ctx->d_ready, sizeof ctx->d_ready);
     return key;
 }
 

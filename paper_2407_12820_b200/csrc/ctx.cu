@@ -107,6 +107,20 @@ unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st) {
     return ctx->d_arrivals;
 }
 
+unsigned* ready_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st) {
+    if (n > ctx->n_ready) {
+        if (ctx->d_ready) {
+            PQKV_CUDA(cudaDeviceSynchronize());
+            PQKV_CUDA(cudaFree(ctx->d_ready));
+        }
+        size_t want = std::max<size_t>(n, 256);
+        PQKV_CUDA(cudaMalloc(&ctx->d_ready, want * sizeof(unsigned)));
+        PQKV_CUDA(cudaMemsetAsync(ctx->d_ready, 0, want * sizeof(unsigned), st));
+        ctx->n_ready = want;
+    }
+    return ctx->d_ready;
+}
+
 namespace {
 
 __global__ void scatter_rows_kernel(const float* src_k, const float* src_v, const int64_t* rows, long long n, int d_h,
@@ -155,6 +169,7 @@ int pqkv_ctx_destroy(pqkv_ctx* ctx) {
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
         if (ctx->d_stats) cudaFree(ctx->d_stats);
         if (ctx->d_arrivals) cudaFree(ctx->d_arrivals);
+        if (ctx->d_ready) cudaFree(ctx->d_ready);
         if (ctx->ws) cudaFree(ctx->ws);
         if (ctx->io) cudaFree(ctx->io);
         if (ctx->d_prof) cudaFree(ctx->d_prof);

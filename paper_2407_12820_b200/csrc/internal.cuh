@@ -23,6 +23,10 @@ struct pqkv_ctx {
     // between launches by the kernel itself).
     unsigned* d_arrivals = nullptr;
     size_t n_arrivals = 0;
+    // Per-unit counts of finished select CTAs of the split key path (the
+    // gather polls them; reset by its combining CTAs).
+    unsigned* d_ready = nullptr;
+    size_t n_ready = 0;
 
     // Profiling mode: attention-kernel phase timestamps of the last launch.
     int profiling = 0;
@@ -105,6 +109,7 @@ void* host_io_staging(pqkv_ctx* ctx, size_t bytes);
 // Multiprocessor count of the current device (cached per device id).
 int current_sm_count();
 unsigned* arrival_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st);
+unsigned* ready_counters(pqkv_ctx* ctx, size_t n, cudaStream_t st);
 
 
 // ---- launchers implemented in the kernel translation units -----------------
