@@ -87,8 +87,9 @@ struct AtArgs {
     int nt;                    // threads per CTA (AT_THREADS, or 1024 for the wide g > 1 plans)
     int claim;                 // wide plans: warps claim rows dynamically (experiment: PQKV_CLAIM=1)
     uint32_t* sel_only;        // SRC_KEYS: write the selection bitmap [P][words] here and stop (split launch)
-    unsigned* ready;           // split key path: [P] select CTAs done per unit (select bumps, gather polls), or null
-    unsigned ready_need;       // gather: select CTAs per unit
+    unsigned* ready_out;       // select-only launch: [P] bumped once per CTA after its words are written, or null
+    unsigned* ready_in;        // gather of a split path: [P] polled until ready_need (instead of the grid wait), or null
+    unsigned ready_need;       // select CTAs per unit
     unsigned long long* prof;  // [grid][PQKV_PROF_SLOTS] phase timestamps (profiling mode) or null
 };
 
@@ -1433,15 +1434,15 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
         cp_async_commit();
         tup_staged = dst;
     }
-    if (a.ready) {
-        // split key path: the bitmap of this unit is complete once its select
+    if (a.ready_in) {
+        // split key / pair paths: the bitmap of this unit is complete once its select
         // CTAs have counted in (the select grid waited for everything before
         // it, and its release publishes that too), so the gather does not
         // wait for the slowest unit's select
         if (tid == 0) {
             unsigned v;
             for (;;) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.ready + p) : "memory");
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.ready_in + p) : "memory");
                 if (v >= a.ready_need) break;
                 __nanosleep(64);
             }
@@ -1490,9 +1491,9 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
                 }
                 // this unit's gather CTAs start as soon as its 8 select CTAs are done
                 __syncthreads();
-                if (a.ready && tid == 0) {
+                if (a.ready_out && tid == 0) {
                     __threadfence();
-                    atomicAdd(&a.ready[p], 1u);
+                    atomicAdd(&a.ready_out[p], 1u);
                 }
                 asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
                 return;
@@ -1663,7 +1664,7 @@ __global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS &
     }
     if (tid == 0) {
         a.arrivals[p] = 0;  // ready for the next launch on this stream
-        if (a.ready) a.ready[p] = 0;
+        if (a.ready_in) a.ready_in[p] = 0;
     }
     if (a.prof && tid == 0) a.prof[cta * PQKV_PROF_SLOTS + 7] = globaltimer_ns();
 }
@@ -2234,10 +2235,12 @@ void plan_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_p
 
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t G,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
-                          cudaStream_t st, size_t k_pairs, size_t k_keys) {
+                          cudaStream_t st, size_t k_pairs, size_t k_keys, unsigned* ready) {
     bind_device(ctx);
     AtArgs a{};
     decode_args(ctx, L, G, k_pairs, k_keys, bitmap != nullptr, cls != nullptr, a);
+    a.ready_in = ready;  // split pair path: one select CTA per head
+    a.ready_need = 1;
     a.queries = queries;
     a.bitmap = bitmap;
     a.cls = cls;
@@ -2246,14 +2249,15 @@ void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queri
     // second bitmap-mode launch with its own (finer) chunking
     if (k_keys && bitmap && decode_keys_split(L, G)) {
         a.sel_only = const_cast<uint32_t*>(bitmap);
-        a.ready = ready_counters(ctx, L.n_heads, st);
+        a.ready_in = nullptr;
+        a.ready_out = ready_counters(ctx, L.n_heads, st);
         launch_attend_kernel(ctx, a, L.n_heads, (int)G, st);
         AtArgs b{};
         decode_args(ctx, L, G, 0, 0, true, false, b);
         b.queries = queries;
         b.bitmap = bitmap;
         b.out = out;
-        b.ready = a.ready;
+        b.ready_in = a.ready_out;
         b.ready_need = (unsigned)a.n_chunks;
         launch_attend_kernel(ctx, b, L.n_heads, (int)G, st);
         return;

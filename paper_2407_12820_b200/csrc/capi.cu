@@ -355,9 +355,10 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
                 char* ws = static_cast<char*>(decode_workspace(ctx, round_up(P * C * C, 256) + P * 2 * sizeof(int)));
                 uint8_t* cls = reinterpret_cast<uint8_t*>(ws);
                 int* cut = reinterpret_cast<int*>(ws + round_up(P * C * C, 256));
+                unsigned* ready = ready_counters(ctx, P, st);
                 launch_tuple_select(ctx, src, L->tuple_hist, L->tuple_chunk_hist, P, s_mid, k, cls, cut, nullptr,
-                                    nullptr, st);
-                launch_decode_attend(ctx, *L, d_queries, g, nullptr, cls, cut, d_out, st);
+                                    nullptr, st, ready);
+                launch_decode_attend(ctx, *L, d_queries, g, nullptr, cls, cut, d_out, st, 0, 0, ready);
                 return;
             }
             default:

@@ -195,7 +195,7 @@ bool decode_keys_fused(const pqkv_layer& L, size_t g);
 bool decode_keys_split(const pqkv_layer& L, size_t g);
 void launch_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, const float* queries, size_t g,
                           const uint32_t* bitmap, const uint8_t* cls, const int* cut, float* out,
-                          cudaStream_t stream, size_t k_pairs = 0, size_t k_keys = 0);
+                          cudaStream_t stream, size_t k_pairs = 0, size_t k_keys = 0, unsigned* ready = nullptr);
 // Geometry of the attention launch launch_decode_attend would make (chunk,
 // CTAs per head, cluster, staging, window, ring depth, shared memory).
 void plan_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, size_t g, size_t k_pairs, size_t k_keys,
@@ -203,7 +203,7 @@ void plan_decode_attend(pqkv_ctx* ctx, const pqkv_layer& L, size_t g, size_t k_p
 // Pair-level select only (writes cls [rows][C*C], cut [rows][2]).
 void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
                          const uint16_t* chist, size_t rows, size_t n, size_t k, uint8_t* cls, int* cut,
-                         uint32_t* tkey, uint32_t* sel_before, cudaStream_t st);
+                         uint32_t* tkey, uint32_t* sel_before, cudaStream_t st, unsigned* ready = nullptr);
 // Device buffer for decode-level intermediates (never aliases the arena).
 void* decode_workspace(pqkv_ctx* ctx, size_t bytes);
 void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_t d_h,

@@ -410,6 +410,7 @@ struct TupArgs {
     int* cut;               // [P][2]: c*, take
     uint32_t* sel_before;   // [P][n_chunks] exclusive prefix of selected rows (ids mode) or null
     long long chunk_stride;  // chunks per head of chist
+    unsigned* ready;        // [P] bumped once a head's classes are written (the attention polls it), or null
 };
 
 template <int NT>
@@ -455,6 +456,12 @@ __global__ void __launch_bounds__(NT, 1) tuple_select_kernel(TupArgs a) {
                 run += hist[c];
             }
         }
+    }
+    // this head's attention CTAs start now, not after the slowest head's select
+    __syncthreads();
+    if (a.ready && tid == 0) {
+        __threadfence();
+        atomicAdd(&a.ready[p], 1u);
     }
 }
 
@@ -697,10 +704,11 @@ void launch_tuple_tables(pqkv_ctx* ctx, const uint16_t* codes, size_t P, size_t 
 
 void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t* thist,
                          const uint16_t* chist, size_t rows, size_t n, size_t k, uint8_t* cls, int* cut,
-                         uint32_t* tkey, uint32_t* sel_before, cudaStream_t st) {
+                         uint32_t* tkey, uint32_t* sel_before, cudaStream_t st, unsigned* ready) {
     bind_device(ctx);
     const size_t C = src.C, n_chunks = ceil_div(n, PQKV_TUPLE_CHUNK);
     TupArgs a{};
+    a.ready = ready;
     a.queries = src.queries;
     a.g = (int)src.g;
     a.d_h = (int)src.d_h;
