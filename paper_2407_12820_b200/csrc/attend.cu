@@ -660,33 +660,35 @@ __device__ void keys_select_words(const AtArgs& a, const float* q, int p, int r0
         __shared__ uint32_t coff[17];
         if (tid == 0) sh[5] = 0;
         __syncthreads();
-        for (int i0 = s0; i0 < s1; i0 += 128) {  // four words per round, loads first
-            float v[4];
+        // thread t builds whole words t, t + NT, ...: 32 consecutive scores
+        // as eight 16-byte loads, visited in a lane-rotated order so the 8
+        // lanes of a load wavefront hit different banks; no ballots
+        const int nwd = (n + 31) / 32;
+        const float4* sc4 = reinterpret_cast<const float4*>(sc_s);
+        for (int w = tid; w < nwd; w += NT) {
+            uint32_t wd = 0, cb = 0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = i0 + 32 * u + lane;
-                v[u] = i < s1 ? sc_s[i] : -INFINITY;
+            for (int j = 0; j < 8; ++j) {
+                const int jj = (j + lane) & 7;
+                const float4 x = sc4[w * 8 + jj];
+                const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int bit = 4 * jj + e;
+                    const bool ok = w * 32 + bit < n;
+                    wd |= (uint32_t)(ok && xv[e] > xhi) << bit;
+                    cb |= (uint32_t)(ok && xv[e] >= ylo && xv[e] <= xhi) << bit;
+                }
             }
-            unsigned wd[4], cb[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                wd[u] = __ballot_sync(FULL, v[u] > xhi);
-                cb[u] = __ballot_sync(FULL, v[u] >= ylo && v[u] <= xhi);
-            }
-            if (lane < 4 && i0 + 32 * lane < s1)
-                words[(i0 >> 5) + lane] = lane == 0 ? wd[0] : lane == 1 ? wd[1] : lane == 2 ? wd[2] : wd[3];
-            if (cb[0] | cb[1] | cb[2] | cb[3]) {  // rare: ~100 scores of a 128K unit
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (!cb[u]) continue;
-                    uint32_t base = 0;
-                    if (lane == 0) base = atomicAdd(&sh[5], (uint32_t)__popc(cb[u]));
-                    base = __shfl_sync(FULL, base, 0);
-                    if ((cb[u] >> lane) & 1u) {
-                        const uint32_t at = base + __popc(cb[u] & lanemask_lt());
-                        cand[at] = v[u];
-                        cidx[at] = (uint32_t)(i0 + 32 * u + lane);
-                    }
+            words[w] = wd;
+            if (cb) {  // rare: ~100 scores of a 128K unit
+                const uint32_t base = atomicAdd(&sh[5], (uint32_t)__popc(cb));
+                uint32_t at = base;
+                for (uint32_t r = cb; r; r &= r - 1) {
+                    const int bit = __ffs(r) - 1;
+                    cand[at] = sc_s[w * 32 + bit];
+                    cidx[at] = (uint32_t)(w * 32 + bit);
+                    ++at;
                 }
             }
         }
