@@ -226,7 +226,29 @@ __device__ void classify_range(const AtArgs& a, int r0, int r1, const uint32_t* 
     const uint32_t C = (uint32_t)a.C;
     const uint32_t eqc = PRELIM ? 3u : 2u;
     const bool gvec = (reinterpret_cast<uintptr_t>(cd_g + r0) & 15) == 0;
-    // ---- step 1: above / equal (pending) words, one word per lane ----
+    // ---- step 1: above / equal (pending) words ----
+    if (!staged && per <= 16) {
+        // few words per warp (wide CTAs): lane l classifies token l of each
+        // word (one coalesced 128-byte load per word, all issued up front)
+        // instead of one word per lane on w1 - w0 lanes
+        uint32_t pv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int t = r0 + 32 * (w0 + u) + lane;
+            pv[u] = (u < w1 - w0 && t < r1) ? cd_g[t] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            if (u >= w1 - w0) break;
+            const bool ok = r0 + 32 * (w0 + u) + lane < r1;
+            const uint32_t cl = ok ? cls[(pv[u] & 0xffffu) * C + (pv[u] >> 16)] : 0u;
+            const uint32_t gt = __ballot_sync(FULL, cl == 1), eq = __ballot_sync(FULL, cl == eqc);
+            if (lane == 0) {
+                words[w0 + u] = gt;
+                eqw[w0 + u] = eq;
+            }
+        }
+    } else
     for (int wb = w0; wb < w1; wb += 32) {
         const int wi = wb + lane;
         if (wi >= w1) continue;
