@@ -318,13 +318,13 @@ static int decode_mode(const pqkv_layer& L, size_t g, size_t k, bool with_ids) {
     return PQKV_MODE_BITMAP;
 }
 
-int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size_t g, size_t k,
-                float* d_out, int64_t* d_ids, void* stream) {
-    return guard([&] {
-        need_ctx(ctx);
-        check_layer(L, g, k);
+// pqkv_decode with the queries possibly in host-mapped memory (q_host):
+// the split pair path's select reads them there and copies them to
+// d_queries for the attention; every other path reads d_queries (filled by
+// the caller).
+static void decode_core(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, const float* q_host, size_t g,
+                        size_t k, float* d_out, int64_t* d_ids, cudaStream_t st) {
         if (L->n_heads == 0) return;
-        cudaStream_t st = as_stream(stream);
         const size_t P = L->n_heads, s_mid = L->total - L->n_init - L->n_local;
         const size_t words = ceil_div(s_mid, 32), C = size_t{1} << L->b;
         const bool tup = tuple_ok(L->m, L->b, L->tuple_hist, L->tuple_chunk_hist, s_mid);
@@ -339,6 +339,7 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         src.codes_head_stride = L->codes_head_stride;
         src.tuple_chunk_stride = L->tuple_chunks;
         const int mode = decode_mode(*L, g, k, d_ids != nullptr);
+        if (q_host && mode != PQKV_MODE_PAIRS_SPLIT) fail(PQKV_EINVAL, "decode: host queries only on the split pair path");
         switch (mode) {
             case PQKV_MODE_PAIRS_FUSED:
                 launch_decode_attend(ctx, *L, d_queries, g, nullptr, nullptr, nullptr, d_out, st, k);
@@ -356,6 +357,10 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
                 uint8_t* cls = reinterpret_cast<uint8_t*>(ws);
                 int* cut = reinterpret_cast<int*>(ws + round_up(P * C * C, 256));
                 unsigned* ready = ready_counters(ctx, P, st);
+                if (q_host) {
+                    src.queries = q_host;
+                    src.queries_copy = const_cast<float*>(d_queries);
+                }
                 launch_tuple_select(ctx, src, L->tuple_hist, L->tuple_chunk_hist, P, s_mid, k, cls, cut, nullptr,
                                     nullptr, st, ready);
                 launch_decode_attend(ctx, *L, d_queries, g, nullptr, cls, cut, d_out, st, 0, 0, ready);
@@ -380,6 +385,14 @@ int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size
         launch_bitmap_rows(ctx, bm, P, words, L->n_init, L->n_local, L->total, T, rows, st);
         launch_exact(ctx, d_queries, P, g, L->d_h, L->keys, L->values, L->kv_head_stride, rows, T, d_out, st);
         PQKV_CUDA(cudaFreeAsync(rows, st));
+}
+
+int pqkv_decode(pqkv_ctx* ctx, const pqkv_layer* L, const float* d_queries, size_t g, size_t k,
+                float* d_out, int64_t* d_ids, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_layer(L, g, k);
+        decode_core(ctx, L, d_queries, nullptr, g, k, d_out, d_ids, as_stream(stream));
     });
 }
 
@@ -496,9 +509,12 @@ static int decode_host_ops(pqkv_ctx* ctx, const pqkv_layer* L, const float* h_qu
         const bool direct = g > 1 && (mode == PQKV_MODE_PAIRS_FUSED || mode == PQKV_MODE_KEYS_FUSED ||
                                       mode == PQKV_MODE_KEYS_SPLIT);
         const float* mapped_q = direct ? static_cast<const float*>(device_view(h_queries)) : nullptr;
-        if (!mapped_q) PQKV_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, st));
-        int rc = pqkv_decode(ctx, L, mapped_q ? mapped_q : d_q, g, k, mapped ? mapped : d_o, nullptr, st);
-        if (rc != PQKV_OK) fail(rc, pqkv_last_error());
+        // split pair path (g = 1 north star): its select kernel reads the
+        // page-locked queries once and copies them for the attention grid
+        const float* sel_q = mode == PQKV_MODE_PAIRS_SPLIT ? static_cast<const float*>(device_view(h_queries)) : nullptr;
+        if (!mapped_q && !sel_q) PQKV_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, st));
+        check_layer(L, g, k);
+        decode_core(ctx, L, mapped_q ? mapped_q : d_q, sel_q, g, k, mapped ? mapped : d_o, nullptr, st);
         if (!mapped) PQKV_CUDA(cudaMemcpyAsync(h_out, d_o, qbytes, cudaMemcpyDeviceToHost, st));
     });
 }

@@ -159,6 +159,7 @@ struct SelectSource {
     const uint16_t* codes = nullptr;
     size_t codes_head_stride = 0;
     size_t tuple_chunk_stride = 0;  // chunks per head of the code-pair chunk table (0 = ceil(n/4096))
+    float* queries_copy = nullptr;  // tuple select: copy each head's queries here (the attention reads them)
     // score mode
     const float* scores = nullptr;
     size_t scores_stride = 0;

@@ -411,6 +411,7 @@ struct TupArgs {
     uint32_t* sel_before;   // [P][n_chunks] exclusive prefix of selected rows (ids mode) or null
     long long chunk_stride;  // chunks per head of chist
     unsigned* ready;        // [P] bumped once a head's classes are written (the attention polls it), or null
+    float* q_copy;          // [P][g][d_h] device copy of the queries for the attention (host-mapped input), or null
 };
 
 template <int NT>
@@ -427,7 +428,17 @@ __global__ void __launch_bounds__(NT, 1) tuple_select_kernel(TupArgs a) {
     // producer, then let the attention grid launch and stage its codes
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
-    pair_select<NT, NT >= 1024 ? 16 : 4096 / NT>(a.queries + (long long)p * a.g * a.d_h, a.g, a.d_h,
+    // host-mapped queries: read once, into the device copy the attention
+    // uses (published with the classes by the ready flag below) and which
+    // the select then reads
+    const float* qp = a.queries + (long long)p * a.g * a.d_h;
+    if (a.q_copy) {
+        float* qc = a.q_copy + (long long)p * a.g * a.d_h;
+        for (int e = tid; e < a.g * a.d_h; e += NT) qc[e] = qp[e];
+        __syncthreads();
+        qp = qc;
+    }
+    pair_select<NT, NT >= 1024 ? 16 : 4096 / NT>(qp, a.g, a.d_h,
                                  a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
                                  ch, a.n_chunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
                                  a.tkey ? a.tkey + (long long)p * C2 : nullptr);
@@ -709,6 +720,7 @@ void launch_tuple_select(pqkv_ctx* ctx, const SelectSource& src, const uint32_t*
     const size_t C = src.C, n_chunks = ceil_div(n, PQKV_TUPLE_CHUNK);
     TupArgs a{};
     a.ready = ready;
+    a.q_copy = ready ? src.queries_copy : nullptr;
     a.queries = src.queries;
     a.g = (int)src.g;
     a.d_h = (int)src.d_h;
