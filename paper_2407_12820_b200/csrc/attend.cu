@@ -1259,21 +1259,32 @@ template <int G, int NT = AT_THREADS>
 __device__ __forceinline__ void write_partial(const AtArgs& a, int p, int c, unsigned char* smem_raw, float (*wm)[G],
                                               float (*wl)[G]) {
     const float* wacc = reinterpret_cast<const float*>(smem_raw);  // [(NT / 32)][G][DH]
+    // per (warp, row) scale to the CTA's running max, computed once: [G][NT/32]
+    __shared__ float wsc[G][NT / 32], wmax[G], wsum[G];
+    if (threadIdx.x < G * 32) {
+        const int r = threadIdx.x / 32, ln = threadIdx.x % 32;
+        float M = -INFINITY;
+        for (int w = ln; w < (NT / 32); w += 32) M = fmaxf(M, wm[w][r]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(FULL, M, o));
+        float L = 0.f;
+        for (int w = ln; w < (NT / 32); w += 32) {
+            const float sc = M != -INFINITY ? safe_scale(wm[w][r], M) : 0.f;
+            wsc[r][w] = sc;
+            L += wl[w][r] * sc;
+        }
+        L = warp_sum(L);
+        if (ln == 0) { wmax[r] = M; wsum[r] = L; }
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < G * DH; e += NT) {
         const int r = e / DH, d = e % DH;
-        float M = -INFINITY;
-        for (int w = 0; w < (NT / 32); ++w) M = fmaxf(M, wm[w][r]);
-        float L = 0.f, O = 0.f;
-        if (M != -INFINITY) {
-            for (int w = 0; w < (NT / 32); ++w) {
-                const float sc = safe_scale(wm[w][r], M);
-                L += wl[w][r] * sc;
-                O += wacc[(w * G + r) * DH + d] * sc;
-            }
-        }
+        float O = 0.f;
+#pragma unroll 8
+        for (int w = 0; w < (NT / 32); ++w) O = fmaf(wacc[(w * G + r) * DH + d], wsc[r][w], O);
         float* o = a.part + (((long long)p * a.n_chunks + c) * G + r) * (DH + 2);
         o[2 + d] = O;
-        if (d == 0) { o[0] = M; o[1] = L; }
+        if (d == 0) { o[0] = wmax[r]; o[1] = wsum[r]; }
     }
 }
 
