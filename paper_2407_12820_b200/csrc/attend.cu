@@ -1390,7 +1390,7 @@ __device__ __forceinline__ void merge_parts(const float* pb, int n, float* dst_p
 // time), SRC_PAIRS or SRC_KEYS -- the fused single-launch modes get their own
 // instantiation so their prologues do not perturb the others' code.
 template <int G, int MODE, int NT = AT_THREADS>
-__global__ void __launch_bounds__(NT, NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS && G > 1) ? 2 : 4)) attend_kernel(AtArgs a) {
+__global__ void __launch_bounds__(NT, NT == 2 * AT_THREADS ? 2 : NT > AT_THREADS ? 1 : ((MODE == SRC_KEYS && G > 1) ? 2 : 4)) attend_kernel(AtArgs a) {
     const int src = MODE == 0 ? a.src : MODE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint32_t wtot[(NT / 32)];
@@ -2054,6 +2054,7 @@ static void launch_attend_g(const AtArgs& a, dim3 grid, size_t smem, int cl, cud
     if constexpr (G > 1) {
         if (a.nt > AT_THREADS) {  // wide g > 1 plans (1024 threads, no key path)
             if (a.src == SRC_PAIRS) launch_attend_gm<G, SRC_PAIRS, 1024>(a, grid, smem, cl, st);
+            else if (a.nt == 2 * AT_THREADS) launch_attend_gm<G, 0, 2 * AT_THREADS>(a, grid, smem, cl, st);
             else launch_attend_gm<G, 0, 1024>(a, grid, smem, cl, st);
             return;
         }
@@ -2217,7 +2218,6 @@ static void decode_args(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_p
     a.values = L.values;
     a.kv_head_stride = (long long)L.kv_head_stride;
     a.src = k_keys ? SRC_KEYS : (k_pairs ? SRC_PAIRS : (tuple_cls ? SRC_TUPLE : SRC_BITMAP));
-    (void)bitmap;
     a.n_init = (int)L.n_init;
     a.n_local = (int)L.n_local;
     a.total = (int)L.total;
@@ -2243,8 +2243,17 @@ static void decode_args(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_p
         // g > 1: one 1024-thread CTA per SM whose 32 warps claim rows
         // dynamically (every SM gets the same share of rows and no warp idles
         // at the end); pair mode selects in every CTA (no clusters)
-        const size_t per_head = std::max<size_t>(1, (size_t)ctx->sm_count / L.n_heads);
-        a.nt = 1024;
+        // bitmap-mode gathers (the key path's second launch) run two
+        // 512-thread CTAs per SM: a CTA (~100 KB, 32K registers) fits beside
+        // a select CTA still running on its SM, so units whose select is done
+        // start gathering there (cfg5 86.7 / 90.9 -> 83.1 / 87.6 us);
+        // PQKV_WIDE_NT=1024 restores one 1024-thread CTA per SM
+        static const int wide_nt = [] {
+            const char* e = std::getenv("PQKV_WIDE_NT");
+            return e && std::atoi(e) == 1024 ? 1024 : 2 * AT_THREADS;
+        }();
+        a.nt = bitmap ? wide_nt : 1024;
+        const size_t per_head = std::max<size_t>(1, (size_t)ctx->sm_count * (1024 / a.nt) / L.n_heads);
         static const bool claim = std::getenv("PQKV_CLAIM") != nullptr;
         a.claim = claim;
         a.chunk = (int)round_up(ceil_div(s_mid, per_head), (size_t)32);

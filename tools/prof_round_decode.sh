@@ -1,5 +1,5 @@
 set -x
-R=r02d
+R=${R:-r02d}
 N="ncu --set full --clock-control none --import-source on"
 timeout 900 python -m pytest tests -m gpu -q --timeout 180 > gpurun_out/${R}_pytest_gpu.txt 2>&1
 tail -3 gpurun_out/${R}_pytest_gpu.txt
