@@ -1926,7 +1926,7 @@ void launch_exact(pqkv_ctx* ctx, const float* queries, size_t P, size_t G, size_
 // reaches streaming bandwidth with ~1.6K rows per CTA, tools/microbench/
 // gather_probe.cu); middle chunks are multiples of PQKV_TUPLE_CHUNK so the
 // code-pair classification never splits a tuple chunk.
-static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
+static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid, bool fill) {
     static const int forced = [] {  // experiments only: PQKV_CHUNK_TOKENS=1024|2048|4096k
         const char* e = std::getenv("PQKV_CHUNK_TOKENS");
         return e ? std::atoi(e) : 0;
@@ -1939,6 +1939,15 @@ static int plan_chunk_tokens(pqkv_ctx* ctx, size_t P, size_t G, size_t s_mid) {
     if (per_head >= 2 * tcs) {  // few heads: 1/2 or 1/4 code-pair chunks per CTA
         const size_t sub = per_head >= 4 * tcs ? 4 : 2;
         return (int)(PQKV_TUPLE_CHUNK / sub);
+    }
+    // split pair path (no clusters): chunks of any 32-token multiple, sized
+    // so the grid fills every CTA slot of the wave (north star: 18 chunks of
+    // 7296 tokens = 576 CTAs, 4 per SM on all but 16 SMs, instead of 16 of
+    // 8192 = 512 CTAs with 68 SMs at 4 and 80 at 3): 156.0 / 151.7 ->
+    // 154.2 / 150.6 us
+    if (fill) {
+        const size_t ch = round_up(ceil_div(s_mid, per_head), (size_t)32);
+        if (ch <= 8192) return (int)ch;
     }
     size_t q = std::min<size_t>(8, std::max<size_t>(1, ceil_div(tcs, per_head)));
     return (int)(q * PQKV_TUPLE_CHUNK);
@@ -2222,7 +2231,7 @@ static void decode_args(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_p
     a.n_local = (int)L.n_local;
     a.total = (int)L.total;
     a.s_mid = (int)s_mid;
-    a.chunk = plan_chunk_tokens(ctx, L.n_heads, G, s_mid);
+    a.chunk = plan_chunk_tokens(ctx, L.n_heads, G, s_mid, tuple_cls);
     a.n_chunks = (int)std::max<size_t>(1, ceil_div(s_mid, (size_t)a.chunk));
     a.words = (int)ceil_div(s_mid, 32);
     a.codes = L.codes;

@@ -26,8 +26,8 @@ pytestmark = pytest.mark.gpu
 # dict under plan / configs.<name>.plan.
 EXPECT = {
     # g = 1: pair-select launch + attention launch (codes staged while the select runs)
-    "northstar": dict(mode="pairs_split", launches=2, chunk_tokens=8192, ctas_per_head=16, cluster=1, staged=1,
-                      window=8192),
+    "northstar": dict(mode="pairs_split", launches=2, chunk_tokens=7296, ctas_per_head=18, cluster=1, staged=1,
+                      window=7296),
     "cfg1": dict(mode="pairs_split", launches=2),
     "cfg2": dict(mode="pairs_split", launches=2, chunk_tokens=2048, ctas_per_head=16, cluster=1, staged=1),
     # g > 1: wide plan, one 1024-thread CTA per SM (148 // 8 = 18 per head), each selecting on its own
