@@ -2231,7 +2231,7 @@ static void decode_args(pqkv_ctx* ctx, const pqkv_layer& L, size_t G, size_t k_p
     a.n_local = (int)L.n_local;
     a.total = (int)L.total;
     a.s_mid = (int)s_mid;
-    a.chunk = plan_chunk_tokens(ctx, L.n_heads, G, s_mid, tuple_cls);
+    a.chunk = plan_chunk_tokens(ctx, L.n_heads, G, s_mid, tuple_cls || (bitmap && !k_pairs && !k_keys));
     a.n_chunks = (int)std::max<size_t>(1, ceil_div(s_mid, (size_t)a.chunk));
     a.words = (int)ceil_div(s_mid, 32);
     a.codes = L.codes;
