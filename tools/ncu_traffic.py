@@ -28,13 +28,15 @@ def val(r, name):
 
 res = {"source": os.path.basename(rep), "launches": []}
 for r in rows[2:]:
-    if "attend_kernel" not in r[hdr.index("Kernel Name")]:
+    name = r[hdr.index("Kernel Name")]
+    if "attend_kernel" not in name and "tuple_select_kernel" not in name:
         continue
     rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
     res["launches"].append({"kernel": r[hdr.index("Kernel Name")], "dram_read_bytes": rd, "dram_write_bytes": wr,
                             "duration_us_under_ncu": val(r, "gpu__time_duration.sum")})
-if res["launches"]:
-    l0 = res["launches"][0]
-    res["attend_kernel_fused"] = l0["dram_read_bytes"] + l0["dram_write_bytes"]
+if res["launches"]:  # per decode step: every captured launch (pair select + attention on the split path)
+    res["attend_kernel_fused"] = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in res["launches"])
+    res["note"] = "per decode step: the pair-select launch + the attention launch"
+
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps(res))
