@@ -110,6 +110,39 @@ def test_decode_host_graph_replay(ctx, orc, g):
                             q.cuda(), k)
 
 
+def test_decode_host_graph_replay_key_path(ctx, orc):
+    """The split key path (m4b8, g = 4: cluster select -> gather polling each
+    unit's select-done counter) replayed as a graph by pqkv_decode_host: the
+    counters reset by each decode must leave every replay equal to the plain
+    decode, and the oracle's selection."""
+    import torch
+
+    P, S, n_init, n_local, g, k = 3, 9000, 4, 64, 4, 900
+    keys, vals, q0 = orc.gen_workload(S, 128, P, g, oracle_kind(), seed=41)
+    s_mid = S - n_init - n_local
+    cen, codes = ctx.pq_build(torch.from_numpy(np.ascontiguousarray(keys[:, n_init:n_init + s_mid])).cuda(), 4, 8,
+                              4, list(range(P)))
+    import paper_2407_12820_b200 as pq
+
+    layer = pq.DecodeLayer(keys=torch.from_numpy(keys).cuda(), values=torch.from_numpy(vals).cuda(), centroids=cen,
+                           codes=codes, total=S, n_init=n_init, n_local=n_local, b=8)
+    assert ctx.decode_plan(layer, g, k)["mode"] == "keys_split"
+    hq = torch.empty((P, g, 128)).pin_memory()
+    ho = torch.empty((P, g, 128)).pin_memory()
+    rng = np.random.default_rng(7)
+    cen_h, codes_h = cen.cpu().numpy(), codes.cpu().numpy().view(np.uint16)
+    for step in range(4):
+        q = q0 + 0.05 * rng.standard_normal(q0.shape).astype(np.float32)
+        hq.copy_(torch.from_numpy(q))
+        ctx.decode_host(layer, hq, ho, k)
+        want = ctx.decode(layer, torch.from_numpy(q).cuda(), k).cpu()
+        assert torch.equal(ho, want), f"step {step}"
+        p = step % P
+        rows = orc.top_k_desc(orc.pq_score_gqa(q[p], cen_h[p], codes_h[p]), k)
+        ref = orc.selective_attention(q[p, 0], keys[p], vals[p], n_init, n_local, rows + n_init)
+        assert np.abs(ho[p, 0].numpy() - ref).max() / np.abs(ref).max() < 1e-3, f"step {step}"
+
+
 def oracle_kind():
     import oracle
 
