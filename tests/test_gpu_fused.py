@@ -77,12 +77,13 @@ def test_fused_decode_selection_exact(ctx, orc, m, b, tables, s, P, g, k):
          tables)
 
 
-@pytest.mark.parametrize("m,b,c_used", [(4, 8, 3), (4, 8, 6), (4, 8, 12), (2, 6, 2)])
+@pytest.mark.parametrize("m,b,c_used", [(4, 8, 1), (4, 8, 3), (4, 8, 6), (4, 8, 12), (2, 6, 2)])
 def test_fused_decode_heavy_ties(ctx, orc, m, b, c_used):
-    """Few distinct codes: thousands of tokens share the threshold score (3 of
-    256 codes used: the key path's value bins cannot split the threshold
-    score's ties, so its radix fallback runs); 6 or 12 codes: a handful of
-    ties at K* inside a small final bin (the candidate path's tie order)."""
+    """Few distinct codes: thousands of tokens share the threshold score (1 or
+    3 of 256 codes used: the key path's value bins cannot split the threshold
+    score's ties -- with one code every score is equal and the refined bin
+    has zero width -- so its radix fallback runs); 6 or 12 codes: a handful
+    of ties at K* inside a small final bin (the candidate path's tie order)."""
     rng = np.random.default_rng(c_used)
     P, s, n_init, n_local, k = 2, 12000, 4, 64, 3000
     s_mid = s - n_init - n_local
