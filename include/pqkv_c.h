@@ -105,7 +105,10 @@ PQKV_API int pqkv_ctx_last_decode_profile(pqkv_ctx* ctx, double out[4]);
  * clock64 at start / after pair select / after the row list / after the
  * gather; globaltimer ns at start / after the row list / after the gather /
  * at exit; clock64 at the pair-select phase marks 0..6 (cluster rank 0) and
- * after the first cluster barrier; [16] SM id, [17] cluster rank.
+ * after the first cluster barrier; [16] SM id, [17] cluster rank.  Key-path
+ * select (PQKV_PROF_SELECT=1 profiles that launch): [8..15] clock64 phase
+ * marks, [21] value passes | candidate path << 8, [22] candidates in the
+ * final bin, [23] that bin's cluster-wide count.
  * *n_ctas = CTAs; copies min(cap, PQKV_PROF_SLOTS*n). */
 PQKV_API int pqkv_ctx_decode_profile_raw(pqkv_ctx* ctx, uint64_t* out, size_t cap, size_t* n_ctas);
 
