@@ -424,6 +424,14 @@ __global__ void __launch_bounds__(NT, 1) tuple_select_kernel(TupArgs a) {
     uint32_t* hist = ps.hist;  // per-chunk counts below (dead radix bins, 2*NB entries with cnt)
     uint8_t* cls = a.cls + (long long)p * C2;
     const uint16_t* ch = a.chist + (long long)p * a.chunk_stride * C2;
+    // the centroid table is staged before the wait (no kernel that lets this
+    // grid launch early writes centroids: only the attention and select
+    // kernels trigger programmatic launches)
+    const float* cen = a.centroids + (long long)p * 2 * C * (a.d_h / 2);
+    float4* stage = pair_lut_stage(C, a.d_h, ps.hist);
+    const bool prestaged =
+        lut_staged((a.q_copy ? a.q_copy : a.queries) + (long long)p * a.g * a.d_h, cen, a.d_h, 2, stage);
+    if (prestaged) stage_centroids(cen, a.d_h, 2, C, stage);
     // launched with programmatic stream serialization: wait for the queries'
     // producer, then let the attention grid launch and stage its codes
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -441,7 +449,7 @@ __global__ void __launch_bounds__(NT, 1) tuple_select_kernel(TupArgs a) {
     pair_select<NT, NT >= 1024 ? 16 : 4096 / NT>(qp, a.g, a.d_h,
                                  a.centroids + (long long)p * 2 * C * (a.d_h / 2), C, a.thist + (long long)p * C2,
                                  ch, a.n_chunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
-                                 a.tkey ? a.tkey + (long long)p * C2 : nullptr);
+                                 a.tkey ? a.tkey + (long long)p * C2 : nullptr, nullptr, prestaged);
     if (tid == 0) {
         a.cut[2 * p] = (int)sh[3];
         a.cut[2 * p + 1] = (int)sh[4];

@@ -156,17 +156,31 @@ __device__ __forceinline__ void lut_entry_staged(double* lut, const float* q, co
 // one CTA pulling a 32 KB table with per-lane row loads (256 B apart) was the
 // slowest part of the pair select (tools/microbench/lut_probe.cu: 3.2 ->
 // 1.9 us warm).
-__device__ inline void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
-                          int C, float4* stage = nullptr) {
+// Whether build_lut stages the centroid table (in `stage`) for these inputs.
+__device__ __forceinline__ bool lut_staged(const float* q, const float* cen, int d_h, int m, const void* stage) {
     const int dm = d_h / m;
-    if (stage && (dm == 64 || dm == 32) && ((reinterpret_cast<uintptr_t>(cen) | reinterpret_cast<uintptr_t>(q)) & 15) == 0 &&
-        (d_h % 4) == 0) {
-        const int cpr = dm / 4, n = m * C * cpr;  // 16-byte chunks per row, in total
-        for (int f = threadIdx.x; f < n; f += blockDim.x) {
-            const int e = f / cpr, u = f % cpr;
-            cp_async16(stage + (long long)e * cpr + (u ^ (e & 7)), cen + 4LL * f);
-        }
-        cp_async_commit();
+    return stage && (dm == 64 || dm == 32) &&
+           ((reinterpret_cast<uintptr_t>(cen) | reinterpret_cast<uintptr_t>(q)) & 15) == 0 && (d_h % 4) == 0;
+}
+
+// The centroid-table staging copies of build_lut (cp.async, one commit group).
+__device__ inline void stage_centroids(const float* cen, int d_h, int m, int C, float4* stage) {
+    const int cpr = d_h / m / 4, n = m * C * cpr;  // 16-byte chunks per row, in total
+    for (int f = threadIdx.x; f < n; f += blockDim.x) {
+        const int e = f / cpr, u = f % cpr;
+        cp_async16(stage + (long long)e * cpr + (u ^ (e & 7)), cen + 4LL * f);
+    }
+    cp_async_commit();
+}
+
+// prestaged: the caller already issued stage_centroids (e.g. before its
+// griddepcontrol.wait: the centroids are not written by a kernel that lets
+// this one launch early)
+__device__ inline void build_lut(double* lut, const float* q, const float* cen, int g, int d_h, int m,
+                          int C, float4* stage = nullptr, bool prestaged = false) {
+    const int dm = d_h / m;
+    if (lut_staged(q, cen, d_h, m, stage)) {
+        if (!prestaged) stage_centroids(cen, d_h, m, C, stage);
         cp_async_wait_all();
         __syncthreads();
         for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
@@ -277,6 +291,12 @@ __device__ void find_digit(const uint32_t* hist, int nb, uint32_t k_rem, uint32_
 }
 
 
+// Where pair_select stages the centroid table: hist[] .. lst[] (2 NB + C^2
+// words, unused before its compaction) when it fits.
+__device__ __forceinline__ float4* pair_lut_stage(int C, int d_h, uint32_t* hist) {
+    return 2 * C * (d_h / 2) <= 2 * NB + C * C ? reinterpret_cast<float4*>(hist) : nullptr;
+}
+
 // Pair-level exact top-k for one head (m == 2): builds the ADC table, the
 // keys of the code pairs that occur (thist > 0), selects the k-th
 // largest key weighted by the pair histogram thist, classifies every pair
@@ -295,7 +315,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
                             const uint32_t* thist, const uint16_t* chist, int n_chunks, int k,
                             double* lut, uint32_t* hist, uint32_t* cnt, uint32_t* lst, uint32_t* ceq,
                             uint32_t* wsum, uint32_t* sh, uint8_t* cls, uint32_t* tkey_out,
-                            unsigned long long* tp = nullptr) {
+                            unsigned long long* tp = nullptr, bool cen_prestaged = false) {
     const int tid = threadIdx.x, C2 = C * C, lane = tid & 31, warp = tid >> 5;
     const int wbits = 32 - (32 - __clz((unsigned)(C2 - 1) | 1u));  // weight bits of a list entry
     const uint32_t wmask = (1u << wbits) - 1u;
@@ -310,7 +330,7 @@ __device__ void pair_select(const float* q, int g, int d_h, const float* cen, in
     }
     // the centroid table is staged in hist[] .. lst[] (2 NB + C^2 words, not
     // used before the compaction below) when it fits
-    build_lut(lut, q, cen, g, d_h, 2, C, 2 * C * (d_h / 2) <= 2 * NB + C * C ? reinterpret_cast<float4*>(hist) : nullptr);
+    build_lut(lut, q, cen, g, d_h, 2, C, pair_lut_stage(C, d_h, hist), cen_prestaged);
     for (int c = tid; c < n_chunks; c += NT) ceq[c] = 0;
     for (int e = tid; e < (C2 + 3) / 4; e += NT) reinterpret_cast<uint32_t*>(cls)[e] = 0u;
     PQKV_T(1);
