@@ -1427,12 +1427,24 @@ __global__ void __launch_bounds__(NT, NT == 2 * AT_THREADS ? 2 : NT > AT_THREADS
         const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
         const char* cd = reinterpret_cast<const char*>(a.codes + p * a.codes_head_stride + 2 * (long long)r0);
         for (int o = tid * 128; o < 4 * (r1 - r0); o += NT * 128) prefetch_l2(cd + o);
-        if ((c & 7) == 0) {  // one CTA per cluster: the head's select tables
+        if ((c & 7) == 0 || NT > AT_THREADS) {  // the selecting CTAs: the head's select tables
             const char* ce = reinterpret_cast<const char*>(a.centroids + (long long)p * 2 * a.C * (DH / 2));
             for (int o = tid * 128; o < 4 * a.C * DH; o += NT * 128) prefetch_l2(ce + o);
             const char* th = reinterpret_cast<const char*>(a.thist + (long long)p * C2);
             for (int o = tid * 128; o < 4 * C2; o += NT * 128) prefetch_l2(th + o);
         }
+    }
+    // wide pair CTAs (each its own selector, nothing else in shared memory
+    // yet) stage the centroid table of their pair select before the wait: no
+    // kernel that lets this grid launch early writes centroids
+    bool cen_pre = false;
+    if (MODE == SRC_PAIRS && NT > AT_THREADS) {
+        PairScratch ps0(smem_raw, a.C, a.n_tchunks);
+        const float* cen = a.centroids + (long long)p * 2 * a.C * (DH / 2);
+        float4* stage = pair_lut_stage(a.C, DH, ps0.hist);
+        // = build_lut's staging predicate: the queries come from q_sh (16-byte aligned), d_m = 64
+        cen_pre = stage && (reinterpret_cast<uintptr_t>(cen) & 15) == 0;
+        if (cen_pre) stage_centroids(cen, DH, 2, a.C, stage);
     }
     if (MODE == SRC_KEYS) {  // this CTA's code rows and its share of the centroids (ADC table)
         const int r0 = c * a.chunk, r1 = min(a.s_mid, r0 + a.chunk);
@@ -1580,7 +1592,7 @@ __global__ void __launch_bounds__(NT, NT == 2 * AT_THREADS ? 2 : NT > AT_THREADS
                                             a.centroids + (long long)p * 2 * C * (DH / 2), C,
                                             a.thist + (long long)p * C2, a.chist + (long long)p * a.tchunk_stride * C2,
                                             a.n_tchunks, a.k, ps.lut, ps.hist, ps.cnt, ps.lst, ps.ceq, ps.wsum, ps.sh, cls,
-                                            nullptr, a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr);
+                                            nullptr, a.prof ? a.prof + cta * PQKV_PROF_SLOTS + 8 : nullptr, cen_pre);
                 const uint32_t* sh = ps.sh;
                 if (tid == 0) { cut_s[0] = sh[3]; cut_s[1] = sh[4]; }
             }
